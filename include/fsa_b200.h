@@ -1,0 +1,188 @@
+/*
+ * fsa_b200.h — C ABI of the B200-native FSA iterative core.
+ *
+ * Drop-in boundary for the iterative path of the reference library `fsagp`
+ * (/root/reference/proj). Every entry point names the reference interface it
+ * replaces. Conventions follow the reference's Eigen types:
+ *   - dense matrices are column-major doubles (den_mat_t, types.h:14), points
+ *     in the caller's original order (LocationSet::coords is n x d);
+ *   - sparse outputs are CSR with int64 row offsets and int32 column indices,
+ *     columns sorted per row (sp_mat_t RowMajor, types.h:15-16);
+ *   - parameter order is (sigma2 = nugget, sigma1_2 = marginal variance, rho)
+ *     (types.h:72-102); gradients follow the same order.
+ * The caller owns all host buffers; device state lives in the opaque handles.
+ * Return codes: FSA_OK, FSA_EINVAL (std::invalid_argument in the reference,
+ * types.h:27-29), FSA_ENUMERIC (fsagp::NumericalError, types.h:22-25),
+ * FSA_ECUDA (device failure). fsa_last_error() gives the message (thread-local).
+ * There is no CPU fallback: every compute entry point needs a CUDA device.
+ */
+#ifndef FSA_B200_H
+#define FSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSA_OK 0
+#define FSA_EINVAL 2
+#define FSA_ENUMERIC 3
+#define FSA_ECUDA 4
+
+typedef struct fsa_ctx fsa_ctx;
+typedef struct fsa_geometry fsa_geometry;
+typedef struct fsa_model fsa_model;
+typedef struct fsa_precond fsa_precond;
+typedef struct fsa_pred fsa_pred;
+
+/* MaternNu / TaperSpec / CovParams / AssembleOptions (types.h:32-102, fsa.h:15-18) */
+typedef struct {
+  int nu_code;       /* 0: nu = 1/2, 1: nu = 3/2, 2: nu = 5/2 */
+  int taper_family;  /* 1: wendland1, 2: wendland2 */
+  double gamma;      /* taper range */
+  double sigma2;     /* nugget */
+  double sigma1_2;   /* marginal variance */
+  double rho;        /* range */
+  double jitter_rel; /* AssembleOptions::jitter_rel, default 1e-10 */
+} fsa_params;
+
+/* CgOptions (krylov.h:28-32) */
+typedef struct {
+  double tol;
+  int max_iter;
+  int error_on_max_iter;
+} fsa_cg_options;
+
+/* IterativeNll (estimation.h:91-97) plus timing diagnostics */
+typedef struct {
+  double nll;
+  double grad[3];
+  double logdet;
+  int cg_iterations;
+  int sweeps;
+  int64_t rhs_iterations; /* sum over columns of CG iterations */
+  double pcg_ms;          /* device time of the PCG solve */
+  double total_ms;        /* device time of the whole evaluation */
+} fsa_nll_result;
+
+/* PredVarResult (prediction.h:37-42) scalars */
+typedef struct {
+  int clamped;
+  int cg_iterations;
+  double det_ms;
+  double sim_ms;
+} fsa_predvar_info;
+
+const char* fsa_last_error(void);
+int fsa_version(void);
+
+/* ---- context (one per device; one host thread per context) ---------------------- */
+int fsa_ctx_create(int device, fsa_ctx** out);
+void fsa_ctx_destroy(fsa_ctx* ctx);
+int fsa_ctx_synchronize(fsa_ctx* ctx);
+int fsa_ctx_stream(fsa_ctx* ctx, void** stream); /* cudaStream_t all kernels run on */
+/* CUDA-event timers around kernel groups (name -> total ms, launches, algorithmic units) */
+int fsa_ctx_set_profiling(fsa_ctx* ctx, int on);
+int fsa_ctx_reset_timers(fsa_ctx* ctx);
+int fsa_ctx_timer_names(fsa_ctx* ctx, char* buf, size_t len); /* newline separated */
+int fsa_ctx_timer(fsa_ctx* ctx, const char* name, double* ms, int64_t* count, double* units);
+
+/* ---- input generators (host; same RNG streams as the reference) -------------------- */
+/* uniform_locations (locations.cpp:9-17) */
+int fsa_uniform_locations(int64_t n, int d, uint64_t seed, double* coords_out);
+/* select_random (inducing.cpp:11-24) */
+int fsa_select_random(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, double* out);
+/* select_kmeanspp (inducing.cpp:48-139), KmeansOptions{max_iter, rel_tol} */
+int fsa_select_kmeanspp(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, int max_iter,
+                        double rel_tol, double* out);
+/* gamma_for_avg_row_nnz (locations.cpp:192-195) */
+double fsa_gamma_for_avg_row_nnz(int64_t n, double target_row_nnz);
+/* synthetic response: random-Fourier-feature Matern draw + N(0, nugget) noise */
+int fsa_simulate_rff(const double* coords, int64_t n, int d, int nu_code, double sigma1_2, double rho,
+                     double nugget, int features, uint64_t seed, double* y_out);
+/* clustered locations: mixture of Gaussian blobs on [0,1]^d */
+int fsa_blob_locations(int64_t n, int d, int blobs, double sd, uint64_t seed, double* coords_out);
+/* probe streams: probe_rng + gaussian_vector / rademacher_vector (types.h:104-129) */
+int fsa_probe_gaussian(uint64_t seed, uint64_t index, int64_t n1, double* e1, int64_t n2, double* e2);
+int fsa_probe_rademacher(uint64_t seed, uint64_t index, int64_t n, double* z);
+
+/* ---- geometry: sorted points + taper pattern (GridIndex/taper_pattern, locations.cpp:19-163) */
+int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, double gamma, fsa_geometry** out);
+void fsa_geometry_destroy(fsa_geometry* g);
+int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz);
+/* taper_pattern output in the caller's order: distances as values */
+int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist);
+/* internal (space-filling-curve) order: perm[internal] = original index */
+int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm);
+
+/* ---- FSA model (FsaModel, fsa.h:40-104) -------------------------------------------- */
+/* FsaModel::assemble(locs, inducing, kern, taper, params, opts) (fsa.h:42-43); builds the geometry */
+int fsa_model_assemble(fsa_ctx* ctx, const double* coords, int64_t n, int d, const double* inducing, int64_t m,
+                       const fsa_params* params, fsa_model** out);
+/* same on a cached geometry (the taper pattern is parameter independent) */
+int fsa_model_assemble_geo(fsa_geometry* g, const double* inducing, int64_t m, const fsa_params* params,
+                           fsa_model** out);
+void fsa_model_destroy(fsa_model* md);
+int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t* n_clamped,
+                   double* logdet_sigma_m);
+/* sigma_s (which = 0) or deriv_sigma_s(2) (which = 1) in the caller's order */
+int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, double* val);
+/* FsaModel::matmat (fsa.cpp:65-68): out = Sigma V, V n x k */
+int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out);
+/* FsaModel::deriv_matmat (fsa.cpp:165-182) */
+int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k, double* out);
+/* diag(Sigma_s) including the nugget (the FITC / Jacobi diagonal) and |U_i|^2 = lowrank diag */
+int fsa_model_diagonals(fsa_model* md, double* sigma_s_diag, double* lowrank_diag);
+
+/* ---- preconditioners (make_preconditioner, estimation.h:81-82; preconditioners.h) -- */
+/* type: 0 none (IdentityPrecond), 1 diagonal (DiagPrecond), 2 fitc (FitcPrecond::from_fsa(model, true)) */
+int fsa_make_preconditioner(fsa_model* md, int type, fsa_precond** out);
+/* DiagPrecond(sigma_s.diagonal()) without derivatives (prediction.cpp:94) */
+int fsa_make_jacobi(fsa_model* md, fsa_precond** out);
+void fsa_precond_destroy(fsa_precond* p);
+int fsa_precond_logdet(fsa_precond* p, double* out);
+int fsa_precond_solve_mat(fsa_precond* p, const double* R, int64_t k, double* out);
+/* Preconditioner::sample_probes (preconditioners.cpp:13-20) */
+int fsa_precond_sample_probes(fsa_precond* p, int num_probes, uint64_t seed, double* Z);
+/* Preconditioner::deriv_trace (preconditioners.cpp:106-115) */
+int fsa_precond_deriv_trace(fsa_precond* p, int which, double* out);
+
+/* ---- Krylov (krylov.h:49-142) -------------------------------------------------------- */
+/* pcg_solve_multi (krylov.cpp:18-106), batched. op_kind: 0 FSA operator, 1 sigma_s only.
+ * tdiag / toff: k x max_iter column-major (column j holds iterations[j] / iterations[j]-1 entries). */
+int fsa_pcg_solve_multi(fsa_model* md, fsa_precond* p, int op_kind, const double* B, int64_t k,
+                        const fsa_cg_options* cg, double* X, int* iterations, int* converged, double* tdiag,
+                        double* toff, int* sweeps);
+/* tridiag_log_quadrature (krylov.cpp:120-142) */
+int fsa_tridiag_log_quadrature(const double* diag, const double* off, int64_t len, double* out);
+/* iterative_nll_grad (estimation.cpp:178-227). X may be NULL when p = 0; beta has p entries.
+ * cv_mode: 0 none, 1 one, 2 optimal (CvMode, krylov.h:87). */
+int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const double* X, int64_t pcols,
+                           int num_probes, uint64_t seed, const fsa_cg_options* cg, int cv_mode, int want_grad,
+                           fsa_nll_result* out, double* beta);
+
+/* ---- prediction (prediction.h:21-56) ------------------------------------------------- */
+/* make_prediction_set (prediction.cpp:7-27) */
+int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** out);
+void fsa_pred_destroy(fsa_pred* pr);
+int fsa_pred_info(fsa_pred* pr, int64_t* np, int64_t* nnz);
+/* cross_apply_t (prediction.cpp:29-31): out (np) = Sigma_np^T u */
+int fsa_cross_apply_t(fsa_pred* pr, const double* u, double* out);
+/* predict_mean_iterative (prediction.cpp:37-43) */
+int fsa_predict_mean_iterative(fsa_pred* pr, const double* resid, fsa_precond* p, const fsa_cg_options* cg,
+                               double* mean_out);
+/* predict_var_sim (prediction.cpp:131-172); SimVarOptions (prediction.h:43-50) */
+int fsa_predict_var_sim(fsa_pred* pr, int num_probes, uint64_t seed, const fsa_cg_options* cg,
+                        const fsa_cg_options* cg_s, int control_variate, double floor_rel, double* var,
+                        double* se, fsa_predvar_info* info);
+/* the deterministic diagonals d1, d2, d3 of predict_var_sim (prediction.cpp:72-110) */
+int fsa_pred_det_pieces(fsa_pred* pr, const fsa_cg_options* cg, const fsa_cg_options* cg_s, double* d1,
+                        double* d2, double* d3, int* cg_iterations);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSA_B200_H */

@@ -1,0 +1,62 @@
+// Column-batched vector kernels and PCG control; see blas1.cu.
+#pragma once
+
+#include "common.cuh"
+
+namespace fsa {
+
+enum { kErrNone = 0, kErrOperatorNotPD = 1, kErrPrecondNotPD = 2 };
+
+// Per-column PCG state, device resident (one entry per RHS column).
+struct CgState {
+  double* rz;
+  double* alpha_prev;
+  double* beta_prev;
+  double* alpha;
+  double* beta;
+  double* scale;
+  int* active;
+  int* converged;
+  int* iterations;
+  double* tdiag;  // [k][max_iter]
+  double* toff;   // [k][max_iter]
+  int* err;
+  int* host_flags;  // mapped pinned memory: [num_active, err]
+};
+
+size_t coldot_scratch(long n, long t);
+void launch_coldot(const double* A, const double* B, long n, long ld, long t, double* out, double* scratch,
+                   cudaStream_t s);
+void launch_coldot_weighted(const double* A, const double* B, const double* w, long n, long ld, long t,
+                            double* out, double* scratch, cudaStream_t s);
+
+// host layout (column-major n x k, original order, already on the device) ->
+// columns [col0, col0 + k) of a row-major n_pad x tp internal-order block (padding rows zeroed)
+void pack_cols(const double* in_dev, long n, long k, const int* perm_dev, long n_pad, long tp, long col0,
+               double* out, cudaStream_t s);
+// dst[i][j] = src[i][j] for i < n, j < k (row-major blocks of different widths)
+void copy_cols(const double* src, long lds, double* dst, long ldd, long n, long k, cudaStream_t s);
+void sum_log(const double* x, long n, double* out_dev, cudaStream_t s);
+// y[i] = (x[i] + a) * b for i < n, 0 on padding
+void affine_vec(double* y, const double* x, double a, double b, long n, long n_pad, cudaStream_t s);
+void pinv_diag(double* out, const double* D, const double* q, long n, long n_pad, cudaStream_t s);
+void add_identity(double* A, long ld, long m, cudaStream_t s);
+// inverse of pack_cols for columns [col0, col0 + k)
+void unpack_cols(const double* in, long n, long k, const int* perm_dev, long tp, long col0, double* out_dev,
+                 cudaStream_t s);
+
+void cg_start(const double* rr, long k, double tol, const CgState& st, cudaStream_t s);
+void cg_start_rz(const double* rz, long k, const CgState& st, cudaStream_t s);
+void cg_alpha(const double* hv, long k, int it, int max_iter, const CgState& st, cudaStream_t s);
+void cg_check(const double* rr, long k, double tol, const CgState& st, cudaStream_t s);
+void cg_beta(const double* rzn, long k, const CgState& st, cudaStream_t s);
+void cg_count(long k, const CgState& st, cudaStream_t s);
+void update_xr(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp, long k,
+               cudaStream_t s);
+void update_h(double* H, const double* Z, const int* active, const double* beta, long n, long tp, long k,
+              cudaStream_t s);
+void init_h(double* H, const double* Z, const int* active, long n, long tp, long k, cudaStream_t s);
+void scale_rows(double* Y, const double* X, const double* w, long n, long tp, cudaStream_t s);
+void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_t s);
+
+}  // namespace fsa

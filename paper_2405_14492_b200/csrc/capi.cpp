@@ -1,0 +1,526 @@
+// extern "C" boundary (include/fsa_b200.h) over the device FSA core.
+#include "../../include/fsa_b200.h"
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "blas1.cuh"
+#include "fsa_core.cuh"
+#include "inputs.h"
+#include "predict.cuh"
+
+using namespace fsa;
+
+struct fsa_ctx {
+  std::unique_ptr<Context> c;
+};
+struct fsa_geometry {
+  fsa_ctx* ctx;
+  std::shared_ptr<Geometry> g;
+};
+struct fsa_model {
+  fsa_ctx* ctx;
+  std::unique_ptr<Model> m;
+};
+struct fsa_precond {
+  fsa_model* md;
+  std::unique_ptr<Precond> p;
+};
+struct fsa_pred {
+  fsa_model* md;
+  std::unique_ptr<PredictionSet> p;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FSA_OK;
+  } catch (const NumericalError& e) {
+    g_err = e.what();
+    return FSA_ENUMERIC;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return FSA_EINVAL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return FSA_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FSA_ECUDA;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + " is null");
+}
+
+Params to_params(const fsa_params* p) {
+  need(p, "params");
+  Params q;
+  q.nu = p->nu_code;
+  q.family = p->taper_family;
+  q.gamma = p->gamma;
+  q.sigma2 = p->sigma2;
+  q.sigma1_2 = p->sigma1_2;
+  q.rho = p->rho;
+  q.jitter_rel = p->jitter_rel;
+  return q;
+}
+
+CgOptions to_cg(const fsa_cg_options* c) {
+  CgOptions o;
+  if (c) {
+    o.tol = c->tol;
+    o.max_iter = c->max_iter;
+    o.error_on_max_iter = c->error_on_max_iter != 0;
+  }
+  return o;
+}
+
+// host column-major (original order) n x k -> device internal block (n_pad x tp)
+DBuf<double> to_device_block(Model* md, const double* host, long k, long tp) {
+  cudaStream_t s = md->ctx->stream;
+  DBuf<double> raw(static_cast<size_t>(md->n * k)), blk(static_cast<size_t>(md->n_pad * tp));
+  FSA_CUDA(cudaMemcpyAsync(raw.get(), host, sizeof(double) * md->n * k, cudaMemcpyHostToDevice, s));
+  FSA_CUDA(cudaMemsetAsync(blk.get(), 0, sizeof(double) * md->n_pad * tp, s));
+  pack_cols(raw.get(), md->n, k, md->geo->pts.perm_d.get(), md->n_pad, tp, 0, blk.get(), s);
+  FSA_CUDA(cudaStreamSynchronize(s));
+  return blk;
+}
+void to_host_block(Model* md, const double* blk, long k, long tp, double* host) {
+  cudaStream_t s = md->ctx->stream;
+  DBuf<double> raw(static_cast<size_t>(md->n * k));
+  unpack_cols(blk, md->n, k, md->geo->pts.perm_d.get(), tp, 0, raw.get(), s);
+  FSA_CUDA(cudaMemcpyAsync(host, raw.get(), sizeof(double) * md->n * k, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+}
+
+// internal CSR (rows/cols in sorted order) -> caller order, columns ascending
+void export_csr(const Csr& pat, const double* vals_dev, const SortedPoints& rows, const SortedPoints& cols,
+                cudaStream_t s, int64_t* rowptr, int32_t* col, double* val) {
+  const long nr = pat.rows, nnz = pat.nnz;
+  std::vector<long> rp(static_cast<size_t>(nr + 1));
+  std::vector<int> ci(static_cast<size_t>(nnz));
+  std::vector<double> v(static_cast<size_t>(nnz));
+  FSA_CUDA(cudaMemcpyAsync(rp.data(), pat.rowptr.get(), sizeof(long) * (nr + 1), cudaMemcpyDeviceToHost, s));
+  if (nnz > 0) {
+    FSA_CUDA(cudaMemcpyAsync(ci.data(), pat.col.get(), sizeof(int) * nnz, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(v.data(), vals_dev, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+  }
+  FSA_CUDA(cudaStreamSynchronize(s));
+  rowptr[0] = 0;
+  for (long ro = 0; ro < nr; ++ro) {
+    const long i = rows.iperm[static_cast<size_t>(ro)];
+    rowptr[ro + 1] = rowptr[ro] + (rp[static_cast<size_t>(i + 1)] - rp[static_cast<size_t>(i)]);
+  }
+  std::vector<std::pair<int, double>> tmp;
+  for (long ro = 0; ro < nr; ++ro) {
+    const long i = rows.iperm[static_cast<size_t>(ro)];
+    tmp.clear();
+    for (long p = rp[static_cast<size_t>(i)]; p < rp[static_cast<size_t>(i + 1)]; ++p)
+      tmp.emplace_back(cols.perm[static_cast<size_t>(ci[static_cast<size_t>(p)])], v[static_cast<size_t>(p)]);
+    std::sort(tmp.begin(), tmp.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    long q = rowptr[ro];
+    for (const auto& e : tmp) {
+      if (col) col[q] = e.first;
+      if (val) val[q] = e.second;
+      ++q;
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* fsa_last_error(void) { return g_err.c_str(); }
+int fsa_version(void) { return 1; }
+
+int fsa_ctx_create(int device, fsa_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    auto c = std::make_unique<fsa_ctx>();
+    c->c = std::make_unique<Context>(device);
+    *out = c.release();
+  });
+}
+void fsa_ctx_destroy(fsa_ctx* ctx) { delete ctx; }
+int fsa_ctx_synchronize(fsa_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->sync();
+  });
+}
+int fsa_ctx_stream(fsa_ctx* ctx, void** stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    *stream = ctx->c->stream;
+  });
+}
+int fsa_ctx_set_profiling(fsa_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->flush_timers();
+    ctx->c->profile = on != 0;
+  });
+}
+int fsa_ctx_reset_timers(fsa_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->flush_timers();
+    ctx->c->totals.clear();
+  });
+}
+int fsa_ctx_timer_names(fsa_ctx* ctx, char* buf, size_t len) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->flush_timers();
+    std::string s;
+    for (const auto& kv : ctx->c->totals) s += kv.first + "\n";
+    if (buf && len > 0) {
+      std::strncpy(buf, s.c_str(), len - 1);
+      buf[len - 1] = 0;
+    }
+  });
+}
+int fsa_ctx_timer(fsa_ctx* ctx, const char* name, double* ms, int64_t* count, double* units) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(name, "name");
+    ctx->c->flush_timers();
+    auto it = ctx->c->totals.find(name);
+    const Context::Acc a = it == ctx->c->totals.end() ? Context::Acc{} : it->second;
+    if (ms) *ms = a.ms;
+    if (count) *count = a.count;
+    if (units) *units = a.units;
+  });
+}
+
+int fsa_uniform_locations(int64_t n, int d, uint64_t seed, double* out) {
+  return guard([&] { uniform_locations(n, d, seed, out); });
+}
+int fsa_select_random(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, double* out) {
+  return guard([&] { select_random(coords, n, d, m, seed, out); });
+}
+int fsa_select_kmeanspp(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, int max_iter,
+                        double rel_tol, double* out) {
+  return guard([&] { select_kmeanspp(coords, n, d, m, seed, max_iter, rel_tol, out); });
+}
+double fsa_gamma_for_avg_row_nnz(int64_t n, double target) {
+  double g = 0.0;
+  if (guard([&] { g = gamma_for_avg_row_nnz(n, target); }) != FSA_OK) return -1.0;
+  return g;
+}
+int fsa_simulate_rff(const double* coords, int64_t n, int d, int nu_code, double sigma1_2, double rho, double nugget,
+                     int features, uint64_t seed, double* y) {
+  return guard([&] { simulate_rff(coords, n, d, nu_code, sigma1_2, rho, nugget, features, seed, y); });
+}
+int fsa_blob_locations(int64_t n, int d, int blobs, double sd, uint64_t seed, double* out) {
+  return guard([&] { blob_locations(n, d, blobs, sd, seed, out); });
+}
+int fsa_probe_gaussian(uint64_t seed, uint64_t index, int64_t n1, double* e1, int64_t n2, double* e2) {
+  return guard([&] { probe_gaussian(seed, index, n1, e1, n2, e2); });
+}
+int fsa_probe_rademacher(uint64_t seed, uint64_t index, int64_t n, double* z) {
+  return guard([&] { probe_rademacher(seed, index, n, z); });
+}
+
+int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, double gamma, fsa_geometry** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(coords, "coords");
+    auto g = std::make_unique<fsa_geometry>();
+    g->ctx = ctx;
+    g->g = make_geometry(ctx->c.get(), coords, n, d, gamma);
+    *out = g.release();
+  });
+}
+void fsa_geometry_destroy(fsa_geometry* g) { delete g; }
+int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz) {
+  return guard([&] {
+    need(g, "geometry");
+    if (n) *n = g->g->pts.n;
+    if (nnz) *nnz = g->g->pat.nnz;
+  });
+}
+int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist) {
+  return guard([&] {
+    need(g, "geometry");
+    export_csr(g->g->pat, g->g->pat.dist.get(), g->g->pts, g->g->pts, g->ctx->c->stream, rowptr, col, dist);
+  });
+}
+int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm) {
+  return guard([&] {
+    need(g, "geometry");
+    std::copy(g->g->pts.perm.begin(), g->g->pts.perm.end(), perm);
+  });
+}
+
+int fsa_model_assemble(fsa_ctx* ctx, const double* coords, int64_t n, int d, const double* inducing, int64_t m,
+                       const fsa_params* params, fsa_model** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(coords, "coords");
+    need(inducing, "inducing");
+    const Params p = to_params(params);
+    require(p.gamma > 0.0, "taper range gamma must be positive");
+    auto geo = make_geometry(ctx->c.get(), coords, n, d, p.gamma);
+    auto md = std::make_unique<fsa_model>();
+    md->ctx = ctx;
+    md->m = Model::assemble(ctx->c.get(), geo, inducing, m, p);
+    *out = md.release();
+  });
+}
+int fsa_model_assemble_geo(fsa_geometry* g, const double* inducing, int64_t m, const fsa_params* params,
+                           fsa_model** out) {
+  return guard([&] {
+    need(g, "geometry");
+    need(inducing, "inducing");
+    auto md = std::make_unique<fsa_model>();
+    md->ctx = g->ctx;
+    md->m = Model::assemble(g->ctx->c.get(), g->g, inducing, m, to_params(params));
+    *out = md.release();
+  });
+}
+void fsa_model_destroy(fsa_model* md) { delete md; }
+int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t* n_clamped, double* ldsm) {
+  return guard([&] {
+    need(md, "model");
+    Model& M = *md->m;
+    if (n) *n = M.n;
+    if (m) *m = M.m;
+    if (nnz) *nnz = M.geo->pat.nnz;
+    if (n_clamped) *n_clamped = M.n_clamped;
+    if (ldsm) *ldsm = M.logdet_sigma_m;
+  });
+}
+int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, double* val) {
+  return guard([&] {
+    need(md, "model");
+    Model& M = *md->m;
+    require(which == 0 || which == 1, "which must be 0 (sigma_s) or 1 (d sigma_s / d rho)");
+    if (which == 1) M.ensure_rho_derivs();
+    export_csr(M.geo->pat, which == 0 ? M.sval.get() : M.dsval.get(), M.geo->pts, M.geo->pts, M.ctx->stream,
+               rowptr, col, val);
+  });
+}
+int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out) {
+  return guard([&] {
+    need(md, "model");
+    Model* M = md->m.get();
+    require(k >= 1, "matrix row mismatch");
+    const long tp = pad_cols(k);
+    DBuf<double> in = to_device_block(M, V, k, tp);
+    DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
+    M->matmat(in.get(), o.get(), tp);
+    to_host_block(M, o.get(), k, tp, out);
+  });
+}
+int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k, double* out) {
+  return guard([&] {
+    need(md, "model");
+    Model* M = md->m.get();
+    require(k >= 1, "matrix row mismatch");
+    const long tp = pad_cols(k);
+    DBuf<double> in = to_device_block(M, V, k, tp);
+    DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
+    M->deriv_matmat(which, in.get(), o.get(), tp);
+    to_host_block(M, o.get(), k, tp, out);
+  });
+}
+int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {
+  return guard([&] {
+    need(md, "model");
+    Model* M = md->m.get();
+    cudaStream_t s = M->ctx->stream;
+    DBuf<double> raw(static_cast<size_t>(M->n));
+    if (sdiag) {
+      unpack_cols(M->D.get(), M->n, 1, M->geo->pts.perm_d.get(), 1, 0, raw.get(), s);
+      FSA_CUDA(cudaMemcpyAsync(sdiag, raw.get(), sizeof(double) * M->n, cudaMemcpyDeviceToHost, s));
+      FSA_CUDA(cudaStreamSynchronize(s));
+    }
+    if (lowrank) {
+      unpack_cols(M->lowrank.get(), M->n, 1, M->geo->pts.perm_d.get(), 1, 0, raw.get(), s);
+      FSA_CUDA(cudaMemcpyAsync(lowrank, raw.get(), sizeof(double) * M->n, cudaMemcpyDeviceToHost, s));
+      FSA_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int fsa_make_preconditioner(fsa_model* md, int type, fsa_precond** out) {
+  return guard([&] {
+    need(md, "model");
+    auto p = std::make_unique<fsa_precond>();
+    p->md = md;
+    p->p = make_preconditioner(md->m.get(), type);
+    *out = p.release();
+  });
+}
+int fsa_make_jacobi(fsa_model* md, fsa_precond** out) {
+  return guard([&] {
+    need(md, "model");
+    auto p = std::make_unique<fsa_precond>();
+    p->md = md;
+    p->p = std::make_unique<DiagPrecond>(md->m.get(), false);
+    *out = p.release();
+  });
+}
+void fsa_precond_destroy(fsa_precond* p) { delete p; }
+int fsa_precond_logdet(fsa_precond* p, double* out) {
+  return guard([&] {
+    need(p, "preconditioner");
+    *out = p->p->logdet();
+  });
+}
+int fsa_precond_solve_mat(fsa_precond* p, const double* R, int64_t k, double* out) {
+  return guard([&] {
+    need(p, "preconditioner");
+    Model* M = p->md->m.get();
+    const long tp = pad_cols(k);
+    DBuf<double> in = to_device_block(M, R, k, tp);
+    DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
+    p->p->solve(in.get(), o.get(), tp);
+    to_host_block(M, o.get(), k, tp, out);
+  });
+}
+int fsa_precond_sample_probes(fsa_precond* p, int L, uint64_t seed, double* Z) {
+  return guard([&] {
+    need(p, "preconditioner");
+    require(L > 0, "need at least one probe");
+    Model* M = p->md->m.get();
+    const long tp = pad_cols(L);
+    DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
+    p->p->sample_probes(L, seed, o.get(), tp);
+    to_host_block(M, o.get(), L, tp, Z);
+  });
+}
+int fsa_precond_deriv_trace(fsa_precond* p, int which, double* out) {
+  return guard([&] {
+    need(p, "preconditioner");
+    require(which >= 0 && which < 3, "parameter index out of range");
+    require(p->p->kind() == 2, "deriv_trace is implemented for the FITC preconditioner");
+    *out = static_cast<FitcPrecond*>(p->p.get())->deriv_trace(which);
+  });
+}
+
+int fsa_pcg_solve_multi(fsa_model* md, fsa_precond* p, int op_kind, const double* B, int64_t k,
+                        const fsa_cg_options* cg, double* X, int* iterations, int* converged, double* tdiag,
+                        double* toff, int* sweeps) {
+  return guard([&] {
+    need(md, "model");
+    need(p, "preconditioner");
+    Model* M = md->m.get();
+    const CgOptions o = to_cg(cg);
+    const long tp = pad_cols(k);
+    DBuf<double> Bd = to_device_block(M, B, k, tp);
+    DBuf<double> Xd(static_cast<size_t>(M->n_pad * tp));
+    FsaOp fop(M);
+    SigmaSOp sop(M);
+    LinOp& op = op_kind == 0 ? static_cast<LinOp&>(fop) : static_cast<LinOp&>(sop);
+    CgResult r = pcg_solve_multi(M, op, *p->p, Bd.get(), k, tp, Xd.get(), o);
+    to_host_block(M, Xd.get(), k, tp, X);
+    for (long j = 0; j < k; ++j) {
+      if (iterations) iterations[j] = r.iterations[static_cast<size_t>(j)];
+      if (converged) converged[j] = r.converged[static_cast<size_t>(j)];
+      if (tdiag) std::copy(r.tdiag[static_cast<size_t>(j)].begin(), r.tdiag[static_cast<size_t>(j)].end(), tdiag + j * o.max_iter);
+      if (toff) std::copy(r.toff[static_cast<size_t>(j)].begin(), r.toff[static_cast<size_t>(j)].end(), toff + j * o.max_iter);
+    }
+    if (sweeps) *sweeps = r.sweeps;
+  });
+}
+int fsa_tridiag_log_quadrature(const double* diag, const double* off, int64_t len, double* out) {
+  return guard([&] {
+    std::vector<double> d(diag, diag + len), e;
+    if (len > 1) e.assign(off, off + len - 1);
+    *out = tridiag_log_quadrature(d, e);
+  });
+}
+int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const double* X, int64_t pcols, int L,
+                           uint64_t seed, const fsa_cg_options* cg, int cv_mode, int want_grad, fsa_nll_result* out,
+                           double* beta) {
+  return guard([&] {
+    need(md, "model");
+    need(p, "preconditioner");
+    need(y, "y");
+    need(out, "out");
+    require(pcols == 0 || X != nullptr, "nll: shape mismatch");
+    require(cv_mode >= 0 && cv_mode <= 2, "unknown control-variate mode");
+    NllResult r = iterative_nll_grad(md->m.get(), *p->p, y, X, pcols, L, seed, to_cg(cg), cv_mode, want_grad != 0);
+    out->nll = r.nll;
+    for (int k = 0; k < 3; ++k) out->grad[k] = r.grad[k];
+    out->logdet = r.logdet;
+    out->cg_iterations = r.cg_iterations;
+    out->sweeps = r.sweeps;
+    out->rhs_iterations = r.rhs_iterations;
+    out->pcg_ms = r.pcg_ms;
+    out->total_ms = r.total_ms;
+    for (long a = 0; a < pcols; ++a)
+      if (beta) beta[a] = r.beta[static_cast<size_t>(a)];
+  });
+}
+
+int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** out) {
+  return guard([&] {
+    need(md, "model");
+    need(pcoords, "pcoords");
+    auto pr = std::make_unique<fsa_pred>();
+    pr->md = md;
+    pr->p = make_prediction_set(md->m.get(), pcoords, np);
+    *out = pr.release();
+  });
+}
+void fsa_pred_destroy(fsa_pred* pr) { delete pr; }
+int fsa_pred_info(fsa_pred* pr, int64_t* np, int64_t* nnz) {
+  return guard([&] {
+    need(pr, "prediction set");
+    if (np) *np = pr->p->np;
+    if (nnz) *nnz = pr->p->rows.nnz;
+  });
+}
+int fsa_cross_apply_t(fsa_pred* pr, const double* u, double* out) {
+  return guard([&] {
+    need(pr, "prediction set");
+    cross_apply_t(*pr->p, u, out);
+  });
+}
+int fsa_predict_mean_iterative(fsa_pred* pr, const double* resid, fsa_precond* p, const fsa_cg_options* cg,
+                               double* mean_out) {
+  return guard([&] {
+    need(pr, "prediction set");
+    need(p, "preconditioner");
+    predict_mean_iterative(*pr->p, resid, *p->p, to_cg(cg), mean_out);
+  });
+}
+int fsa_predict_var_sim(fsa_pred* pr, int num_probes, uint64_t seed, const fsa_cg_options* cg,
+                        const fsa_cg_options* cg_s, int control_variate, double floor_rel, double* var, double* se,
+                        fsa_predvar_info* info) {
+  return guard([&] {
+    need(pr, "prediction set");
+    PredVarInfo pi = predict_var_sim(*pr->p, num_probes, seed, to_cg(cg), to_cg(cg_s), control_variate != 0,
+                                     floor_rel, var, se);
+    if (info) {
+      info->clamped = pi.clamped;
+      info->cg_iterations = pi.cg_iterations;
+      info->det_ms = pi.det_ms;
+      info->sim_ms = pi.sim_ms;
+    }
+  });
+}
+int fsa_pred_det_pieces(fsa_pred* pr, const fsa_cg_options* cg, const fsa_cg_options* cg_s, double* d1, double* d2,
+                        double* d3, int* cg_iterations) {
+  return guard([&] {
+    need(pr, "prediction set");
+    int it = 0;
+    deterministic_pieces_host(*pr->p, to_cg(cg), to_cg(cg_s), d1, d2, d3, &it);
+    if (cg_iterations) *cg_iterations = it;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Shared helpers for the B200 (sm_100a) FSA iterative core.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace fsa {
+
+// ---- errors: mirror fsagp::NumericalError / std::invalid_argument (types.h:22-29)
+struct NumericalError : std::runtime_error {
+  explicit NumericalError(const std::string& w) : std::runtime_error(w) {}
+};
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+inline void require(bool c, const char* msg) {
+  if (!c) throw std::invalid_argument(msg);
+}
+
+#define FSA_CUDA(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::fsa::CudaError(std::string("CUDA error ") + cudaGetErrorString(e_) + " at " + \
+                             __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+
+#define FSA_LAUNCH_CHECK() FSA_CUDA(cudaGetLastError())
+
+inline long round_up(long x, long a) { return (x + a - 1) / a * a; }
+inline long cdiv(long x, long a) { return (x + a - 1) / a; }
+
+// column padding of an n x t right-hand-side block (row-major, ld = tpad)
+inline long pad_cols(long t) { return t <= 72 ? round_up(t < 1 ? 1 : t, 8) : round_up(t, 64); }
+
+constexpr int kNumSMs = 148;
+
+// ---- device buffers ------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    n = count;
+    if (count) FSA_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void zero(cudaStream_t s) {
+    if (n) FSA_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+}  // namespace fsa

@@ -1,0 +1,138 @@
+// Launchers for the DMMA fp64 GEMMs declared in dgemm.cuh.
+#include "dgemm.cuh"
+
+namespace fsa {
+
+namespace {
+
+// expand: 4 warps x 32 rows (BM = 128), all N columns of the tile per warp.
+template <int NT>
+using ExpandCfg = GemmCfg<NT, 4, 4, false, 16, 3>;
+// reduce: 4 warps x 16 rows (BM = 64), A is [k][m].
+template <int NT>
+using ReduceCfg = GemmCfg<NT, 2, 4, true, 16, 3>;
+
+template <class Cfg, class Epi>
+void launch(const double* A, long lda, const double* B, long ldb, const double* scale, long K, long kchunk,
+            dim3 grid, Epi epi, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    FSA_CUDA(cudaFuncSetAttribute(k_dgemm<Cfg, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  k_dgemm<Cfg, Epi><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(A, lda, B, ldb, scale, K, kchunk, epi);
+  FSA_LAUNCH_CHECK();
+}
+
+// N (padded RHS width) -> number of 8-column DMMA tiles handled by one CTA
+inline int tile_nt(long N) { return N <= 72 ? static_cast<int>(N / 8) : 8; }
+
+template <template <int> class CfgT, class Epi>
+void dispatch_nt(int nt, const double* A, long lda, const double* B, long ldb, const double* scale, long K,
+                 long kchunk, dim3 grid, Epi epi, cudaStream_t s) {
+  switch (nt) {
+    case 1: launch<CfgT<1>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 2: launch<CfgT<2>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 3: launch<CfgT<3>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 4: launch<CfgT<4>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 5: launch<CfgT<5>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 6: launch<CfgT<6>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 7: launch<CfgT<7>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 8: launch<CfgT<8>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    case 9: launch<CfgT<9>>(A, lda, B, ldb, scale, K, kchunk, grid, epi, s); break;
+    default: throw std::invalid_argument("gemm: unsupported column tile");
+  }
+}
+
+template <class Epi>
+void expand(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N, Epi epi,
+            cudaStream_t s) {
+  require(rows % 128 == 0 && K % 16 == 0 && N == pad_cols(N), "gemm_expand: unpadded shape");
+  if (rows == 0) return;
+  const int nt = tile_nt(N);
+  dim3 grid(static_cast<unsigned>(rows / 128), static_cast<unsigned>(N / (nt * 8)), 1);
+  dispatch_nt<ExpandCfg>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
+}
+
+struct ReducePlan {
+  int nt;
+  long tiles, splits, kchunk;
+};
+ReducePlan plan_reduce(long Mr, long N, long K) {
+  ReducePlan p;
+  p.nt = tile_nt(N);
+  p.tiles = (Mr / 64) * (N / (p.nt * 8));
+  const long kblocks = K / 16;
+  long splits = cdiv(2 * kNumSMs, p.tiles);
+  splits = splits < 1 ? 1 : splits;
+  splits = splits > kblocks ? kblocks : splits;
+  splits = splits < 1 ? 1 : splits;
+  p.kchunk = round_up(cdiv(K, splits), 16);
+  p.splits = cdiv(K, p.kchunk);
+  if (p.splits < 1) p.splits = 1;
+  return p;
+}
+
+__global__ void k_splitk_reduce(const double* __restrict__ W, long splits, long Mr, long N, double* out, long ldo,
+                                double alpha, double beta) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= Mr * N) return;
+  const long r = idx / N, c = idx % N;
+  double acc = 0.0;
+  for (long z = 0; z < splits; ++z) acc += W[(z * Mr + r) * N + c];
+  double* o = out + r * ldo + c;
+  *o = beta == 0.0 ? alpha * acc : alpha * acc + beta * *o;
+}
+
+}  // namespace
+
+void gemm_expand_store(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                       double* Y, long ldy, double alpha, double beta, cudaStream_t s) {
+  if (beta == 0.0)
+    expand(M, ldm, rows, K, W, ldw, N, EpiStore{Y, ldy, alpha}, s);
+  else
+    expand(M, ldm, rows, K, W, ldw, N, EpiAxpby{Y, ldy, alpha, beta}, s);
+}
+void gemm_expand_probe(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                       double* Y, long ld, const double* sqrtD, const double* E2, cudaStream_t s) {
+  expand(M, ldm, rows, K, W, ldw, N, EpiProbe{Y, ld, sqrtD, E2}, s);
+}
+void gemm_expand_woodbury(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                          double* Z, const double* R, long ld, const double* Dinv, cudaStream_t s) {
+  expand(M, ldm, rows, K, W, ldw, N, EpiWoodbury{Z, R, ld, Dinv}, s);
+}
+
+void gemm_km(const double* A, long lda, long Mr, long K, const double* B, long ldb, long N, double* Y, long ldy,
+             double alpha, double beta, cudaStream_t s) {
+  require(Mr % 64 == 0 && K % 16 == 0 && N == pad_cols(N), "gemm_km: unpadded shape");
+  if (Mr == 0 || N == 0) return;
+  const int nt = tile_nt(N);
+  dim3 grid(static_cast<unsigned>(Mr / 64), static_cast<unsigned>(N / (nt * 8)), 1);
+  if (beta == 0.0)
+    dispatch_nt<ReduceCfg>(nt, A, lda, B, ldb, nullptr, K, K, grid, EpiStore{Y, ldy, alpha}, s);
+  else
+    dispatch_nt<ReduceCfg>(nt, A, lda, B, ldb, nullptr, K, K, grid, EpiAxpby{Y, ldy, alpha, beta}, s);
+}
+
+size_t gemm_reduce_scratch(long Mr, long N, long K) {
+  const ReducePlan p = plan_reduce(Mr, N, K);
+  return static_cast<size_t>(p.splits * Mr * N);
+}
+
+void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, long ldv, long N,
+                 const double* scale, double* out, long ldo, double alpha, double beta, double* scratch,
+                 cudaStream_t s) {
+  require(Mr % 64 == 0 && K % 16 == 0 && N == pad_cols(N), "gemm_reduce: unpadded shape");
+  if (Mr == 0 || N == 0) return;
+  const ReducePlan p = plan_reduce(Mr, N, K);
+  dim3 grid(static_cast<unsigned>(Mr / 64), static_cast<unsigned>(N / (p.nt * 8)),
+            static_cast<unsigned>(p.splits));
+  dispatch_nt<ReduceCfg>(p.nt, M, ldm, V, ldv, scale, K, p.kchunk, grid, EpiPartial{scratch, Mr, N}, s);
+  const long total = Mr * N;
+  k_splitk_reduce<<<static_cast<unsigned>(cdiv(total, 256)), 256, 0, s>>>(scratch, p.splits, Mr, N, out, ldo,
+                                                                         alpha, beta);
+  FSA_LAUNCH_CHECK();
+}
+
+}  // namespace fsa

@@ -1,0 +1,901 @@
+// Host orchestration of the FSA iterative core on one B200; see fsa_core.cuh.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+
+#include "blas1.cuh"
+#include "dgemm.cuh"
+#include "fsa_core.cuh"
+#include "kernels.cuh"
+#include "sparse.cuh"
+
+namespace fsa {
+
+// ---- RNG (types.h:104-129; identical libstdc++ distributions) ------------------------------
+unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+static std::mt19937_64 probe_rng(unsigned long long seed, unsigned long long i) {
+  return std::mt19937_64(splitmix64(splitmix64(seed) ^ splitmix64(i + 0x51ed2701ULL)));
+}
+void probe_gaussian(unsigned long long seed, unsigned long long i, long n1, double* e1, long n2, double* e2) {
+  std::mt19937_64 rng = probe_rng(seed, i);
+  {
+    std::normal_distribution<double> N01(0.0, 1.0);  // fresh object per vector
+    for (long j = 0; j < n1; ++j) e1[j] = N01(rng);
+  }
+  {
+    std::normal_distribution<double> N01(0.0, 1.0);
+    for (long j = 0; j < n2; ++j) e2[j] = N01(rng);
+  }
+}
+void probe_rademacher(unsigned long long seed, unsigned long long i, long n, double* z) {
+  std::mt19937_64 rng = probe_rng(seed, i);
+  std::bernoulli_distribution coin(0.5);
+  for (long j = 0; j < n; ++j) z[j] = coin(rng) ? 1.0 : -1.0;
+}
+
+// ---- context ------------------------------------------------------------------------------
+Context::Context(int dev) : device(dev) {
+  FSA_CUDA(cudaSetDevice(dev));
+  FSA_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  FSA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags), 4 * sizeof(int), cudaHostAllocMapped));
+  FSA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_flags_dev), host_flags, 0));
+}
+Context::~Context() {
+  cudaStreamSynchronize(stream);
+  for (auto& r : pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : pool) cudaEventDestroy(e);
+  if (host_flags) cudaFreeHost(host_flags);
+  if (stream) cudaStreamDestroy(stream);
+}
+cudaEvent_t Context::ev() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FSA_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void Context::flush_timers() {
+  FSA_CUDA(cudaStreamSynchronize(stream));
+  for (auto& r : pending) {
+    float ms = 0.f;
+    FSA_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    Acc& a = totals[r.name];
+    a.ms += ms;
+    a.count += 1;
+    a.units += r.units;
+    pool.push_back(r.a);
+    pool.push_back(r.b);
+  }
+  pending.clear();
+}
+void Context::sync() { FSA_CUDA(cudaStreamSynchronize(stream)); }
+
+KTimer::KTimer(Context* ctx, const char* name, double units) : c(ctx) {
+  if (!c->profile) return;
+  Context::Rec r{name, c->ev(), c->ev(), units};
+  FSA_CUDA(cudaEventRecord(r.a, c->stream));
+  c->pending.push_back(r);
+  idx = c->pending.size() - 1;
+}
+KTimer::~KTimer() {
+  if (idx == static_cast<size_t>(-1)) return;
+  cudaEventRecord(c->pending[idx].b, c->stream);
+}
+
+// ---- geometry --------------------------------------------------------------------------------
+std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long n, int d, double gamma) {
+  require(n > 0, "empty location set");
+  require(gamma > 0.0, "taper range gamma must be positive");
+  require(d >= 1 && d <= 3, "dimension must be 1, 2 or 3");
+  auto g = std::make_shared<Geometry>();
+  g->gamma = gamma;
+  g->coords_host.assign(coords, coords + n * d);
+  const CellGrid grid = make_grid(coords, n, d, gamma, nullptr, 0);
+  sort_points(coords, n, d, grid, round_up(n, 128), g->pts, ctx->stream);
+  build_pattern(g->pts, g->pts, gamma, true, g->pat, ctx->stream);
+  ctx->sync();
+  return g;
+}
+
+// ---- model --------------------------------------------------------------------------------------
+static void validate(const Params& p) {  // types.h:80-84, fsa.cpp:9-13
+  require(p.sigma2 > 0.0 && std::isfinite(p.sigma2), "sigma2 must be positive and finite");
+  require(p.sigma1_2 > 0.0 && std::isfinite(p.sigma1_2), "sigma1_2 must be positive and finite");
+  require(p.rho > 0.0 && std::isfinite(p.rho), "rho must be positive and finite");
+  require(p.gamma > 0.0, "taper range gamma must be positive");
+  require(p.nu >= 0 && p.nu <= 2, "Matern smoothness must be one of 0.5, 1.5, 2.5");
+  require(p.family == 1 || p.family == 2, "taper family must be wendland1 or wendland2");
+}
+
+double* Model::mt_buf(int which, long tp) {
+  DBuf<double>& b = which == 0 ? mt1 : mt2;
+  const size_t need = static_cast<size_t>(m_pad * tp);
+  if (b.n < need) b.alloc(need);
+  return b.get();
+}
+
+void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
+  const size_t need = gemm_reduce_scratch(m_pad, tp, n_pad);
+  if (red_scratch.n < need) red_scratch.alloc(need);
+  KTimer t(ctx, "lowrank_project", 2.0 * m_pad * n_pad * tp);
+  gemm_reduce(M, m_pad, m_pad, n_pad, V, tp, tp, scale, out, tp, 1.0, 0.0, red_scratch.get(), ctx->stream);
+}
+
+std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> geo, const double* inducing, long m,
+                                       const Params& p) {
+  validate(p);
+  require(geo != nullptr, "geometry missing");
+  require(m > 0, "empty inducing set");
+  require(std::fabs(geo->gamma - p.gamma) == 0.0, "geometry built for another taper range");
+  auto md = std::make_unique<Model>();
+  Model& M = *md;
+  cudaStream_t s = ctx->stream;
+  M.ctx = ctx;
+  M.geo = geo;
+  M.P = p;
+  M.n = geo->pts.n;
+  M.n_pad = geo->pts.n_pad;
+  M.d = geo->pts.d;
+  M.m = m;
+  M.m_pad = round_up(m, 128);
+  require(M.m_pad <= 1024, "more than 1024 inducing points are not supported");
+  const long mp = M.m_pad, np = M.n_pad;
+  M.ind_host.assign(inducing, inducing + m * M.d);
+  M.ind.alloc(m * M.d);
+  FSA_CUDA(cudaMemcpyAsync(M.ind.get(), inducing, sizeof(double) * m * M.d, cudaMemcpyHostToDevice, s));
+  M.info.alloc(4);
+  M.dinv_scratch.alloc(mp * 64);
+  M.dot_scratch.alloc(coldot_scratch(np, 128));
+  DBuf<double> scal(4);
+
+  // Sigma_m + jitter, Cholesky (fsa.cpp:23-30)
+  M.Sm.alloc(mp * mp);
+  M.L.alloc(mp * mp);
+  {
+    KTimer t(ctx, "setup_sigma_m");
+    launch_sigma_m(M.ind.get(), m, m, mp, M.d, p.nu, p.sigma1_2, p.rho, p.jitter_rel * p.sigma1_2, 0, M.Sm.get(), s);
+    FSA_CUDA(cudaMemcpyAsync(M.L.get(), M.Sm.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s));
+    potrf_lower(M.L.get(), mp, M.info.get(), M.dinv_scratch.get(), s);
+    launch_logdet_diag(M.L.get(), mp, m, scal.get(), s);
+  }
+  // U = L^{-1} Sigma_mn (fsa.cpp:32-35)
+  M.U.alloc(mp * np);
+  M.lowrank.alloc(np);
+  {
+    KTimer t(ctx, "setup_cross_cov");
+    launch_cross_cov(M.ind.get(), m, m, geo->pts.coords.get(), np, M.n, np, M.d, p.nu, p.sigma1_2, p.rho, 0,
+                     M.U.get(), mp, s);
+  }
+  {
+    KTimer t(ctx, "setup_trsm", 1.0 * mp * mp * np);
+    trsm_lower_cols(M.L.get(), mp, M.U.get(), mp, np, M.dinv_scratch.get(), s);
+  }
+  colnorm2(M.U.get(), mp, mp, M.n, np, M.lowrank.get(), s);
+  // Sigma_s on the taper pattern (fsa.cpp:37-56)
+  const Csr& pat = geo->pat;
+  M.sval.alloc(pat.nnz > 0 ? pat.nnz : 1);
+  SddmmParams sp{p.nu, p.family, p.sigma2, p.sigma1_2, p.rho, p.gamma};
+  {
+    KTimer t(ctx, "setup_sddmm", 2.0 * mp * pat.nnz);
+    sddmm_sigma_s(M.U.get(), mp, pat, M.lowrank.get(), sp, M.sval.get(), M.info.get() + 1, s);
+  }
+  M.D.alloc(np);
+  M.Dinv.alloc(np);
+  M.sqrtD.alloc(np);
+  extract_diag(M.sval.get(), pat.diagpos.get(), M.n, np, M.D.get(), M.Dinv.get(), M.sqrtD.get(), s);
+  int hinfo[2] = {0, 0};
+  double hld = 0.0;
+  FSA_CUDA(cudaMemcpyAsync(hinfo, M.info.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpyAsync(&hld, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  if (hinfo[0] != 0) throw NumericalError("inducing covariance is not positive definite");
+  M.logdet_sigma_m = hld;
+  M.n_clamped = hinfo[1];
+  return md;
+}
+
+void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
+  if (have_rho) return;
+  cudaStream_t s = ctx->stream;
+  const long mp = m_pad, np = n_pad;
+  KTimer t(ctx, "setup_rho_derivs");
+  // K2 = L^{-1} dSigma_m/drho L^{-T}
+  K2.alloc(mp * mp);
+  DBuf<double> tmp(mp * mp);
+  launch_sigma_m(ind.get(), m, m, mp, d, P.nu, P.sigma1_2, P.rho, 0.0, 1, tmp.get(), s);
+  trsm_lower_cols(L.get(), mp, tmp.get(), mp, mp, dinv_scratch.get(), s);  // X = L^{-1} dSm
+  launch_transpose(tmp.get(), mp, mp, mp, K2.get(), mp, s);
+  trsm_lower_cols(L.get(), mp, K2.get(), mp, mp, dinv_scratch.get(), s);   // L^{-1} X^T
+  // U1 = L^{-1} dSigma_mn/drho ; T = U1 - K2 U
+  U1.alloc(mp * np);
+  T.alloc(mp * np);
+  launch_cross_cov(ind.get(), m, m, geo->pts.coords.get(), np, n, np, d, P.nu, P.sigma1_2, P.rho, 1, U1.get(), mp, s);
+  trsm_lower_cols(L.get(), mp, U1.get(), mp, np, dinv_scratch.get(), s);
+  FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+  gemm_expand_store(U.get(), mp, np, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+  const Csr& pat = geo->pat;
+  dsval.alloc(pat.nnz > 0 ? pat.nnz : 1);
+  SddmmParams sp{P.nu, P.family, P.sigma2, P.sigma1_2, P.rho, P.gamma};
+  sddmm_drho(U.get(), U1.get(), T.get(), mp, pat, lowrank.get(), sp, dsval.get(), s);
+  dD.alloc(np);
+  extract_diag(dsval.get(), pat.diagpos.get(), n, np, dD.get(), nullptr, nullptr, s);
+  // padding rows of dD must be zero (extract_diag writes 1)
+  affine_vec(dD.get(), dD.get(), 0.0, 1.0, n, np, s);
+  have_rho = true;
+}
+
+void Model::sigma_s_mat(const double* H, double* V, long tp, double alpha, double beta) {
+  KTimer t(ctx, "spmm", 8.0 * (12.0 * geo->pat.nnz + 2.0 * n * tp));
+  launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta, ctx->stream);
+}
+
+// V = Sigma H = U^T (U H) + Sigma_s H   (fsa.cpp:65-68)
+void Model::matmat(const double* H, double* V, long tp) {
+  double* W1 = mt_buf(0, tp);
+  project(U.get(), H, tp, W1);
+  {
+    KTimer t(ctx, "lowrank_expand", 2.0 * m_pad * n_pad * tp);
+    gemm_expand_store(U.get(), m_pad, n_pad, m_pad, W1, tp, tp, V, tp, 1.0, 0.0, ctx->stream);
+  }
+  sigma_s_mat(H, V, tp, 1.0, 1.0);
+}
+
+// deriv_matmat (fsa.cpp:165-182) in U-form
+void Model::deriv_matmat(int which, const double* V, double* out, long tp) {
+  require(which >= 0 && which < 3, "parameter index out of range");
+  cudaStream_t s = ctx->stream;
+  const long len = n_pad * tp;
+  if (which == 0) {
+    FSA_CUDA(cudaMemcpyAsync(out, V, sizeof(double) * len, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (which == 1) {  // (Sigma V - sigma2 V) / sigma1_2
+    matmat(V, out, tp);
+    axpby(out, V, -P.sigma2 / P.sigma1_2, 1.0 / P.sigma1_2, len, s);
+    return;
+  }
+  ensure_rho_derivs();
+  double* UV = mt_buf(0, tp);
+  double* W = mt_buf(1, tp);
+  project(U.get(), V, tp, UV);
+  project(U1.get(), V, tp, W);  // W = U1 V
+  gemm_km(K2.get(), m_pad, m_pad, m_pad, UV, tp, tp, W, tp, -1.0, 1.0, s);  // W = U1 V - K2 U V
+  gemm_expand_store(U.get(), m_pad, n_pad, m_pad, W, tp, tp, out, tp, 1.0, 0.0, s);
+  gemm_expand_store(U1.get(), m_pad, n_pad, m_pad, UV, tp, tp, out, tp, 1.0, 1.0, s);
+  launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), dsval.get(), n, V, tp, out, tp, tp, 1.0, 1.0, s);
+}
+
+// ---- preconditioners ------------------------------------------------------------------------------
+struct PinnedBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    FSA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(double)));
+    n = count;
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// upload a host column-major (original order) n x k block into columns [0, k) of Z
+static void upload_pack(Model* md, const double* host, long k, double* Z, long tp) {
+  cudaStream_t s = md->ctx->stream;
+  DBuf<double> raw(static_cast<size_t>(md->n * k));
+  FSA_CUDA(cudaMemcpyAsync(raw.get(), host, sizeof(double) * md->n * k, cudaMemcpyHostToDevice, s));
+  pack_cols(raw.get(), md->n, k, md->geo->pts.perm_d.get(), md->n_pad, tp, 0, Z, s);
+  FSA_CUDA(cudaStreamSynchronize(s));
+}
+
+void IdentityPrecond::solve(const double* R, double* Z, long tp) {
+  FSA_CUDA(cudaMemcpyAsync(Z, R, sizeof(double) * md->n_pad * tp, cudaMemcpyDeviceToDevice, md->ctx->stream));
+}
+void IdentityPrecond::sample_probes(int L, unsigned long long seed, double* Z, long tp) {
+  std::vector<double> h(static_cast<size_t>(md->n * L));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int i = 0; i < L; ++i) probe_rademacher(seed, static_cast<unsigned long long>(i), md->n, h.data() + i * md->n);
+  FSA_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * md->n_pad * tp, md->ctx->stream));
+  upload_pack(md, h.data(), L, Z, tp);
+}
+
+DiagPrecond::DiagPrecond(Model* m, bool d) : md(m), derivs(d) {
+  DBuf<double> out(1);
+  sum_log(md->D.get(), md->n, out.get(), md->ctx->stream);
+  FSA_CUDA(cudaMemcpyAsync(&ld, out.get(), sizeof(double), cudaMemcpyDeviceToHost, md->ctx->stream));
+  md->ctx->sync();
+  if (derivs) md->ensure_rho_derivs();
+}
+void DiagPrecond::solve(const double* R, double* Z, long tp) {
+  scale_rows(Z, R, md->Dinv.get(), md->n_pad, tp, md->ctx->stream);
+}
+void DiagPrecond::sample_probes(int L, unsigned long long seed, double* Z, long tp) {
+  std::vector<double> h(static_cast<size_t>(md->n * L));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int i = 0; i < L; ++i) {
+    std::vector<double> dummy;
+    probe_gaussian(seed, static_cast<unsigned long long>(i), 0, dummy.data(), md->n, h.data() + i * md->n);
+  }
+  FSA_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * md->n_pad * tp, md->ctx->stream));
+  upload_pack(md, h.data(), L, Z, tp);
+  scale_rows(Z, Z, md->sqrtD.get(), md->n_pad, tp, md->ctx->stream);
+}
+
+FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs) {
+  cudaStream_t s = md->ctx->stream;
+  const long mp = md->m_pad, np = md->n_pad;
+  KTimer t(md->ctx, "setup_fitc", 2.0 * mp * mp * np);
+  Q.alloc(mp * mp);
+  LQ.alloc(mp * mp);
+  Qinv.alloc(mp * mp);
+  // Q = I + U D^{-1} U^T  (= L^{-1} core L^{-T}, preconditioners.cpp:49)
+  {
+    const size_t need = gemm_reduce_scratch(mp, mp, np);
+    if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+    gemm_reduce(md->U.get(), mp, mp, np, md->U.get(), mp, mp, md->Dinv.get(), Q.get(), mp, 1.0, 0.0,
+                md->red_scratch.get(), s);
+  }
+  add_identity(Q.get(), mp, mp, s);
+  FSA_CUDA(cudaMemcpyAsync(LQ.get(), Q.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s));
+  potrf_lower(LQ.get(), mp, md->info.get(), md->dinv_scratch.get(), s);
+  DBuf<double> scal(2);
+  launch_logdet_diag(LQ.get(), mp, mp, scal.get(), s);
+  sum_log(md->D.get(), md->n, scal.get() + 1, s);
+  // Qinv = LQ^{-T} LQ^{-1}
+  {
+    DBuf<double> X(mp * mp), Xt(mp * mp);
+    FSA_CUDA(cudaMemsetAsync(X.get(), 0, sizeof(double) * mp * mp, s));
+    add_identity(X.get(), mp, mp, s);
+    trsm_lower_cols(LQ.get(), mp, X.get(), mp, mp, md->dinv_scratch.get(), s);  // X[j][r] = LQinv(r, j)
+    launch_transpose(X.get(), mp, mp, mp, Xt.get(), mp, s);                       // Xt[k][r] = LQinv(k, r)
+    const size_t need = gemm_reduce_scratch(mp, mp, mp);
+    if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+    gemm_reduce(Xt.get(), mp, mp, mp, Xt.get(), mp, mp, nullptr, Qinv.get(), mp, 1.0, 0.0, md->red_scratch.get(), s);
+    int hinfo = 0;
+    double hs[2];
+    FSA_CUDA(cudaMemcpyAsync(&hinfo, md->info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hs, scal.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    if (hinfo != 0) throw NumericalError("preconditioner core matrix is not positive definite");
+    logdetQ = hs[0];
+    ld = hs[0] + hs[1];  // logdet(core) - logdet(Sigma_m) + sum log d   (preconditioners.cpp:53-55)
+  }
+  if (derivs) md->ensure_rho_derivs();
+}
+
+// P^{-1} R = D^{-1} R - D^{-1} U^T Q^{-1} U D^{-1} R   (preconditioners.cpp:58-67)
+void FitcPrecond::solve(const double* R, double* Z, long tp) {
+  cudaStream_t s = md->ctx->stream;
+  double* S = md->mt_buf(0, tp);
+  double* W = md->mt_buf(1, tp);
+  md->project(md->U.get(), R, tp, S, md->Dinv.get());
+  {
+    KTimer t(md->ctx, "core_solve", 2.0 * md->m_pad * md->m_pad * tp);
+    gemm_km(Qinv.get(), md->m_pad, md->m_pad, md->m_pad, S, tp, tp, W, tp, 1.0, 0.0, s);
+  }
+  KTimer t(md->ctx, "lowrank_expand", 2.0 * md->m_pad * md->n_pad * tp);
+  gemm_expand_woodbury(md->U.get(), md->m_pad, md->n_pad, md->m_pad, W, tp, tp, Z, R, tp, md->Dinv.get(), s);
+}
+
+// z = Sigma_mn^T L^{-T} e1 + sqrt(D) e2 = U^T e1 + sqrt(D) e2  (preconditioners.cpp:69-73)
+void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long tp) {
+  const long m = md->m, n = md->n, mp = md->m_pad, np = md->n_pad;
+  cudaStream_t s = md->ctx->stream;
+  static thread_local PinnedBuf e1h, e2h;
+  e1h.ensure(static_cast<size_t>(mp * tp));
+  e2h.ensure(static_cast<size_t>(n * L));
+  std::memset(e1h.p, 0, sizeof(double) * mp * tp);
+  std::vector<double> e1col(static_cast<size_t>(m) * L);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int i = 0; i < L; ++i)
+    probe_gaussian(seed, static_cast<unsigned long long>(i), m, e1col.data() + static_cast<long>(i) * m, n,
+                   e2h.p + static_cast<long>(i) * n);
+  for (int i = 0; i < L; ++i)
+    for (long r = 0; r < m; ++r) e1h.p[r * tp + i] = e1col[static_cast<size_t>(i) * m + r];
+  DBuf<double> E1(mp * tp), E2(np * tp), raw(n * L);
+  FSA_CUDA(cudaMemcpyAsync(E1.get(), e1h.p, sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
+  FSA_CUDA(cudaMemcpyAsync(raw.get(), e2h.p, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
+  FSA_CUDA(cudaMemsetAsync(E2.get(), 0, sizeof(double) * np * tp, s));
+  pack_cols(raw.get(), n, L, md->geo->pts.perm_d.get(), np, tp, 0, E2.get(), s);
+  {
+    KTimer t(md->ctx, "probe_expand", 2.0 * mp * np * tp);
+    gemm_expand_probe(md->U.get(), mp, np, mp, E1.get(), tp, tp, Z, tp, md->sqrtD.get(), E2.get(), s);
+  }
+  FSA_CUDA(cudaStreamSynchronize(s));
+}
+
+// exact Tr(P^{-1} dP_k) in U-form:
+//   k = 0: sum_i pinv_i
+//   k = 1: pinv . d_1 + (m - Tr Q^{-1}) / sigma1_2
+//   k = 2: pinv . dD + 2 <Q^{-1}, F> - Tr(K2) + <K2, Q^{-1}>,  F = U D^{-1} U1^T
+double FitcPrecond::deriv_trace(int k) {
+  require(derivs, "FITC preconditioner built without derivatives");
+  if (!have_traces) {
+    cudaStream_t s = md->ctx->stream;
+    const long mp = md->m_pad, np = md->n_pad, n = md->n;
+    md->ensure_rho_derivs();
+    DBuf<double> V(mp * np), q(np), pinv(np), d1(np), F(mp * mp);
+    FSA_CUDA(cudaMemcpyAsync(V.get(), md->U.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+    trsm_lower_cols(LQ.get(), mp, V.get(), mp, np, md->dinv_scratch.get(), s);
+    colnorm2(V.get(), mp, mp, n, np, q.get(), s);
+    pinv_diag(pinv.get(), md->D.get(), q.get(), n, np, s);
+    affine_vec(d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, s);
+    // sum pinv (k = 0), pinv . d1, pinv . dD
+    std::vector<double> hp(static_cast<size_t>(np)), hd1(static_cast<size_t>(np)), hdD(static_cast<size_t>(np));
+    FSA_CUDA(cudaMemcpyAsync(hp.data(), pinv.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hd1.data(), d1.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hdD.data(), md->dD.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+    const size_t need = gemm_reduce_scratch(mp, mp, np);
+    if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+    gemm_reduce(md->U.get(), mp, mp, np, md->U1.get(), mp, mp, md->Dinv.get(), F.get(), mp, 1.0, 0.0,
+                md->red_scratch.get(), s);
+    std::vector<double> hQi(static_cast<size_t>(mp * mp)), hF(hQi.size()), hK2(hQi.size());
+    FSA_CUDA(cudaMemcpyAsync(hQi.data(), Qinv.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hF.data(), F.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hK2.data(), md->K2.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (long i = 0; i < n; ++i) {
+      s0 += hp[static_cast<size_t>(i)];
+      s1 += hp[static_cast<size_t>(i)] * hd1[static_cast<size_t>(i)];
+      s2 += hp[static_cast<size_t>(i)] * hdD[static_cast<size_t>(i)];
+    }
+    double trQi = 0, qf = 0, trK2 = 0, k2q = 0;
+    for (long r = 0; r < mp; ++r) {
+      trQi += hQi[static_cast<size_t>(r * mp + r)];
+      trK2 += hK2[static_cast<size_t>(r * mp + r)];
+    }
+    for (size_t idx = 0; idx < hQi.size(); ++idx) {
+      qf += hQi[idx] * hF[idx];
+      k2q += hK2[idx] * hQi[idx];
+    }
+    trace[0] = s0;
+    trace[1] = s1 + (static_cast<double>(mp) - trQi) / md->P.sigma1_2;
+    trace[2] = s2 + 2.0 * qf - (trK2 - k2q);
+    have_traces = true;
+  }
+  return trace[k];
+}
+
+std::unique_ptr<Precond> make_preconditioner(Model* md, int type) {  // estimation.cpp:160-176
+  switch (type) {
+    case 0: return std::make_unique<IdentityPrecond>(md);
+    case 1: return std::make_unique<DiagPrecond>(md, true);
+    case 2: return std::make_unique<FitcPrecond>(md, true);
+  }
+  throw std::invalid_argument("unknown preconditioner type");
+}
+
+// ---- Krylov -------------------------------------------------------------------------------------------
+bool CgResult::all_converged() const {
+  for (int c : converged)
+    if (!c) return false;
+  return true;
+}
+int CgResult::max_iterations() const {
+  int m = 0;
+  for (int v : iterations) m = std::max(m, v);
+  return m;
+}
+
+namespace {
+struct CgWork {
+  DBuf<double> R, H, V, Z, dots, dbl;
+  DBuf<int> ints;
+  DBuf<double> tri;
+};
+}  // namespace
+
+CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long k, long tp, double* X,
+                         const CgOptions& opts) {
+  require(opts.tol > 0.0 && opts.max_iter > 0, "cg: invalid options");
+  require(k >= 1 && k <= tp, "cg: column count mismatch");
+  Context* ctx = md->ctx;
+  cudaStream_t s = ctx->stream;
+  const long np = md->n_pad, n = md->n;
+  const int maxit = opts.max_iter;
+  const size_t blk = static_cast<size_t>(np * tp);
+  static thread_local CgWork w;
+  if (w.R.n < blk) {
+    w.R.alloc(blk);
+    w.H.alloc(blk);
+    w.V.alloc(blk);
+    w.Z.alloc(blk);
+  }
+  w.dots.alloc(static_cast<size_t>(4 * tp));
+  w.dbl.alloc(static_cast<size_t>(6 * k));
+  w.ints.alloc(static_cast<size_t>(3 * k + 1));
+  w.tri.alloc(static_cast<size_t>(2 * k * maxit));
+  CgState st;
+  st.rz = w.dbl.get();
+  st.alpha_prev = st.rz + k;
+  st.beta_prev = st.rz + 2 * k;
+  st.alpha = st.rz + 3 * k;
+  st.beta = st.rz + 4 * k;
+  st.scale = st.rz + 5 * k;
+  st.active = w.ints.get();
+  st.converged = st.active + k;
+  st.iterations = st.active + 2 * k;
+  st.err = st.active + 3 * k;
+  st.tdiag = w.tri.get();
+  st.toff = st.tdiag + k * maxit;
+  st.host_flags = ctx->host_flags_dev;
+  double* rr = w.dots.get();
+  double* hv = rr + tp;
+  double* rz = rr + 2 * tp;
+  if (md->dot_scratch.n < coldot_scratch(np, tp)) md->dot_scratch.alloc(coldot_scratch(np, tp));
+  double* sc = md->dot_scratch.get();
+  FSA_CUDA(cudaMemsetAsync(st.err, 0, sizeof(int), s));
+  FSA_CUDA(cudaMemsetAsync(st.tdiag, 0, sizeof(double) * 2 * k * maxit, s));
+  FSA_CUDA(cudaMemcpyAsync(w.R.get(), B, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
+  FSA_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * blk, s));
+
+  auto blas = [&](const char* nm) { return KTimer(ctx, nm); };
+  {
+    auto t = blas("cg_blas1");
+    launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, sc, s);
+    cg_start(rr, k, opts.tol, st, s);
+  }
+  P.solve(w.R.get(), w.Z.get(), tp);
+  {
+    auto t = blas("cg_blas1");
+    launch_coldot(w.R.get(), w.Z.get(), n, tp, k, rz, sc, s);
+    cg_start_rz(rz, k, st, s);
+    init_h(w.H.get(), w.Z.get(), st.active, np, tp, k, s);
+    cg_count(k, st, s);
+  }
+  FSA_CUDA(cudaStreamSynchronize(s));
+  auto check_err = [&]() {
+    const int e = ctx->host_flags[1];
+    if (e == kErrOperatorNotPD) throw NumericalError("cg: operator is not positive definite");
+    if (e == kErrPrecondNotPD) throw NumericalError("cg: preconditioner is not positive definite");
+  };
+  check_err();
+  int num_active = ctx->host_flags[0];
+  CgResult res;
+  for (int it = 0; it < maxit && num_active > 0; ++it) {
+    A.apply(w.H.get(), w.V.get(), tp);
+    {
+      auto t = blas("cg_blas1");
+      launch_coldot(w.H.get(), w.V.get(), n, tp, k, hv, sc, s);
+      cg_alpha(hv, k, it, maxit, st, s);
+      update_xr(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, np, tp, k, s);
+      launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, sc, s);
+      cg_check(rr, k, opts.tol, st, s);
+    }
+    P.solve(w.R.get(), w.Z.get(), tp);
+    {
+      auto t = blas("cg_blas1");
+      launch_coldot(w.R.get(), w.Z.get(), n, tp, k, rz, sc, s);
+      cg_beta(rz, k, st, s);
+      update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
+      cg_count(k, st, s);
+    }
+    FSA_CUDA(cudaStreamSynchronize(s));
+    check_err();
+    num_active = ctx->host_flags[0];
+    ++res.sweeps;
+  }
+  if (num_active > 0 && opts.error_on_max_iter) throw NumericalError("cg: no convergence within max_iter");
+  res.iterations.resize(static_cast<size_t>(k));
+  res.converged.resize(static_cast<size_t>(k));
+  std::vector<double> td(static_cast<size_t>(2 * k * maxit));
+  FSA_CUDA(cudaMemcpyAsync(res.iterations.data(), st.iterations, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpyAsync(res.converged.data(), st.converged, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpyAsync(td.data(), st.tdiag, sizeof(double) * 2 * k * maxit, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  res.tdiag.resize(static_cast<size_t>(k));
+  res.toff.resize(static_cast<size_t>(k));
+  for (long j = 0; j < k; ++j) {
+    const int it = res.iterations[static_cast<size_t>(j)];
+    res.tdiag[static_cast<size_t>(j)].assign(td.begin() + j * maxit, td.begin() + j * maxit + it);
+    if (it > 1)
+      res.toff[static_cast<size_t>(j)].assign(td.begin() + k * maxit + j * maxit,
+                                              td.begin() + k * maxit + j * maxit + it - 1);
+  }
+  return res;
+}
+
+// e1' log(T) e1 (krylov.cpp:120-142): implicit-QL eigensolve of the symmetric
+// tridiagonal, tracking only the first row of the eigenvector matrix.
+double tridiag_log_quadrature(const std::vector<double>& diag, const std::vector<double>& off) {
+  const long n = static_cast<long>(diag.size());
+  if (n == 0) return 0.0;
+  std::vector<double> d(diag), e(static_cast<size_t>(n), 0.0), z(static_cast<size_t>(n), 0.0);
+  for (long i = 0; i + 1 < n; ++i) e[static_cast<size_t>(i)] = off[static_cast<size_t>(i)];
+  z[0] = 1.0;
+  for (long l = 0; l < n; ++l) {
+    int iter = 0;
+    long mm;
+    do {
+      for (mm = l; mm < n - 1; ++mm) {
+        const double dd = std::fabs(d[static_cast<size_t>(mm)]) + std::fabs(d[static_cast<size_t>(mm + 1)]);
+        if (std::fabs(e[static_cast<size_t>(mm)]) <= std::numeric_limits<double>::epsilon() * dd) break;
+      }
+      if (mm != l) {
+        if (iter++ == 60) throw NumericalError("tridiagonal eigendecomposition failed");
+        double g = (d[static_cast<size_t>(l + 1)] - d[static_cast<size_t>(l)]) / (2.0 * e[static_cast<size_t>(l)]);
+        double r = std::hypot(g, 1.0);
+        g = d[static_cast<size_t>(mm)] - d[static_cast<size_t>(l)] + e[static_cast<size_t>(l)] / (g + std::copysign(r, g));
+        double sn = 1.0, c = 1.0, p = 0.0;
+        bool early = false;
+        for (long i = mm - 1; i >= l; --i) {
+          double f = sn * e[static_cast<size_t>(i)];
+          const double b = c * e[static_cast<size_t>(i)];
+          r = std::hypot(f, g);
+          e[static_cast<size_t>(i + 1)] = r;
+          if (r == 0.0) {
+            d[static_cast<size_t>(i + 1)] -= p;
+            e[static_cast<size_t>(mm)] = 0.0;
+            early = true;
+            break;
+          }
+          sn = f / r;
+          c = g / r;
+          g = d[static_cast<size_t>(i + 1)] - p;
+          r = (d[static_cast<size_t>(i)] - g) * sn + 2.0 * c * b;
+          p = sn * r;
+          d[static_cast<size_t>(i + 1)] = g + p;
+          g = c * r - b;
+          f = z[static_cast<size_t>(i + 1)];
+          z[static_cast<size_t>(i + 1)] = sn * z[static_cast<size_t>(i)] + c * f;
+          z[static_cast<size_t>(i)] = c * z[static_cast<size_t>(i)] - sn * f;
+        }
+        if (early) continue;
+        d[static_cast<size_t>(l)] -= p;
+        e[static_cast<size_t>(l)] = g;
+        e[static_cast<size_t>(mm)] = 0.0;
+      }
+    } while (mm != l);
+  }
+  double q = 0.0;
+  for (long i = 0; i < n; ++i) {
+    const double lam = d[static_cast<size_t>(i)];
+    if (!(lam > 0.0)) throw NumericalError("tridiagonal has a nonpositive Ritz value");
+    q += z[static_cast<size_t>(i)] * z[static_cast<size_t>(i)] * std::log(lam);
+  }
+  return q;
+}
+
+static std::vector<double> small_spd_solve(std::vector<double> G, long p, std::vector<double> b) {
+  // Cholesky of the p x p symmetrised GLS matrix (estimation.cpp:207 uses LDLT)
+  for (long j = 0; j < p; ++j) {
+    double sdiag = G[static_cast<size_t>(j + j * p)];
+    for (long k = 0; k < j; ++k) sdiag -= G[static_cast<size_t>(j + k * p)] * G[static_cast<size_t>(j + k * p)];
+    if (!(sdiag > 0.0)) throw NumericalError("nll: GLS normal matrix is not positive definite");
+    const double ljj = std::sqrt(sdiag);
+    G[static_cast<size_t>(j + j * p)] = ljj;
+    for (long i = j + 1; i < p; ++i) {
+      double t = G[static_cast<size_t>(i + j * p)];
+      for (long k = 0; k < j; ++k) t -= G[static_cast<size_t>(i + k * p)] * G[static_cast<size_t>(j + k * p)];
+      G[static_cast<size_t>(i + j * p)] = t / ljj;
+    }
+  }
+  for (long i = 0; i < p; ++i) {
+    double t = b[static_cast<size_t>(i)];
+    for (long k = 0; k < i; ++k) t -= G[static_cast<size_t>(i + k * p)] * b[static_cast<size_t>(k)];
+    b[static_cast<size_t>(i)] = t / G[static_cast<size_t>(i + i * p)];
+  }
+  for (long i = p - 1; i >= 0; --i) {
+    double t = b[static_cast<size_t>(i)];
+    for (long k = i + 1; k < p; ++k) t -= G[static_cast<size_t>(k + i * p)] * b[static_cast<size_t>(k)];
+    b[static_cast<size_t>(i)] = t / G[static_cast<size_t>(i + i * p)];
+  }
+  return b;
+}
+
+static double dotv(const double* a, const double* b, long n) {
+  double s = 0.0;
+  for (long i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* Xc, long p, int L,
+                             unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad) {
+  require(L > 0, "nll: need at least one probe");
+  Context* ctx = md->ctx;
+  cudaStream_t s = ctx->stream;
+  const long n = md->n, np = md->n_pad, mp = md->m_pad;
+  const long k = L + 1 + p;
+  const long tp = pad_cols(k);
+  cudaEvent_t e0 = ctx->ev(), e1 = ctx->ev(), e2 = ctx->ev(), e3 = ctx->ev();
+  FSA_CUDA(cudaEventRecord(e0, s));
+  DBuf<double> B(static_cast<size_t>(np * tp)), Xs(static_cast<size_t>(np * tp));
+  P.sample_probes(L, seed, B.get(), tp);  // columns [0, L)
+  {
+    std::vector<double> yx(static_cast<size_t>(n * (1 + p)));
+    std::copy(y, y + n, yx.begin());
+    if (p > 0) std::copy(Xc, Xc + n * p, yx.begin() + n);
+    DBuf<double> raw(static_cast<size_t>(n * (1 + p)));
+    FSA_CUDA(cudaMemcpyAsync(raw.get(), yx.data(), sizeof(double) * n * (1 + p), cudaMemcpyHostToDevice, s));
+    pack_cols(raw.get(), n, 1 + p, md->geo->pts.perm_d.get(), np, tp, L, B.get(), s);
+    FSA_CUDA(cudaStreamSynchronize(s));
+  }
+  FsaOp op(md);
+  FSA_CUDA(cudaEventRecord(e1, s));
+  CgResult sol = pcg_solve_multi(md, op, P, B.get(), k, tp, Xs.get(), cg);
+  FSA_CUDA(cudaEventRecord(e2, s));
+  if (!sol.all_converged()) throw NumericalError("nll: cg did not converge");
+  NllResult out;
+  out.cg_iterations = sol.max_iterations();
+  out.sweeps = sol.sweeps;
+  for (int it : sol.iterations) out.rhs_iterations += it;
+  std::vector<double> q(static_cast<size_t>(L));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int i = 0; i < L; ++i)
+    q[static_cast<size_t>(i)] = tridiag_log_quadrature(sol.tdiag[static_cast<size_t>(i)], sol.toff[static_cast<size_t>(i)]);
+  double acc = 0.0;
+  for (int i = 0; i < L; ++i) acc += q[static_cast<size_t>(i)];
+  out.logdet = static_cast<double>(n) / static_cast<double>(L) * acc + P.logdet();  // estimation.cpp:198-200
+
+  // u and the GLS coefficients (estimation.cpp:202-212), original order on the host
+  std::vector<double> uS(static_cast<size_t>(n * (1 + p)));
+  {
+    DBuf<double> raw(static_cast<size_t>(n * (1 + p)));
+    unpack_cols(Xs.get(), n, 1 + p, md->geo->pts.perm_d.get(), tp, L, raw.get(), s);
+    FSA_CUDA(cudaMemcpyAsync(uS.data(), raw.get(), sizeof(double) * n * (1 + p), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<double> u(uS.begin(), uS.begin() + n), resid(y, y + n);
+  if (p > 0) {
+    const double* SX = uS.data() + n;
+    std::vector<double> G(static_cast<size_t>(p * p)), Gs(G.size()), rhs(static_cast<size_t>(p));
+    for (long a = 0; a < p; ++a)
+      for (long b = 0; b < p; ++b) G[static_cast<size_t>(a + b * p)] = dotv(Xc + a * n, SX + b * n, n);
+    for (long a = 0; a < p; ++a)
+      for (long b = 0; b < p; ++b)
+        Gs[static_cast<size_t>(a + b * p)] = 0.5 * (G[static_cast<size_t>(a + b * p)] + G[static_cast<size_t>(b + a * p)]);
+    for (long a = 0; a < p; ++a) rhs[static_cast<size_t>(a)] = dotv(SX + a * n, y, n);
+    out.beta = small_spd_solve(Gs, p, rhs);
+    for (long a = 0; a < p; ++a)
+      for (long i = 0; i < n; ++i) {
+        u[static_cast<size_t>(i)] -= SX[i + a * n] * out.beta[static_cast<size_t>(a)];
+        resid[static_cast<size_t>(i)] -= Xc[i + a * n] * out.beta[static_cast<size_t>(a)];
+      }
+  }
+  constexpr double log2pi = 1.8378770664093454836;
+  out.nll = 0.5 * (out.logdet + dotv(resid.data(), u.data(), n) + static_cast<double>(n) * log2pi);
+
+  if (want_grad) {
+    // STE gradient traces (krylov.cpp:163-206, estimation.cpp:217-225), U-form:
+    // columns [0, L) hold the probes, column L holds u so that u' dSigma_k u comes
+    // out of the same batched quadratic forms.
+    const long t2 = pad_cols(L + 1);
+    DBuf<double> Zb(np * t2), Wb(np * t2), Yb(np * t2), SY(np * t2), ub(np);
+    FSA_CUDA(cudaMemsetAsync(Zb.get(), 0, sizeof(double) * np * t2, s));
+    FSA_CUDA(cudaMemsetAsync(Wb.get(), 0, sizeof(double) * np * t2, s));
+    copy_cols(B.get(), tp, Zb.get(), t2, np, L, s);
+    copy_cols(Xs.get(), tp, Wb.get(), t2, np, L, s);
+    {
+      DBuf<double> raw(n);
+      FSA_CUDA(cudaMemcpyAsync(raw.get(), u.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Zb.get(), s);
+      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Wb.get(), s);
+      P.solve(Zb.get(), Yb.get(), t2);
+      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Yb.get(), s);
+      FSA_CUDA(cudaStreamSynchronize(s));
+    }
+    const bool rho_needed = true;
+    if (rho_needed) md->ensure_rho_derivs();
+    DBuf<double> UY(mp * t2), UW(mp * t2), U1Y(mp * t2), U1W(mp * t2), K2UY(mp * t2), d1(np);
+    md->project(md->U.get(), Yb.get(), t2, UY.get());
+    md->project(md->U.get(), Wb.get(), t2, UW.get());
+    md->project(md->U1.get(), Yb.get(), t2, U1Y.get());
+    md->project(md->U1.get(), Wb.get(), t2, U1W.get());
+    gemm_km(md->K2.get(), mp, mp, mp, UY.get(), t2, t2, K2UY.get(), t2, 1.0, 0.0, s);
+    affine_vec(d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, s);
+    const long nd = 12;
+    DBuf<double> dots(static_cast<size_t>(nd * t2));
+    double* sc = md->dot_scratch.get();
+    auto dd = [&](int slot) { return dots.get() + slot * t2; };
+    launch_coldot(Wb.get(), Yb.get(), n, t2, t2, dd(0), sc, s);           // w.y
+    launch_coldot(Yb.get(), Yb.get(), n, t2, t2, dd(1), sc, s);           // y.y
+    md->sigma_s_mat(Yb.get(), SY.get(), t2);
+    launch_coldot(Wb.get(), SY.get(), n, t2, t2, dd(2), sc, s);           // w.Ss y
+    launch_coldot(UW.get(), UY.get(), mp, t2, t2, dd(3), sc, s);          // Uw.Uy
+    launch_coldot_weighted(Yb.get(), Yb.get(), d1.get(), n, t2, t2, dd(4), sc, s);  // y.d1 y
+    launch_coldot(UY.get(), UY.get(), mp, t2, t2, dd(5), sc, s);          // |Uy|^2
+    launch_spmm(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->dsval.get(), n, Yb.get(), t2, SY.get(), t2,
+                t2, 1.0, 0.0, s);
+    launch_coldot(Wb.get(), SY.get(), n, t2, t2, dd(6), sc, s);           // w.dSs y
+    launch_coldot(U1W.get(), UY.get(), mp, t2, t2, dd(7), sc, s);         // U1w.Uy
+    launch_coldot(UW.get(), U1Y.get(), mp, t2, t2, dd(8), sc, s);         // Uw.U1y
+    launch_coldot(UW.get(), K2UY.get(), mp, t2, t2, dd(9), sc, s);        // Uw.K2Uy
+    launch_coldot_weighted(Yb.get(), Yb.get(), md->dD.get(), n, t2, t2, dd(10), sc, s);  // y.dD y
+    launch_coldot(U1Y.get(), UY.get(), mp, t2, t2, dd(11), sc, s);        // U1y.Uy  (dd(9)-style K2 term below)
+    std::vector<double> h(static_cast<size_t>(nd * t2));
+    DBuf<double> uk(t2);
+    launch_coldot(UY.get(), K2UY.get(), mp, t2, t2, uk.get(), sc, s);    // Uy.K2Uy
+    std::vector<double> hk(static_cast<size_t>(t2));
+    FSA_CUDA(cudaMemcpyAsync(h.data(), dots.get(), sizeof(double) * nd * t2, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(hk.data(), uk.get(), sizeof(double) * t2, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    auto H = [&](int slot, long i) { return h[static_cast<size_t>(slot * t2 + i)]; };
+    const double s2 = md->P.sigma2, s12 = md->P.sigma1_2;
+    for (int kk = 0; kk < 3; ++kk) {
+      std::vector<double> a(static_cast<size_t>(L + 1)), b(static_cast<size_t>(L));
+      for (long i = 0; i <= L; ++i) {
+        double av;
+        if (kk == 0) av = H(0, i);
+        else if (kk == 1) av = ((H(2, i) - s2 * H(0, i)) + H(3, i)) / s12;
+        else av = ((H(6, i) + H(7, i)) + H(8, i)) - H(9, i);
+        a[static_cast<size_t>(i)] = av;
+        if (i < L) {
+          double bv;
+          if (kk == 0) bv = H(1, i);
+          else if (kk == 1) bv = H(4, i) + H(5, i) / s12;
+          else bv = (H(10, i) + 2.0 * H(11, i)) - hk[static_cast<size_t>(i)];
+          b[static_cast<size_t>(i)] = bv;
+        }
+      }
+      const double quad = a[static_cast<size_t>(L)];  // u' dSigma_k u
+      const double dl = static_cast<double>(L);
+      double abar = 0.0;
+      for (long i = 0; i < L; ++i) abar += a[static_cast<size_t>(i)];
+      abar /= dl;
+      double value = abar;
+      const bool cv_on = cv_mode != 0 && P.has_derivs();
+      if (cv_on) {
+        double exact_b = 0.0;
+        if (P.kind() == 2) exact_b = static_cast<FitcPrecond&>(P).deriv_trace(kk);
+        else exact_b = -1.0;  // set below for the diagonal preconditioner
+        if (P.kind() == 1) {
+          // Tr(D^{-1} dD_k) with dD_0 = 1, dD_1 = d1, dD_2 = dD
+          std::vector<double> hD(static_cast<size_t>(np)), hv(static_cast<size_t>(np));
+          FSA_CUDA(cudaMemcpy(hD.data(), md->D.get(), sizeof(double) * np, cudaMemcpyDeviceToHost));
+          const double* src = kk == 1 ? d1.get() : md->dD.get();
+          if (kk > 0) FSA_CUDA(cudaMemcpy(hv.data(), src, sizeof(double) * np, cudaMemcpyDeviceToHost));
+          exact_b = 0.0;
+          for (long i = 0; i < n; ++i) exact_b += (kk == 0 ? 1.0 : hv[static_cast<size_t>(i)]) / hD[static_cast<size_t>(i)];
+          // diagonal preconditioner: b_i = y_i' dD_k y_i (no low-rank part)
+          for (long i = 0; i < L; ++i) b[static_cast<size_t>(i)] = kk == 0 ? H(1, i) : (kk == 1 ? H(4, i) : H(10, i));
+        }
+        double bbar = 0.0;
+        for (long i = 0; i < L; ++i) bbar += b[static_cast<size_t>(i)];
+        bbar /= dl;
+        double c = 1.0;
+        if (cv_mode == 2) {
+          double sbb = 0.0, sab = 0.0, mx = 0.0;
+          for (long i = 0; i < L; ++i) {
+            sbb += (b[static_cast<size_t>(i)] - bbar) * (b[static_cast<size_t>(i)] - bbar);
+            sab += (a[static_cast<size_t>(i)] - abar) * (b[static_cast<size_t>(i)] - bbar);
+            mx = std::max(mx, std::fabs(b[static_cast<size_t>(i)]));
+          }
+          const double scale = std::max(mx, 1.0);
+          c = sbb > dl * 1e-28 * scale * scale ? sab / sbb : 0.0;  // krylov.cpp:192-197
+        }
+        value = abar - c * (bbar - exact_b);
+      }
+      out.grad[kk] = 0.5 * (value - quad);
+    }
+  }
+  FSA_CUDA(cudaEventRecord(e3, s));
+  FSA_CUDA(cudaEventSynchronize(e3));
+  float ms1 = 0.f, ms2 = 0.f;
+  FSA_CUDA(cudaEventElapsedTime(&ms1, e1, e2));
+  FSA_CUDA(cudaEventElapsedTime(&ms2, e0, e3));
+  out.pcg_ms = ms1;
+  out.total_ms = ms2;
+  ctx->pool.push_back(e0);
+  ctx->pool.push_back(e1);
+  ctx->pool.push_back(e2);
+  ctx->pool.push_back(e3);
+  return out;
+}
+
+}  // namespace fsa

@@ -1,0 +1,225 @@
+// Host side of the B200 FSA iterative core. Mirrors the reference's operator
+// API (FsaModel::assemble, make_preconditioner, pcg_solve_multi,
+// iterative_nll_grad, make_prediction_set, predict_mean_iterative,
+// predict_var_sim) over device-resident state.
+//
+// Everything runs in the "U-form" of the FSA covariance:
+//   Sigma = U^T U + Sigma_s,  U = L^{-1} Sigma_mn,  L L^T = Sigma_m (+ jitter)
+// which is the reference's Sigma_mn^T Sigma_m^{-1} Sigma_mn low-rank part
+// (fsa.cpp:62-68) without forming A = Sigma_m^{-1} Sigma_mn: one m x n matrix
+// serves both the projection and the expansion, and the FITC Woodbury core
+// becomes Q = I + U D^{-1} U^T = L^{-1} (Sigma_m + Sigma_mn D^{-1} Sigma_mn^T) L^{-T}.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "blas1.cuh"
+#include "common.cuh"
+#include "pattern.cuh"
+
+namespace fsa {
+
+// ---- context: device, stream, timers ----------------------------------------------------
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* host_flags = nullptr;  // pinned, mapped
+  int* host_flags_dev = nullptr;
+  bool profile = false;
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+    double units;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  struct Acc {
+    double ms = 0.0;
+    long count = 0;
+    double units = 0.0;
+  };
+  std::map<std::string, Acc> totals;
+  long launches = 0;  // kernels issued by the library (approximate: per host call site)
+
+  explicit Context(int dev);
+  ~Context();
+  cudaEvent_t ev();
+  void flush_timers();  // synchronises the stream
+  void sync();
+};
+
+// RAII event pair around a kernel group when profiling is on
+struct KTimer {
+  Context* c;
+  size_t idx = static_cast<size_t>(-1);
+  KTimer(Context* ctx, const char* name, double units = 0.0);
+  ~KTimer();
+};
+
+struct Params {
+  int nu = 1;          // 0: 1/2, 1: 3/2, 2: 5/2
+  int family = 1;      // 1: wendland1, 2: wendland2
+  double gamma = 0.1;  // taper range
+  double sigma2 = 1.0, sigma1_2 = 1.0, rho = 0.1;
+  double jitter_rel = 1e-10;
+};
+
+// Parameter-independent geometry: sorted points and the taper pattern. The
+// reference rebuilds it on every evaluation (fsa.cpp:37, estimation.cpp:260);
+// here it is built once and shared by every Model assembled on it.
+struct Geometry {
+  SortedPoints pts;
+  Csr pat;
+  double gamma = 0.0;
+  std::vector<double> coords_host;  // original order, n x d column-major
+};
+std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long n, int d, double gamma);
+
+class Model {
+ public:
+  Context* ctx = nullptr;
+  std::shared_ptr<Geometry> geo;
+  Params P;
+  long n = 0, m = 0, n_pad = 0, m_pad = 0;
+  int d = 2;
+  std::vector<double> ind_host;  // m x d column-major
+  DBuf<double> ind;              // same, device
+  DBuf<double> Sm, L;            // Sigma_m (+jitter), its Cholesky factor (col-major, m_pad^2)
+  double logdet_sigma_m = 0.0;
+  DBuf<double> U;                // m_pad x n_pad, one column per point
+  DBuf<double> lowrank;          // |U_i|^2
+  DBuf<double> sval;             // Sigma_s values on geo->pat
+  DBuf<double> D, Dinv, sqrtD;   // diag(Sigma_s) (FITC / Jacobi diagonal)
+  long n_clamped = 0;
+  // rho derivative blocks (lazy, fsa.cpp:101-124)
+  bool have_rho = false;
+  DBuf<double> U1, T, K2, dsval, dD;
+  // scratch
+  DBuf<double> red_scratch, dot_scratch, dinv_scratch, mt1, mt2;
+  DBuf<int> info;
+
+  static std::unique_ptr<Model> assemble(Context* ctx, std::shared_ptr<Geometry> geo, const double* inducing, long m,
+                                         const Params& p);
+  void ensure_rho_derivs();
+  // device, internal layout (row-major n_pad x tp)
+  void matmat(const double* H, double* V, long tp);
+  void sigma_s_mat(const double* H, double* V, long tp, double alpha = 1.0, double beta = 0.0);
+  void deriv_matmat(int which, const double* V, double* out, long tp);
+  // m_pad x tp projection U V (deterministic split-K)
+  void project(const double* M, const double* V, long tp, double* out, const double* scale = nullptr);
+  double* mt_buf(int which, long tp);
+};
+
+// ---- preconditioners (preconditioners.h:16-115) ------------------------------------------
+class Precond {
+ public:
+  virtual ~Precond() = default;
+  virtual int kind() const = 0;  // 0 none, 1 diagonal, 2 fitc
+  virtual void solve(const double* R, double* Z, long tp) = 0;
+  virtual double logdet() const = 0;
+  // probes keyed by (seed, i): writes n_pad x tp internal-layout block, columns [0, L)
+  virtual void sample_probes(int L, unsigned long long seed, double* Z, long tp) = 0;
+  virtual bool has_derivs() const { return false; }
+};
+
+class IdentityPrecond final : public Precond {
+ public:
+  explicit IdentityPrecond(Model* m) : md(m) {}
+  int kind() const override { return 0; }
+  void solve(const double* R, double* Z, long tp) override;
+  double logdet() const override { return 0.0; }
+  void sample_probes(int L, unsigned long long seed, double* Z, long tp) override;
+  Model* md;
+};
+
+class DiagPrecond final : public Precond {
+ public:
+  explicit DiagPrecond(Model* m, bool derivs);
+  int kind() const override { return 1; }
+  void solve(const double* R, double* Z, long tp) override;
+  double logdet() const override { return ld; }
+  void sample_probes(int L, unsigned long long seed, double* Z, long tp) override;
+  bool has_derivs() const override { return derivs; }
+  Model* md;
+  double ld = 0.0;
+  bool derivs = false;
+};
+
+class FitcPrecond final : public Precond {
+ public:
+  FitcPrecond(Model* m, bool with_derivs);
+  int kind() const override { return 2; }
+  void solve(const double* R, double* Z, long tp) override;
+  double logdet() const override { return ld; }
+  void sample_probes(int L, unsigned long long seed, double* Z, long tp) override;
+  bool has_derivs() const override { return derivs; }
+  // exact Tr(P^{-1} dP_k), k = 0, 1, 2 (preconditioners.cpp:106-115, U-form)
+  double deriv_trace(int k);
+  Model* md;
+  DBuf<double> Q, LQ, Qinv;  // I + U D^{-1} U^T, its factor, its inverse
+  double ld = 0.0, logdetQ = 0.0;
+  bool derivs = false;
+  bool have_traces = false;
+  double trace[3] = {0, 0, 0};
+};
+
+std::unique_ptr<Precond> make_preconditioner(Model* md, int type);
+
+// ---- Krylov ---------------------------------------------------------------------------------
+struct CgOptions {
+  double tol = 1e-3;
+  int max_iter = 1000;
+  bool error_on_max_iter = false;
+};
+struct CgResult {
+  std::vector<int> iterations;
+  std::vector<int> converged;
+  std::vector<std::vector<double>> tdiag, toff;
+  int sweeps = 0;
+  bool all_converged() const;
+  int max_iterations() const;
+};
+struct LinOp {
+  virtual ~LinOp() = default;
+  virtual void apply(const double* H, double* V, long tp) = 0;
+};
+
+// the full FSA operator (krylov.cpp:10-16) and the short-range block alone (prediction.cpp:90-93)
+struct FsaOp final : LinOp {
+  Model* md;
+  explicit FsaOp(Model* m) : md(m) {}
+  void apply(const double* H, double* V, long tp) override { md->matmat(H, V, tp); }
+};
+struct SigmaSOp final : LinOp {
+  Model* md;
+  explicit SigmaSOp(Model* m) : md(m) {}
+  void apply(const double* H, double* V, long tp) override { md->sigma_s_mat(H, V, tp); }
+};
+
+// Lockstep multi-RHS PCG (krylov.cpp:18-106) on device blocks B, X (n_pad x tp, internal).
+CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long k, long tp, double* X,
+                         const CgOptions& opts);
+double tridiag_log_quadrature(const std::vector<double>& diag, const std::vector<double>& off);
+
+struct NllResult {
+  double nll = 0.0, grad[3] = {0, 0, 0}, logdet = 0.0;
+  int cg_iterations = 0;
+  std::vector<double> beta;
+  // diagnostics
+  double pcg_ms = 0.0, total_ms = 0.0;
+  long rhs_iterations = 0;
+  int sweeps = 0;
+};
+// iterative_nll_grad (estimation.cpp:178-227); y (n), X (n x p) host, original order
+NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* X, long p, int num_probes,
+                             unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad);
+
+// ---- host RNG identical to the reference (types.h:104-129) ------------------------------------
+unsigned long long splitmix64(unsigned long long x);
+void probe_gaussian(unsigned long long seed, unsigned long long i, long n1, double* e1, long n2, double* e2);
+void probe_rademacher(unsigned long long seed, unsigned long long i, long n, double* z);
+
+}  // namespace fsa

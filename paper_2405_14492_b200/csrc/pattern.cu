@@ -1,0 +1,280 @@
+// Device taper-neighbour search; see pattern.cuh.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.cuh"
+#include "pattern.cuh"
+
+namespace fsa {
+
+namespace {
+
+constexpr unsigned kHilbertBits = 21;
+constexpr long kMaxCells = (1L << kHilbertBits) - 2;
+
+__host__ __device__ inline unsigned long long hilbert_xy2d(unsigned long long x, unsigned long long y) {
+  const unsigned long long n = 1ULL << kHilbertBits;
+  unsigned long long d = 0;
+  for (unsigned long long s = n / 2; s > 0; s /= 2) {
+    const unsigned long long rx = (x & s) > 0 ? 1 : 0;
+    const unsigned long long ry = (y & s) > 0 ? 1 : 0;
+    d += s * s * ((3 * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = n - 1 - x;
+        y = n - 1 - y;
+      }
+      const unsigned long long t = x;
+      x = y;
+      y = t;
+    }
+  }
+  return d;
+}
+__host__ __device__ inline unsigned long long spread3(unsigned long long v) {
+  unsigned long long r = 0;
+  for (int b = 0; b < 21; ++b) r |= ((v >> b) & 1ULL) << (3 * b);
+  return r;
+}
+template <int D>
+__host__ __device__ inline unsigned long long cell_key(const long* c) {
+  if (D == 1) return static_cast<unsigned long long>(c[0]);
+  if (D == 2) return hilbert_xy2d(static_cast<unsigned long long>(c[0]), static_cast<unsigned long long>(c[1]));
+  return spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+}
+
+struct GridArgs {
+  double o0, o1, o2, h;
+};
+template <int D>
+__device__ inline void cell_of(const double* x, long ld, long i, const GridArgs& g, long* c) {
+  const double o[3] = {g.o0, g.o1, g.o2};
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    long v = static_cast<long>(floor((x[i + k * ld] - o[k]) / g.h));
+    v = v < 0 ? 0 : (v > kMaxCells ? kMaxCells : v);
+    c[k] = v;
+  }
+}
+
+template <int D>
+__global__ void k_point_keys(const double* __restrict__ xs, long n, GridArgs g, unsigned long long* keys,
+                             int* idx) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long c[3] = {0, 0, 0};
+  cell_of<D>(xs, n, i, g, c);
+  keys[i] = cell_key<D>(c);
+  idx[i] = static_cast<int>(i);
+}
+
+__global__ void k_gather_coords(const double* __restrict__ xs, long n, int d, const int* __restrict__ perm,
+                                long n_pad, double* __restrict__ out, int* __restrict__ iperm) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  if (i < n) {
+    const long o = perm[i];
+    for (int k = 0; k < d; ++k) out[i + k * n_pad] = xs[o + k * n];
+    iperm[o] = static_cast<int>(i);
+  } else {
+    for (int k = 0; k < d; ++k) out[i + k * n_pad] = 0.0;
+  }
+}
+
+__device__ inline long lower_bound_key(const unsigned long long* keys, long n, unsigned long long k) {
+  long lo = 0, hi = n;
+  while (lo < hi) {
+    const long mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Visit every column point j within gamma of row point i, in ascending internal
+// column order (neighbour cells sorted by key; points within a cell are contiguous).
+template <int D, class F>
+__device__ inline void visit_neighbours(const double* __restrict__ rx, long rld, long i,
+                                        const double* __restrict__ cx, long cld,
+                                        const unsigned long long* __restrict__ ckeys, long cn, const GridArgs& g,
+                                        double gamma, F&& f) {
+  long base[3] = {0, 0, 0};
+  cell_of<D>(rx, rld, i, g, base);
+  constexpr int NC = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  unsigned long long ks[NC];
+  int nk = 0;
+  for (int q = 0; q < NC; ++q) {
+    long c[3] = {0, 0, 0};
+    int t = q;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      c[k] = base[k] + (t % 3) - 1;
+      t /= 3;
+      if (c[k] < 0 || c[k] > kMaxCells) ok = false;
+    }
+    if (!ok) continue;
+    const unsigned long long key = cell_key<D>(c);
+    bool dup = false;
+    for (int a = 0; a < nk; ++a) dup |= ks[a] == key;
+    if (!dup) ks[nk++] = key;
+  }
+  // insertion sort of the (<= 27) keys
+  for (int a = 1; a < nk; ++a) {
+    const unsigned long long v = ks[a];
+    int b = a - 1;
+    while (b >= 0 && ks[b] > v) {
+      ks[b + 1] = ks[b];
+      --b;
+    }
+    ks[b + 1] = v;
+  }
+  for (int a = 0; a < nk; ++a) {
+    long p = lower_bound_key(ckeys, cn, ks[a]);
+    for (; p < cn && ckeys[p] == ks[a]; ++p) {
+      const double dd = pdist_soa<D>(rx, rld, i, cx, cld, p);
+      if (dd < gamma) f(p, dd);
+    }
+  }
+}
+
+template <int D>
+__global__ void k_count(const double* rx, long rld, long rn, const double* cx, long cld,
+                        const unsigned long long* ckeys, long cn, GridArgs g, double gamma, long* counts) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rn) return;
+  long cnt = 0;
+  visit_neighbours<D>(rx, rld, i, cx, cld, ckeys, cn, g, gamma, [&](long, double) { ++cnt; });
+  counts[i] = cnt;
+}
+
+template <int D>
+__global__ void k_fill(const double* rx, long rld, long rn, const double* cx, long cld,
+                       const unsigned long long* ckeys, long cn, GridArgs g, double gamma, const long* rowptr,
+                       int* col, double* dist, long* diagpos, int square) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rn) return;
+  long p = rowptr[i];
+  long dp = -1;
+  visit_neighbours<D>(rx, rld, i, cx, cld, ckeys, cn, g, gamma, [&](long j, double dd) {
+    col[p] = static_cast<int>(j);
+    if (square && j == i) {
+      dp = p;
+      dd = 0.0;
+    }
+    dist[p] = dd;
+    ++p;
+  });
+  if (square) diagpos[i] = dp;
+}
+
+}  // namespace
+
+CellGrid make_grid(const double* coords, long n, int d, double gamma, const double* coords2, long n2) {
+  require(d >= 1 && d <= 3, "dimension must be 1, 2 or 3");
+  require(gamma > 0.0, "taper range must be positive");
+  CellGrid g;
+  g.d = d;
+  double ext = 0.0;
+  for (int k = 0; k < d; ++k) {
+    double lo = coords[k * n], hi = coords[k * n];
+    for (long i = 1; i < n; ++i) {
+      lo = std::min(lo, coords[i + k * n]);
+      hi = std::max(hi, coords[i + k * n]);
+    }
+    for (long i = 0; coords2 && i < n2; ++i) {
+      lo = std::min(lo, coords2[i + k * n2]);
+      hi = std::max(hi, coords2[i + k * n2]);
+    }
+    g.origin[k] = lo;
+    ext = std::max(ext, hi - lo);
+  }
+  // cells of edge >= gamma keep the 3^d neighbourhood exhaustive
+  g.h = std::max(gamma, ext / static_cast<double>(kMaxCells - 2));
+  return g;
+}
+
+void sort_points(const double* coords_host, long n, int d, const CellGrid& g, long n_pad, SortedPoints& out,
+                 cudaStream_t s) {
+  require(n > 0, "empty location set");
+  out.n = n;
+  out.n_pad = n_pad;
+  out.d = d;
+  out.grid = g;
+  DBuf<double> raw(static_cast<size_t>(n * d));
+  FSA_CUDA(cudaMemcpyAsync(raw.get(), coords_host, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+  DBuf<unsigned long long> keys_in(n);
+  DBuf<int> idx_in(n);
+  out.keys.alloc(n);
+  out.perm_d.alloc(n);
+  out.iperm_d.alloc(n);
+  out.coords.alloc(static_cast<size_t>(d * n_pad));
+  GridArgs ga{g.origin[0], g.origin[1], g.origin[2], g.h};
+  const unsigned nb = static_cast<unsigned>(cdiv(n, 256));
+  switch (d) {
+    case 1: k_point_keys<1><<<nb, 256, 0, s>>>(raw.get(), n, ga, keys_in.get(), idx_in.get()); break;
+    case 2: k_point_keys<2><<<nb, 256, 0, s>>>(raw.get(), n, ga, keys_in.get(), idx_in.get()); break;
+    default: k_point_keys<3><<<nb, 256, 0, s>>>(raw.get(), n, ga, keys_in.get(), idx_in.get()); break;
+  }
+  FSA_LAUNCH_CHECK();
+  size_t tmp_bytes = 0;
+  FSA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in.get(), out.keys.get(), idx_in.get(),
+                                           out.perm_d.get(), static_cast<int>(n), 0, 64, s));
+  DBuf<unsigned char> tmp(tmp_bytes);
+  FSA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys_in.get(), out.keys.get(), idx_in.get(),
+                                           out.perm_d.get(), static_cast<int>(n), 0, 64, s));
+  k_gather_coords<<<static_cast<unsigned>(cdiv(n_pad, 256)), 256, 0, s>>>(raw.get(), n, d, out.perm_d.get(), n_pad,
+                                                                         out.coords.get(), out.iperm_d.get());
+  FSA_LAUNCH_CHECK();
+  out.perm.resize(n);
+  out.iperm.resize(n);
+  FSA_CUDA(cudaMemcpyAsync(out.perm.data(), out.perm_d.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpyAsync(out.iperm.data(), out.iperm_d.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+}
+
+void build_pattern(const SortedPoints& rows, const SortedPoints& cols, double gamma, bool force_diag, Csr& out,
+                   cudaStream_t s) {
+  require(rows.d == cols.d, "location sets must share the dimension");
+  const int d = rows.d;
+  const CellGrid& g = cols.grid;
+  GridArgs ga{g.origin[0], g.origin[1], g.origin[2], g.h};
+  out.rows = rows.n;
+  out.cols = cols.n;
+  DBuf<long> counts(rows.n + 1);
+  const unsigned nb = static_cast<unsigned>(cdiv(rows.n, 128));
+#define FSA_PAT_ARGS rows.coords.get(), rows.n_pad, rows.n, cols.coords.get(), cols.n_pad, cols.keys.get(), cols.n, ga, gamma
+  switch (d) {
+    case 1: k_count<1><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, counts.get()); break;
+    case 2: k_count<2><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, counts.get()); break;
+    default: k_count<3><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, counts.get()); break;
+  }
+  FSA_LAUNCH_CHECK();
+  FSA_CUDA(cudaMemsetAsync(counts.get() + rows.n, 0, sizeof(long), s));
+  out.rowptr.alloc(rows.n + 1);
+  size_t tmp_bytes = 0;
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.get(), out.rowptr.get(),
+                                         static_cast<int>(rows.n + 1), s));
+  DBuf<unsigned char> tmp(tmp_bytes);
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, counts.get(), out.rowptr.get(),
+                                         static_cast<int>(rows.n + 1), s));
+  long nnz = 0;
+  FSA_CUDA(cudaMemcpyAsync(&nnz, out.rowptr.get() + rows.n, sizeof(long), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  out.nnz = nnz;
+  out.col.alloc(nnz > 0 ? nnz : 1);
+  out.dist.alloc(nnz > 0 ? nnz : 1);
+  if (force_diag) out.diagpos.alloc(rows.n);
+  long* dp = force_diag ? out.diagpos.get() : nullptr;
+  const int sq = force_diag ? 1 : 0;
+  switch (d) {
+    case 1: k_fill<1><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, out.rowptr.get(), out.col.get(), out.dist.get(), dp, sq); break;
+    case 2: k_fill<2><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, out.rowptr.get(), out.col.get(), out.dist.get(), dp, sq); break;
+    default: k_fill<3><<<nb, 128, 0, s>>>(FSA_PAT_ARGS, out.rowptr.get(), out.col.get(), out.dist.get(), dp, sq); break;
+  }
+#undef FSA_PAT_ARGS
+  FSA_LAUNCH_CHECK();
+}
+
+}  // namespace fsa

@@ -1,0 +1,53 @@
+// Taper-neighbour search on the device (reference GridIndex / taper_pattern /
+// cross_taper_pattern, locations.cpp:19-62,139-184).
+//
+// Points are binned into cells of edge h >= gamma, the cells are ordered along a
+// Hilbert curve (d = 2; row-major for d = 1, Morton for d = 3) and the points are
+// radix-sorted by (cell key, original index). That order is the library's
+// internal point order: it makes the 3^d-cell neighbourhood of a row a handful of
+// contiguous index ranges (L2-friendly SpMM gathers) and is the row-sharding order
+// for multiple GPUs. Rows list their columns in ascending internal order.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace fsa {
+
+struct CellGrid {
+  int d = 2;
+  double origin[3] = {0, 0, 0};
+  double h = 1.0;
+};
+
+// A point set in internal (cell-sorted) order.
+struct SortedPoints {
+  long n = 0, n_pad = 0;
+  int d = 2;
+  CellGrid grid;
+  std::vector<int> perm;        // internal -> original (host)
+  std::vector<int> iperm;       // original -> internal (host)
+  DBuf<int> perm_d, iperm_d;    // same on device
+  DBuf<double> coords;          // SoA [d][n_pad], internal order, zero padding
+  DBuf<unsigned long long> keys;  // sorted cell keys, length n
+};
+
+struct Csr {
+  long rows = 0, cols = 0, nnz = 0;
+  DBuf<long> rowptr;   // rows + 1
+  DBuf<int> col;       // internal column index
+  DBuf<double> dist;   // stored distances (parameter independent)
+  DBuf<long> diagpos;  // position of (i,i) (square patterns only)
+};
+
+// grid covering both point sets (cross patterns use one grid for rows and cols)
+CellGrid make_grid(const double* coords, long n, int d, double gamma, const double* coords2, long n2);
+void sort_points(const double* coords_host, long n, int d, const CellGrid& g, long n_pad, SortedPoints& out,
+                 cudaStream_t s);
+// rows x cols pattern of pairs with |x_row - x_col| < gamma; force_diag adds (i,i)
+// (rows and cols must be the same set then).
+void build_pattern(const SortedPoints& rows, const SortedPoints& cols, double gamma, bool force_diag, Csr& out,
+                   cudaStream_t s);
+
+}  // namespace fsa
