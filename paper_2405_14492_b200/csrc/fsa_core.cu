@@ -396,17 +396,20 @@ void FitcPrecond::solve(const double* R, double* Z, long tp) {
 void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long tp) {
   const long m = md->m, n = md->n, mp = md->m_pad, np = md->n_pad;
   cudaStream_t s = md->ctx->stream;
-  static thread_local PinnedBuf e1h, e2h;
+  static PinnedBuf e1h, e2h;  // host staging (one host thread per context)
   e1h.ensure(static_cast<size_t>(mp * tp));
   e2h.ensure(static_cast<size_t>(n * L));
-  std::memset(e1h.p, 0, sizeof(double) * mp * tp);
+  double* e1p = e1h.p;
+  double* e2p = e2h.p;
+  std::memset(e1p, 0, sizeof(double) * mp * tp);
   std::vector<double> e1col(static_cast<size_t>(m) * L);
+  double* e1c = e1col.data();
 #pragma omp parallel for schedule(dynamic, 1)
   for (int i = 0; i < L; ++i)
-    probe_gaussian(seed, static_cast<unsigned long long>(i), m, e1col.data() + static_cast<long>(i) * m, n,
-                   e2h.p + static_cast<long>(i) * n);
+    probe_gaussian(seed, static_cast<unsigned long long>(i), m, e1c + static_cast<long>(i) * m, n,
+                   e2p + static_cast<long>(i) * n);
   for (int i = 0; i < L; ++i)
-    for (long r = 0; r < m; ++r) e1h.p[r * tp + i] = e1col[static_cast<size_t>(i) * m + r];
+    for (long r = 0; r < m; ++r) e1p[r * tp + i] = e1col[static_cast<size_t>(i) * m + r];
   DBuf<double> E1(mp * tp), E2(np * tp), raw(n * L);
   FSA_CUDA(cudaMemcpyAsync(E1.get(), e1h.p, sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
   FSA_CUDA(cudaMemcpyAsync(raw.get(), e2h.p, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
