@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FSA iterative core (BASELINE.json metric).
+
+One step = one FSA log-likelihood + gradient evaluation as the reference's fit
+objective performs it (estimation.cpp:255-284): FsaModel::assemble at the current
+parameters, FitcPrecond::from_fsa, iterative_nll_grad (probes, lockstep FITC-PCG
+over [Z | y], SLQ log-determinant, STE gradient traces with the optimal control
+variate). The taper pattern (parameter independent) is built once per run.
+
+value  = PCG RHS-iterations per second over the whole evaluation (inputs resident
+         in HBM: response and probe draws cached on the device, as in a fit loop)
+e2e    = the same metric through the reference-facing C-ABI calls with host buffers
+         (fsa_model_assemble + fsa_make_preconditioner + fsa_iterative_nll_grad),
+         host<->device copies inside the timed region.
+`--impl reference` times the CPU oracle port of the reference path (oracle/) on
+the host cores: a bounded FITC-PCG sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(n=10_000, m=200, inducing="random", nu=0.5, s12=1.0, rho=0.1, s2=0.1, nnz=30, L=50, tol=1e-3,
+            points="uniform"),
+    2: dict(n=100_000, m=500, inducing="kmeans", nu=1.5, s12=1.0, rho=0.05, s2=0.05, nnz=80, L=50, tol=1e-3,
+            points="uniform"),
+    4: dict(n=1_000_000, m=1000, inducing="kmeans", nu=1.5, s12=1.0, rho=0.03, s2=0.05, nnz=80, L=64, tol=1e-3,
+            points="uniform"),
+    5: dict(n=200_000, m=1000, inducing="kmeans", nu=2.5, s12=1.0, rho=0.3, s2=1e-3, nnz=120, L=50, tol=1e-4,
+            points="blobs"),
+}
+METRIC = "PCG RHS-iterations/s over FSA loglik+grad evaluations"
+
+
+def make_inputs(cfg, fsa):
+    n, m = cfg["n"], cfg["m"]
+    if cfg["points"] == "uniform":
+        coords = fsa.uniform_locations(n, 2, 1)
+        gamma = fsa.gamma_for_avg_row_nnz(n, cfg["nnz"])
+    else:
+        coords = fsa.blob_locations(n, 2, 50, 0.01, 1)
+        gamma = None
+    if cfg["inducing"] == "random":
+        ind = fsa.select_random(coords, m, 2)
+    else:
+        ind = fsa.select_kmeanspp(coords, m, 2)
+    y = fsa.simulate_rff(coords, cfg["nu"], cfg["s12"], cfg["rho"], cfg["s2"], 1024, 3)
+    return coords, ind, gamma, y
+
+
+def calibrate_gamma(coords, target, fsa, ctx):
+    """bisection on the measured nnz/row (clustered points)."""
+    n = coords.shape[0]
+    lo, hi = 1e-5, 0.2
+    for _ in range(30):
+        mid = math.sqrt(lo * hi)
+        g = fsa.Geometry(coords, mid, ctx)
+        avg = g.nnz() / n
+        del g
+        if avg < target:
+            lo = mid
+        else:
+            hi = mid
+        if abs(avg - target) / target < 0.02:
+            return mid
+    return math.sqrt(lo * hi)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measure_fp64_peak(torch):
+    """cuBLAS DGEMM throughput (FP64 peak is absent from MEASURED_PEAKS.json)."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        torch.matmul(a, b)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 8192 ** 3 / (ms * 1e-3) / 1e12
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def cpu_pcg_sample(cfg, coords, ind, gamma, sweeps=2):
+    """The oracle port at the full workload: FITC setup untimed, then a bounded
+    number of lockstep PCG sweeps on the [Z | y] block; RHS-iterations / s."""
+    from oracle import oracle as O
+
+    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    om = O.Model(coords, ind, **kw)
+    P = O.Precond(om, "fitc", plain=True)
+    Z = P.sample_probes(cfg["L"], 0)
+    y = np.random.default_rng(0).standard_normal(cfg["n"])
+    B = np.asfortranarray(np.column_stack([Z, y]))
+    t0 = time.perf_counter()
+    r = O.pcg_solve_multi(om, P, B, tol=cfg["tol"], max_iter=sweeps)
+    dt = time.perf_counter() - t0
+    its = int(np.sum(r["iterations"]))
+    return its / dt, its, dt
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2405_14492_b200 import fsa
+
+    coords, ind, gamma, y = make_inputs(cfg, fsa)
+    if gamma is None:
+        gamma = fsa.gamma_for_avg_row_nnz(cfg["n"], cfg["nnz"])
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, its, dt = cpu_pcg_sample(cfg, coords, ind, gamma, sweeps=args.ref_sweeps)
+        if i >= args.warmup:
+            vals.append((v, its, dt))
+    value = statistics.median(v for v, _, _ in vals)
+    cores = os.cpu_count()
+    sample = (f"oracle port (oracle/fsa_oracle.cpp, C++ restatement of krylov.cpp:18-106 + "
+              f"preconditioners.cpp:58-61, OpenMP over RHS columns) at n={cfg['n']}, m={cfg['m']}, "
+              f"t={cfg['L'] + 1}: {args.ref_sweeps} PCG sweeps per step, FITC setup untimed")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "RHS-iterations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(dt for _, _, dt in vals), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": f"config{args.config}", **{k: cfg[k] for k in ("n", "m", "nnz", "L", "tol")}},
+            "cpu_baseline": {"value": value, "unit": "RHS-iterations/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "RHS-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+
+    from paper_2405_14492_b200 import fsa
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = fsa.Context(local)
+    coords, ind, gamma, y = make_inputs(cfg, fsa)
+    if gamma is None:
+        gamma = calibrate_gamma(coords, cfg["nnz"], fsa, ctx)
+    fp64_peak = measure_fp64_peak(torch)
+    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    L, tol = cfg["L"], cfg["tol"]
+    stream = torch.cuda.ExternalStream(ctx.stream())
+
+    # ---- device-resident fit-loop step (value) ---------------------------------------
+    geo = fsa.Geometry(coords, gamma, ctx)
+    geo.set_response(y)
+    geo.cache_probes(True)
+    nnz = geo.nnz()
+
+    def step():
+        md = fsa.FsaModel.assemble(None, ind, geometry=geo, **kw)
+        P = fsa.make_preconditioner(md, "fitc")
+        r = fsa.iterative_nll_grad(md, P, None, num_probes=L, seed=0, tol=tol)
+        del P, md
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    ctx.set_profiling(True)
+    ctx.reset_timers()
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    l0 = fsa.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = fsa.launch_count() - l0
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms)
+    timers = ctx.timers()
+    ctx.set_profiling(False)
+    rhs_its = sum(r["rhs_iterations"] for r in results) * world
+    value = rhs_its / (ms * 1e-3)
+    pcg_ms = statistics.median(r["pcg_ms"] for r in results)
+    pcg_rate = results[-1]["rhs_iterations"] / (pcg_ms * 1e-3)
+
+    # roofline of the dominant kernel group (FP64 DMMA GEMMs) + the SpMM (HBM)
+    gemm = {k: v for k, v in timers.items() if k in ("lowrank_project", "lowrank_expand")}
+    dom = max(gemm, key=lambda k: gemm[k]["ms"])
+    d = gemm[dom]
+    achieved = d["units"] / (d["ms"] * 1e-3) / 1e12
+    sp = timers.get("spmm", {"ms": 0.0, "units": 0.0, "count": 0})
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    step_ms = ms / args.steps
+    roofline = {"bound": "tensor", "kernel": f"k_dgemm ({dom}, DMMA.8x8x4 fp64)", "achieved": achieved,
+                "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in MEASURED_PEAKS.json)",
+                "share_of_step": d["ms"] / ms, "avg_launch_ms": d["ms"] / max(d["count"], 1),
+                "flops_per_launch": d["units"] / max(d["count"], 1),
+                "spmm": {"bound": "hbm", "achieved": sp["units"] / max(sp["ms"], 1e-9) / 1e6 if sp["ms"] else None,
+                         "peak": hbm, "unit": "GB/s",
+                         "frac": (sp["units"] / max(sp["ms"], 1e-9) / 1e6) / hbm if sp["ms"] else None,
+                         "share_of_step": sp["ms"] / ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+
+    # ---- end to end through the reference-facing API with host buffers (e2e) -------
+    del geo
+    e2e_ms = []
+    n, m = cfg["n"], cfg["m"]
+    for i in range(1 + args.e2e_steps if args.e2e_steps > 0 else 0):
+        barrier()
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        md = fsa.FsaModel.assemble(coords, ind, ctx=ctx, **kw)
+        P = fsa.make_preconditioner(md, "fitc")
+        r = fsa.iterative_nll_grad(md, P, y, num_probes=L, seed=0, tol=tol)
+        ctx.synchronize()
+        dt = time.perf_counter() - t0
+        del P, md
+        if i > 0:
+            e2e_ms.append(max_over_ranks(dt * 1e3))
+    e2e_step_ms = statistics.median(e2e_ms) if e2e_ms else float("nan")
+    e2e_value = results[-1]["rhs_iterations"] * world / (e2e_step_ms * 1e-3) if e2e_ms else None
+    k = L + 1
+    tp = k if k <= 72 else k
+    h2d = 8 * (n * 2 + m * 2 + n + m * L + n * L + n)
+    d2h = 8 * (n + 2 * k * 1000 + 2 * n)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, its, dt = cpu_pcg_sample(cfg, coords, ind, gamma, sweeps=args.ref_sweeps)
+            cpu = {"value": v, "unit": "RHS-iterations/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"oracle port, FITC setup untimed, {args.ref_sweeps} lockstep PCG sweeps on the "
+                             f"full n={n}, t={k} block ({its} RHS-iterations in {dt:.2f} s)"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "RHS-iterations/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        last = results[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": "RHS-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config)",
+            "config": {"workload": f"config{args.config}: loglik+grad, FITC-PCG", "n": n, "m": m, "nnz": nnz,
+                       "avg_row_nnz": nnz / n, "probes": L, "rhs": k, "tol": tol, "nu": cfg["nu"],
+                       "rho": cfg["rho"], "sigma2": cfg["s2"], "sigma1_2": cfg["s12"], "gamma": gamma,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (U is m x n fp64 = %.0f MB)" % (8 * m * n / 1e6)},
+            "loglik_grad_ms": step_ms, "pcg_ms": pcg_ms, "pcg_only_rhs_iter_per_s": pcg_rate,
+            "cg_iterations": last["cg_iterations"], "sweeps": last["sweeps"], "nll": last["nll"],
+            "grad": list(last["grad"]), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "RHS-iterations/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms},
+            "gpu_launches": launches, "clocks": clocks,
+            "timers_ms": {k2: round(v["ms"] / args.steps, 3) for k2, v in timers.items()},
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

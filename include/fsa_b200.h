@@ -116,6 +116,13 @@ int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz);
 int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist);
 /* internal (space-filling-curve) order: perm[internal] = original index */
 int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm);
+/* Fit-loop residency (the reference's fit_fsa objective, estimation.cpp:255-284, re-uploads
+ * these every evaluation): keep [y | X] in HBM — fsa_iterative_nll_grad with y == NULL then
+ * uses it — and cache the parameter-independent probe draws e1/e2 across evaluations. */
+int fsa_geometry_set_response(fsa_geometry* g, const double* y, const double* X, int64_t pcols);
+int fsa_geometry_cache_probes(fsa_geometry* g, int on);
+/* kernels launched by this library so far (process wide) */
+int64_t fsa_launch_count(void);
 
 /* ---- FSA model (FsaModel, fsa.h:40-104) -------------------------------------------- */
 /* FsaModel::assemble(locs, inducing, kern, taper, params, opts) (fsa.h:42-43); builds the geometry */

@@ -263,6 +263,35 @@ int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm) {
   });
 }
 
+int fsa_geometry_set_response(fsa_geometry* g, const double* y, const double* X, int64_t pcols) {
+  return guard([&] {
+    need(g, "geometry");
+    need(y, "y");
+    require(pcols >= 0 && (pcols == 0 || X != nullptr), "nll: shape mismatch");
+    Geometry& G = *g->g;
+    const long n = G.pts.n;
+    G.resp_host.assign(y, y + n);
+    if (pcols > 0) G.resp_host.insert(G.resp_host.end(), X, X + n * pcols);
+    G.resp_dev.alloc(static_cast<size_t>(n * (1 + pcols)));
+    FSA_CUDA(cudaMemcpyAsync(G.resp_dev.get(), G.resp_host.data(), sizeof(double) * n * (1 + pcols),
+                             cudaMemcpyHostToDevice, g->ctx->c->stream));
+    FSA_CUDA(cudaStreamSynchronize(g->ctx->c->stream));
+    G.resp_p = pcols;
+  });
+}
+int fsa_geometry_cache_probes(fsa_geometry* g, int on) {
+  return guard([&] {
+    need(g, "geometry");
+    g->g->cache_probes = on != 0;
+    if (!on) {
+      g->g->probes.valid = false;
+      g->g->probes.E1.release();
+      g->g->probes.E2.release();
+    }
+  });
+}
+int64_t fsa_launch_count(void) { return launch_counter().load(); }
+
 int fsa_model_assemble(fsa_ctx* ctx, const double* coords, int64_t n, int d, const double* inducing, int64_t m,
                        const fsa_params* params, fsa_model** out) {
   return guard([&] {
@@ -448,7 +477,6 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
   return guard([&] {
     need(md, "model");
     need(p, "preconditioner");
-    need(y, "y");
     need(out, "out");
     require(pcols == 0 || X != nullptr, "nll: shape mismatch");
     require(cv_mode >= 0 && cv_mode <= 2, "unknown control-variate mode");

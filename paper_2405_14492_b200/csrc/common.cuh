@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -28,7 +29,17 @@ inline void require(bool c, const char* msg) {
                              __FILE__ + ":" + std::to_string(__LINE__));                     \
   } while (0)
 
-#define FSA_LAUNCH_CHECK() FSA_CUDA(cudaGetLastError())
+// number of kernels this library has launched (every launch site ends with FSA_LAUNCH_CHECK)
+inline std::atomic<long>& launch_counter() {
+  static std::atomic<long> c{0};
+  return c;
+}
+
+#define FSA_LAUNCH_CHECK()                        \
+  do {                                            \
+    ::fsa::launch_counter().fetch_add(1);         \
+    FSA_CUDA(cudaGetLastError());                 \
+  } while (0)
 
 inline long round_up(long x, long a) { return (x + a - 1) / a * a; }
 inline long cdiv(long x, long a) { return (x + a - 1) / a; }

@@ -396,6 +396,12 @@ void FitcPrecond::solve(const double* R, double* Z, long tp) {
 void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long tp) {
   const long m = md->m, n = md->n, mp = md->m_pad, np = md->n_pad;
   cudaStream_t s = md->ctx->stream;
+  Geometry::ProbeCache& pc = md->geo->probes;
+  if (md->geo->cache_probes && pc.valid && pc.seed == seed && pc.L == L && pc.tp == tp && pc.m == m) {
+    KTimer t(md->ctx, "probe_expand", 2.0 * mp * np * tp);
+    gemm_expand_probe(md->U.get(), mp, np, mp, pc.E1.get(), tp, tp, Z, tp, md->sqrtD.get(), pc.E2.get(), s);
+    return;
+  }
   static PinnedBuf e1h, e2h;  // host staging (one host thread per context)
   e1h.ensure(static_cast<size_t>(mp * tp));
   e2h.ensure(static_cast<size_t>(n * L));
@@ -420,6 +426,15 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
     gemm_expand_probe(md->U.get(), mp, np, mp, E1.get(), tp, tp, Z, tp, md->sqrtD.get(), E2.get(), s);
   }
   FSA_CUDA(cudaStreamSynchronize(s));
+  if (md->geo->cache_probes) {
+    pc.valid = true;
+    pc.seed = seed;
+    pc.L = L;
+    pc.tp = tp;
+    pc.m = m;
+    pc.E1 = std::move(E1);
+    pc.E2 = std::move(E2);
+  }
 }
 
 // exact Tr(P^{-1} dP_k) in U-form:
@@ -711,6 +726,13 @@ static double dotv(const double* a, const double* b, long n) {
 NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* Xc, long p, int L,
                              unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad) {
   require(L > 0, "nll: need at least one probe");
+  const bool resident = y == nullptr;
+  if (resident) {  // response kept in HBM by fsa_geometry_set_response
+    require(md->geo->resp_p >= 0, "nll: no resident response on the geometry");
+    p = md->geo->resp_p;
+    y = md->geo->resp_host.data();
+    Xc = p > 0 ? md->geo->resp_host.data() + md->n : nullptr;
+  }
   Context* ctx = md->ctx;
   cudaStream_t s = ctx->stream;
   const long n = md->n, np = md->n_pad, mp = md->m_pad;
@@ -720,7 +742,9 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   FSA_CUDA(cudaEventRecord(e0, s));
   DBuf<double> B(static_cast<size_t>(np * tp)), Xs(static_cast<size_t>(np * tp));
   P.sample_probes(L, seed, B.get(), tp);  // columns [0, L)
-  {
+  if (resident) {
+    pack_cols(md->geo->resp_dev.get(), n, 1 + p, md->geo->pts.perm_d.get(), np, tp, L, B.get(), s);
+  } else {
     std::vector<double> yx(static_cast<size_t>(n * (1 + p)));
     std::copy(y, y + n, yx.begin());
     if (p > 0) std::copy(Xc, Xc + n * p, yx.begin() + n);

@@ -75,6 +75,19 @@ struct Geometry {
   Csr pat;
   double gamma = 0.0;
   std::vector<double> coords_host;  // original order, n x d column-major
+  // Fit-loop residency: the response [y | X] and the FITC probe
+  // draws e1/e2 are parameter independent, so a fit keeps them in HBM.
+  std::vector<double> resp_host;    // n x (1 + p), original order
+  DBuf<double> resp_dev;            // same on the device
+  long resp_p = -1;
+  bool cache_probes = false;
+  struct ProbeCache {
+    bool valid = false;
+    unsigned long long seed = 0;
+    int L = 0;
+    long tp = 0, m = 0;
+    DBuf<double> E1, E2;
+  } probes;
 };
 std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long n, int d, double gamma);
 

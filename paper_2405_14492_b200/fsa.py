@@ -85,6 +85,9 @@ _SIGS = {
     "fsa_geometry_info": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
     "fsa_geometry_pattern": (C.c_int, [_vp, _lp, _ip, _dp]),
     "fsa_geometry_permutation": (C.c_int, [_vp, _ip]),
+    "fsa_geometry_set_response": (C.c_int, [_vp, _dp, _vp, _i64]),
+    "fsa_geometry_cache_probes": (C.c_int, [_vp, C.c_int]),
+    "fsa_launch_count": (C.c_int64, []),
     "fsa_model_assemble": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _i64, C.POINTER(Params), C.POINTER(_vp)]),
     "fsa_model_assemble_geo": (C.c_int, [_vp, _dp, _i64, C.POINTER(Params), C.POINTER(_vp)]),
     "fsa_model_destroy": (None, [_vp]),
@@ -104,7 +107,7 @@ _SIGS = {
     "fsa_pcg_solve_multi": (C.c_int, [_vp, _vp, C.c_int, _dp, _i64, C.POINTER(CgOptions), _dp, _ip, _ip, _dp, _dp,
                                       C.POINTER(C.c_int)]),
     "fsa_tridiag_log_quadrature": (C.c_int, [_dp, _dp, _i64, C.POINTER(C.c_double)]),
-    "fsa_iterative_nll_grad": (C.c_int, [_vp, _vp, _dp, _vp, _i64, C.c_int, _u64, C.POINTER(CgOptions), C.c_int,
+    "fsa_iterative_nll_grad": (C.c_int, [_vp, _vp, _vp, _vp, _i64, C.c_int, _u64, C.POINTER(CgOptions), C.c_int,
                                          C.c_int, C.POINTER(NllResult), _vp]),
     "fsa_pred_setup": (C.c_int, [_vp, _dp, _i64, C.POINTER(_vp)]),
     "fsa_pred_destroy": (None, [_vp]),
@@ -199,6 +202,11 @@ def probe_gaussian(seed, index, n1, n2):
     return e1[:n1], e2[:n2]
 
 
+def launch_count() -> int:
+    """Kernels launched by libfsa_b200.so so far in this process."""
+    return int(lib().fsa_launch_count())
+
+
 def tridiag_log_quadrature(diag, off):
     d = _F(diag)
     o = _F(off) if len(off) else _F(np.zeros(1))
@@ -290,6 +298,16 @@ class Geometry:
         p = np.zeros(self.n, np.int32)
         _check(lib().fsa_geometry_permutation(self.h, p))
         return p
+
+    def set_response(self, y, X=None):
+        """Keep [y | X] resident in HBM; iterative_nll_grad(..., y=None) then uses it."""
+        self._y = _F(y)
+        p = 0 if X is None else np.asarray(X).reshape(self.n, -1).shape[1]
+        self._X = None if p == 0 else _F(np.asarray(X).reshape(self.n, p))
+        _check(lib().fsa_geometry_set_response(self.h, self._y, None if p == 0 else self._X.ctypes.data, p))
+
+    def cache_probes(self, on=True):
+        _check(lib().fsa_geometry_cache_probes(self.h, 1 if on else 0))
 
 
 class FsaModel:
@@ -427,13 +445,17 @@ def pcg_solve_multi(model: FsaModel, P: Preconditioner, B, tol=1e-3, max_iter=10
 def iterative_nll_grad(model: FsaModel, P: Preconditioner, y, X=None, num_probes=50, seed=0, tol=1e-3,
                        max_iter=1000, cv="optimal", want_grad=True):
     """iterative_nll_grad (estimation.cpp:178-227)."""
-    y = _F(y)
+    y = None if y is None else _F(y)
     p = 0 if X is None else np.asarray(X).reshape(model.n, -1).shape[1]
     Xf = None if p == 0 else _F(np.asarray(X).reshape(model.n, p))
+    if y is None:  # resident response (Geometry.set_response)
+        p = model.geometry._X.shape[1] if getattr(model.geometry, "_X", None) is not None else 0
     beta = _F(np.zeros(max(p, 1)))
     res = NllResult()
     cg = _cg(tol, max_iter)
-    _check(lib().fsa_iterative_nll_grad(model.h, P.h, y, None if Xf is None else Xf.ctypes.data, p, num_probes, seed,
+    beta = _F(np.zeros(max(p, 1)))
+    _check(lib().fsa_iterative_nll_grad(model.h, P.h, None if y is None else y.ctypes.data,
+                                        None if Xf is None else Xf.ctypes.data, p, num_probes, seed,
                                         C.byref(cg), CV_CODE[cv], 1 if want_grad else 0, C.byref(res),
                                         beta.ctypes.data))
     return {"nll": res.nll, "grad": np.array(res.grad[:]), "logdet": res.logdet, "cg_iterations": res.cg_iterations,

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "fsa_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int|void|double)\s+(fsa_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|int|void|double)\s+(fsa_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
