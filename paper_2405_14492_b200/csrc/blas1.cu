@@ -9,45 +9,6 @@ namespace fsa {
 
 namespace {
 
-constexpr int kDotBlocks = 2 * kNumSMs;
-constexpr int kDotThreads = 256;
-
-// partial[b][c] for columns c in [0, t); rows split into kDotBlocks contiguous chunks
-template <bool W>
-__global__ void __launch_bounds__(kDotThreads) k_coldot_partial(const double* __restrict__ A,
-                                                               const double* __restrict__ B,
-                                                               const double* __restrict__ w, long n, long ld, long t,
-                                                               double* __restrict__ partial) {
-  __shared__ double red[kDotThreads];
-  const long chunk = (n + gridDim.x - 1) / gridDim.x;
-  const long r0 = static_cast<long>(blockIdx.x) * chunk;
-  const long r1 = r0 + chunk < n ? r0 + chunk : n;
-  const int tid = threadIdx.x;
-  const int cl = tid % 64, rl = tid / 64;  // 64 columns x 4 row lanes
-  for (long c0 = 0; c0 < t; c0 += 64) {
-    const long c = c0 + cl;
-    double s = 0.0;
-    if (c < t)
-      for (long r = r0 + rl; r < r1; r += 4) {
-        const double v = A[r * ld + c] * B[r * ld + c];
-        s += W ? v * w[r] : v;
-      }
-    red[tid] = s;
-    __syncthreads();
-    if (rl == 0 && c < t)
-      partial[static_cast<long>(blockIdx.x) * t + c] = (red[cl] + red[cl + 64]) + (red[cl + 128] + red[cl + 192]);
-    __syncthreads();
-  }
-}
-
-__global__ void k_coldot_final(const double* __restrict__ partial, int nb, long t, double* __restrict__ out) {
-  const long c = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= t) return;
-  double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += partial[static_cast<long>(b) * t + c];
-  out[c] = s;
-}
-
 __global__ void k_pack(const double* __restrict__ in, long n, long k, const int* __restrict__ perm, long n_pad,
                        long tp, long col0, double* __restrict__ out) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -238,26 +199,141 @@ __global__ void k_axpby(double* __restrict__ Y, const double* __restrict__ X, do
 
 inline unsigned nblk(long total, int th = 256) { return static_cast<unsigned>(cdiv(total, th)); }
 
+// Warp-per-row column dots (fixed grid -> fixed reduction order). Columns
+// [c0, c0 + 64*NCH) of row-major blocks; optional row weight w.
+// Mode 0: plain dot A.B.  Mode 1: X += alpha H, R -= alpha V (active columns), dot R.R.
+template <int NCH, int MODE>
+__global__ void __launch_bounds__(256) k_rowdot_cols(const double* __restrict__ A, const double* __restrict__ B,
+                                                    const double* __restrict__ w, long n, long ld, long t, long c0,
+                                                    double* __restrict__ X, double* __restrict__ R,
+                                                    const double* __restrict__ alpha, double* __restrict__ partial,
+                                                    long ldp) {
+  __shared__ double red[8][64 * NCH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double d0[NCH], d1[NCH], al0[NCH], al1[NCH];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    d0[q] = d1[q] = 0.0;
+    if (MODE == 1) {
+      const long c = c0 + q * 64 + 2 * lane;
+      al0[q] = c < t ? alpha[c] : 0.0;
+      al1[q] = c + 1 < t ? alpha[c + 1] : 0.0;
+    }
+  }
+  for (long r = static_cast<long>(blockIdx.x) * 8 + warp; r < n; r += 8L * gridDim.x) {
+    const double wr = w != nullptr ? w[r] : 1.0;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const long c = c0 + q * 64 + 2 * lane;
+      if (c >= t) break;
+      if (MODE == 0) {
+        const double2 a = *reinterpret_cast<const double2*>(A + r * ld + c);
+        const double2 b = *reinterpret_cast<const double2*>(B + r * ld + c);
+        d0[q] = fma(a.x * b.x, wr, d0[q]);
+        d1[q] = fma(a.y * b.y, wr, d1[q]);
+      } else {
+        // A = H, B = V
+        double2 x = *reinterpret_cast<const double2*>(X + r * ld + c);
+        double2 rr = *reinterpret_cast<const double2*>(R + r * ld + c);
+        if (al0[q] != 0.0 || al1[q] != 0.0) {
+          const double2 h = *reinterpret_cast<const double2*>(A + r * ld + c);
+          const double2 v = *reinterpret_cast<const double2*>(B + r * ld + c);
+          x.x += al0[q] * h.x;
+          x.y += al1[q] * h.y;
+          rr.x -= al0[q] * v.x;
+          rr.y -= al1[q] * v.y;
+          *reinterpret_cast<double2*>(X + r * ld + c) = x;
+          *reinterpret_cast<double2*>(R + r * ld + c) = rr;
+        }
+        d0[q] = fma(rr.x, rr.x, d0[q]);
+        d1[q] = fma(rr.y, rr.y, d1[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    red[warp][q * 64 + 2 * lane] = d0[q];
+    red[warp][q * 64 + 2 * lane + 1] = d1[q];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 64 * NCH; c += blockDim.x) {
+    if (c0 + c >= t) break;
+    double sacc = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) sacc += red[ww][c];
+    partial[static_cast<long>(blockIdx.x) * ldp + c0 + c] = sacc;
+  }
+}
+
+__global__ void k_colsum(const double* __restrict__ partial, long nb, long ldp, double* __restrict__ out) {
+  const long c = blockIdx.x;
+  const int lane = threadIdx.x;
+  double sacc = 0.0;
+  for (long b = lane; b < nb; b += 32) sacc += partial[b * ldp + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if (lane == 0) out[c] = sacc;
+}
+
+long rowdot_blocks(long n) {
+  const long b = cdiv(n, 8);
+  return b < 4 * kNumSMs ? (b < 1 ? 1 : b) : 4 * kNumSMs;
+}
+
+template <int MODE>
+void rowdot_launch(const double* A, const double* B, const double* w, long n, long ld, long t, double* X, double* R,
+                   const double* alpha, double* out, double* partial, cudaStream_t s) {
+  if (t == 0) return;
+  const long nb = rowdot_blocks(n);
+  const unsigned g = static_cast<unsigned>(nb);
+  for (long c0 = 0; c0 < t; c0 += 256) {
+    const long rem = t - c0;
+    if (rem <= 64)
+      k_rowdot_cols<1, MODE><<<g, 256, 0, s>>>(A, B, w, n, ld, t, c0, X, R, alpha, partial, t);
+    else if (rem <= 128)
+      k_rowdot_cols<2, MODE><<<g, 256, 0, s>>>(A, B, w, n, ld, t, c0, X, R, alpha, partial, t);
+    else
+      k_rowdot_cols<4, MODE><<<g, 256, 0, s>>>(A, B, w, n, ld, t, c0, X, R, alpha, partial, t);
+    FSA_LAUNCH_CHECK();
+  }
+  k_colsum<<<static_cast<unsigned>(t), 32, 0, s>>>(partial, nb, t, out);
+  FSA_LAUNCH_CHECK();
+}
+
+__global__ void k_update_uh(double* __restrict__ UH, const double* __restrict__ W, const int* __restrict__ active,
+                            const double* __restrict__ beta, long len, long tp, long k, int init) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= len) return;
+  const long j = idx % tp;
+  if (init) {
+    UH[idx] = (j < k && active[j]) ? W[idx] : 0.0;
+  } else if (j < k && active[j]) {
+    UH[idx] = W[idx] + beta[j] * UH[idx];
+  }
+}
+
 }  // namespace
 
-size_t coldot_scratch(long n, long t) {
-  (void)n;
-  return static_cast<size_t>(kDotBlocks) * static_cast<size_t>(t);
-}
+size_t coldot_scratch(long n, long t) { return static_cast<size_t>(rowdot_blocks(n)) * static_cast<size_t>(t); }
 
 void launch_coldot(const double* A, const double* B, long n, long ld, long t, double* out, double* scratch,
                    cudaStream_t s) {
-  k_coldot_partial<false><<<kDotBlocks, kDotThreads, 0, s>>>(A, B, nullptr, n, ld, t, scratch);
-  FSA_LAUNCH_CHECK();
-  k_coldot_final<<<nblk(t, 128), 128, 0, s>>>(scratch, kDotBlocks, t, out);
-  FSA_LAUNCH_CHECK();
+  rowdot_launch<0>(A, B, nullptr, n, ld, t, nullptr, nullptr, nullptr, out, scratch, s);
 }
 
 void launch_coldot_weighted(const double* A, const double* B, const double* w, long n, long ld, long t,
                             double* out, double* scratch, cudaStream_t s) {
-  k_coldot_partial<true><<<kDotBlocks, kDotThreads, 0, s>>>(A, B, w, n, ld, t, scratch);
-  FSA_LAUNCH_CHECK();
-  k_coldot_final<<<nblk(t, 128), 128, 0, s>>>(scratch, kDotBlocks, t, out);
+  rowdot_launch<0>(A, B, w, n, ld, t, nullptr, nullptr, nullptr, out, scratch, s);
+}
+
+void update_xr_dot(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
+                   long k, double* rr, double* scratch, cudaStream_t s) {
+  rowdot_launch<1>(H, V, nullptr, n, tp, k, X, R, alpha, rr, scratch, s);
+}
+
+void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
+               bool init, cudaStream_t s) {
+  k_update_uh<<<nblk(mpad * tp), 256, 0, s>>>(UH, W, active, beta, mpad * tp, tp, k, init ? 1 : 0);
   FSA_LAUNCH_CHECK();
 }
 

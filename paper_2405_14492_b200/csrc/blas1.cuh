@@ -53,6 +53,12 @@ void cg_beta(const double* rzn, long k, const CgState& st, cudaStream_t s);
 void cg_count(long k, const CgState& st, cudaStream_t s);
 void update_xr(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp, long k,
                cudaStream_t s);
+// fused: X += alpha H, R -= alpha V (columns with alpha != 0) and rr[c] = |R_c|^2 (c < k)
+void update_xr_dot(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
+                   long k, double* rr, double* scratch, cudaStream_t s);
+// m-space recurrence of U H for the active columns: UH = W + beta UH (init: UH = active ? W : 0)
+void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
+               bool init, cudaStream_t s);
 void update_h(double* H, const double* Z, const int* active, const double* beta, long n, long tp, long k,
               cudaStream_t s);
 void init_h(double* H, const double* Z, const int* active, long n, long tp, long k, cudaStream_t s);

@@ -50,6 +50,14 @@ inline long pad_cols(long t) { return t <= 72 ? round_up(t < 1 ? 1 : t, 8) : rou
 constexpr int kNumSMs = 148;
 
 // ---- device buffers ------------------------------------------------------------
+// Stream-ordered allocation from the device's default memory pool (release
+// threshold raised by Context), so per-evaluation temporaries neither hit
+// cudaMalloc nor serialise the stream on cudaFree.
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -68,10 +76,10 @@ struct DBuf {
     if (count == n && p) return;
     release();
     n = count;
-    if (count) FSA_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) FSA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, alloc_stream());
     p = nullptr;
     n = 0;
   }

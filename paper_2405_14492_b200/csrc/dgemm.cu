@@ -1,6 +1,8 @@
 // Launchers for the DMMA fp64 GEMMs declared in dgemm.cuh.
 #include "dgemm.cuh"
 
+#include <cstdlib>
+
 namespace fsa {
 
 namespace {
@@ -8,9 +10,29 @@ namespace {
 // expand: 4 warps x 32 rows (BM = 128), all N columns of the tile per warp.
 template <int NT>
 using ExpandCfg = GemmCfg<NT, 4, 4, false, 16, 3>;
+// expand, 8 warps x 16 rows (BM = 128): twice the warps per SM at the same smem
+template <int NT>
+using ExpandCfg8 = GemmCfg<NT, 2, 8, false, 16, 3>;
 // reduce: 4 warps x 16 rows (BM = 64), A is [k][m].
 template <int NT>
 using ReduceCfg = GemmCfg<NT, 2, 4, true, 16, 3>;
+// reduce, 8 warps x 16 rows (BM = 128)
+template <int NT>
+using ReduceCfg8 = GemmCfg<NT, 2, 8, true, 16, 3>;
+
+// tile variant knobs (FSA_GEMM_EXPAND / FSA_GEMM_REDUCE = 0 | 1), read once
+int knob(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+int expand_variant() {
+  static const int v = knob("FSA_GEMM_EXPAND", 0);  // 4 warps x 32 rows: measured faster (r01)
+  return v;
+}
+int reduce_variant() {
+  static const int v = knob("FSA_GEMM_REDUCE", 1);  // 8 warps: measured faster (r01)
+  return v;
+}
 
 template <class Cfg, class Epi>
 void launch(const double* A, long lda, const double* B, long ldb, const double* scale, long K, long kchunk,
@@ -52,17 +74,21 @@ void expand(const double* M, long ldm, long rows, long K, const double* W, long 
   if (rows == 0) return;
   const int nt = tile_nt(N);
   dim3 grid(static_cast<unsigned>(rows / 128), static_cast<unsigned>(N / (nt * 8)), 1);
-  dispatch_nt<ExpandCfg>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
+  if (expand_variant() == 1)
+    dispatch_nt<ExpandCfg8>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
+  else
+    dispatch_nt<ExpandCfg>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
 }
 
 struct ReducePlan {
-  int nt;
+  int nt, bm;
   long tiles, splits, kchunk;
 };
 ReducePlan plan_reduce(long Mr, long N, long K) {
   ReducePlan p;
   p.nt = tile_nt(N);
-  p.tiles = (Mr / 64) * (N / (p.nt * 8));
+  p.bm = (reduce_variant() == 1 && Mr % 128 == 0) ? 128 : 64;
+  p.tiles = (Mr / p.bm) * (N / (p.nt * 8));
   const long kblocks = K / 16;
   long splits = cdiv(2 * kNumSMs, p.tiles);
   splits = splits < 1 ? 1 : splits;
@@ -100,7 +126,35 @@ void gemm_expand_probe(const double* M, long ldm, long rows, long K, const doubl
 }
 void gemm_expand_woodbury(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
                           double* Z, const double* R, long ld, const double* Dinv, cudaStream_t s) {
-  expand(M, ldm, rows, K, W, ldw, N, EpiWoodbury{Z, R, ld, Dinv}, s);
+  expand(M, ldm, rows, K, W, ldw, N, EpiWoodbury{nullptr, 0, Z, R, ld, Dinv}, s);
+}
+void gemm_expand_woodbury_dot(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                              double* Z, const double* R, long ld, const double* Dinv, double* rz, double* partial,
+                              cudaStream_t s) {
+  expand(M, ldm, rows, K, W, ldw, N, EpiWoodburyDot{partial, N, Z, R, ld, Dinv}, s);
+  colsum_partials(partial, rows / 128, N, N, rz, s);
+}
+
+void gemm_expand_woodbury_keep(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                               double* Z, double* Lw, const double* R, long ld, const double* Dinv, double* rz,
+                               double* partial, cudaStream_t s) {
+  expand(M, ldm, rows, K, W, ldw, N, EpiWoodburyKeep{partial, N, Z, Lw, R, ld, Dinv}, s);
+  colsum_partials(partial, rows / 128, N, N, rz, s);
+}
+
+__global__ void k_colsum_partials(const double* __restrict__ partial, long nb, long ldp, double* __restrict__ out) {
+  const long c = blockIdx.x;
+  const int lane = threadIdx.x;
+  double sacc = 0.0;
+  for (long b = lane; b < nb; b += 32) sacc += partial[b * ldp + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if (lane == 0) out[c] = sacc;
+}
+void colsum_partials(const double* partial, long nb, long ldp, long t, double* out, cudaStream_t s) {
+  if (t == 0) return;
+  k_colsum_partials<<<static_cast<unsigned>(t), 32, 0, s>>>(partial, nb, ldp, out);
+  FSA_LAUNCH_CHECK();
 }
 
 void gemm_km(const double* A, long lda, long Mr, long K, const double* B, long ldb, long N, double* Y, long ldy,
@@ -126,9 +180,12 @@ void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, lo
   require(Mr % 64 == 0 && K % 16 == 0 && N == pad_cols(N), "gemm_reduce: unpadded shape");
   if (Mr == 0 || N == 0) return;
   const ReducePlan p = plan_reduce(Mr, N, K);
-  dim3 grid(static_cast<unsigned>(Mr / 64), static_cast<unsigned>(N / (p.nt * 8)),
+  dim3 grid(static_cast<unsigned>(Mr / p.bm), static_cast<unsigned>(N / (p.nt * 8)),
             static_cast<unsigned>(p.splits));
-  dispatch_nt<ReduceCfg>(p.nt, M, ldm, V, ldv, scale, K, p.kchunk, grid, EpiPartial{scratch, Mr, N}, s);
+  if (p.bm == 128)
+    dispatch_nt<ReduceCfg8>(p.nt, M, ldm, V, ldv, scale, K, p.kchunk, grid, EpiPartial{scratch, Mr, N}, s);
+  else
+    dispatch_nt<ReduceCfg>(p.nt, M, ldm, V, ldv, scale, K, p.kchunk, grid, EpiPartial{scratch, Mr, N}, s);
   const long total = Mr * N;
   k_splitk_reduce<<<static_cast<unsigned>(cdiv(total, 256)), 256, 0, s>>>(scratch, p.splits, Mr, N, out, ldo,
                                                                          alpha, beta);

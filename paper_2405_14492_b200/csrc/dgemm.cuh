@@ -135,66 +135,145 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   }
   cp_async_wait<0>();
 
+  double dacc[NT][2];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) dacc[j][0] = dacc[j][1] = 0.0;
 #pragma unroll
   for (int i = 0; i < WMT; ++i) {
     const long row = m0 + wm0 + i * 8 + g;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const long col = n0 + j * 8 + 2 * tig;
-      epi(row, col, acc[i][j][0], acc[i][j][1]);
+      const double2 c = epi(row, col, acc[i][j][0], acc[i][j][1]);
+      if constexpr (Epi::kDot) {
+        dacc[j][0] += c.x;
+        dacc[j][1] += c.y;
+      }
+    }
+  }
+  if constexpr (Epi::kDot) {
+    // per-column partial of the epilogue's dot contributions over this tile's rows:
+    // lanes sharing tig (xor 4, 8, 16), then warps in order -> partial[blockIdx.x][col]
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = dacc[j][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        dacc[j][e] = v;
+      }
+    __syncthreads();
+    double* red = smem;  // [WARPS][BN]
+    if (g == 0)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        red[warp * BN + j * 8 + 2 * tig] = dacc[j][0];
+        red[warp * BN + j * 8 + 2 * tig + 1] = dacc[j][1];
+      }
+    __syncthreads();
+    for (int c = tid; c < BN; c += THREADS) {
+      double sacc = 0.0;
+      for (int w = 0; w < Cfg::WARPS; ++w) sacc += red[w * BN + c];
+      epi.partial[static_cast<long>(blockIdx.x) * epi.ldp + n0 + c] = sacc;
     }
   }
 }
 
 // ---- epilogues -------------------------------------------------------------------
-struct EpiStore {  // Y = alpha * v
+struct EpiNoDot {
+  static constexpr bool kDot = false;
+  double* partial = nullptr;
+  long ldp = 0;
+};
+struct EpiStore : EpiNoDot {  // Y = alpha * v
   double* Y;
   long ldy;
   double alpha;
-  __device__ void operator()(long r, long c, double v0, double v1) const {
+  EpiStore(double* y, long l, double a) : Y(y), ldy(l), alpha(a) {}
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
     double2 o = make_double2(alpha * v0, alpha * v1);
     *reinterpret_cast<double2*>(Y + r * ldy + c) = o;
+    return make_double2(0.0, 0.0);
   }
 };
-struct EpiAxpby {  // Y = alpha * v + beta * Y
+struct EpiAxpby : EpiNoDot {  // Y = alpha * v + beta * Y
   double* Y;
   long ldy;
   double alpha, beta;
-  __device__ void operator()(long r, long c, double v0, double v1) const {
+  EpiAxpby(double* y, long l, double a, double b) : Y(y), ldy(l), alpha(a), beta(b) {}
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
     double2* p = reinterpret_cast<double2*>(Y + r * ldy + c);
     double2 o = *p;
     o.x = alpha * v0 + beta * o.x;
     o.y = alpha * v1 + beta * o.y;
     *p = o;
+    return make_double2(0.0, 0.0);
   }
 };
-struct EpiPartial {  // split-K partial tile: W[z][r][c]
+struct EpiPartial : EpiNoDot {  // split-K partial tile: W[z][r][c]
   double* W;
   long M, N;
-  __device__ void operator()(long r, long c, double v0, double v1) const {
+  EpiPartial(double* w, long m, long n) : W(w), M(m), N(n) {}
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
     *reinterpret_cast<double2*>(W + (static_cast<long>(blockIdx.z) * M + r) * N + c) = make_double2(v0, v1);
+    return make_double2(0.0, 0.0);
   }
 };
-struct EpiProbe {  // z = U^T e1 + sqrt(D) e2  (FITC sample, preconditioners.cpp:69-73)
+struct EpiProbe : EpiNoDot {  // z = U^T e1 + sqrt(D) e2  (FITC sample, preconditioners.cpp:69-73)
   double* Y;
   long ld;
   const double* sqrtD;
   const double* E2;
-  __device__ void operator()(long r, long c, double v0, double v1) const {
+  EpiProbe(double* y, long l, const double* s, const double* e) : Y(y), ld(l), sqrtD(s), E2(e) {}
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
     const double s = sqrtD[r];
     const double2 e = *reinterpret_cast<const double2*>(E2 + r * ld + c);
     *reinterpret_cast<double2*>(Y + r * ld + c) = make_double2(v0 + s * e.x, v1 + s * e.y);
+    return make_double2(0.0, 0.0);
   }
 };
-struct EpiWoodbury {  // Z = D^{-1} (R - U^T w)  (Woodbury tail of P^{-1} R)
+// Z = D^{-1} (R - U^T w)  (Woodbury tail of P^{-1} R); with kDot also the
+// per-CTA partial of r . z per column (the PCG's rz, krylov.cpp:84)
+template <bool DOT>
+struct EpiWoodburyT {
+  static constexpr bool kDot = DOT;
+  double* partial;
+  long ldp;
   double* Z;
   const double* R;
   long ld;
   const double* Dinv;
-  __device__ void operator()(long r, long c, double v0, double v1) const {
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
     const double di = Dinv[r];
     const double2 x = *reinterpret_cast<const double2*>(R + r * ld + c);
-    *reinterpret_cast<double2*>(Z + r * ld + c) = make_double2((x.x - v0) * di, (x.y - v1) * di);
+    const double z0 = (x.x - v0) * di, z1 = (x.y - v1) * di;
+    *reinterpret_cast<double2*>(Z + r * ld + c) = make_double2(z0, z1);
+    return make_double2(x.x * z0, x.y * z1);
+  }
+};
+using EpiWoodbury = EpiWoodburyT<false>;
+using EpiWoodburyDot = EpiWoodburyT<true>;
+
+// Woodbury tail that also keeps Lw = U^T w (the low-rank part of Sigma Z, used by
+// the PCG's m-space recurrence for Sigma H) and the per-CTA r . z partials
+struct EpiWoodburyKeep {
+  static constexpr bool kDot = true;
+  double* partial;
+  long ldp;
+  double* Z;
+  double* Lw;
+  const double* R;
+  long ld;
+  const double* Dinv;
+  __device__ double2 operator()(long r, long c, double v0, double v1) const {
+    const double di = Dinv[r];
+    const double2 x = *reinterpret_cast<const double2*>(R + r * ld + c);
+    const double z0 = (x.x - v0) * di, z1 = (x.y - v1) * di;
+    *reinterpret_cast<double2*>(Z + r * ld + c) = make_double2(z0, z1);
+    *reinterpret_cast<double2*>(Lw + r * ld + c) = make_double2(v0, v1);
+    return make_double2(x.x * z0, x.y * z1);
   }
 };
 
@@ -209,6 +288,17 @@ void gemm_expand_probe(const double* M, long ldm, long rows, long K, const doubl
                        double* Y, long ld, const double* sqrtD, const double* E2, cudaStream_t s);
 void gemm_expand_woodbury(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
                           double* Z, const double* R, long ld, const double* Dinv, cudaStream_t s);
+// same, plus rz[c] = sum_rows R[r][c] Z[r][c] for c < N (deterministic two-level reduction);
+// partial must hold (rows / 128) * N doubles
+void gemm_expand_woodbury_dot(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                              double* Z, const double* R, long ld, const double* Dinv, double* rz, double* partial,
+                              cudaStream_t s);
+// same with Lw = U^T w kept (n_pad x N, ld)
+void gemm_expand_woodbury_keep(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
+                               double* Z, double* Lw, const double* R, long ld, const double* Dinv, double* rz,
+                               double* partial, cudaStream_t s);
+// out[c] = sum_{b < nb} partial[b * ldp + c], c < t (fixed order)
+void colsum_partials(const double* partial, long nb, long ldp, long t, double* out, cudaStream_t s);
 
 // out[Mr x N] (row-major, ldo) = alpha * sum_{i<K} M[i*ldm + r] s_i V[i*ldv + n] + beta * out
 // Mr % 64 == 0, K % 16 == 0. Deterministic split-K. `scratch` must hold

@@ -14,6 +14,7 @@
 
 namespace fsa {
 
+
 // ---- RNG (types.h:104-129; identical libstdc++ distributions) ------------------------------
 unsigned long long splitmix64(unsigned long long x) {
   x += 0x9e3779b97f4a7c15ULL;
@@ -45,11 +46,19 @@ void probe_rademacher(unsigned long long seed, unsigned long long i, long n, dou
 Context::Context(int dev) : device(dev) {
   FSA_CUDA(cudaSetDevice(dev));
   FSA_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  alloc_stream() = stream;
+  cudaMemPool_t pool = nullptr;
+  FSA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  unsigned long long keep = ~0ULL;  // keep freed blocks for reuse across evaluations
+  FSA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   FSA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags), 4 * sizeof(int), cudaHostAllocMapped));
   FSA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_flags_dev), host_flags, 0));
 }
 Context::~Context() {
   cudaStreamSynchronize(stream);
+  cgw.reset();
+  cudaStreamSynchronize(stream);
+  if (alloc_stream() == stream) alloc_stream() = nullptr;  // later frees go to the legacy stream
   for (auto& r : pending) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -107,6 +116,7 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
   const CellGrid grid = make_grid(coords, n, d, gamma, nullptr, 0);
   sort_points(coords, n, d, grid, round_up(n, 128), g->pts, ctx->stream);
   build_pattern(g->pts, g->pts, gamma, true, g->pat, ctx->stream);
+  build_row_blocks(g->pat, ctx->stream);
   ctx->sync();
   return g;
 }
@@ -131,7 +141,7 @@ double* Model::mt_buf(int which, long tp) {
 void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
   const size_t need = gemm_reduce_scratch(m_pad, tp, n_pad);
   if (red_scratch.n < need) red_scratch.alloc(need);
-  KTimer t(ctx, "lowrank_project", 2.0 * m_pad * n_pad * tp);
+  KTimer t(ctx, "lowrank_project", 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp));
   gemm_reduce(M, m_pad, m_pad, n_pad, V, tp, tp, scale, out, tp, 1.0, 0.0, red_scratch.get(), ctx->stream);
 }
 
@@ -239,8 +249,12 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
 }
 
 void Model::sigma_s_mat(const double* H, double* V, long tp, double alpha, double beta) {
-  KTimer t(ctx, "spmm", 8.0 * (12.0 * geo->pat.nnz + 2.0 * n * tp));
-  launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta, ctx->stream);
+  KTimer t(ctx, "spmm", 12.0 * geo->pat.nnz + (beta == 0.0 ? 16.0 : 24.0) * n * (cols_hint > 0 ? cols_hint : tp));
+  if (tp <= 128 && geo->pat.nblk > 0)
+    spmm_staged(geo->pat, sval.get(), H, tp, V, tp, tp, alpha, beta, nullptr, nullptr, ctx->stream);
+  else
+    launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta,
+                ctx->stream);
 }
 
 // V = Sigma H = U^T (U H) + Sigma_s H   (fsa.cpp:65-68)
@@ -280,20 +294,6 @@ void Model::deriv_matmat(int which, const double* V, double* out, long tp) {
 }
 
 // ---- preconditioners ------------------------------------------------------------------------------
-struct PinnedBuf {
-  double* p = nullptr;
-  size_t n = 0;
-  void ensure(size_t count) {
-    if (count <= n) return;
-    if (p) cudaFreeHost(p);
-    FSA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(double)));
-    n = count;
-  }
-  ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
-  }
-};
-
 // upload a host column-major (original order) n x k block into columns [0, k) of Z
 static void upload_pack(Model* md, const double* host, long k, double* Z, long tp) {
   cudaStream_t s = md->ctx->stream;
@@ -402,7 +402,8 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
     gemm_expand_probe(md->U.get(), mp, np, mp, pc.E1.get(), tp, tp, Z, tp, md->sqrtD.get(), pc.E2.get(), s);
     return;
   }
-  static PinnedBuf e1h, e2h;  // host staging (one host thread per context)
+  PinnedBuf& e1h = md->ctx->pin1;  // host staging owned by the context
+  PinnedBuf& e2h = md->ctx->pin2;
   e1h.ensure(static_cast<size_t>(mp * tp));
   e2h.ensure(static_cast<size_t>(n * L));
   double* e1p = e1h.p;
@@ -511,30 +512,40 @@ int CgResult::max_iterations() const {
   return m;
 }
 
-namespace {
-struct CgWork {
-  DBuf<double> R, H, V, Z, dots, dbl;
-  DBuf<int> ints;
-  DBuf<double> tri;
-};
-}  // namespace
-
+// Lockstep PCG. With the FSA operator and the FITC preconditioner a sweep is
+//   V = U^T (U H) + Sigma_s H   [expand + fused SpMM/h.v]   alpha, tridiagonal
+//   X += alpha H, R -= alpha V  [fused with |R|^2]          convergence test
+//   S = U D^{-1} R, w = Q^{-1} S, Z = D^{-1}(R - U^T w)  [project, core, expand + r.z]
+//   H = Z + beta H, U H = w + beta U H   (U Z = Q^{-1} S = w exactly, so the
+//                                         projection of H is an m-space update)
+// i.e. one projection and two expansions over U per sweep instead of the
+// reference sequence's four dense passes (krylov.cpp:56-93, preconditioners.cpp:58-61).
 CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long k, long tp, double* X,
                          const CgOptions& opts) {
   require(opts.tol > 0.0 && opts.max_iter > 0, "cg: invalid options");
   require(k >= 1 && k <= tp, "cg: column count mismatch");
   Context* ctx = md->ctx;
   cudaStream_t s = ctx->stream;
-  const long np = md->n_pad, n = md->n;
+  const long np = md->n_pad, n = md->n, mp = md->m_pad;
   const int maxit = opts.max_iter;
   const size_t blk = static_cast<size_t>(np * tp);
-  static thread_local CgWork w;
+  FsaOp* fop = dynamic_cast<FsaOp*>(&A);
+  FitcPrecond* fitc = dynamic_cast<FitcPrecond*>(&P);
+  const bool fused = fop != nullptr && fitc != nullptr;
+  CgWork& w = *ctx->cgw;
   if (w.R.n < blk) {
     w.R.alloc(blk);
     w.H.alloc(blk);
     w.V.alloc(blk);
     w.Z.alloc(blk);
   }
+  if (fused && w.Lw.n < blk) {
+    w.Lw.alloc(blk);
+    w.Vlr.alloc(blk);
+  }
+  const size_t npart = std::max(static_cast<size_t>(std::max(np / 128, spmm_dot_blocks(n)) * tp),
+                                coldot_scratch(n, tp));
+  if (w.part.n < npart) w.part.alloc(npart);
   w.dots.alloc(static_cast<size_t>(4 * tp));
   w.dbl.alloc(static_cast<size_t>(6 * k));
   w.ints.alloc(static_cast<size_t>(3 * k + 1));
@@ -556,25 +567,47 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   double* rr = w.dots.get();
   double* hv = rr + tp;
   double* rz = rr + 2 * tp;
-  if (md->dot_scratch.n < coldot_scratch(np, tp)) md->dot_scratch.alloc(coldot_scratch(np, tp));
-  double* sc = md->dot_scratch.get();
+  double* part = w.part.get();
   FSA_CUDA(cudaMemsetAsync(st.err, 0, sizeof(int), s));
   FSA_CUDA(cudaMemsetAsync(st.tdiag, 0, sizeof(double) * 2 * k * maxit, s));
   FSA_CUDA(cudaMemcpyAsync(w.R.get(), B, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
   FSA_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * blk, s));
+  const double flops_mn = 2.0 * md->m * n * k;
+  md->cols_hint = k;
 
-  auto blas = [&](const char* nm) { return KTimer(ctx, nm); };
+  // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
+  auto precond = [&](double* rzout) {
+    if (fused) {
+      double* S = md->mt_buf(0, tp);
+      double* W = md->mt_buf(1, tp);
+      md->project(md->U.get(), w.R.get(), tp, S, md->Dinv.get());
+      {
+        KTimer t(ctx, "core_solve", 2.0 * md->m * md->m * k);
+        const size_t need = gemm_reduce_scratch(mp, tp, mp);
+        if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+        gemm_reduce(fitc->Qinv.get(), mp, mp, mp, S, tp, tp, nullptr, W, tp, 1.0, 0.0, md->red_scratch.get(), s);
+      }
+      KTimer t(ctx, "lowrank_expand", flops_mn);
+      gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
+                                md->Dinv.get(), rzout, part, s);
+    } else {
+      P.solve(w.R.get(), w.Z.get(), tp);
+      KTimer t(ctx, "cg_blas1");
+      launch_coldot(w.R.get(), w.Z.get(), n, tp, k, rzout, part, s);
+    }
+  };
+
   {
-    auto t = blas("cg_blas1");
-    launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, sc, s);
+    KTimer t(ctx, "cg_blas1");
+    launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, part, s);
     cg_start(rr, k, opts.tol, st, s);
   }
-  P.solve(w.R.get(), w.Z.get(), tp);
+  precond(rz);
   {
-    auto t = blas("cg_blas1");
-    launch_coldot(w.R.get(), w.Z.get(), n, tp, k, rz, sc, s);
+    KTimer t(ctx, "cg_blas1");
     cg_start_rz(rz, k, st, s);
     init_h(w.H.get(), w.Z.get(), st.active, np, tp, k, s);
+    if (fused) init_h(w.Vlr.get(), w.Lw.get(), st.active, np, tp, k, s);  // U^T U H_0 = U^T w_0
     cg_count(k, st, s);
   }
   FSA_CUDA(cudaStreamSynchronize(s));
@@ -587,21 +620,27 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   int num_active = ctx->host_flags[0];
   CgResult res;
   for (int it = 0; it < maxit && num_active > 0; ++it) {
-    A.apply(w.H.get(), w.V.get(), tp);
+    if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
+      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
+      spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
+               tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
+    } else {
+      A.apply(w.H.get(), w.V.get(), tp);
+      KTimer t(ctx, "cg_blas1");
+      launch_coldot(w.H.get(), w.V.get(), n, tp, k, hv, part, s);
+    }
     {
-      auto t = blas("cg_blas1");
-      launch_coldot(w.H.get(), w.V.get(), n, tp, k, hv, sc, s);
+      KTimer t(ctx, "cg_blas1");
       cg_alpha(hv, k, it, maxit, st, s);
-      update_xr(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, np, tp, k, s);
-      launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, sc, s);
+      update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
       cg_check(rr, k, opts.tol, st, s);
     }
-    P.solve(w.R.get(), w.Z.get(), tp);
+    precond(rz);
     {
-      auto t = blas("cg_blas1");
-      launch_coldot(w.R.get(), w.Z.get(), n, tp, k, rz, sc, s);
+      KTimer t(ctx, "cg_blas1");
       cg_beta(rz, k, st, s);
       update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
+      if (fused) update_h(w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);  // Vlr = U^T w + beta Vlr
       cg_count(k, st, s);
     }
     FSA_CUDA(cudaStreamSynchronize(s));
@@ -609,6 +648,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     num_active = ctx->host_flags[0];
     ++res.sweeps;
   }
+  md->cols_hint = 0;
   if (num_active > 0 && opts.error_on_max_iter) throw NumericalError("cg: no convergence within max_iter");
   res.iterations.resize(static_cast<size_t>(k));
   res.converged.resize(static_cast<size_t>(k));

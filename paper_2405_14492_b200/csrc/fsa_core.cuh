@@ -22,8 +22,31 @@
 
 namespace fsa {
 
+// PCG workspace (owned by the context so it is released before the stream)
+struct CgWork {
+  DBuf<double> R, H, V, Z, Lw, Vlr, dots, dbl, part;
+  DBuf<int> ints;
+  DBuf<double> tri;
+};
+
+struct PinnedBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    FSA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(double)));
+    n = count;
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 // ---- context: device, stream, timers ----------------------------------------------------
 struct Context {
+  std::unique_ptr<CgWork> cgw{new CgWork()};
+  PinnedBuf pin1, pin2;
   int device = 0;
   cudaStream_t stream = nullptr;
   int* host_flags = nullptr;  // pinned, mapped
@@ -97,6 +120,7 @@ class Model {
   std::shared_ptr<Geometry> geo;
   Params P;
   long n = 0, m = 0, n_pad = 0, m_pad = 0;
+  long cols_hint = 0;  // real RHS columns of the running solve (timer units)
   int d = 2;
   std::vector<double> ind_host;  // m x d column-major
   DBuf<double> ind;              // same, device

@@ -149,6 +149,99 @@ __global__ void k_count(const double* rx, long rld, long rn, const double* cx, l
   counts[i] = cnt;
 }
 
+// Union of the column indices of kRowBlock consecutive rows: bitonic sort of the
+// block's entries in shared memory, unique, then each entry's local index.
+constexpr int kUnionSort = 8192;  // max entries per row block handled by the sort
+__global__ void __launch_bounds__(512) k_row_block_union(const long* __restrict__ rowptr, const int* __restrict__ col,
+                                                         long nrows, int* __restrict__ ucols,
+                                                         int* __restrict__ ucount,
+                                                         unsigned short* __restrict__ lidx) {
+  extern __shared__ int keys[];  // [kUnionSort] + [kUnionSort] scan
+  int* flag = keys + kUnionSort;
+  const long b = blockIdx.x;
+  const long r0 = b * kRowBlock;
+  const long r1 = r0 + kRowBlock < nrows ? r0 + kRowBlock : nrows;
+  const long p0 = rowptr[r0], p1 = rowptr[r1];
+  const long cnt = p1 - p0;
+  const int tid = threadIdx.x;
+  if (cnt > kUnionSort) {
+    if (tid == 0) ucount[b] = -1;
+    return;
+  }
+  int size = 1;
+  while (size < cnt) size <<= 1;
+  for (int i = tid; i < size; i += blockDim.x) keys[i] = i < cnt ? col[p0 + i] : 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= size; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < size; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const int a = keys[i], c = keys[l];
+          if ((a > c) == up) {
+            keys[i] = c;
+            keys[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // unique: flag first occurrences, inclusive scan (single warp over the array)
+  for (int i = tid; i < size; i += blockDim.x) flag[i] = (i < cnt && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
+  __syncthreads();
+  if (tid < 32) {
+    int carry = 0;
+    for (int base = 0; base < size; base += 32) {
+      int v = flag[base + tid];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (tid >= o) v += u;
+      }
+      flag[base + tid] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const int U = cnt > 0 ? flag[cnt - 1] : 0;
+  if (U > kUnionCap) {
+    if (tid == 0) ucount[b] = -1;
+    return;
+  }
+  int* out = ucols + b * kUnionCap;
+  for (int i = tid; i < cnt; i += blockDim.x)
+    if (i == 0 || keys[i] != keys[i - 1]) out[flag[i] - 1] = keys[i];
+  __syncthreads();
+  for (long p = p0 + tid; p < p1; p += blockDim.x) {
+    const int c = col[p];
+    int lo = 0, hi = U;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (out[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    lidx[p] = static_cast<unsigned short>(lo);
+  }
+  if (tid == 0) ucount[b] = U;
+}
+
+// mirror[p] = position of (c, r) for p = (r, c): binary search of r in row c (warp per row)
+__global__ void k_mirror(const long* __restrict__ rowptr, const int* __restrict__ col, long n,
+                         long* __restrict__ mirror) {
+  const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) {
+    const long c = col[p];
+    long lo = rowptr[c], hi = rowptr[c + 1];
+    while (lo < hi) {
+      const long mid = (lo + hi) >> 1;
+      if (col[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    mirror[p] = lo;
+  }
+}
+
 template <int D>
 __global__ void k_fill(const double* rx, long rld, long rn, const double* cx, long cld,
                        const unsigned long long* ckeys, long cn, GridArgs g, double gamma, const long* rowptr,
@@ -234,6 +327,24 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
   FSA_CUDA(cudaStreamSynchronize(s));
 }
 
+void build_row_blocks(Csr& pat, cudaStream_t s) {
+  pat.nblk = cdiv(pat.rows, kRowBlock);
+  if (pat.nblk == 0 || pat.nnz == 0) return;
+  pat.ucols.alloc(static_cast<size_t>(pat.nblk) * kUnionCap);
+  pat.ucount.alloc(pat.nblk);
+  pat.lidx.alloc(pat.nnz);
+  const int smem = 2 * kUnionSort * static_cast<int>(sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_row_block_union, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_row_block_union<<<static_cast<unsigned>(pat.nblk), 512, smem, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows,
+                                                                        pat.ucols.get(), pat.ucount.get(),
+                                                                        pat.lidx.get());
+  FSA_LAUNCH_CHECK();
+}
+
 void build_pattern(const SortedPoints& rows, const SortedPoints& cols, double gamma, bool force_diag, Csr& out,
                    cudaStream_t s) {
   require(rows.d == cols.d, "location sets must share the dimension");
@@ -275,6 +386,12 @@ void build_pattern(const SortedPoints& rows, const SortedPoints& cols, double ga
   }
 #undef FSA_PAT_ARGS
   FSA_LAUNCH_CHECK();
+  if (force_diag && nnz > 0) {  // transposed positions: the pattern is symmetric
+    out.mirror.alloc(nnz);
+    k_mirror<<<static_cast<unsigned>(cdiv(rows.n * 32, 256)), 256, 0, s>>>(out.rowptr.get(), out.col.get(), rows.n,
+                                                                           out.mirror.get());
+    FSA_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace fsa

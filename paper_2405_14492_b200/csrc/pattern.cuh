@@ -39,7 +39,18 @@ struct Csr {
   DBuf<int> col;       // internal column index
   DBuf<double> dist;   // stored distances (parameter independent)
   DBuf<long> diagpos;  // position of (i,i) (square patterns only)
+  DBuf<long> mirror;   // position of (c,r) for the entry (r,c) (square patterns only)
+  // Row blocks of kRowBlock consecutive rows with the union of their columns:
+  // the SpMM stages those RHS rows in shared memory once per block.
+  long nblk = 0;
+  DBuf<int> ucols;             // [nblk][kUnionCap] sorted union of the block's columns
+  DBuf<int> ucount;            // union size per block (-1: exceeds kUnionCap)
+  DBuf<unsigned short> lidx;   // per entry: index of its column in the block's union
 };
+constexpr int kRowBlock = 16;
+constexpr int kUnionCap = 1024;
+// builds nblk / ucols / ucount / lidx for an existing pattern
+void build_row_blocks(Csr& pat, cudaStream_t s);
 
 // grid covering both point sets (cross patterns use one grid for rows and cols)
 CellGrid make_grid(const double* coords, long n, int d, double gamma, const double* coords2, long n2);

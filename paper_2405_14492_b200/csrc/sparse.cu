@@ -6,6 +6,7 @@
 //  * the cross block to prediction points (prediction.cpp:16-24);
 //  * CSR x dense SpMM on row-major RHS blocks.
 // One warp per CSR row; the row's m-vector lives in registers (m/32 per lane).
+#include "dgemm.cuh"
 #include "kernels.cuh"
 #include "sparse.cuh"
 
@@ -33,18 +34,23 @@ __device__ __forceinline__ double dot_vec(const double* v, const double* __restr
 }
 
 // Sigma_s values on the pattern (rows and cols are the same internal point set)
+// The pattern and the values are symmetric (the warp dot is bitwise symmetric in
+// its operands), so each unordered pair is evaluated once: the entry (r, c), c > r,
+// also writes its transposed position mirror[p].
 template <int MQ>
 __global__ void k_sddmm_sigma_s(const double* __restrict__ U, long ldu, const long* __restrict__ rowptr,
-                                const int* __restrict__ col, const double* __restrict__ dist,
-                                const double* __restrict__ lowrank_diag, long n, SddmmParams P,
-                                double* __restrict__ val, int* __restrict__ n_clamped) {
+                                const int* __restrict__ col, const long* __restrict__ mirror,
+                                const double* __restrict__ dist, const double* __restrict__ lowrank_diag, long n,
+                                SddmmParams P, double* __restrict__ val, int* __restrict__ n_clamped) {
   const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
   double ur[MQ];
   load_vec<MQ>(U + r * ldu, lane, ur);
   const long pe = rowptr[r + 1];
-  for (long p = rowptr[r]; p < pe; ++p) {
+  long p = rowptr[r];
+  while (p < pe && col[p] < r) ++p;  // columns ascend: skip the lower triangle
+  for (; p < pe; ++p) {
     const long c = col[p];
     if (c == r) {
       if (lane == 0) {
@@ -60,19 +66,22 @@ __global__ void k_sddmm_sigma_s(const double* __restrict__ U, long ldu, const lo
     const double dt = dot_vec<MQ>(ur, U + c * ldu, lane);
     if (lane == 0) {
       const double d = dist[p];
-      val[p] = (matern_d(d, P.nu, P.sigma1_2, P.rho) - dt) * taper_d(d, P.family, P.gamma);
+      const double v = (matern_d(d, P.nu, P.sigma1_2, P.rho) - dt) * taper_d(d, P.family, P.gamma);
+      val[p] = v;
+      val[mirror[p]] = v;
     }
   }
 }
 
 // d Sigma_s / d rho (U-form of fsa.cpp:107-122): dl = U1_r.U_c + U_r.T_c with
 // U1 = L^{-1} dSigma_mn/drho, T = U1 - K2 U, K2 = L^{-1} dSigma_m/drho L^{-T}
+// (dl is symmetric in (r, c) because K2 is: evaluated once per unordered pair)
 template <int MQ>
 __global__ void k_sddmm_drho(const double* __restrict__ U, const double* __restrict__ U1,
                              const double* __restrict__ T, long ldu, const long* __restrict__ rowptr,
-                             const int* __restrict__ col, const double* __restrict__ dist,
-                             const double* __restrict__ lowrank_diag, long n, SddmmParams P,
-                             double* __restrict__ val) {
+                             const int* __restrict__ col, const long* __restrict__ mirror,
+                             const double* __restrict__ dist, const double* __restrict__ lowrank_diag, long n,
+                             SddmmParams P, double* __restrict__ val) {
   const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
@@ -80,7 +89,9 @@ __global__ void k_sddmm_drho(const double* __restrict__ U, const double* __restr
   load_vec<MQ>(U + r * ldu, lane, ur);
   load_vec<MQ>(U1 + r * ldu, lane, u1r);
   const long pe = rowptr[r + 1];
-  for (long p = rowptr[r]; p < pe; ++p) {
+  long p = rowptr[r];
+  while (p < pe && col[p] < r) ++p;
+  for (; p < pe; ++p) {
     const long c = col[p];
     double s = 0.0;
 #pragma unroll
@@ -95,7 +106,9 @@ __global__ void k_sddmm_drho(const double* __restrict__ U, const double* __restr
         val[p] = clamped ? 0.0 : -dl;
       } else {
         const double d = dist[p];
-        val[p] = (matern_drho_d(d, P.nu, P.sigma1_2, P.rho) - dl) * taper_d(d, P.family, P.gamma);
+        const double v = (matern_drho_d(d, P.nu, P.sigma1_2, P.rho) - dl) * taper_d(d, P.family, P.gamma);
+        val[p] = v;
+        val[mirror[p]] = v;
       }
     }
   }
@@ -180,6 +193,195 @@ __global__ void k_spmm(const long* __restrict__ rowptr, const int* __restrict__ 
   }
 }
 
+// Fused SpMM + per-column dot: Y = alpha S X + beta Y and dot[c] = sum_r X[r][c] Y[r][c]
+// (the PCG's h.v, krylov.cpp:66). Fixed grid: warp w of block b owns rows
+// b*8+w, +8*gridDim.x, ...; each lane owns columns 2*lane(+1) of every 64-column chunk,
+// so the per-column partials reduce in a fixed order (bitwise reproducible).
+template <int NCH>
+__global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowptr, const int* __restrict__ col,
+                                                 const double* __restrict__ val, long nrows,
+                                                 const double* __restrict__ X, long ldx, double* Y,
+                                                 long ldy, long ncols, double alpha, double beta,
+                                                 double* __restrict__ partial, const double* Y0) {
+  __shared__ double red[8][64 * NCH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double d0[NCH], d1[NCH];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) d0[q] = d1[q] = 0.0;
+  for (long r = static_cast<long>(blockIdx.x) * 8 + warp; r < nrows; r += 8L * gridDim.x) {
+    const long pb = rowptr[r], pe = rowptr[r + 1];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const long c = q * 64 + 2 * lane;
+      if (c >= ncols) break;
+      double a0 = 0.0, a1 = 0.0;
+      for (long p = pb; p < pe; ++p) {
+        const double v = val[p];
+        const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
+        a0 = fma(v, x.x, a0);
+        a1 = fma(v, x.y, a1);
+      }
+      double2* y = reinterpret_cast<double2*>(Y + r * ldy + c);
+      double2 o;
+      if (beta == 0.0) {
+        o = make_double2(alpha * a0, alpha * a1);
+      } else {
+        o = *reinterpret_cast<const double2*>(Y0 + r * ldy + c);
+        o.x = alpha * a0 + beta * o.x;
+        o.y = alpha * a1 + beta * o.y;
+      }
+      *y = o;
+      const double2 h = *reinterpret_cast<const double2*>(X + r * ldx + c);
+      d0[q] = fma(h.x, o.x, d0[q]);
+      d1[q] = fma(h.y, o.y, d1[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    red[warp][q * 64 + 2 * lane] = d0[q];
+    red[warp][q * 64 + 2 * lane + 1] = d1[q];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 64 * NCH && c < ncols; c += blockDim.x) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += red[w][c];
+    partial[static_cast<long>(blockIdx.x) * ncols + c] = sacc;
+  }
+}
+
+// Staged SpMM + dot: one CTA (8 warps, 2 rows each) per row block of kRowBlock
+// consecutive rows. The RHS rows of the block's column union (precomputed once per
+// geometry, build_row_blocks) are copied into shared memory with cp.async, together
+// with the block's column-local indices and values; every nonzero then reads its RHS
+// row from smem. Row blocks are contiguous in the Hilbert order, so the union is
+// several times smaller than the block's nonzero count (that factor comes off the
+// L2 gather traffic). Two CTAs per SM overlap one block's copy with the other's
+// arithmetic. Blocks whose union or nonzero count exceeds the smem budget read the
+// RHS from global memory instead.
+constexpr int kStagedNnz = 2048;  // nonzeros of one row block staged in smem
+template <int NCH>
+__global__ void __launch_bounds__(256, 2) k_spmm_staged(const long* __restrict__ rowptr, const int* __restrict__ col,
+                                                       const unsigned short* __restrict__ lidx,
+                                                       const double* __restrict__ val, const int* __restrict__ ucols,
+                                                       const int* __restrict__ ucount, long nrows,
+                                                       const double* __restrict__ X, long ldx, double* __restrict__ Y,
+                                                       long ldy, long ncols, double alpha, double beta,
+                                                       double* __restrict__ partial, int cap) {
+  extern __shared__ __align__(16) double sx[];  // [cap][ldx] then vals[kStagedNnz], idx[kStagedNnz]
+  __shared__ double red[8][64 * NCH];
+  double* sv = sx + static_cast<long>(cap) * ldx;
+  unsigned short* si = reinterpret_cast<unsigned short*>(sv + kStagedNnz);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long b = blockIdx.x;
+  const long r0 = b * kRowBlock;
+  const long r1 = r0 + kRowBlock < nrows ? r0 + kRowBlock : nrows;
+  const long p0 = rowptr[r0];
+  const int U = ucount[b];
+  const bool staged = U >= 0 && U <= cap && rowptr[r1] - p0 <= kStagedNnz;
+  if (staged) {
+    const int half = static_cast<int>(ldx / 2);
+    const int* uc = ucols + b * kUnionCap;
+    for (int q = tid; q < U * half; q += blockDim.x) {
+      const int rr = q / half, c2 = (q - rr * half) * 2;
+      cp_async16(sx + rr * ldx + c2, X + static_cast<long>(uc[rr]) * ldx + c2);
+    }
+    cp_async_commit();
+    const long cnt = rowptr[r1] - p0;
+    for (long q = tid; q < cnt; q += blockDim.x) {
+      sv[q] = val[p0 + q];
+      si[q] = lidx[p0 + q];
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  double d0[NCH], d1[NCH];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) d0[q] = d1[q] = 0.0;
+  for (long r = r0 + warp; r < r1; r += 8) {
+    const long pb = rowptr[r], pe = rowptr[r + 1];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const long c = q * 64 + 2 * lane;
+      if (c >= ncols) break;
+      double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;  // chains: even / odd nonzeros
+      long p = pb;
+      if (staged) {
+        double f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
+        long l = pb - p0;
+        const long le = pe - p0;
+        for (; l + 3 < le; l += 4) {
+          const double2 x = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l]) * ldx + c);
+          const double2 y = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 1]) * ldx + c);
+          const double2 z = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 2]) * ldx + c);
+          const double2 u = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 3]) * ldx + c);
+          a0 = fma(sv[l], x.x, a0);
+          a1 = fma(sv[l], x.y, a1);
+          e0 = fma(sv[l + 1], y.x, e0);
+          e1 = fma(sv[l + 1], y.y, e1);
+          f0 = fma(sv[l + 2], z.x, f0);
+          f1 = fma(sv[l + 2], z.y, f1);
+          g0 = fma(sv[l + 3], u.x, g0);
+          g1 = fma(sv[l + 3], u.y, g1);
+        }
+        for (; l < le; ++l) {
+          const double2 x = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l]) * ldx + c);
+          a0 = fma(sv[l], x.x, a0);
+          a1 = fma(sv[l], x.y, a1);
+        }
+        a0 += f0;
+        a1 += f1;
+        e0 += g0;
+        e1 += g1;
+      } else {
+        for (; p + 1 < pe; p += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
+          const double2 y = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p + 1]) * ldx + c);
+          a0 = fma(val[p], x.x, a0);
+          a1 = fma(val[p], x.y, a1);
+          e0 = fma(val[p + 1], y.x, e0);
+          e1 = fma(val[p + 1], y.y, e1);
+        }
+        if (p < pe) {
+          const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
+          a0 = fma(val[p], x.x, a0);
+          a1 = fma(val[p], x.y, a1);
+        }
+      }
+      a0 += e0;
+      a1 += e1;
+      double2* y = reinterpret_cast<double2*>(Y + r * ldy + c);
+      double2 o;
+      if (beta == 0.0) {
+        o = make_double2(alpha * a0, alpha * a1);
+      } else {
+        o = *y;
+        o.x = alpha * a0 + beta * o.x;
+        o.y = alpha * a1 + beta * o.y;
+      }
+      *y = o;
+      if (partial != nullptr) {
+        const double2 h = *reinterpret_cast<const double2*>(X + r * ldx + c);
+        d0[q] = fma(h.x, o.x, d0[q]);
+        d1[q] = fma(h.y, o.y, d1[q]);
+      }
+    }
+  }
+  if (partial == nullptr) return;
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    red[warp][q * 64 + 2 * lane] = d0[q];
+    red[warp][q * 64 + 2 * lane + 1] = d1[q];
+  }
+  __syncthreads();
+  for (int c = tid; c < 64 * NCH && c < ncols; c += blockDim.x) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += red[w][c];
+    partial[b * ncols + c] = sacc;
+  }
+}
+
 #define FSA_DISPATCH_MQ(KERNEL, mpad, grid, s, ...)                                      \
   do {                                                                                  \
     switch (static_cast<int>((mpad) / 32)) {                                            \
@@ -203,16 +405,16 @@ void sddmm_sigma_s(const double* U, long ldu, const Csr& pat, const double* lowr
   FSA_CUDA(cudaMemsetAsync(n_clamped_dev, 0, sizeof(int), s));
   const unsigned grid = static_cast<unsigned>(cdiv(pat.rows * 32, 256));
   if (grid == 0) return;
-  FSA_DISPATCH_MQ(k_sddmm_sigma_s, ldu, grid, s, U, ldu, pat.rowptr.get(), pat.col.get(), pat.dist.get(),
-                  lowrank_diag, pat.rows, P, val, n_clamped_dev);
+  FSA_DISPATCH_MQ(k_sddmm_sigma_s, ldu, grid, s, U, ldu, pat.rowptr.get(), pat.col.get(), pat.mirror.get(),
+                  pat.dist.get(), lowrank_diag, pat.rows, P, val, n_clamped_dev);
 }
 
 void sddmm_drho(const double* U, const double* U1, const double* T, long ldu, const Csr& pat,
                 const double* lowrank_diag, const SddmmParams& P, double* val, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>(cdiv(pat.rows * 32, 256));
   if (grid == 0) return;
-  FSA_DISPATCH_MQ(k_sddmm_drho, ldu, grid, s, U, U1, T, ldu, pat.rowptr.get(), pat.col.get(), pat.dist.get(),
-                  lowrank_diag, pat.rows, P, val);
+  FSA_DISPATCH_MQ(k_sddmm_drho, ldu, grid, s, U, U1, T, ldu, pat.rowptr.get(), pat.col.get(), pat.mirror.get(),
+                  pat.dist.get(), lowrank_diag, pat.rows, P, val);
 }
 
 void sddmm_cross(const double* Rm, long ldr, const double* Cm, long ldc, const Csr& pat, const SddmmParams& P,
@@ -232,6 +434,58 @@ void extract_diag(const double* val, const long* diagpos, long n, long n_pad, do
                   double* sqrtD, cudaStream_t s) {
   k_extract_diag<<<static_cast<unsigned>(cdiv(n_pad, 256)), 256, 0, s>>>(val, diagpos, n, n_pad, D, Dinv, sqrtD);
   FSA_LAUNCH_CHECK();
+}
+
+constexpr int kStagedSmem = 104 * 1024;  // two CTAs per SM
+
+void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, double* Y, long ldy, long ncols,
+                 double alpha, double beta, double* dot, double* partial, cudaStream_t s) {
+  require(ncols <= 128 && ldx % 2 == 0, "spmm_staged: at most 128 columns");
+  if (pat.rows == 0) return;
+  const long nz_bytes = kStagedNnz * static_cast<long>(sizeof(double) + sizeof(unsigned short));
+  const int cap = static_cast<int>((kStagedSmem - nz_bytes) / (ldx * static_cast<long>(sizeof(double))));
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_spmm_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmem));
+    FSA_CUDA(cudaFuncSetAttribute(k_spmm_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmem));
+    attr = true;
+  }
+  const unsigned g = static_cast<unsigned>(pat.nblk);
+  double* part = dot != nullptr ? partial : nullptr;
+  if (ncols <= 64)
+    k_spmm_staged<1><<<g, 256, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
+                                                 pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
+                                                 alpha, beta, part, cap);
+  else
+    k_spmm_staged<2><<<g, 256, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
+                                                 pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
+                                                 alpha, beta, part, cap);
+  FSA_LAUNCH_CHECK();
+  if (dot != nullptr) colsum_partials(partial, pat.nblk, ncols, ncols, dot, s);
+}
+
+long spmm_dot_blocks(long nrows) {  // one row per warp (the L1-friendly geometry of k_spmm)
+  const long b = cdiv(nrows, 8);
+  return b < 1 ? 1 : b;
+}
+
+void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
+              long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
+              const double* Y0) {
+  if (nrows == 0) return;
+  const long nb = spmm_dot_blocks(nrows);
+  const int nch = static_cast<int>(cdiv(ncols, 64));
+  const unsigned g = static_cast<unsigned>(nb);
+  const double* y0 = Y0 != nullptr ? Y0 : Y;
+  switch (nch) {
+    case 1: k_spmm_dot<1><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
+    case 2: k_spmm_dot<2><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
+    case 3:
+    case 4: k_spmm_dot<4><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
+    default: throw std::invalid_argument("spmm_dot: more than 256 columns");
+  }
+  FSA_LAUNCH_CHECK();
+  colsum_partials(partial, nb, ncols, ncols, dot, s);
 }
 
 void launch_spmm(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx,

@@ -17,6 +17,17 @@ void sddmm_drho(const double* U, const double* U1, const double* T, long ldu, co
                 const double* lowrank_diag, const SddmmParams& P, double* val, cudaStream_t s);
 void sddmm_cross(const double* Rm, long ldr, const double* Cm, long ldc, const Csr& pat, const SddmmParams& P,
                  double* val, cudaStream_t s);
+// Y = alpha S X + beta Y (first ncols <= 256 columns) fused with dot[c] = sum_r X[r][c] Y[r][c];
+// partial must hold spmm_dot_blocks(nrows) * ncols doubles
+long spmm_dot_blocks(long nrows);
+// staged variant on a pattern with row blocks (ncols <= 128): Y = alpha S X + beta Y and,
+// when dot != null, dot[c] = sum_r X[r][c] Y[r][c]; partial holds pat.nblk * ncols doubles
+void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, double* Y, long ldy, long ncols,
+                 double alpha, double beta, double* dot, double* partial, cudaStream_t s);
+// (Y0, when given, replaces Y as the beta term: Y = alpha S X + beta Y0)
+void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
+              long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
+              const double* Y0 = nullptr);
 // out[i] = |U_i|^2 for i < n, 0 for padding
 void colnorm2(const double* U, long ldu, long mpad, long n, long n_pad, double* out, cudaStream_t s);
 // D[i] = val[diagpos[i]] (1 on padding), Dinv = 1/D, sqrtD = sqrt(D) (either may be null)
