@@ -4,6 +4,7 @@
 // scalar recurrences with Lanczos-tridiagonal capture, and the host<->device
 // layout conversions (column-major original order <-> row-major internal order).
 #include "blas1.cuh"
+#include "dgemm.cuh"
 
 namespace fsa {
 
@@ -175,6 +176,32 @@ __global__ void k_update_h(double* __restrict__ H, const double* __restrict__ Z,
   H[idx] = Z[idx] + beta[j] * H[idx];
 }
 
+// H = Z + beta H and Vlr = Lw + beta Vlr for active columns (two columns per thread)
+__global__ void k_update_h2(double* __restrict__ H, const double* __restrict__ Z, double* __restrict__ Vlr,
+                            const double* __restrict__ Lw, const int* __restrict__ active,
+                            const double* __restrict__ beta, long n, long tp, long k) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;  // pair index
+  if (idx >= n * tp / 2) return;
+  const long j = (2 * idx) % tp;
+  const bool a0 = j < k && active[j], a1 = j + 1 < k && active[j + 1];
+  if (!a0 && !a1) return;
+  const double b0 = a0 ? beta[j] : 0.0, b1 = a1 ? beta[j + 1] : 0.0;
+  double2 h = reinterpret_cast<double2*>(H)[idx];
+  double2 v = reinterpret_cast<double2*>(Vlr)[idx];
+  const double2 z = reinterpret_cast<const double2*>(Z)[idx];
+  const double2 l = reinterpret_cast<const double2*>(Lw)[idx];
+  if (a0) {
+    h.x = z.x + b0 * h.x;
+    v.x = l.x + b0 * v.x;
+  }
+  if (a1) {
+    h.y = z.y + b1 * h.y;
+    v.y = l.y + b1 * v.y;
+  }
+  reinterpret_cast<double2*>(H)[idx] = h;
+  reinterpret_cast<double2*>(Vlr)[idx] = v;
+}
+
 // H = Z on active columns, 0 elsewhere
 __global__ void k_init_h(double* __restrict__ H, const double* __restrict__ Z, const int* __restrict__ active,
                          long n, long tp, long k) {
@@ -265,7 +292,8 @@ __global__ void __launch_bounds__(256) k_rowdot_cols(const double* __restrict__ 
   }
 }
 
-__global__ void k_colsum(const double* __restrict__ partial, long nb, long ldp, double* __restrict__ out) {
+[[maybe_unused]] __global__ void k_colsum(const double* __restrict__ partial, long nb, long ldp,
+                                         double* __restrict__ out) {
   const long c = blockIdx.x;
   const int lane = threadIdx.x;
   double sacc = 0.0;
@@ -296,8 +324,7 @@ void rowdot_launch(const double* A, const double* B, const double* w, long n, lo
       k_rowdot_cols<4, MODE><<<g, 256, 0, s>>>(A, B, w, n, ld, t, c0, X, R, alpha, partial, t);
     FSA_LAUNCH_CHECK();
   }
-  k_colsum<<<static_cast<unsigned>(t), 32, 0, s>>>(partial, nb, t, out);
-  FSA_LAUNCH_CHECK();
+  colsum_partials(partial, nb, t, t, out, s);
 }
 
 __global__ void k_update_uh(double* __restrict__ UH, const double* __restrict__ W, const int* __restrict__ active,
@@ -403,6 +430,11 @@ void update_xr(double* X, double* R, const double* H, const double* V, const dou
 void update_h(double* H, const double* Z, const int* active, const double* beta, long n, long tp, long k,
               cudaStream_t s) {
   k_update_h<<<nblk(n * tp), 256, 0, s>>>(H, Z, active, beta, n, tp, k);
+  FSA_LAUNCH_CHECK();
+}
+void update_h2(double* H, const double* Z, double* Vlr, const double* Lw, const int* active, const double* beta,
+               long n, long tp, long k, cudaStream_t s) {
+  k_update_h2<<<nblk(n * tp / 2), 256, 0, s>>>(H, Z, Vlr, Lw, active, beta, n, tp, k);
   FSA_LAUNCH_CHECK();
 }
 void init_h(double* H, const double* Z, const int* active, long n, long tp, long k, cudaStream_t s) {

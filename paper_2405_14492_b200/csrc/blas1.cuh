@@ -62,6 +62,9 @@ void update_uh(double* UH, const double* W, const int* active, const double* bet
 void update_h(double* H, const double* Z, const int* active, const double* beta, long n, long tp, long k,
               cudaStream_t s);
 void init_h(double* H, const double* Z, const int* active, long n, long tp, long k, cudaStream_t s);
+// H = Z + beta H and Vlr = Lw + beta Vlr on the active columns (tp even)
+void update_h2(double* H, const double* Z, double* Vlr, const double* Lw, const int* active, const double* beta,
+               long n, long tp, long k, cudaStream_t s);
 void scale_rows(double* Y, const double* X, const double* w, long n, long tp, cudaStream_t s);
 void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_t s);
 

@@ -13,6 +13,21 @@ using ExpandCfg = GemmCfg<NT, 4, 4, false, 16, 3>;
 // expand, 8 warps x 16 rows (BM = 128): twice the warps per SM at the same smem
 template <int NT>
 using ExpandCfg8 = GemmCfg<NT, 2, 8, false, 16, 3>;
+// expand, 2 stages (3 CTAs per SM)
+template <int NT>
+using ExpandCfgS2 = GemmCfg<NT, 4, 4, false, 16, 2>;
+// expand, BM = 64 (4 warps x 16 rows), 3 stages: 3 CTAs per SM, twice the CTAs
+template <int NT>
+using ExpandCfg64 = GemmCfg<NT, 2, 4, false, 16, 3>;
+// expand, BM = 64 as 2 warps x 32 rows (twice the independent accumulators per warp)
+template <int NT>
+using ExpandCfg64w2 = GemmCfg<NT, 4, 2, false, 16, 3>;
+// same with 2 stages (more CTAs per SM)
+template <int NT>
+using ExpandCfg64w2s2 = GemmCfg<NT, 4, 2, false, 16, 2>;
+// BM = 64, 4 warps x 16 rows, BK = 32, 2 stages (half the barriers per k)
+template <int NT>
+using ExpandCfg64k32 = GemmCfg<NT, 2, 4, false, 32, 2>;
 // reduce: 4 warps x 16 rows (BM = 64), A is [k][m].
 template <int NT>
 using ReduceCfg = GemmCfg<NT, 2, 4, true, 16, 3>;
@@ -26,8 +41,12 @@ int knob(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 int expand_variant() {
-  static const int v = knob("FSA_GEMM_EXPAND", 0);  // 4 warps x 32 rows: measured faster (r01)
+  static const int v = knob("FSA_GEMM_EXPAND", 3);  // BM = 64, 3 CTAs/SM: measured fastest (r01)
   return v;
+}
+long expand_bm() {
+  const int v = expand_variant();
+  return (v >= 3 && v <= 6) ? 64 : 128;
 }
 int reduce_variant() {
   static const int v = knob("FSA_GEMM_REDUCE", 1);  // 8 warps: measured faster (r01)
@@ -73,11 +92,19 @@ void expand(const double* M, long ldm, long rows, long K, const double* W, long 
   require(rows % 128 == 0 && K % 16 == 0 && N == pad_cols(N), "gemm_expand: unpadded shape");
   if (rows == 0) return;
   const int nt = tile_nt(N);
-  dim3 grid(static_cast<unsigned>(rows / 128), static_cast<unsigned>(N / (nt * 8)), 1);
-  if (expand_variant() == 1)
-    dispatch_nt<ExpandCfg8>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
-  else
-    dispatch_nt<ExpandCfg>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s);
+  const int v = expand_variant();
+  const long bm = expand_bm();
+  require(v != 6 || K % 32 == 0, "gemm_expand: K must be a multiple of 32 for this tile");
+  dim3 grid(static_cast<unsigned>(rows / bm), static_cast<unsigned>(N / (nt * 8)), 1);
+  switch (v) {
+    case 1: dispatch_nt<ExpandCfg8>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    case 2: dispatch_nt<ExpandCfgS2>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    case 3: dispatch_nt<ExpandCfg64>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    case 4: dispatch_nt<ExpandCfg64w2>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    case 5: dispatch_nt<ExpandCfg64w2s2>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    case 6: dispatch_nt<ExpandCfg64k32>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+    default: dispatch_nt<ExpandCfg>(nt, M, ldm, W, ldw, nullptr, K, K, grid, epi, s); break;
+  }
 }
 
 struct ReducePlan {
@@ -87,10 +114,10 @@ struct ReducePlan {
 ReducePlan plan_reduce(long Mr, long N, long K) {
   ReducePlan p;
   p.nt = tile_nt(N);
-  p.bm = (reduce_variant() == 1 && Mr % 128 == 0) ? 128 : 64;
+  p.bm = (reduce_variant() >= 1 && Mr % 128 == 0) ? 128 : 64;
   p.tiles = (Mr / p.bm) * (N / (p.nt * 8));
   const long kblocks = K / 16;
-  long splits = cdiv(2 * kNumSMs, p.tiles);
+  long splits = cdiv((reduce_variant() == 2 ? 4 : 2) * kNumSMs, p.tiles);
   splits = splits < 1 ? 1 : splits;
   splits = splits > kblocks ? kblocks : splits;
   splits = splits < 1 ? 1 : splits;
@@ -132,28 +159,44 @@ void gemm_expand_woodbury_dot(const double* M, long ldm, long rows, long K, cons
                               double* Z, const double* R, long ld, const double* Dinv, double* rz, double* partial,
                               cudaStream_t s) {
   expand(M, ldm, rows, K, W, ldw, N, EpiWoodburyDot{partial, N, Z, R, ld, Dinv}, s);
-  colsum_partials(partial, rows / 128, N, N, rz, s);
+  colsum_partials(partial, rows / expand_bm(), N, N, rz, s);
 }
 
 void gemm_expand_woodbury_keep(const double* M, long ldm, long rows, long K, const double* W, long ldw, long N,
                                double* Z, double* Lw, const double* R, long ld, const double* Dinv, double* rz,
                                double* partial, cudaStream_t s) {
   expand(M, ldm, rows, K, W, ldw, N, EpiWoodburyKeep{partial, N, Z, Lw, R, ld, Dinv}, s);
-  colsum_partials(partial, rows / 128, N, N, rz, s);
+  colsum_partials(partial, rows / expand_bm(), N, N, rz, s);
 }
 
-__global__ void k_colsum_partials(const double* __restrict__ partial, long nb, long ldp, double* __restrict__ out) {
+// out[c] = sum_b partial[b][c]: one 256-thread block per column, fixed strided
+// assignment + fixed tree (bitwise reproducible)
+__global__ void __launch_bounds__(256) k_colsum_partials(const double* __restrict__ partial, long nb, long ldp,
+                                                         double* __restrict__ out) {
+  __shared__ double red[8];
   const long c = blockIdx.x;
-  const int lane = threadIdx.x;
-  double sacc = 0.0;
-  for (long b = lane; b < nb; b += 32) sacc += partial[b * ldp + c];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double s0 = 0.0, s1 = 0.0;
+  long b = tid;
+  for (; b + 256 < nb; b += 512) {
+    s0 += partial[b * ldp + c];
+    s1 += partial[(b + 256) * ldp + c];
+  }
+  if (b < nb) s0 += partial[b * ldp + c];
+  double sacc = s0 + s1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-  if (lane == 0) out[c] = sacc;
+  if (lane == 0) red[warp] = sacc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[c] = t;
+  }
 }
 void colsum_partials(const double* partial, long nb, long ldp, long t, double* out, cudaStream_t s) {
   if (t == 0) return;
-  k_colsum_partials<<<static_cast<unsigned>(t), 32, 0, s>>>(partial, nb, ldp, out);
+  k_colsum_partials<<<static_cast<unsigned>(t), 256, 0, s>>>(partial, nb, ldp, out);
   FSA_LAUNCH_CHECK();
 }
 

@@ -543,7 +543,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     w.Lw.alloc(blk);
     w.Vlr.alloc(blk);
   }
-  const size_t npart = std::max(static_cast<size_t>(std::max(np / 128, spmm_dot_blocks(n)) * tp),
+  const size_t npart = std::max(static_cast<size_t>(std::max(np / 64, spmm_dot_blocks(n)) * tp),
                                 coldot_scratch(n, tp));
   if (w.part.n < npart) w.part.alloc(npart);
   w.dots.alloc(static_cast<size_t>(4 * tp));
@@ -622,8 +622,13 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   for (int it = 0; it < maxit && num_active > 0; ++it) {
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-      spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
-               tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
+      static const int staged = std::getenv("FSA_SPMM") ? std::atoi(std::getenv("FSA_SPMM")) : 0;
+      if (staged && tp <= 128 && md->geo->pat.nblk > 0)
+        spmm_staged(md->geo->pat, md->sval.get(), w.H.get(), tp, w.V.get(), tp, tp, 1.0, 1.0, hv, part, s,
+                    w.Vlr.get());
+      else
+        spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
+                 tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
     } else {
       A.apply(w.H.get(), w.V.get(), tp);
       KTimer t(ctx, "cg_blas1");
@@ -639,8 +644,10 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     {
       KTimer t(ctx, "cg_blas1");
       cg_beta(rz, k, st, s);
-      update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
-      if (fused) update_h(w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);  // Vlr = U^T w + beta Vlr
+      if (fused)  // H = Z + beta H, Vlr = U^T w + beta Vlr
+        update_h2(w.H.get(), w.Z.get(), w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);
+      else
+        update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
       cg_count(k, st, s);
     }
     FSA_CUDA(cudaStreamSynchronize(s));

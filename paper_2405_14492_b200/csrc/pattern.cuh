@@ -47,7 +47,7 @@ struct Csr {
   DBuf<int> ucount;            // union size per block (-1: exceeds kUnionCap)
   DBuf<unsigned short> lidx;   // per entry: index of its column in the block's union
 };
-constexpr int kRowBlock = 16;
+constexpr int kRowBlock = 32;
 constexpr int kUnionCap = 1024;
 // builds nblk / ucols / ucount / lidx for an existing pattern
 void build_row_blocks(Csr& pat, cudaStream_t s);

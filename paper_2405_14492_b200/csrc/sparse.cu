@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
     const long pb = rowptr[r], pe = rowptr[r + 1];
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
+      if (q * 64 >= ncols) break;  // warp-uniform
       const long c = q * 64 + 2 * lane;
-      if (c >= ncols) break;
+      const bool on = c < ncols;
+      if (!on) continue;
       double a0 = 0.0, a1 = 0.0;
       for (long p = pb; p < pe; ++p) {
         const double v = val[p];
@@ -259,17 +261,18 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 // L2 gather traffic). Two CTAs per SM overlap one block's copy with the other's
 // arithmetic. Blocks whose union or nonzero count exceeds the smem budget read the
 // RHS from global memory instead.
-constexpr int kStagedNnz = 2048;  // nonzeros of one row block staged in smem
+constexpr int kStagedNnz = 4096;  // nonzeros of one row block staged in smem
+constexpr int kStagedWarps = 16;
 template <int NCH>
-__global__ void __launch_bounds__(256, 2) k_spmm_staged(const long* __restrict__ rowptr, const int* __restrict__ col,
+__global__ void __launch_bounds__(32 * kStagedWarps, 1) k_spmm_staged(const long* __restrict__ rowptr, const int* __restrict__ col,
                                                        const unsigned short* __restrict__ lidx,
                                                        const double* __restrict__ val, const int* __restrict__ ucols,
                                                        const int* __restrict__ ucount, long nrows,
-                                                       const double* __restrict__ X, long ldx, double* __restrict__ Y,
+                                                       const double* __restrict__ X, long ldx, double* Y,
                                                        long ldy, long ncols, double alpha, double beta,
-                                                       double* __restrict__ partial, int cap) {
+                                                       double* __restrict__ partial, int cap, const double* Y0) {
   extern __shared__ __align__(16) double sx[];  // [cap][ldx] then vals[kStagedNnz], idx[kStagedNnz]
-  __shared__ double red[8][64 * NCH];
+  __shared__ double red[kStagedWarps][64 * NCH];
   double* sv = sx + static_cast<long>(cap) * ldx;
   unsigned short* si = reinterpret_cast<unsigned short*>(sv + kStagedNnz);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_staged(const long* __restrict__
   double d0[NCH], d1[NCH];
 #pragma unroll
   for (int q = 0; q < NCH; ++q) d0[q] = d1[q] = 0.0;
-  for (long r = r0 + warp; r < r1; r += 8) {
+  for (long r = r0 + warp; r < r1; r += kStagedWarps) {
     const long pb = rowptr[r], pe = rowptr[r + 1];
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_staged(const long* __restrict__
       if (beta == 0.0) {
         o = make_double2(alpha * a0, alpha * a1);
       } else {
-        o = *y;
+        o = *reinterpret_cast<const double2*>(Y0 + r * ldy + c);
         o.x = alpha * a0 + beta * o.x;
         o.y = alpha * a1 + beta * o.y;
       }
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_staged(const long* __restrict__
   for (int c = tid; c < 64 * NCH && c < ncols; c += blockDim.x) {
     double sacc = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) sacc += red[w][c];
+    for (int w = 0; w < kStagedWarps; ++w) sacc += red[w][c];
     partial[b * ncols + c] = sacc;
   }
 }
@@ -436,11 +439,12 @@ void extract_diag(const double* val, const long* diagpos, long n, long n_pad, do
   FSA_LAUNCH_CHECK();
 }
 
-constexpr int kStagedSmem = 104 * 1024;  // two CTAs per SM
+constexpr int kStagedSmem = 184 * 1024;  // one 16-warp CTA per SM
 
 void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, double* Y, long ldy, long ncols,
-                 double alpha, double beta, double* dot, double* partial, cudaStream_t s) {
+                 double alpha, double beta, double* dot, double* partial, cudaStream_t s, const double* Y0) {
   require(ncols <= 128 && ldx % 2 == 0, "spmm_staged: at most 128 columns");
+  if (Y0 == nullptr) Y0 = Y;
   if (pat.rows == 0) return;
   const long nz_bytes = kStagedNnz * static_cast<long>(sizeof(double) + sizeof(unsigned short));
   const int cap = static_cast<int>((kStagedSmem - nz_bytes) / (ldx * static_cast<long>(sizeof(double))));
@@ -453,13 +457,13 @@ void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, d
   const unsigned g = static_cast<unsigned>(pat.nblk);
   double* part = dot != nullptr ? partial : nullptr;
   if (ncols <= 64)
-    k_spmm_staged<1><<<g, 256, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
+    k_spmm_staged<1><<<g, 32 * kStagedWarps, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
                                                  pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
-                                                 alpha, beta, part, cap);
+                                                 alpha, beta, part, cap, Y0);
   else
-    k_spmm_staged<2><<<g, 256, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
+    k_spmm_staged<2><<<g, 32 * kStagedWarps, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
                                                  pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
-                                                 alpha, beta, part, cap);
+                                                 alpha, beta, part, cap, Y0);
   FSA_LAUNCH_CHECK();
   if (dot != nullptr) colsum_partials(partial, pat.nblk, ncols, ncols, dot, s);
 }

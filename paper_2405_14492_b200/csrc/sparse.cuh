@@ -23,7 +23,8 @@ long spmm_dot_blocks(long nrows);
 // staged variant on a pattern with row blocks (ncols <= 128): Y = alpha S X + beta Y and,
 // when dot != null, dot[c] = sum_r X[r][c] Y[r][c]; partial holds pat.nblk * ncols doubles
 void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, double* Y, long ldy, long ncols,
-                 double alpha, double beta, double* dot, double* partial, cudaStream_t s);
+                 double alpha, double beta, double* dot, double* partial, cudaStream_t s,
+                 const double* Y0 = nullptr);
 // (Y0, when given, replaces Y as the beta term: Y = alpha S X + beta Y0)
 void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
               long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
