@@ -37,6 +37,8 @@ CONFIGS = {
             points="uniform"),
     2: dict(n=100_000, m=500, inducing="kmeans", nu=1.5, s12=1.0, rho=0.05, s2=0.05, nnz=80, L=50, tol=1e-3,
             points="uniform"),
+    3: dict(n=100_000, m=500, inducing="kmeans", nu=1.5, s12=1.0, rho=0.05, s2=0.05, nnz=80, L=1000, tol=1e-3,
+            points="uniform", np=100_000),
     4: dict(n=1_000_000, m=1000, inducing="kmeans", nu=1.5, s12=1.0, rho=0.03, s2=0.05, nnz=80, L=64, tol=1e-3,
             points="uniform"),
     5: dict(n=200_000, m=1000, inducing="kmeans", nu=2.5, s12=1.0, rho=0.3, s2=1e-3, nnz=120, L=50, tol=1e-4,
@@ -206,6 +208,58 @@ def run_reference(args, cfg):
     print(json.dumps(line))
 
 
+def run_prediction(args, cfg):
+    """Config 3: make_prediction_set + predict_var_sim (1000 Rademacher simulation vectors,
+    FITC-PCG with m RHS + Jacobi-PCG on Sigma_s), device-timed per evaluation."""
+    import torch
+
+    from paper_2405_14492_b200 import fsa
+
+    torch.cuda.set_device(0)
+    ctx = fsa.Context(0)
+    coords, ind, gamma, y = make_inputs(cfg, fsa)
+    plocs = fsa.uniform_locations(cfg["np"], 2, 101)
+    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    geo = fsa.Geometry(coords, gamma, ctx)
+    md = fsa.FsaModel.assemble(None, ind, geometry=geo, **kw)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+
+    def step():
+        pr = fsa.make_prediction_set(md, plocs)
+        return pr.predict_var_sim(num_probes=cfg["L"], seed=0, tol=cfg["tol"], tol_s=cfg["tol"])
+
+    for _ in range(args.warmup):
+        step()
+    ctx.set_profiling(True)
+    ctx.reset_timers()
+    sampler = ClockSampler(0)
+    sampler.start()
+    ctx.synchronize()
+    l0 = fsa.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    timers = ctx.timers()
+    last = res[-1]
+    line = {"metric": "predictive-variance wall time (make_prediction_set + predict_var_sim)", "value": ms,
+            "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE config 3)",
+            "config": {"workload": "config3: predict_var_sim", "n": cfg["n"], "np": cfg["np"], "m": cfg["m"],
+                       "probes": cfg["L"], "tol": cfg["tol"], "gamma": gamma},
+            "det_ms": last["det_ms"], "sim_ms": last["sim_ms"], "cg_iterations": last["cg_iterations"],
+            "clamped": last["clamped"], "var_mean": float(np.mean(last["var"])),
+            "se_mean": float(np.mean(last["se"])), "gpu_launches": fsa.launch_count() - l0, "clocks": clocks,
+            "cpu_baseline": None,
+            "timers_ms": {k: round(v["ms"] / args.steps, 3) for k, v in timers.items()}}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -220,6 +274,9 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+        return
+    if args.config == 3:
+        run_prediction(args, cfg)
         return
 
     import torch

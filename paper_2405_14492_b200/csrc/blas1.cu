@@ -432,6 +432,64 @@ void update_h(double* H, const double* Z, const int* active, const double* beta,
   k_update_h<<<nblk(n * tp), 256, 0, s>>>(H, Z, active, beta, n, tp, k);
   FSA_LAUNCH_CHECK();
 }
+// out[0..3] = sum_i p_i, p.d1, p.dD, f_i / D_i over i < n; out[4..6] = tr Qi, tr K2,
+// <K2, Qi> over the m x m blocks. One 1024-thread block, fixed order.
+__global__ void __launch_bounds__(1024) k_trace_sums(const double* __restrict__ p, const double* __restrict__ d1,
+                                                     const double* __restrict__ dD, const double* __restrict__ f,
+                                                     const double* __restrict__ D, long n,
+                                                     const double* __restrict__ Qi, const double* __restrict__ K2,
+                                                     long m, double* __restrict__ out) {
+  __shared__ double red[7][32];
+  double a[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (long i = threadIdx.x; i < n; i += blockDim.x) {
+    a[0] += p[i];
+    a[1] += p[i] * d1[i];
+    a[2] += p[i] * dD[i];
+    a[3] += f[i] / D[i];
+  }
+  for (long i = threadIdx.x; i < m; i += blockDim.x) {
+    a[4] += Qi[i * m + i];
+    a[5] += K2[i * m + i];
+  }
+  for (long i = threadIdx.x; i < m * m; i += blockDim.x) a[6] += K2[i] * Qi[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double v = a[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    double v = 0.0;
+    for (int w = 0; w < 32; ++w) v += red[threadIdx.x][w];
+    out[threadIdx.x] = v;
+  }
+}
+void trace_sums(const double* p, const double* d1, const double* dD, const double* f, const double* D, long n,
+                const double* Qi, const double* K2, long m, double* out, cudaStream_t s) {
+  k_trace_sums<<<1, 1024, 0, s>>>(p, d1, dD, f, D, n, Qi, K2, m, out);
+  FSA_LAUNCH_CHECK();
+}
+
+__global__ void k_row_dots(const double* __restrict__ A, const double* __restrict__ B, long ld, long len, long n,
+                           long n_pad, double* __restrict__ out) {
+  const long i = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_pad) return;
+  double sacc = 0.0;
+  if (i < n)
+    for (long r = lane; r < len; r += 32) sacc = fma(A[i * ld + r], B[i * ld + r], sacc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if (lane == 0) out[i] = sacc;
+}
+void row_dots(const double* A, const double* B, long ld, long len, long n, long n_pad, double* out, cudaStream_t s) {
+  k_row_dots<<<nblk(n_pad * 32), 256, 0, s>>>(A, B, ld, len, n, n_pad, out);
+  FSA_LAUNCH_CHECK();
+}
+
 void update_h2(double* H, const double* Z, double* Vlr, const double* Lw, const int* active, const double* beta,
                long n, long tp, long k, cudaStream_t s) {
   k_update_h2<<<nblk(n * tp / 2), 256, 0, s>>>(H, Z, Vlr, Lw, active, beta, n, tp, k);

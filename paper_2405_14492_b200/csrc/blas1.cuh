@@ -62,6 +62,11 @@ void update_uh(double* UH, const double* W, const int* active, const double* bet
 void update_h(double* H, const double* Z, const int* active, const double* beta, long n, long tp, long k,
               cudaStream_t s);
 void init_h(double* H, const double* Z, const int* active, long n, long tp, long k, cudaStream_t s);
+// scalar sums of the exact FITC traces: out[7] (see blas1.cu)
+void trace_sums(const double* p, const double* d1, const double* dD, const double* f, const double* D, long n,
+                const double* Qi, const double* K2, long m, double* out, cudaStream_t s);
+// out[i] = sum_{r < len} A[i*ld + r] B[i*ld + r] for i < n (0 for n <= i < n_pad); warp per row
+void row_dots(const double* A, const double* B, long ld, long len, long n, long n_pad, double* out, cudaStream_t s);
 // H = Z + beta H and Vlr = Lw + beta Vlr on the active columns (tp even)
 void update_h2(double* H, const double* Z, double* Vlr, const double* Lw, const int* active, const double* beta,
                long n, long tp, long k, cudaStream_t s);

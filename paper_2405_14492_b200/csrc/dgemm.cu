@@ -235,4 +235,31 @@ void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, lo
   FSA_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void k_mirror_lower(double* A, long ld, long m) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= m * m) return;
+  const long r = idx / m, c = idx % m;
+  if (c > r) A[r * ld + c] = A[c * ld + r];
+}
+}  // namespace
+
+void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, double* out, long ldo, double alpha,
+               double* scratch, cudaStream_t s) {
+  require(Mr % 128 == 0 && K % 16 == 0, "gemm_syrk: unpadded shape");
+  if (Mr == 0) return;
+  const long N = Mr;
+  const ReducePlan p = plan_reduce(Mr, N, K);
+  dim3 grid(static_cast<unsigned>(Mr / p.bm), static_cast<unsigned>(N / (p.nt * 8)), static_cast<unsigned>(p.splits));
+  if (p.bm == 128)
+    dispatch_nt<ReduceCfg8>(p.nt, M, ldm, M, ldm, scale, K, p.kchunk, grid, EpiPartialLower{scratch, Mr, N}, s);
+  else
+    dispatch_nt<ReduceCfg>(p.nt, M, ldm, M, ldm, scale, K, p.kchunk, grid, EpiPartialLower{scratch, Mr, N}, s);
+  k_splitk_reduce<<<static_cast<unsigned>(cdiv(Mr * N, 256)), 256, 0, s>>>(scratch, p.splits, Mr, N, out, ldo, alpha,
+                                                                         0.0);
+  FSA_LAUNCH_CHECK();
+  k_mirror_lower<<<static_cast<unsigned>(cdiv(Mr * N, 256)), 256, 0, s>>>(out, ldo, Mr);
+  FSA_LAUNCH_CHECK();
+}
+
 }  // namespace fsa

@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(Cfg::THREADS)
   const long n0 = static_cast<long>(blockIdx.y) * BN;
   const long kb = static_cast<long>(blockIdx.z) * kchunk;
   const long ke = kb + kchunk < K ? kb + kchunk : K;
+  if constexpr (Epi::kLower) {  // symmetric result: tiles strictly above the diagonal are mirrored later
+    if (n0 >= m0 + BM) return;
+  }
   const int nk = ke > kb ? static_cast<int>((ke - kb) / BK) : 0;
 
   auto load_stage = [&](int st, long k0) {
@@ -184,6 +187,7 @@ __global__ void __launch_bounds__(Cfg::THREADS)
 // ---- epilogues -------------------------------------------------------------------
 struct EpiNoDot {
   static constexpr bool kDot = false;
+  static constexpr bool kLower = false;
   double* partial = nullptr;
   long ldp = 0;
 };
@@ -221,6 +225,10 @@ struct EpiPartial : EpiNoDot {  // split-K partial tile: W[z][r][c]
     return make_double2(0.0, 0.0);
   }
 };
+struct EpiPartialLower : EpiPartial {  // lower-triangle tiles only (symmetric products)
+  static constexpr bool kLower = true;
+  using EpiPartial::EpiPartial;
+};
 struct EpiProbe : EpiNoDot {  // z = U^T e1 + sqrt(D) e2  (FITC sample, preconditioners.cpp:69-73)
   double* Y;
   long ld;
@@ -239,6 +247,7 @@ struct EpiProbe : EpiNoDot {  // z = U^T e1 + sqrt(D) e2  (FITC sample, precondi
 template <bool DOT>
 struct EpiWoodburyT {
   static constexpr bool kDot = DOT;
+  static constexpr bool kLower = false;
   double* partial;
   long ldp;
   double* Z;
@@ -260,6 +269,7 @@ using EpiWoodburyDot = EpiWoodburyT<true>;
 // the PCG's m-space recurrence for Sigma H) and the per-CTA r . z partials
 struct EpiWoodburyKeep {
   static constexpr bool kDot = true;
+  static constexpr bool kLower = false;
   double* partial;
   long ldp;
   double* Z;
@@ -311,5 +321,8 @@ void gemm_km(const double* A, long lda, long Mr, long K, const double* B, long l
 void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, long ldv, long N,
                  const double* scale, double* out, long ldo, double alpha, double beta, double* scratch,
                  cudaStream_t s);
+// symmetric variant (V = M, N = Mr): out = alpha M diag(s) M^T, lower tiles computed and mirrored
+void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, double* out, long ldo, double alpha,
+               double* scratch, cudaStream_t s);
 
 }  // namespace fsa

@@ -234,13 +234,22 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   U1.alloc(mp * np);
   T.alloc(mp * np);
   launch_cross_cov(ind.get(), m, m, geo->pts.coords.get(), np, n, np, d, P.nu, P.sigma1_2, P.rho, 1, U1.get(), mp, s);
-  trsm_lower_cols(L.get(), mp, U1.get(), mp, np, dinv_scratch.get(), s);
-  FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
-  gemm_expand_store(U.get(), mp, np, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+  {
+    KTimer t1(ctx, "rho_trsm", 1.0 * mp * mp * np);
+    trsm_lower_cols(L.get(), mp, U1.get(), mp, np, dinv_scratch.get(), s);
+  }
+  {
+    KTimer t2(ctx, "rho_T_gemm", 2.0 * m * m * n);
+    FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+    gemm_expand_store(U.get(), mp, np, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+  }
   const Csr& pat = geo->pat;
   dsval.alloc(pat.nnz > 0 ? pat.nnz : 1);
   SddmmParams sp{P.nu, P.family, P.sigma2, P.sigma1_2, P.rho, P.gamma};
-  sddmm_drho(U.get(), U1.get(), T.get(), mp, pat, lowrank.get(), sp, dsval.get(), s);
+  {
+    KTimer t3(ctx, "rho_sddmm", 4.0 * m * pat.nnz / 2);
+    sddmm_drho(U.get(), U1.get(), T.get(), mp, pat, lowrank.get(), sp, dsval.get(), s);
+  }
   dD.alloc(np);
   extract_diag(dsval.get(), pat.diagpos.get(), n, np, dD.get(), nullptr, nullptr, s);
   // padding rows of dD must be zero (extract_diag writes 1)
@@ -347,8 +356,8 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
   {
     const size_t need = gemm_reduce_scratch(mp, mp, np);
     if (md->red_scratch.n < need) md->red_scratch.alloc(need);
-    gemm_reduce(md->U.get(), mp, mp, np, md->U.get(), mp, mp, md->Dinv.get(), Q.get(), mp, 1.0, 0.0,
-                md->red_scratch.get(), s);
+    KTimer tq(md->ctx, "setup_fitc_syrk", 1.0 * mp * mp * np);
+    gemm_syrk(md->U.get(), mp, mp, np, md->Dinv.get(), Q.get(), mp, 1.0, md->red_scratch.get(), s);
   }
   add_identity(Q.get(), mp, mp, s);
   FSA_CUDA(cudaMemcpyAsync(LQ.get(), Q.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s));
@@ -448,41 +457,25 @@ double FitcPrecond::deriv_trace(int k) {
     cudaStream_t s = md->ctx->stream;
     const long mp = md->m_pad, np = md->n_pad, n = md->n;
     md->ensure_rho_derivs();
-    DBuf<double> V(mp * np), q(np), pinv(np), d1(np), F(mp * mp);
+    KTimer tt(md->ctx, "grad_exact_traces", 2.0 * mp * mp * np);
+    // V = LQ^{-1} U, W1 = LQ^{-1} U1: q_i = |V_i|^2 (diag P^{-1}), and
+    // <Q^{-1}, U D^{-1} U1^T> = sum_i (V_i . W1_i) / D_i
+    DBuf<double> V(mp * np), W1(mp * np), q(np), f(np), pinv(np), d1(np);
     FSA_CUDA(cudaMemcpyAsync(V.get(), md->U.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+    FSA_CUDA(cudaMemcpyAsync(W1.get(), md->U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
     trsm_lower_cols(LQ.get(), mp, V.get(), mp, np, md->dinv_scratch.get(), s);
+    trsm_lower_cols(LQ.get(), mp, W1.get(), mp, np, md->dinv_scratch.get(), s);
     colnorm2(V.get(), mp, mp, n, np, q.get(), s);
+    row_dots(V.get(), W1.get(), mp, mp, n, np, f.get(), s);
     pinv_diag(pinv.get(), md->D.get(), q.get(), n, np, s);
     affine_vec(d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, s);
-    // sum pinv (k = 0), pinv . d1, pinv . dD
-    std::vector<double> hp(static_cast<size_t>(np)), hd1(static_cast<size_t>(np)), hdD(static_cast<size_t>(np));
-    FSA_CUDA(cudaMemcpyAsync(hp.data(), pinv.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaMemcpyAsync(hd1.data(), d1.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaMemcpyAsync(hdD.data(), md->dD.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
-    const size_t need = gemm_reduce_scratch(mp, mp, np);
-    if (md->red_scratch.n < need) md->red_scratch.alloc(need);
-    gemm_reduce(md->U.get(), mp, mp, np, md->U1.get(), mp, mp, md->Dinv.get(), F.get(), mp, 1.0, 0.0,
-                md->red_scratch.get(), s);
-    std::vector<double> hQi(static_cast<size_t>(mp * mp)), hF(hQi.size()), hK2(hQi.size());
-    FSA_CUDA(cudaMemcpyAsync(hQi.data(), Qinv.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaMemcpyAsync(hF.data(), F.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaMemcpyAsync(hK2.data(), md->K2.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToHost, s));
+    DBuf<double> sums(8);
+    trace_sums(pinv.get(), d1.get(), md->dD.get(), f.get(), md->D.get(), n, Qinv.get(), md->K2.get(), mp,
+               sums.get(), s);
+    double hs[7];
+    FSA_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
-    double s0 = 0, s1 = 0, s2 = 0;
-    for (long i = 0; i < n; ++i) {
-      s0 += hp[static_cast<size_t>(i)];
-      s1 += hp[static_cast<size_t>(i)] * hd1[static_cast<size_t>(i)];
-      s2 += hp[static_cast<size_t>(i)] * hdD[static_cast<size_t>(i)];
-    }
-    double trQi = 0, qf = 0, trK2 = 0, k2q = 0;
-    for (long r = 0; r < mp; ++r) {
-      trQi += hQi[static_cast<size_t>(r * mp + r)];
-      trK2 += hK2[static_cast<size_t>(r * mp + r)];
-    }
-    for (size_t idx = 0; idx < hQi.size(); ++idx) {
-      qf += hQi[idx] * hF[idx];
-      k2q += hK2[idx] * hQi[idx];
-    }
+    const double s0 = hs[0], s1 = hs[1], s2 = hs[2], qf = hs[3], trQi = hs[4], trK2 = hs[5], k2q = hs[6];
     trace[0] = s0;
     trace[1] = s1 + (static_cast<double>(mp) - trQi) / md->P.sigma1_2;
     trace[2] = s2 + 2.0 * qf - (trK2 - k2q);
@@ -659,19 +652,25 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   if (num_active > 0 && opts.error_on_max_iter) throw NumericalError("cg: no convergence within max_iter");
   res.iterations.resize(static_cast<size_t>(k));
   res.converged.resize(static_cast<size_t>(k));
-  std::vector<double> td(static_cast<size_t>(2 * k * maxit));
-  FSA_CUDA(cudaMemcpyAsync(res.iterations.data(), st.iterations, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
-  FSA_CUDA(cudaMemcpyAsync(res.converged.data(), st.converged, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
-  FSA_CUDA(cudaMemcpyAsync(td.data(), st.tdiag, sizeof(double) * 2 * k * maxit, cudaMemcpyDeviceToHost, s));
+  // only the first `sweeps` entries of each column's tridiagonal can be set: strided copy
+  // into pinned staging (2 k sweeps doubles instead of 2 k max_iter)
+  const long used = res.sweeps > 0 ? res.sweeps : 1;
+  ctx->pin1.ensure(static_cast<size_t>(2 * k * used + 2 * k));
+  double* td = ctx->pin1.p;
+  int* hint = reinterpret_cast<int*>(td + 2 * k * used);
+  FSA_CUDA(cudaMemcpyAsync(hint, st.iterations, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpyAsync(hint + k, st.converged, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaMemcpy2DAsync(td, sizeof(double) * used, st.tdiag, sizeof(double) * maxit, sizeof(double) * used,
+                             2 * k, cudaMemcpyDeviceToHost, s));
   FSA_CUDA(cudaStreamSynchronize(s));
+  res.iterations.assign(hint, hint + k);
+  res.converged.assign(hint + k, hint + 2 * k);
   res.tdiag.resize(static_cast<size_t>(k));
   res.toff.resize(static_cast<size_t>(k));
   for (long j = 0; j < k; ++j) {
     const int it = res.iterations[static_cast<size_t>(j)];
-    res.tdiag[static_cast<size_t>(j)].assign(td.begin() + j * maxit, td.begin() + j * maxit + it);
-    if (it > 1)
-      res.toff[static_cast<size_t>(j)].assign(td.begin() + k * maxit + j * maxit,
-                                              td.begin() + k * maxit + j * maxit + it - 1);
+    res.tdiag[static_cast<size_t>(j)].assign(td + j * used, td + j * used + it);
+    if (it > 1) res.toff[static_cast<size_t>(j)].assign(td + (k + j) * used, td + (k + j) * used + it - 1);
   }
   return res;
 }
@@ -822,8 +821,10 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   {
     DBuf<double> raw(static_cast<size_t>(n * (1 + p)));
     unpack_cols(Xs.get(), n, 1 + p, md->geo->pts.perm_d.get(), tp, L, raw.get(), s);
-    FSA_CUDA(cudaMemcpyAsync(uS.data(), raw.get(), sizeof(double) * n * (1 + p), cudaMemcpyDeviceToHost, s));
+    ctx->pin2.ensure(static_cast<size_t>(n * (1 + p)));
+    FSA_CUDA(cudaMemcpyAsync(ctx->pin2.p, raw.get(), sizeof(double) * n * (1 + p), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
+    std::copy(ctx->pin2.p, ctx->pin2.p + n * (1 + p), uS.begin());
   }
   std::vector<double> u(uS.begin(), uS.begin() + n), resid(y, y + n);
   if (p > 0) {

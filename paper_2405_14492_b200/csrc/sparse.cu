@@ -478,18 +478,20 @@ void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows,
               const double* Y0) {
   if (nrows == 0) return;
   const long nb = spmm_dot_blocks(nrows);
-  const int nch = static_cast<int>(cdiv(ncols, 64));
   const unsigned g = static_cast<unsigned>(nb);
   const double* y0 = Y0 != nullptr ? Y0 : Y;
-  switch (nch) {
-    case 1: k_spmm_dot<1><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
-    case 2: k_spmm_dot<2><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
-    case 3:
-    case 4: k_spmm_dot<4><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X, ldx, Y, ldy, ncols, alpha, beta, partial, y0); break;
-    default: throw std::invalid_argument("spmm_dot: more than 256 columns");
+  for (long c0 = 0; c0 < ncols; c0 += 256) {  // 256-column slabs (prediction solves use ~m columns)
+    const long w = ncols - c0 < 256 ? ncols - c0 : 256;
+    const int nch = static_cast<int>(cdiv(w, 64));
+    double* part = partial + c0 * nb;
+    switch (nch) {
+      case 1: k_spmm_dot<1><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+      case 2: k_spmm_dot<2><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+      default: k_spmm_dot<4><<<g, 256, 0, s>>>(rowptr, col, val, nrows, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+    }
+    FSA_LAUNCH_CHECK();
+    colsum_partials(part, nb, w, w, dot + c0, s);
   }
-  FSA_LAUNCH_CHECK();
-  colsum_partials(partial, nb, ncols, ncols, dot, s);
 }
 
 void launch_spmm(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx,

@@ -220,6 +220,22 @@ def test_prediction_matches_oracle():
     assert np.abs(cvs["var"] - ocv["var"]).max() < 1e-6
 
 
+def test_prediction_many_inducing_matches_oracle():
+    """m = 300 inducing points: the deterministic pieces solve with m_pad = 384 right-hand
+    sides (column slabs in the SpMM, N-tiled GEMMs)."""
+    locs, ind, kw, md, om = setup(n=3000, m=300, seed=43, gamma=0.05, rho=0.08)
+    plocs = O.uniform_locations(500, 2, 143)
+    pr, opr = fsa.make_prediction_set(md, plocs), O.PredictionSet(om, plocs)
+    d = pr.det_pieces(tol=1e-3, tol_s=1e-3)
+    od = opr.det_pieces(tol=1e-3, tol_s=1e-3)
+    assert d[3] == od[3]
+    for a, b in zip(d[:3], od[:3]):
+        assert np.abs(a - b).max() < 1e-8 * max(1.0, np.abs(b).max())
+    sim = pr.predict_var_sim(num_probes=260, seed=3)  # two probe batches (256 + 4)
+    osim = opr.predict_var_sim(num_probes=260, seed=3)
+    assert np.abs(sim["var"] - osim["var"]).max() < 1e-6
+
+
 def test_sim_variance_converges_to_exact():  # test_prediction.cpp:105-125
     locs = O.uniform_locations(200, 2, 17)
     plocs = O.uniform_locations(50, 2, 117)
