@@ -89,6 +89,24 @@ int fsa_ctx_reset_timers(fsa_ctx* ctx);
 int fsa_ctx_timer_names(fsa_ctx* ctx, char* buf, size_t len); /* newline separated */
 int fsa_ctx_timer(fsa_ctx* ctx, const char* name, double* ms, int64_t* count, double* units);
 
+/* ---- row-sharded contexts (multi-GPU fit path; no reference counterpart: the
+ * reference is one process over OpenMP threads, fsa.cpp / krylov.cpp) ------------------
+ * Rank r of W owns a contiguous block of the space-filling-curve-sorted points. Each PCG
+ * sweep exchanges halo rows with the ranks whose points are within the taper range and
+ * sums the m x t projections and per-column dots. Host inputs stay global (every rank
+ * passes all n points, in the caller's order); results (nll, gradient, beta) are identical
+ * on every rank. On a sharded context only the geometry / assemble / FITC preconditioner /
+ * iterative_nll_grad path is available; the host-block entry points return FSA_EINVAL. */
+/* 128-byte NCCL unique id (rank 0 creates it and broadcasts it, e.g. over torch.distributed) */
+int fsa_nccl_unique_id(void* id_out);
+/* one process per GPU: NCCL over NVLink/NVSwitch (libnccl.so.2 is loaded on first use) */
+int fsa_ctx_create_nccl(int device, int rank, int world, const void* unique_id, fsa_ctx** out);
+/* W contexts on one device whose collectives are host barriers + device copies; each context
+ * must be driven by its own host thread, all making the same calls (test vehicle for the
+ * sharded decomposition on a single GPU) */
+int fsa_ctx_group_create(int device, int world, fsa_ctx** out /* array of world handles */);
+int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world);
+
 /* ---- input generators (host; same RNG streams as the reference) -------------------- */
 /* uniform_locations (locations.cpp:9-17) */
 int fsa_uniform_locations(int64_t n, int d, uint64_t seed, double* coords_out);
@@ -111,7 +129,9 @@ int fsa_probe_rademacher(uint64_t seed, uint64_t index, int64_t n, double* z);
 /* ---- geometry: sorted points + taper pattern (GridIndex/taper_pattern, locations.cpp:19-163) */
 int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, double gamma, fsa_geometry** out);
 void fsa_geometry_destroy(fsa_geometry* g);
-int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz);
+int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz); /* nnz of this rank's rows */
+/* this rank's block [r0, r1) of the internal order and its halo size (0, n, 0 on one rank) */
+int fsa_geometry_shard_info(fsa_geometry* g, int64_t* r0, int64_t* r1, int64_t* n_halo);
 /* taper_pattern output in the caller's order: distances as values */
 int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist);
 /* internal (space-filling-curve) order: perm[internal] = original index */

@@ -10,12 +10,12 @@ namespace fsa {
 
 namespace {
 
-__global__ void k_pack(const double* __restrict__ in, long n, long k, const int* __restrict__ perm, long n_pad,
-                       long tp, long col0, double* __restrict__ out) {
+__global__ void k_pack(const double* __restrict__ in, long ld_in, long n, long k, const int* __restrict__ perm,
+                       long n_pad, long tp, long col0, double* __restrict__ out) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n_pad * k) return;
   const long i = idx / k, j = idx % k;
-  out[i * tp + col0 + j] = i < n ? in[static_cast<long>(perm[i]) + j * n] : 0.0;
+  out[i * tp + col0 + j] = i < n ? in[static_cast<long>(perm[i]) + j * ld_in] : 0.0;
 }
 
 __global__ void k_copy_cols(const double* __restrict__ src, long lds, double* __restrict__ dst, long ldd, long n,
@@ -367,7 +367,13 @@ void update_uh(double* UH, const double* W, const int* active, const double* bet
 void pack_cols(const double* in_dev, long n, long k, const int* perm_dev, long n_pad, long tp, long col0,
                double* out, cudaStream_t s) {
   if (k == 0) return;
-  k_pack<<<nblk(n_pad * k), 256, 0, s>>>(in_dev, n, k, perm_dev, n_pad, tp, col0, out);
+  k_pack<<<nblk(n_pad * k), 256, 0, s>>>(in_dev, n, n, k, perm_dev, n_pad, tp, col0, out);
+  FSA_LAUNCH_CHECK();
+}
+void pack_cols_ld(const double* in_dev, long ld_in, long n, long k, const int* perm_dev, long n_pad, long tp,
+                  long col0, double* out, cudaStream_t s) {
+  if (k == 0) return;
+  k_pack<<<nblk(n_pad * k), 256, 0, s>>>(in_dev, ld_in, n, k, perm_dev, n_pad, tp, col0, out);
   FSA_LAUNCH_CHECK();
 }
 void copy_cols(const double* src, long lds, double* dst, long ldd, long n, long k, cudaStream_t s) {
@@ -487,6 +493,67 @@ __global__ void k_row_dots(const double* __restrict__ A, const double* __restric
 }
 void row_dots(const double* A, const double* B, long ld, long len, long n, long n_pad, double* out, cudaStream_t s) {
   k_row_dots<<<nblk(n_pad * 32), 256, 0, s>>>(A, B, ld, len, n, n_pad, out);
+  FSA_LAUNCH_CHECK();
+}
+
+// cross Gram of two narrow column groups: partial[b][a*q + c] over block b's rows, then a
+// fixed-order sum over the blocks (deterministic, independent of timing)
+constexpr int kGramBlocks = kNumSMs;
+__global__ void __launch_bounds__(256) k_cross_gram(const double* __restrict__ A, long lda,
+                                                    const double* __restrict__ B, long ldb, long n, int q,
+                                                    double* __restrict__ partial) {
+  __shared__ double red[8];
+  const long per = (n + gridDim.x - 1) / gridDim.x;
+  const long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int pr = 0; pr < q * q; ++pr) {
+    const int a = pr / q, c = pr % q;
+    double v = 0.0;
+    for (long i = i0 + threadIdx.x; i < i1; i += blockDim.x) v = fma(A[i * lda + a], B[i * ldb + c], v);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      partial[static_cast<long>(blockIdx.x) * q * q + pr] = t;
+    }
+    __syncthreads();
+  }
+}
+__global__ void k_cross_gram_sum(const double* __restrict__ partial, int nb, int qq, double* __restrict__ out) {
+  const int pr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pr >= qq) return;
+  double t = 0.0;
+  for (int b = 0; b < nb; ++b) t += partial[static_cast<long>(b) * qq + pr];
+  out[pr] = t;
+}
+size_t cross_gram_scratch(long q) { return static_cast<size_t>(kGramBlocks) * static_cast<size_t>(q * q); }
+void cross_gram(const double* A, long lda, const double* B, long ldb, long n, long q, double* out, double* scratch,
+                cudaStream_t s) {
+  if (q == 0) return;
+  k_cross_gram<<<kGramBlocks, 256, 0, s>>>(A, lda, B, ldb, n, static_cast<int>(q), scratch);
+  FSA_LAUNCH_CHECK();
+  k_cross_gram_sum<<<nblk(q * q, 128), 128, 0, s>>>(scratch, kGramBlocks, static_cast<int>(q * q), out);
+  FSA_LAUNCH_CHECK();
+}
+
+// out[i * ldo] = X[i * ldx] - sum_a X[i * ldx + 1 + a] coef[a] for i < n (0 on padding rows < n_pad)
+__global__ void k_gls_residual(const double* __restrict__ X, long ldx, long p, const double* __restrict__ coef,
+                               long n, long n_pad, double* __restrict__ out, long ldo) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  double v = 0.0;
+  if (i < n) {
+    v = X[i * ldx];
+    for (long a = 0; a < p; ++a) v -= X[i * ldx + 1 + a] * coef[a];
+  }
+  out[i * ldo] = v;
+}
+void gls_residual(const double* X, long ldx, long p, const double* coef_dev, long n, long n_pad, double* out, long ldo,
+                  cudaStream_t s) {
+  k_gls_residual<<<nblk(n_pad), 256, 0, s>>>(X, ldx, p, coef_dev, n, n_pad, out, ldo);
   FSA_LAUNCH_CHECK();
 }
 

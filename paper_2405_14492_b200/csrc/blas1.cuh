@@ -34,6 +34,9 @@ void launch_coldot_weighted(const double* A, const double* B, const double* w, l
 // columns [col0, col0 + k) of a row-major n_pad x tp internal-order block (padding rows zeroed)
 void pack_cols(const double* in_dev, long n, long k, const int* perm_dev, long n_pad, long tp, long col0,
                double* out, cudaStream_t s);
+// same with an input column stride ld_in (n rows of a longer array: a rank's rows)
+void pack_cols_ld(const double* in_dev, long ld_in, long n, long k, const int* perm_dev, long n_pad, long tp,
+                  long col0, double* out, cudaStream_t s);
 // dst[i][j] = src[i][j] for i < n, j < k (row-major blocks of different widths)
 void copy_cols(const double* src, long lds, double* dst, long ldd, long n, long k, cudaStream_t s);
 void sum_log(const double* x, long n, double* out_dev, cudaStream_t s);
@@ -70,6 +73,13 @@ void row_dots(const double* A, const double* B, long ld, long len, long n, long 
 // H = Z + beta H and Vlr = Lw + beta Vlr on the active columns (tp even)
 void update_h2(double* H, const double* Z, double* Vlr, const double* Lw, const int* active, const double* beta,
                long n, long tp, long k, cudaStream_t s);
+// out[a * q + c] = sum_{i < n} A[i * lda + a] B[i * ldb + c] (a, c < q; deterministic)
+size_t cross_gram_scratch(long q);
+void cross_gram(const double* A, long lda, const double* B, long ldb, long n, long q, double* out, double* scratch,
+                cudaStream_t s);
+// GLS residual column: out[i * ldo] = X[i * ldx] - sum_a X[i * ldx + 1 + a] coef[a]
+void gls_residual(const double* X, long ldx, long p, const double* coef_dev, long n, long n_pad, double* out, long ldo,
+                  cudaStream_t s);
 void scale_rows(double* Y, const double* X, const double* w, long n, long tp, cudaStream_t s);
 void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_t s);
 

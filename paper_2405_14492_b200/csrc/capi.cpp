@@ -62,6 +62,13 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + " is null");
 }
 
+// entry points whose host buffers hold every point (caller order) exist on one rank only;
+// a row-sharded context runs the fit path (iterative_nll_grad) alone
+void single_rank(const Context* c, const char* what) {
+  if (c->comm->size() != 1)
+    throw std::invalid_argument(std::string(what) + " is not available on a row-sharded context");
+}
+
 Params to_params(const fsa_params* p) {
   need(p, "params");
   Params q;
@@ -152,6 +159,45 @@ int fsa_ctx_create(int device, fsa_ctx** out) {
   });
 }
 void fsa_ctx_destroy(fsa_ctx* ctx) { delete ctx; }
+int fsa_nccl_unique_id(void* id_out) {
+  return guard([&] {
+    need(id_out, "id_out");
+    nccl_unique_id(id_out);
+  });
+}
+int fsa_ctx_create_nccl(int device, int rank, int world, const void* unique_id, fsa_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    need(unique_id, "unique_id");
+    require(world >= 1 && rank >= 0 && rank < world, "rank out of range");
+    auto c = std::make_unique<fsa_ctx>();
+    c->c = std::make_unique<Context>(device);
+    if (world > 1) c->c->comm = std::make_unique<NcclComm>(rank, world, unique_id);
+    *out = c.release();
+  });
+}
+int fsa_ctx_group_create(int device, int world, fsa_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    require(world >= 1, "group size must be positive");
+    std::vector<std::unique_ptr<fsa_ctx>> made;
+    auto comms = make_thread_group(world);
+    for (int r = 0; r < world; ++r) {
+      auto c = std::make_unique<fsa_ctx>();
+      c->c = std::make_unique<Context>(device);
+      c->c->comm = std::move(comms[static_cast<size_t>(r)]);
+      made.push_back(std::move(c));
+    }
+    for (int r = 0; r < world; ++r) out[r] = made[static_cast<size_t>(r)].release();
+  });
+}
+int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (rank) *rank = ctx->c->comm->rank();
+    if (world) *world = ctx->c->comm->size();
+  });
+}
 int fsa_ctx_synchronize(fsa_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");
@@ -250,9 +296,20 @@ int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz) {
     if (nnz) *nnz = g->g->pat.nnz;
   });
 }
+int fsa_geometry_shard_info(fsa_geometry* g, int64_t* r0, int64_t* r1, int64_t* n_halo) {
+  return guard([&] {
+    need(g, "geometry");
+    const ShardPlan& sp = g->g->shard;
+    const bool one = sp.world <= 1;
+    if (r0) *r0 = one ? 0 : sp.r0;
+    if (r1) *r1 = one ? g->g->pts.n : sp.r1;
+    if (n_halo) *n_halo = one ? 0 : sp.n_halo;
+  });
+}
 int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist) {
   return guard([&] {
     need(g, "geometry");
+    single_rank(g->ctx->c.get(), "taper_pattern export");
     export_csr(g->g->pat, g->g->pat.dist.get(), g->g->pts, g->g->pts, g->ctx->c->stream, rowptr, col, dist);
   });
 }
@@ -323,7 +380,7 @@ int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t*
   return guard([&] {
     need(md, "model");
     Model& M = *md->m;
-    if (n) *n = M.n;
+    if (n) *n = M.geo->pts.n;  // all points (a sharded rank owns a row block of them)
     if (m) *m = M.m;
     if (nnz) *nnz = M.geo->pat.nnz;
     if (n_clamped) *n_clamped = M.n_clamped;
@@ -334,6 +391,7 @@ int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, d
   return guard([&] {
     need(md, "model");
     Model& M = *md->m;
+    single_rank(M.ctx, "Sigma_s export");
     require(which == 0 || which == 1, "which must be 0 (sigma_s) or 1 (d sigma_s / d rho)");
     if (which == 1) M.ensure_rho_derivs();
     export_csr(M.geo->pat, which == 0 ? M.sval.get() : M.dsval.get(), M.geo->pts, M.geo->pts, M.ctx->stream,
@@ -344,6 +402,7 @@ int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out) {
   return guard([&] {
     need(md, "model");
     Model* M = md->m.get();
+    single_rank(M->ctx, "matmat");
     require(k >= 1, "matrix row mismatch");
     const long tp = pad_cols(k);
     DBuf<double> in = to_device_block(M, V, k, tp);
@@ -356,6 +415,7 @@ int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k,
   return guard([&] {
     need(md, "model");
     Model* M = md->m.get();
+    single_rank(M->ctx, "matmat");
     require(k >= 1, "matrix row mismatch");
     const long tp = pad_cols(k);
     DBuf<double> in = to_device_block(M, V, k, tp);
@@ -368,6 +428,7 @@ int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {
   return guard([&] {
     need(md, "model");
     Model* M = md->m.get();
+    single_rank(M->ctx, "diagonals");
     cudaStream_t s = M->ctx->stream;
     DBuf<double> raw(static_cast<size_t>(M->n));
     if (sdiag) {
@@ -397,6 +458,7 @@ int fsa_make_jacobi(fsa_model* md, fsa_precond** out) {
     need(md, "model");
     auto p = std::make_unique<fsa_precond>();
     p->md = md;
+    single_rank(md->m->ctx, "the Jacobi preconditioner");
     p->p = std::make_unique<DiagPrecond>(md->m.get(), false);
     *out = p.release();
   });
@@ -412,6 +474,7 @@ int fsa_precond_solve_mat(fsa_precond* p, const double* R, int64_t k, double* ou
   return guard([&] {
     need(p, "preconditioner");
     Model* M = p->md->m.get();
+    single_rank(M->ctx, "solve_mat");
     const long tp = pad_cols(k);
     DBuf<double> in = to_device_block(M, R, k, tp);
     DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
@@ -424,6 +487,7 @@ int fsa_precond_sample_probes(fsa_precond* p, int L, uint64_t seed, double* Z) {
     need(p, "preconditioner");
     require(L > 0, "need at least one probe");
     Model* M = p->md->m.get();
+    single_rank(M->ctx, "sample_probes");
     const long tp = pad_cols(L);
     DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
     p->p->sample_probes(L, seed, o.get(), tp);
@@ -446,6 +510,7 @@ int fsa_pcg_solve_multi(fsa_model* md, fsa_precond* p, int op_kind, const double
     need(md, "model");
     need(p, "preconditioner");
     Model* M = md->m.get();
+    single_rank(M->ctx, "pcg_solve_multi on host blocks");
     const CgOptions o = to_cg(cg);
     const long tp = pad_cols(k);
     DBuf<double> Bd = to_device_block(M, B, k, tp);
@@ -498,6 +563,7 @@ int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** 
   return guard([&] {
     need(md, "model");
     need(pcoords, "pcoords");
+    single_rank(md->m->ctx, "prediction");
     auto pr = std::make_unique<fsa_pred>();
     pr->md = md;
     pr->p = make_prediction_set(md->m.get(), pcoords, np);

@@ -115,10 +115,48 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
   g->coords_host.assign(coords, coords + n * d);
   const CellGrid grid = make_grid(coords, n, d, gamma, nullptr, 0);
   sort_points(coords, n, d, grid, round_up(n, 128), g->pts, ctx->stream);
-  build_pattern(g->pts, g->pts, gamma, true, g->pat, ctx->stream);
+  const int world = ctx->comm->size(), rank = ctx->comm->rank();
+  if (world == 1) {
+    build_pattern(g->pts, g->pts, gamma, true, g->pat, ctx->stream);
+    g->shard.n = g->shard.n_loc = g->shard.r1 = n;
+    g->shard.n_loc_pad = g->shard.n_ext_pad = g->pts.n_pad;
+  } else {
+    // every rank derives the same global order and pattern, then keeps its row block
+    Csr full;
+    build_pattern(g->pts, g->pts, gamma, true, full, ctx->stream);
+    shard_pattern(full, g->pts, rank, world, g->shard, g->pat, ctx->stream);
+  }
   build_row_blocks(g->pat, ctx->stream);
   ctx->sync();
   return g;
+}
+
+// Matern (mode 0) or its rho derivative (mode 1) between the inducing points and the
+// extended point set (owned rows, zero padding, halo points): column-per-point m_pad x n_ext_pad
+void Model::cross_cov_ext(int mode, double* out) {
+  const ShardPlan& sp = geo->shard;
+  cudaStream_t s = ctx->stream;
+  launch_cross_cov(ind.get(), m, m, geo->coords_ext(), n_ext_pad, n, n_pad, d, P.nu, P.sigma1_2, P.rho, mode, out,
+                   m_pad, s);
+  if (n_ext_pad > n_pad)
+    launch_cross_cov(ind.get(), m, m, geo->coords_ext() + n_pad, n_ext_pad, sp.n_halo, n_ext_pad - n_pad, d, P.nu,
+                     P.sigma1_2, P.rho, mode, out + n_pad * m_pad, m_pad, s);
+}
+
+void Model::halo_exchange(double* X, long tp) {
+  if (world() == 1) return;
+  const ShardPlan& sp = geo->shard;
+  cudaStream_t s = ctx->stream;
+  KTimer t(ctx, "halo_exchange");
+  long total = 0;
+  for (long c : sp.send_cnt) total += c;
+  if (halo_send.n < static_cast<size_t>(total * tp)) halo_send.alloc(static_cast<size_t>(total * tp));
+  gather_rows(X, tp, sp.send_idx.get(), total, halo_send.get(), s);
+  std::vector<HaloPeer> peers;
+  for (size_t q = 0; q < sp.peer.size(); ++q)
+    peers.push_back(HaloPeer{sp.peer[q], halo_send.get() + sp.send_off[q] * tp, sp.send_cnt[q] * tp,
+                             X + (n_pad + sp.recv_off[q]) * tp, sp.recv_cnt[q] * tp});
+  ctx->comm->exchange(peers, s);
 }
 
 // ---- model --------------------------------------------------------------------------------------
@@ -141,8 +179,14 @@ double* Model::mt_buf(int which, long tp) {
 void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
   const size_t need = gemm_reduce_scratch(m_pad, tp, n_pad);
   if (red_scratch.n < need) red_scratch.alloc(need);
-  KTimer t(ctx, "lowrank_project", 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp));
-  gemm_reduce(M, m_pad, m_pad, n_pad, V, tp, tp, scale, out, tp, 1.0, 0.0, red_scratch.get(), ctx->stream);
+  {
+    KTimer t(ctx, "lowrank_project", 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp));
+    gemm_reduce(M, m_pad, m_pad, n_pad, V, tp, tp, scale, out, tp, 1.0, 0.0, red_scratch.get(), ctx->stream);
+  }
+  if (world() > 1) {  // m x t partials of the row blocks
+    KTimer t(ctx, "allreduce");
+    ctx->comm->allreduce(out, m_pad * tp, ctx->stream);
+  }
 }
 
 std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> geo, const double* inducing, long m,
@@ -157,13 +201,15 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   M.ctx = ctx;
   M.geo = geo;
   M.P = p;
-  M.n = geo->pts.n;
-  M.n_pad = geo->pts.n_pad;
+  require(geo->shard.world == ctx->comm->size(), "geometry built for another communicator");
+  M.n = geo->shard.n_loc;
+  M.n_pad = geo->shard.n_loc_pad;
+  M.n_ext_pad = geo->shard.n_ext_pad;
   M.d = geo->pts.d;
   M.m = m;
   M.m_pad = round_up(m, 128);
   require(M.m_pad <= 1024, "more than 1024 inducing points are not supported");
-  const long mp = M.m_pad, np = M.n_pad;
+  const long mp = M.m_pad, np = M.n_pad, ne = M.n_ext_pad;
   M.ind_host.assign(inducing, inducing + m * M.d);
   M.ind.alloc(m * M.d);
   FSA_CUDA(cudaMemcpyAsync(M.ind.get(), inducing, sizeof(double) * m * M.d, cudaMemcpyHostToDevice, s));
@@ -182,17 +228,16 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
     potrf_lower(M.L.get(), mp, M.info.get(), M.dinv_scratch.get(), s);
     launch_logdet_diag(M.L.get(), mp, m, scal.get(), s);
   }
-  // U = L^{-1} Sigma_mn (fsa.cpp:32-35)
-  M.U.alloc(mp * np);
+  // U = L^{-1} Sigma_mn (fsa.cpp:32-35), for the owned and the halo points
+  M.U.alloc(mp * ne);
   M.lowrank.alloc(np);
   {
     KTimer t(ctx, "setup_cross_cov");
-    launch_cross_cov(M.ind.get(), m, m, geo->pts.coords.get(), np, M.n, np, M.d, p.nu, p.sigma1_2, p.rho, 0,
-                     M.U.get(), mp, s);
+    M.cross_cov_ext(0, M.U.get());
   }
   {
-    KTimer t(ctx, "setup_trsm", 1.0 * mp * mp * np);
-    trsm_lower_cols(M.L.get(), mp, M.U.get(), mp, np, M.dinv_scratch.get(), s);
+    KTimer t(ctx, "setup_trsm", 1.0 * mp * mp * ne);
+    trsm_lower_cols(M.L.get(), mp, M.U.get(), mp, ne, M.dinv_scratch.get(), s);
   }
   colnorm2(M.U.get(), mp, mp, M.n, np, M.lowrank.get(), s);
   // Sigma_s on the taper pattern (fsa.cpp:37-56)
@@ -231,17 +276,18 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   launch_transpose(tmp.get(), mp, mp, mp, K2.get(), mp, s);
   trsm_lower_cols(L.get(), mp, K2.get(), mp, mp, dinv_scratch.get(), s);   // L^{-1} X^T
   // U1 = L^{-1} dSigma_mn/drho ; T = U1 - K2 U
-  U1.alloc(mp * np);
-  T.alloc(mp * np);
-  launch_cross_cov(ind.get(), m, m, geo->pts.coords.get(), np, n, np, d, P.nu, P.sigma1_2, P.rho, 1, U1.get(), mp, s);
+  const long ne = n_ext_pad;
+  U1.alloc(mp * ne);
+  T.alloc(mp * ne);
+  cross_cov_ext(1, U1.get());
   {
-    KTimer t1(ctx, "rho_trsm", 1.0 * mp * mp * np);
-    trsm_lower_cols(L.get(), mp, U1.get(), mp, np, dinv_scratch.get(), s);
+    KTimer t1(ctx, "rho_trsm", 1.0 * mp * mp * ne);
+    trsm_lower_cols(L.get(), mp, U1.get(), mp, ne, dinv_scratch.get(), s);
   }
   {
     KTimer t2(ctx, "rho_T_gemm", 2.0 * m * m * n);
-    FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
-    gemm_expand_store(U.get(), mp, np, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+    FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * ne, cudaMemcpyDeviceToDevice, s));
+    gemm_expand_store(U.get(), mp, ne, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
   }
   const Csr& pat = geo->pat;
   dsval.alloc(pat.nnz > 0 ? pat.nnz : 1);
@@ -259,11 +305,8 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
 
 void Model::sigma_s_mat(const double* H, double* V, long tp, double alpha, double beta) {
   KTimer t(ctx, "spmm", 12.0 * geo->pat.nnz + (beta == 0.0 ? 16.0 : 24.0) * n * (cols_hint > 0 ? cols_hint : tp));
-  if (tp <= 128 && geo->pat.nblk > 0)
-    spmm_staged(geo->pat, sval.get(), H, tp, V, tp, tp, alpha, beta, nullptr, nullptr, ctx->stream);
-  else
-    launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta,
-                ctx->stream);
+  launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta,
+              ctx->stream);
 }
 
 // V = Sigma H = U^T (U H) + Sigma_s H   (fsa.cpp:65-68)
@@ -358,6 +401,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     if (md->red_scratch.n < need) md->red_scratch.alloc(need);
     KTimer tq(md->ctx, "setup_fitc_syrk", 1.0 * mp * mp * np);
     gemm_syrk(md->U.get(), mp, mp, np, md->Dinv.get(), Q.get(), mp, 1.0, md->red_scratch.get(), s);
+    md->ctx->comm->allreduce(Q.get(), mp * mp, s);  // sum of the row blocks' U_i D_i^{-1} U_i^T
   }
   add_identity(Q.get(), mp, mp, s);
   FSA_CUDA(cudaMemcpyAsync(LQ.get(), Q.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s));
@@ -381,6 +425,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     FSA_CUDA(cudaMemcpyAsync(hs, scal.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
     if (hinfo != 0) throw NumericalError("preconditioner core matrix is not positive definite");
+    md->ctx->comm->allreduce_host(hs + 1, 1, s);  // sum log d over all rows
     logdetQ = hs[0];
     ld = hs[0] + hs[1];  // logdet(core) - logdet(Sigma_m) + sum log d   (preconditioners.cpp:53-55)
   }
@@ -411,10 +456,12 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
     gemm_expand_probe(md->U.get(), mp, np, mp, pc.E1.get(), tp, tp, Z, tp, md->sqrtD.get(), pc.E2.get(), s);
     return;
   }
+  // each probe's stream draws e1 (m) then e2 over ALL n points; a rank keeps its rows of e2
+  const long nf = md->geo->shard.n, r0 = md->geo->shard.r0;
   PinnedBuf& e1h = md->ctx->pin1;  // host staging owned by the context
   PinnedBuf& e2h = md->ctx->pin2;
   e1h.ensure(static_cast<size_t>(mp * tp));
-  e2h.ensure(static_cast<size_t>(n * L));
+  e2h.ensure(static_cast<size_t>(nf * L));
   double* e1p = e1h.p;
   double* e2p = e2h.p;
   std::memset(e1p, 0, sizeof(double) * mp * tp);
@@ -422,15 +469,15 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
   double* e1c = e1col.data();
 #pragma omp parallel for schedule(dynamic, 1)
   for (int i = 0; i < L; ++i)
-    probe_gaussian(seed, static_cast<unsigned long long>(i), m, e1c + static_cast<long>(i) * m, n,
-                   e2p + static_cast<long>(i) * n);
+    probe_gaussian(seed, static_cast<unsigned long long>(i), m, e1c + static_cast<long>(i) * m, nf,
+                   e2p + static_cast<long>(i) * nf);
   for (int i = 0; i < L; ++i)
     for (long r = 0; r < m; ++r) e1p[r * tp + i] = e1col[static_cast<size_t>(i) * m + r];
-  DBuf<double> E1(mp * tp), E2(np * tp), raw(n * L);
+  DBuf<double> E1(mp * tp), E2(np * tp), raw(nf * L);
   FSA_CUDA(cudaMemcpyAsync(E1.get(), e1h.p, sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
-  FSA_CUDA(cudaMemcpyAsync(raw.get(), e2h.p, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
+  FSA_CUDA(cudaMemcpyAsync(raw.get(), e2h.p, sizeof(double) * nf * L, cudaMemcpyHostToDevice, s));
   FSA_CUDA(cudaMemsetAsync(E2.get(), 0, sizeof(double) * np * tp, s));
-  pack_cols(raw.get(), n, L, md->geo->pts.perm_d.get(), np, tp, 0, E2.get(), s);
+  pack_cols_ld(raw.get(), nf, n, L, md->geo->pts.perm_d.get() + r0, np, tp, 0, E2.get(), s);
   {
     KTimer t(md->ctx, "probe_expand", 2.0 * mp * np * tp);
     gemm_expand_probe(md->U.get(), mp, np, mp, E1.get(), tp, tp, Z, tp, md->sqrtD.get(), E2.get(), s);
@@ -475,6 +522,7 @@ double FitcPrecond::deriv_trace(int k) {
     double hs[7];
     FSA_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
+    md->ctx->comm->allreduce_host(hs, 4, s);  // sums over rows; the m x m sums are replicated
     const double s0 = hs[0], s1 = hs[1], s2 = hs[2], qf = hs[3], trQi = hs[4], trK2 = hs[5], k2q = hs[6];
     trace[0] = s0;
     trace[1] = s1 + (static_cast<double>(mp) - trQi) / md->P.sigma1_2;
@@ -485,6 +533,7 @@ double FitcPrecond::deriv_trace(int k) {
 }
 
 std::unique_ptr<Precond> make_preconditioner(Model* md, int type) {  // estimation.cpp:160-176
+  require(md->world() == 1 || type == 2, "row-sharded models support the FITC preconditioner only");
   switch (type) {
     case 0: return std::make_unique<IdentityPrecond>(md);
     case 1: return std::make_unique<DiagPrecond>(md, true);
@@ -525,13 +574,16 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   FsaOp* fop = dynamic_cast<FsaOp*>(&A);
   FitcPrecond* fitc = dynamic_cast<FitcPrecond*>(&P);
   const bool fused = fop != nullptr && fitc != nullptr;
+  require(fused || md->world() == 1, "row-sharded solves need the FSA operator with the FITC preconditioner");
+  Comm& comm = *ctx->comm;
   CgWork& w = *ctx->cgw;
   if (w.R.n < blk) {
     w.R.alloc(blk);
-    w.H.alloc(blk);
     w.V.alloc(blk);
     w.Z.alloc(blk);
   }
+  const size_t ext_blk = static_cast<size_t>(md->n_ext_pad * tp);  // H carries the halo rows
+  if (w.H.n < ext_blk) w.H.alloc(ext_blk);
   if (fused && w.Lw.n < blk) {
     w.Lw.alloc(blk);
     w.Vlr.alloc(blk);
@@ -583,6 +635,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       KTimer t(ctx, "lowrank_expand", flops_mn);
       gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
                                 md->Dinv.get(), rzout, part, s);
+      comm.allreduce(rzout, tp, s);
     } else {
       P.solve(w.R.get(), w.Z.get(), tp);
       KTimer t(ctx, "cg_blas1");
@@ -593,6 +646,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   {
     KTimer t(ctx, "cg_blas1");
     launch_coldot(w.R.get(), w.R.get(), n, tp, k, rr, part, s);
+    comm.allreduce(rr, k, s);
     cg_start(rr, k, opts.tol, st, s);
   }
   precond(rz);
@@ -614,6 +668,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   CgResult res;
   for (int it = 0; it < maxit && num_active > 0; ++it) {
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
+      md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
       static const int staged = std::getenv("FSA_SPMM") ? std::atoi(std::getenv("FSA_SPMM")) : 0;
       if (staged && tp <= 128 && md->geo->pat.nblk > 0)
@@ -622,6 +677,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       else
         spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
                  tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
+      comm.allreduce(hv, tp, s);
     } else {
       A.apply(w.H.get(), w.V.get(), tp);
       KTimer t(ctx, "cg_blas1");
@@ -631,6 +687,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       KTimer t(ctx, "cg_blas1");
       cg_alpha(hv, k, it, maxit, st, s);
       update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
+      comm.allreduce(rr, k, s);
       cg_check(rr, k, opts.tol, st, s);
     }
     precond(rz);
@@ -763,12 +820,6 @@ static std::vector<double> small_spd_solve(std::vector<double> G, long p, std::v
   return b;
 }
 
-static double dotv(const double* a, const double* b, long n) {
-  double s = 0.0;
-  for (long i = 0; i < n; ++i) s += a[i] * b[i];
-  return s;
-}
-
 NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* Xc, long p, int L,
                              unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad) {
   require(L > 0, "nll: need at least one probe");
@@ -781,6 +832,10 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   }
   Context* ctx = md->ctx;
   cudaStream_t s = ctx->stream;
+  // Row sharding: this rank holds rows [r0, r0 + n) of the N sorted points; every
+  // global scalar (dots, Gram, traces) is a sum of rank partials.
+  Comm& comm = *ctx->comm;
+  const long N = md->geo->pts.n, r0 = md->world() > 1 ? md->geo->shard.r0 : 0;
   const long n = md->n, np = md->n_pad, mp = md->m_pad;
   const long k = L + 1 + p;
   const long tp = pad_cols(k);
@@ -788,15 +843,16 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   FSA_CUDA(cudaEventRecord(e0, s));
   DBuf<double> B(static_cast<size_t>(np * tp)), Xs(static_cast<size_t>(np * tp));
   P.sample_probes(L, seed, B.get(), tp);  // columns [0, L)
+  const int* perm_loc = md->geo->pts.perm_d.get() + r0;
   if (resident) {
-    pack_cols(md->geo->resp_dev.get(), n, 1 + p, md->geo->pts.perm_d.get(), np, tp, L, B.get(), s);
+    pack_cols_ld(md->geo->resp_dev.get(), N, n, 1 + p, perm_loc, np, tp, L, B.get(), s);
   } else {
-    std::vector<double> yx(static_cast<size_t>(n * (1 + p)));
-    std::copy(y, y + n, yx.begin());
-    if (p > 0) std::copy(Xc, Xc + n * p, yx.begin() + n);
-    DBuf<double> raw(static_cast<size_t>(n * (1 + p)));
-    FSA_CUDA(cudaMemcpyAsync(raw.get(), yx.data(), sizeof(double) * n * (1 + p), cudaMemcpyHostToDevice, s));
-    pack_cols(raw.get(), n, 1 + p, md->geo->pts.perm_d.get(), np, tp, L, B.get(), s);
+    std::vector<double> yx(static_cast<size_t>(N * (1 + p)));
+    std::copy(y, y + N, yx.begin());
+    if (p > 0) std::copy(Xc, Xc + N * p, yx.begin() + N);
+    DBuf<double> raw(static_cast<size_t>(N * (1 + p)));
+    FSA_CUDA(cudaMemcpyAsync(raw.get(), yx.data(), sizeof(double) * N * (1 + p), cudaMemcpyHostToDevice, s));
+    pack_cols_ld(raw.get(), N, n, 1 + p, perm_loc, np, tp, L, B.get(), s);
     FSA_CUDA(cudaStreamSynchronize(s));
   }
   FsaOp op(md);
@@ -808,63 +864,66 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   out.cg_iterations = sol.max_iterations();
   out.sweeps = sol.sweeps;
   for (int it : sol.iterations) out.rhs_iterations += it;
-  std::vector<double> q(static_cast<size_t>(L));
+  std::vector<double> quad(static_cast<size_t>(L));
 #pragma omp parallel for schedule(dynamic, 1)
   for (int i = 0; i < L; ++i)
-    q[static_cast<size_t>(i)] = tridiag_log_quadrature(sol.tdiag[static_cast<size_t>(i)], sol.toff[static_cast<size_t>(i)]);
+    quad[static_cast<size_t>(i)] =
+        tridiag_log_quadrature(sol.tdiag[static_cast<size_t>(i)], sol.toff[static_cast<size_t>(i)]);
   double acc = 0.0;
-  for (int i = 0; i < L; ++i) acc += q[static_cast<size_t>(i)];
-  out.logdet = static_cast<double>(n) / static_cast<double>(L) * acc + P.logdet();  // estimation.cpp:198-200
+  for (int i = 0; i < L; ++i) acc += quad[static_cast<size_t>(i)];
+  out.logdet = static_cast<double>(N) / static_cast<double>(L) * acc + P.logdet();  // estimation.cpp:198-200
 
-  // u and the GLS coefficients (estimation.cpp:202-212), original order on the host
-  std::vector<double> uS(static_cast<size_t>(n * (1 + p)));
+  // u and the GLS coefficients (estimation.cpp:202-212) from the cross Gram
+  // C[a][c] = [y|X]_a . Sigma^{-1}[y|X]_c of the packed columns (q = 1 + p)
+  const long q = 1 + p;
+  std::vector<double> C(static_cast<size_t>(q * q));
   {
-    DBuf<double> raw(static_cast<size_t>(n * (1 + p)));
-    unpack_cols(Xs.get(), n, 1 + p, md->geo->pts.perm_d.get(), tp, L, raw.get(), s);
-    ctx->pin2.ensure(static_cast<size_t>(n * (1 + p)));
-    FSA_CUDA(cudaMemcpyAsync(ctx->pin2.p, raw.get(), sizeof(double) * n * (1 + p), cudaMemcpyDeviceToHost, s));
+    DBuf<double> Cd(static_cast<size_t>(q * q)), scr(cross_gram_scratch(q));
+    cross_gram(B.get() + L, tp, Xs.get() + L, tp, n, q, Cd.get(), scr.get(), s);
+    comm.allreduce(Cd.get(), q * q, s);
+    FSA_CUDA(cudaMemcpyAsync(C.data(), Cd.get(), sizeof(double) * q * q, cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
-    std::copy(ctx->pin2.p, ctx->pin2.p + n * (1 + p), uS.begin());
   }
-  std::vector<double> u(uS.begin(), uS.begin() + n), resid(y, y + n);
+  auto Cx = [&](long a, long c) { return C[static_cast<size_t>(a * q + c)]; };
+  double quad_form = Cx(0, 0);  // resid' Sigma^{-1} resid = y'u0 - 2 b'(X'u0) + b'Gb (G symmetric part)
   if (p > 0) {
-    const double* SX = uS.data() + n;
-    std::vector<double> G(static_cast<size_t>(p * p)), Gs(G.size()), rhs(static_cast<size_t>(p));
+    std::vector<double> Gs(static_cast<size_t>(p * p)), rhs(static_cast<size_t>(p));
     for (long a = 0; a < p; ++a)
-      for (long b = 0; b < p; ++b) G[static_cast<size_t>(a + b * p)] = dotv(Xc + a * n, SX + b * n, n);
-    for (long a = 0; a < p; ++a)
-      for (long b = 0; b < p; ++b)
-        Gs[static_cast<size_t>(a + b * p)] = 0.5 * (G[static_cast<size_t>(a + b * p)] + G[static_cast<size_t>(b + a * p)]);
-    for (long a = 0; a < p; ++a) rhs[static_cast<size_t>(a)] = dotv(SX + a * n, y, n);
+      for (long b = 0; b < p; ++b) Gs[static_cast<size_t>(a + b * p)] = 0.5 * (Cx(1 + a, 1 + b) + Cx(1 + b, 1 + a));
+    for (long a = 0; a < p; ++a) rhs[static_cast<size_t>(a)] = Cx(0, 1 + a);  // y . Sigma^{-1} X_a
     out.beta = small_spd_solve(Gs, p, rhs);
-    for (long a = 0; a < p; ++a)
-      for (long i = 0; i < n; ++i) {
-        u[static_cast<size_t>(i)] -= SX[i + a * n] * out.beta[static_cast<size_t>(a)];
-        resid[static_cast<size_t>(i)] -= Xc[i + a * n] * out.beta[static_cast<size_t>(a)];
-      }
+    for (long a = 0; a < p; ++a) {
+      const double ba = out.beta[static_cast<size_t>(a)];
+      quad_form -= ba * (Cx(1 + a, 0) + Cx(0, 1 + a));
+      for (long b = 0; b < p; ++b) quad_form += ba * Cx(1 + a, 1 + b) * out.beta[static_cast<size_t>(b)];
+    }
   }
   constexpr double log2pi = 1.8378770664093454836;
-  out.nll = 0.5 * (out.logdet + dotv(resid.data(), u.data(), n) + static_cast<double>(n) * log2pi);
+  out.nll = 0.5 * (out.logdet + quad_form + static_cast<double>(N) * log2pi);
 
   if (want_grad) {
     // STE gradient traces (krylov.cpp:163-206, estimation.cpp:217-225), U-form:
     // columns [0, L) hold the probes, column L holds u so that u' dSigma_k u comes
     // out of the same batched quadratic forms.
     const long t2 = pad_cols(L + 1);
-    DBuf<double> Zb(np * t2), Wb(np * t2), Yb(np * t2), SY(np * t2), ub(np);
+    const long ne = md->n_ext_pad;  // Yb carries the halo rows for the Sigma_s products
+    DBuf<double> Zb(np * t2), Wb(np * t2), Yb(ne * t2), SY(np * t2);
     FSA_CUDA(cudaMemsetAsync(Zb.get(), 0, sizeof(double) * np * t2, s));
     FSA_CUDA(cudaMemsetAsync(Wb.get(), 0, sizeof(double) * np * t2, s));
     copy_cols(B.get(), tp, Zb.get(), t2, np, L, s);
     copy_cols(Xs.get(), tp, Wb.get(), t2, np, L, s);
     {
-      DBuf<double> raw(n);
-      FSA_CUDA(cudaMemcpyAsync(raw.get(), u.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
-      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Zb.get(), s);
-      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Wb.get(), s);
+      // u = Sigma^{-1} (y - X beta) = Xs[:, L] - SX beta, written into column L
+      DBuf<double> coef(static_cast<size_t>(std::max<long>(p, 1)));
+      if (p > 0)
+        FSA_CUDA(cudaMemcpyAsync(coef.get(), out.beta.data(), sizeof(double) * p, cudaMemcpyHostToDevice, s));
+      gls_residual(Xs.get() + L, tp, p, coef.get(), n, np, Zb.get() + L, t2, s);
+      copy_cols(Zb.get() + L, t2, Wb.get() + L, t2, np, 1, s);
       P.solve(Zb.get(), Yb.get(), t2);
-      pack_cols(raw.get(), n, 1, md->geo->pts.perm_d.get(), np, t2, L, Yb.get(), s);
+      copy_cols(Zb.get() + L, t2, Yb.get() + L, t2, np, 1, s);
       FSA_CUDA(cudaStreamSynchronize(s));
     }
+    md->halo_exchange(Yb.get(), t2);
     const bool rho_needed = true;
     if (rho_needed) md->ensure_rho_derivs();
     DBuf<double> UY(mp * t2), UW(mp * t2), U1Y(mp * t2), U1W(mp * t2), K2UY(mp * t2), d1(np);
@@ -876,22 +935,26 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
     affine_vec(d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, s);
     const long nd = 12;
     DBuf<double> dots(static_cast<size_t>(nd * t2));
+    FSA_CUDA(cudaMemsetAsync(dots.get(), 0, sizeof(double) * nd * t2, s));
     double* sc = md->dot_scratch.get();
     auto dd = [&](int slot) { return dots.get() + slot * t2; };
+    // n-space dots (rank partials, summed below) ...
     launch_coldot(Wb.get(), Yb.get(), n, t2, t2, dd(0), sc, s);           // w.y
     launch_coldot(Yb.get(), Yb.get(), n, t2, t2, dd(1), sc, s);           // y.y
     md->sigma_s_mat(Yb.get(), SY.get(), t2);
     launch_coldot(Wb.get(), SY.get(), n, t2, t2, dd(2), sc, s);           // w.Ss y
-    launch_coldot(UW.get(), UY.get(), mp, t2, t2, dd(3), sc, s);          // Uw.Uy
     launch_coldot_weighted(Yb.get(), Yb.get(), d1.get(), n, t2, t2, dd(4), sc, s);  // y.d1 y
-    launch_coldot(UY.get(), UY.get(), mp, t2, t2, dd(5), sc, s);          // |Uy|^2
     launch_spmm(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->dsval.get(), n, Yb.get(), t2, SY.get(), t2,
                 t2, 1.0, 0.0, s);
     launch_coldot(Wb.get(), SY.get(), n, t2, t2, dd(6), sc, s);           // w.dSs y
+    launch_coldot_weighted(Yb.get(), Yb.get(), md->dD.get(), n, t2, t2, dd(10), sc, s);  // y.dD y
+    comm.allreduce(dots.get(), nd * t2, s);
+    // ... m-space dots of the (already summed) projections
+    launch_coldot(UW.get(), UY.get(), mp, t2, t2, dd(3), sc, s);          // Uw.Uy
+    launch_coldot(UY.get(), UY.get(), mp, t2, t2, dd(5), sc, s);          // |Uy|^2
     launch_coldot(U1W.get(), UY.get(), mp, t2, t2, dd(7), sc, s);         // U1w.Uy
     launch_coldot(UW.get(), U1Y.get(), mp, t2, t2, dd(8), sc, s);         // Uw.U1y
     launch_coldot(UW.get(), K2UY.get(), mp, t2, t2, dd(9), sc, s);        // Uw.K2Uy
-    launch_coldot_weighted(Yb.get(), Yb.get(), md->dD.get(), n, t2, t2, dd(10), sc, s);  // y.dD y
     launch_coldot(U1Y.get(), UY.get(), mp, t2, t2, dd(11), sc, s);        // U1y.Uy  (dd(9)-style K2 term below)
     std::vector<double> h(static_cast<size_t>(nd * t2));
     DBuf<double> uk(t2);

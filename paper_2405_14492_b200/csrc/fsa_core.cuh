@@ -17,8 +17,10 @@
 #include <vector>
 
 #include "blas1.cuh"
+#include "comm.cuh"
 #include "common.cuh"
 #include "pattern.cuh"
+#include "shard.cuh"
 
 namespace fsa {
 
@@ -47,6 +49,7 @@ struct PinnedBuf {
 struct Context {
   std::unique_ptr<CgWork> cgw{new CgWork()};
   PinnedBuf pin1, pin2;
+  std::unique_ptr<Comm> comm{new SelfComm()};  // rank / world of the row sharding
   int device = 0;
   cudaStream_t stream = nullptr;
   int* host_flags = nullptr;  // pinned, mapped
@@ -94,9 +97,11 @@ struct Params {
 // reference rebuilds it on every evaluation (fsa.cpp:37, estimation.cpp:260);
 // here it is built once and shared by every Model assembled on it.
 struct Geometry {
-  SortedPoints pts;
-  Csr pat;
+  SortedPoints pts;   // all points, global internal (Hilbert) order
+  Csr pat;            // this rank's rows; columns in extended (local | halo) indexing
+  ShardPlan shard;    // row block, halo and exchange plan (trivial for one rank)
   double gamma = 0.0;
+  const double* coords_ext() const { return shard.world > 1 ? shard.coords_ext.get() : pts.coords.get(); }
   std::vector<double> coords_host;  // original order, n x d column-major
   // Fit-loop residency: the response [y | X] and the FITC probe
   // draws e1/e2 are parameter independent, so a fit keeps them in HBM.
@@ -119,7 +124,8 @@ class Model {
   Context* ctx = nullptr;
   std::shared_ptr<Geometry> geo;
   Params P;
-  long n = 0, m = 0, n_pad = 0, m_pad = 0;
+  long n = 0, m = 0, n_pad = 0, m_pad = 0;  // n, n_pad: rows owned by this rank
+  long n_ext_pad = 0;  // owned + halo points (U, U1, T and gathered RHS blocks have this many rows)
   long cols_hint = 0;  // real RHS columns of the running solve (timer units)
   int d = 2;
   std::vector<double> ind_host;  // m x d column-major
@@ -145,9 +151,14 @@ class Model {
   void matmat(const double* H, double* V, long tp);
   void sigma_s_mat(const double* H, double* V, long tp, double alpha = 1.0, double beta = 0.0);
   void deriv_matmat(int which, const double* V, double* out, long tp);
-  // m_pad x tp projection U V (deterministic split-K)
+  // m_pad x tp projection U V (deterministic split-K), summed over ranks
   void project(const double* M, const double* V, long tp, double* out, const double* scale = nullptr);
   double* mt_buf(int which, long tp);
+  // refresh the halo rows [n_pad, n_pad + n_halo) of an extended block (no-op on one rank)
+  void halo_exchange(double* X, long tp);
+  void cross_cov_ext(int mode, double* out);
+  int world() const { return ctx->comm->size(); }
+  DBuf<double> halo_send;
 };
 
 // ---- preconditioners (preconditioners.h:16-115) ------------------------------------------

@@ -68,7 +68,7 @@ __global__ void k_sddmm_sigma_s(const double* __restrict__ U, long ldu, const lo
       const double d = dist[p];
       const double v = (matern_d(d, P.nu, P.sigma1_2, P.rho) - dt) * taper_d(d, P.family, P.gamma);
       val[p] = v;
-      val[mirror[p]] = v;
+      if (mirror[p] >= 0) val[mirror[p]] = v;  // halo columns: the mirror lives on another rank
     }
   }
 }
@@ -108,7 +108,7 @@ __global__ void k_sddmm_drho(const double* __restrict__ U, const double* __restr
         const double d = dist[p];
         const double v = (matern_drho_d(d, P.nu, P.sigma1_2, P.rho) - dl) * taper_d(d, P.family, P.gamma);
         val[p] = v;
-        val[mirror[p]] = v;
+        if (mirror[p] >= 0) val[mirror[p]] = v;  // halo columns: the mirror lives on another rank
       }
     }
   }

@@ -65,6 +65,10 @@ _SIGS = {
     "fsa_version": (C.c_int, []),
     "fsa_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "fsa_ctx_destroy": (None, [_vp]),
+    "fsa_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "fsa_ctx_create_nccl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
+    "fsa_ctx_group_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_vp)]),
+    "fsa_ctx_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fsa_ctx_synchronize": (C.c_int, [_vp]),
     "fsa_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fsa_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
@@ -84,6 +88,7 @@ _SIGS = {
     "fsa_geometry_destroy": (None, [_vp]),
     "fsa_geometry_info": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
     "fsa_geometry_pattern": (C.c_int, [_vp, _lp, _ip, _dp]),
+    "fsa_geometry_shard_info": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
     "fsa_geometry_permutation": (C.c_int, [_vp, _ip]),
     "fsa_geometry_set_response": (C.c_int, [_vp, _dp, _vp, _i64]),
     "fsa_geometry_cache_probes": (C.c_int, [_vp, C.c_int]),
@@ -216,13 +221,45 @@ def tridiag_log_quadrature(diag, off):
 
 
 # ---- device objects -------------------------------------------------------------------------
-class Context:
-    """One CUDA device + stream (one host thread per context)."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id; rank 0 creates it and broadcasts it to the other ranks."""
+    buf = C.create_string_buffer(128)
+    _check(lib().fsa_nccl_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, device=0):
-        h = _vp()
-        _check(lib().fsa_ctx_create(device, C.byref(h)))
+
+class Context:
+    """One CUDA device + stream (one host thread per context).
+
+    ``Context.nccl(device, rank, world, uid)`` makes rank ``rank`` of a row-sharded
+    multi-GPU job (one process per GPU); ``Context.group(device, world)`` makes ``world``
+    sharded ranks on one device, each to be driven by its own host thread.
+    """
+
+    def __init__(self, device=0, _handle=None):
+        if _handle is None:
+            h = _vp()
+            _check(lib().fsa_ctx_create(device, C.byref(h)))
+        else:
+            h = _handle
         self.h = h
+
+    @classmethod
+    def nccl(cls, device, rank, world, unique_id: bytes):
+        h = _vp()
+        _check(lib().fsa_ctx_create_nccl(device, rank, world, bytes(unique_id), C.byref(h)))
+        return cls(_handle=h)
+
+    @classmethod
+    def group(cls, device, world):
+        hs = (_vp * world)()
+        _check(lib().fsa_ctx_group_create(device, world, hs))
+        return [cls(_handle=_vp(hs[r])) for r in range(world)]
+
+    def rank_world(self):
+        r, w = C.c_int(), C.c_int()
+        _check(lib().fsa_ctx_rank(self.h, C.byref(r), C.byref(w)))
+        return r.value, w.value
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -293,6 +330,12 @@ class Geometry:
         val = _F(np.zeros(max(nnz, 1)))
         _check(lib().fsa_geometry_pattern(self.h, ptr, idx, val))
         return ptr, idx[:nnz], val[:nnz]
+
+    def shard_info(self):
+        """(r0, r1, n_halo): this rank's block of the internal order and its halo size."""
+        a, b, c = _i64(), _i64(), _i64()
+        _check(lib().fsa_geometry_shard_info(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     def permutation(self):
         p = np.zeros(self.n, np.int32)
