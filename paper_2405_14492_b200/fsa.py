@@ -498,7 +498,8 @@ def iterative_nll_grad(model: FsaModel, P: Preconditioner, y, X=None, num_probes
     cg = _cg(tol, max_iter)
     beta = _F(np.zeros(max(p, 1)))
     _check(lib().fsa_iterative_nll_grad(model.h, P.h, None if y is None else y.ctypes.data,
-                                        None if Xf is None else Xf.ctypes.data, p, num_probes, seed,
+                                        None if Xf is None else Xf.ctypes.data, 0 if y is None else p,
+                                        num_probes, seed,
                                         C.byref(cg), CV_CODE[cv], 1 if want_grad else 0, C.byref(res),
                                         beta.ctypes.data))
     return {"nll": res.nll, "grad": np.array(res.grad[:]), "logdet": res.logdet, "cg_iterations": res.cg_iterations,
