@@ -178,6 +178,10 @@ def cpu_pcg_sample(cfg, coords, ind, gamma, sweeps=2):
     return its / dt, its, dt
 
 
+def last_sweeps(results):
+    return int(results[-1]["sweeps"]) if results else 0
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -270,8 +274,14 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--mode", default="weak", choices=["weak", "strong", "replicas"],
+                    help="N>1: weak = n scales with N (row-sharded, n/N rows per GPU fixed); strong = the "
+                         "config's n row-sharded over N GPUs; replicas = N independent copies")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env > 1 and args.mode == "weak":
+        cfg["n"] = cfg["n"] * world_env
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -306,7 +316,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    ctx = fsa.Context(local)
+    # rows of one problem split over the ranks: NCCL halo exchange + allreduce (--mode strong at
+    # N = 1 runs the same NCCL-context code path with one rank)
+    sharded = args.mode != "replicas" and (world > 1 or args.mode == "strong")
+    if sharded:
+        uid = [fsa.nccl_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
+        ctx = fsa.Context.nccl(local, rank, world, uid[0])
+    else:
+        ctx = fsa.Context(local)
     coords, ind, gamma, y = make_inputs(cfg, fsa)
     if gamma is None:
         gamma = calibrate_gamma(coords, cfg["nnz"], fsa, ctx)
@@ -351,7 +370,8 @@ def main():
     ms = max_over_ranks(ms)
     timers = ctx.timers()
     ctx.set_profiling(False)
-    rhs_its = sum(r["rhs_iterations"] for r in results) * world
+    copies = 1 if sharded else world  # replicas each solve the whole problem
+    rhs_its = sum(r["rhs_iterations"] for r in results) * copies
     value = rhs_its / (ms * 1e-3)
     pcg_ms = statistics.median(r["pcg_ms"] for r in results)
     pcg_rate = results[-1]["rhs_iterations"] / (pcg_ms * 1e-3)
@@ -392,11 +412,13 @@ def main():
         if i > 0:
             e2e_ms.append(max_over_ranks(dt * 1e3))
     e2e_step_ms = statistics.median(e2e_ms) if e2e_ms else float("nan")
-    e2e_value = results[-1]["rhs_iterations"] * world / (e2e_step_ms * 1e-3) if e2e_ms else None
+    e2e_value = results[-1]["rhs_iterations"] * copies / (e2e_step_ms * 1e-3) if e2e_ms else None
     k = L + 1
     tp = k if k <= 72 else k
-    h2d = 8 * (n * 2 + m * 2 + n + m * L + n * L + n)
-    d2h = 8 * (n + 2 * k * 1000 + 2 * n)
+    # every rank uploads coords (n x 2), inducing (m x 2) and y (n); reads back nll, grad and the
+    # Lanczos coefficients of its columns
+    h2d = 8 * world * (n * 2 + m * 2 + n)
+    d2h = 8 * world * (5 + 2 * k * last_sweeps(results))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -414,11 +436,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "RHS-iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config)",
-            "config": {"workload": f"config{args.config}: loglik+grad, FITC-PCG", "n": n, "m": m, "nnz": nnz,
+            "scaling": "strong" if (sharded and args.mode == "strong") else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded; BASELINE config)",
+            "config": {"workload": (f"config{args.config}: loglik+grad, FITC-PCG"
+                                    + (f", n = {n // world} x {world} GPUs" if sharded and args.mode == "weak" else "")),
+                       "n": n, "m": m, "nnz": nnz,
                        "avg_row_nnz": nnz / n, "probes": L, "rhs": k, "tol": tol, "nu": cfg["nu"],
                        "rho": cfg["rho"], "sigma2": cfg["s2"], "sigma1_2": cfg["s12"], "gamma": gamma,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"row-sharded x{world} ({args.mode}; NCCL halo exchange + allreduce)"
+                                       if sharded else ("replicas" if world > 1 else "single")),
                        "l2": "inputs larger than L2 (U is m x n fp64 = %.0f MB)" % (8 * m * n / 1e6)},
             "loglik_grad_ms": step_ms, "pcg_ms": pcg_ms, "pcg_only_rhs_iter_per_s": pcg_rate,
             "cg_iterations": last["cg_iterations"], "sweeps": last["sweeps"], "nll": last["nll"],

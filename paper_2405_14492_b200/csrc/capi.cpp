@@ -172,7 +172,7 @@ int fsa_ctx_create_nccl(int device, int rank, int world, const void* unique_id, 
     require(world >= 1 && rank >= 0 && rank < world, "rank out of range");
     auto c = std::make_unique<fsa_ctx>();
     c->c = std::make_unique<Context>(device);
-    if (world > 1) c->c->comm = std::make_unique<NcclComm>(rank, world, unique_id);
+    c->c->comm = std::make_unique<NcclComm>(rank, world, unique_id);
     *out = c.release();
   });
 }

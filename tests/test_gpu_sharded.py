@@ -134,3 +134,15 @@ def test_sharded_context_rejects_host_block_calls():
         return errs
 
     assert run_ranks(fsa.Context.group(0, 2), body) == [4, 4]
+
+
+def test_nccl_context_single_rank():
+    """NCCL communicator path (dlopen, unique id, init) at world size 1 gives the plain answer."""
+    locs, ind, kw, y, X = problem(2500, 40, 0.06, 51, p=1)
+    one = nll_on(fsa.Context(0), locs, ind, kw, y, X, L=6)
+    uid = fsa.nccl_unique_id()
+    assert len(uid) == 128
+    c = fsa.Context.nccl(0, 0, 1, uid)
+    assert c.rank_world() == (0, 1)
+    r = nll_on(c, locs, ind, kw, y, X, L=6)
+    assert r["nll"] == one["nll"] and np.array_equal(r["grad"], one["grad"])
