@@ -83,6 +83,9 @@ int fsa_ctx_create(int device, fsa_ctx** out);
 void fsa_ctx_destroy(fsa_ctx* ctx);
 int fsa_ctx_synchronize(fsa_ctx* ctx);
 int fsa_ctx_stream(fsa_ctx* ctx, void** stream); /* cudaStream_t all kernels run on */
+/* dense m x n passes with the low-rank factor: 0 auto (INT8 tensor-core Ozaki emulation of the fp64
+ * product when the RHS block has <= 64 columns, DMMA fp64 otherwise), 1 DMMA fp64 always, 2 Ozaki */
+int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode);
 /* CUDA-event timers around kernel groups (name -> total ms, launches, algorithmic units) */
 int fsa_ctx_set_profiling(fsa_ctx* ctx, int on);
 int fsa_ctx_reset_timers(fsa_ctx* ctx);
@@ -160,6 +163,11 @@ int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, d
 int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out);
 /* FsaModel::deriv_matmat (fsa.cpp:165-182) */
 int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k, double* out);
+/* the low-rank factor U = L^{-1} Sigma_mn (L L^T = Sigma_m + jitter) of the assembled model, applied
+ * through the context's GEMM path: out (m x k) = U V for V (n x k); out (n x k) = U^T W for W (m x k).
+ * Diagnostics of the dense passes (the reference's A = Sigma_m^{-1} Sigma_mn, fsa.cpp:62-68, is L^{-T} U). */
+int fsa_model_lowrank_project(fsa_model* md, const double* V, int64_t k, double* out);
+int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* out);
 /* diag(Sigma_s) including the nugget (the FITC / Jacobi diagonal) and |U_i|^2 = lowrank diag */
 int fsa_model_diagonals(fsa_model* md, double* sigma_s_diag, double* lowrank_diag);
 

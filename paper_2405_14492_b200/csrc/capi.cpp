@@ -198,6 +198,13 @@ int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world) {
     if (world) *world = ctx->c->comm->size();
   });
 }
+int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode) {
+  return guard([&] {
+    need(ctx, "ctx");
+    require(mode >= 0 && mode <= 2, "gemm mode must be 0 (auto), 1 (dmma) or 2 (ozaki)");
+    ctx->c->gemm_mode = mode;
+  });
+}
 int fsa_ctx_synchronize(fsa_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");
@@ -422,6 +429,44 @@ int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k,
     DBuf<double> o(static_cast<size_t>(M->n_pad * tp));
     M->deriv_matmat(which, in.get(), o.get(), tp);
     to_host_block(M, o.get(), k, tp, out);
+  });
+}
+int fsa_model_lowrank_project(fsa_model* md, const double* V, int64_t k, double* out) {
+  return guard([&] {
+    need(md, "model");
+    need(V, "V");
+    need(out, "out");
+    Model* M = md->m.get();
+    single_rank(M->ctx, "lowrank_project");
+    require(k >= 1, "matrix row mismatch");
+    const long tp = pad_cols(k), mp = M->m_pad;
+    DBuf<double> in = to_device_block(M, V, k, tp);
+    DBuf<double> o(static_cast<size_t>(mp * tp));
+    M->project(M->U.get(), in.get(), tp, o.get());
+    std::vector<double> h(static_cast<size_t>(mp * tp));
+    FSA_CUDA(cudaMemcpyAsync(h.data(), o.get(), sizeof(double) * mp * tp, cudaMemcpyDeviceToHost, M->ctx->stream));
+    FSA_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    for (long c = 0; c < k; ++c)
+      for (long r = 0; r < M->m; ++r) out[r + c * M->m] = h[static_cast<size_t>(r * tp + c)];
+  });
+}
+int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* out) {
+  return guard([&] {
+    need(md, "model");
+    need(W, "W");
+    need(out, "out");
+    Model* M = md->m.get();
+    single_rank(M->ctx, "lowrank_expand");
+    require(k >= 1, "matrix row mismatch");
+    const long tp = pad_cols(k), mp = M->m_pad;
+    std::vector<double> h(static_cast<size_t>(mp * tp), 0.0);
+    for (long c = 0; c < k; ++c)
+      for (long r = 0; r < M->m; ++r) h[static_cast<size_t>(r * tp + c)] = W[r + c * M->m];
+    cudaStream_t s = M->ctx->stream;
+    DBuf<double> Wd(static_cast<size_t>(mp * tp)), Y(static_cast<size_t>(M->n_pad * tp));
+    FSA_CUDA(cudaMemcpyAsync(Wd.get(), h.data(), sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
+    M->expand(Wd.get(), tp, Y.get());
+    to_host_block(M, Y.get(), k, tp, out);
   });
 }
 int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {

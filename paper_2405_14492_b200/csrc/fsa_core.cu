@@ -53,6 +53,7 @@ Context::Context(int dev) : device(dev) {
   FSA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   FSA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags), 4 * sizeof(int), cudaHostAllocMapped));
   FSA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_flags_dev), host_flags, 0));
+  if (const char* g = std::getenv("FSA_GEMM")) gemm_mode = std::strcmp(g, "dmma") == 0 ? 1 : (std::strcmp(g, "ozaki") == 0 ? 2 : 0);
 }
 Context::~Context() {
   cudaStreamSynchronize(stream);
@@ -176,16 +177,37 @@ double* Model::mt_buf(int which, long tp) {
   return b.get();
 }
 
+void Model::ensure_ozaki() {
+  if (oz.ready && oz.U == U.get()) return;
+  KTimer t(ctx, "ozaki_prepare", 16.0 * m_pad * n_pad);
+  ozaki_prepare(oz, U.get(), m_pad, n_pad, ctx->stream);
+}
+
 void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
-  const size_t need = gemm_reduce_scratch(m_pad, tp, n_pad);
-  if (red_scratch.n < need) red_scratch.alloc(need);
-  {
-    KTimer t(ctx, "lowrank_project", 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp));
+  const double flops = 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp);
+  if (M == U.get() && use_ozaki(tp)) {  // INT8 tensor cores, fp64-accurate (ozaki.cuh)
+    ensure_ozaki();
+    KTimer t(ctx, "lowrank_project", flops);
+    ozaki_project_plain(oz, V, tp, scale, out, ctx->stream);
+  } else {
+    const size_t need = gemm_reduce_scratch(m_pad, tp, n_pad);
+    if (red_scratch.n < need) red_scratch.alloc(need);
+    KTimer t(ctx, "lowrank_project", flops);
     gemm_reduce(M, m_pad, m_pad, n_pad, V, tp, tp, scale, out, tp, 1.0, 0.0, red_scratch.get(), ctx->stream);
   }
   if (world() > 1) {  // m x t partials of the row blocks
     KTimer t(ctx, "allreduce");
     ctx->comm->allreduce(out, m_pad * tp, ctx->stream);
+  }
+}
+
+void Model::expand(const double* W, long tp, double* Y) {
+  KTimer t(ctx, "lowrank_expand", 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp));
+  if (use_ozaki(tp)) {
+    ensure_ozaki();
+    ozaki_expand_plain(oz, W, tp, Y, ctx->stream);
+  } else {
+    gemm_expand_store(U.get(), m_pad, n_pad, m_pad, W, tp, tp, Y, tp, 1.0, 0.0, ctx->stream);
   }
 }
 
@@ -633,8 +655,11 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         gemm_reduce(fitc->Qinv.get(), mp, mp, mp, S, tp, tp, nullptr, W, tp, 1.0, 0.0, md->red_scratch.get(), s);
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
-      gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
-                                md->Dinv.get(), rzout, part, s);
+      if (md->use_ozaki(tp))
+        ozaki_expand_keep(md->oz, W, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
+      else
+        gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
+                                  md->Dinv.get(), rzout, part, s);
       comm.allreduce(rzout, tp, s);
     } else {
       P.solve(w.R.get(), w.Z.get(), tp);

@@ -19,6 +19,7 @@
 #include "blas1.cuh"
 #include "comm.cuh"
 #include "common.cuh"
+#include "ozaki.cuh"
 #include "pattern.cuh"
 #include "shard.cuh"
 
@@ -69,6 +70,8 @@ struct Context {
   };
   std::map<std::string, Acc> totals;
   long launches = 0;  // kernels issued by the library (approximate: per host call site)
+  // dense m x n passes with U: 0 auto (INT8 tensor-core Ozaki path when t_pad <= 64), 1 DMMA fp64, 2 Ozaki
+  int gemm_mode = 0;
 
   explicit Context(int dev);
   ~Context();
@@ -153,12 +156,18 @@ class Model {
   void deriv_matmat(int which, const double* V, double* out, long tp);
   // m_pad x tp projection U V (deterministic split-K), summed over ranks
   void project(const double* M, const double* V, long tp, double* out, const double* scale = nullptr);
+  // n_pad x tp block U^T W for W m_pad x tp (ld tp)
+  void expand(const double* W, long tp, double* Y);
   double* mt_buf(int which, long tp);
   // refresh the halo rows [n_pad, n_pad + n_halo) of an extended block (no-op on one rank)
   void halo_exchange(double* X, long tp);
   void cross_cov_ext(int mode, double* out);
   int world() const { return ctx->comm->size(); }
   DBuf<double> halo_send;
+  // INT8 digit planes of U for the tensor-core projection / expansion (built lazily)
+  OzakiPlan oz;
+  bool use_ozaki(long tp) const { return ctx->gemm_mode != 1 && ozaki_supported(tp); }
+  void ensure_ozaki();
 };
 
 // ---- preconditioners (preconditioners.h:16-115) ------------------------------------------

@@ -1,0 +1,676 @@
+// INT8 tensor-core (tcgen05) emulation of the fp64 skinny GEMMs; see ozaki.cuh.
+#include <algorithm>
+
+#include "dgemm.cuh"
+#include "ozaki.cuh"
+
+namespace fsa {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kKb = 32;                            // K bytes per stage = one kind::i8 MMA
+constexpr int kATile = kOzSlices * 128 * kKb;      // 32 KB: 8 planes x 128 rows x 32 K
+constexpr int kBTile = kOzSlices * kOzCols * kKb;  // 16 KB: 8 planes x 64 cols x 32 K
+constexpr int kSmem = kStages * (kATile + kBTile);
+constexpr long kMaxChunk = 16384;  // int32 exactness: 8 pairs x K x 127^2 < 2^31
+
+// ---- PTX wrappers ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "OZ_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra OZ_DONE;\n\t"
+      "bra OZ_WAIT;\n\t"
+      "OZ_DONE:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B,
+// lbo = byte stride between the two 16-B K halves, sbo = byte stride between 8-row groups
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  return d;                             // base offset 0, layout SWIZZLE_NONE
+}
+// instruction descriptor: s8 x s8 -> s32, both K-major
+__device__ __forceinline__ uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+// 16 columns [col0, col0 + 16) of this lane's row: sum_d 2^{-7d} C_d with the eight int32
+// accumulators combined exactly in two int64 halves (|hi|, |lo| < 2^53: exact conversions)
+__device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[16]) {
+  uint32_t v[kOzSlices][16];
+#pragma unroll
+  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * kOzCols + col0), v[dd]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const long long hi = (static_cast<long long>(static_cast<int>(v[0][c])) << 21) +
+                         (static_cast<long long>(static_cast<int>(v[1][c])) << 14) +
+                         (static_cast<long long>(static_cast<int>(v[2][c])) << 7) + static_cast<int>(v[3][c]);
+    const long long lo = (static_cast<long long>(static_cast<int>(v[4][c])) << 21) +
+                         (static_cast<long long>(static_cast<int>(v[5][c])) << 14) +
+                         (static_cast<long long>(static_cast<int>(v[6][c])) << 7) + static_cast<int>(v[7][c]);
+    out[c] = fma(static_cast<double>(hi), 0x1p-35, static_cast<double>(lo) * 0x1p-63);
+  }
+}
+
+// exponent e with |x| < 2^e for all x of a group whose max magnitude is mx (0 -> 0)
+__device__ __forceinline__ int group_exp(double mx) {
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  return e;
+}
+// exact 2^k (normal range; ldexp outside it)
+__device__ __forceinline__ double pow2(int k) {
+  return (k > -1023 && k < 1024) ? __hiloint2double((k + 1023) << 20, 0) : ldexp(1.0, k);
+}
+// 16 values -> 8 digit planes of 16 signed bytes each
+__device__ __forceinline__ void digits16(double (&v)[16], int e, int4 (&out)[kOzSlices]) {
+  const double sc = pow2(-e);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] *= sc;
+#pragma unroll
+  for (int a = 0; a < kOzSlices; ++a) {
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double t = v[q] * 128.0;
+      const double d = trunc(t);
+      v[q] = t - d;
+      // integer d in [-127, 127]: two's-complement low bits of d + 1.5 2^52
+      const uint32_t di = static_cast<uint32_t>(__double2loint(d + 6755399441055744.0));
+      w[q >> 2] |= (di & 0xFFu) << (8 * (q & 3));
+    }
+    out[a] = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]),
+                       static_cast<int>(w[3]));
+  }
+}
+
+// ---- the GEMM ---------------------------------------------------------------------------------
+// CTA (blockIdx.x = 128-row tile of A, blockIdx.y = K chunk). A planes: [tile][kb][plane][kc][rg][8][16],
+// B planes: [kb][kc][plane * 8 + col / 8][col % 8][16]. All MMAs of a stage are issued by one thread
+// into 8 TMEM accumulators (weights d = 2..9), 4-stage bulk-copy pipeline, epilogue per mode:
+//   0: project partials   part[chunk][row][c] = acc * 2^(er[chunk][row] + f[chunk][c])
+//   1: expand keep        Lw, Z = Dinv (R - Lw), per-tile column partials of R.Z
+//   2: expand plain       Y = acc * 2^(ec[row] + h[c])
+struct OzEpi {
+  int mode;
+  long m_pad;   // mode 0: rows of the partial blocks
+  long tp;      // real columns to write (modes 1, 2)
+  const int* erow;  // exponents of A rows: mode 0 [nchunks][m_pad], else [n_pad]
+  const int* ecol;  // exponents of B columns: mode 0 [nchunks][64], else [64]
+  double* part;     // mode 0 partials / mode 1 rz partials [tiles][tp]
+  double* Z;
+  double* Lw;       // modes 1, 2 (Y)
+  const double* R;
+  const double* Dinv;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    k_oz_gemm(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int nkb_all, int kb_per_chunk, OzEpi epi) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], done;
+  __shared__ uint32_t tmem_base_s;
+  const int tile = blockIdx.x, chunk = blockIdx.y;
+  const int kb0 = chunk * kb_per_chunk;
+  const int nk = min(nkb_all - kb0, kb_per_chunk);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kATile;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (tid == 0) {
+    const int8_t* Ablk = A + (static_cast<long>(tile) * nkb_all + kb0) * kATile;
+    const int8_t* Bblk = B + static_cast<long>(kb0) * kBTile;
+    auto load = [&](int j) {
+      const int st = j % kStages;
+      mbar_expect_tx(&full[st], kATile + kBTile);
+      bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
+      bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * kBTile, kBTile, &full[st]);
+    };
+    const int pre = min(nk, kStages);
+    for (int j = 0; j < pre; ++j) load(j);
+    for (int j = 0; j < nk; ++j) {
+      const int st = j % kStages;
+      mbar_wait(&full[st], (j / kStages) & 1);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+#pragma unroll
+      for (int a = 1; a <= kOzSlices; ++a) {
+#pragma unroll
+        for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
+          const int nb = min(4, kOzSlices + 2 - a - bs);
+          const uint64_t ad = umma_desc(a0 + (a - 1) * 4096, 2048, 128);
+          const uint64_t bd = umma_desc(b0 + (bs - 1) * 1024, 8192, 128);
+          mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * kOzCols), ad, bd, idesc_i8(128, nb * kOzCols),
+                 (j > 0 || a > 1) ? 1u : 0u);
+        }
+      }
+      mma_commit(&empty[st]);
+      if (j >= 1 && j - 1 + kStages < nk) {
+        const int sp = (j - 1) % kStages;
+        mbar_wait(&empty[sp], ((j - 1) / kStages) & 1);
+        load(j - 1 + kStages);
+      }
+    }
+    mma_commit(&done);
+  }
+  __syncwarp();
+  mbar_wait(&done, 0);
+  tc_fence_after();
+
+  // ---- epilogue: warp w owns TMEM lanes [32 w, 32 w + 32) = rows of the tile ----
+  const int row = warp * 32 + lane;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  // modes 1, 2: [128][kLd] tiles of Lw and R.Z in the (now idle) pipeline buffers
+  constexpr int kLd = kOzCols + 1;
+  double* lws = reinterpret_cast<double*>(smem);
+  double* rzs = lws + 128 * kLd;
+  for (int hh = 0; hh < 2; ++hh) {
+    double acc[32];
+    {
+      double y0[16], y1[16];
+      drain16(trow, hh * 32, y0);
+      drain16(trow, hh * 32 + 16, y1);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        acc[c] = y0[c];
+        acc[16 + c] = y1[c];
+      }
+    }
+    if (epi.mode == 0) {
+      const long r = static_cast<long>(tile) * 128 + row;
+      const int er = epi.erow[static_cast<long>(chunk) * epi.m_pad + r];
+      double* out = epi.part + (static_cast<long>(chunk) * epi.m_pad + r) * kOzCols + hh * 32;
+      const int* fc = epi.ecol + static_cast<long>(chunk) * kOzCols + hh * 32;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2)
+        *reinterpret_cast<double2*>(out + c) = make_double2(acc[c] * pow2(er + fc[c]), acc[c + 1] * pow2(er + fc[c + 1]));
+    } else {  // modes 1, 2: Lw (and Z) through shared memory, coalesced row copies
+      const long i = static_cast<long>(tile) * 128 + row;
+      const double sci = pow2(epi.erow[i]);
+      const int* hc = epi.ecol + hh * 32;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) lws[row * kLd + hh * 32 + c] = acc[c] * sci * pow2(hc[c]);
+    }
+  }
+  if (epi.mode != 0) {
+    const long r0 = static_cast<long>(tile) * 128;
+    const long tp = epi.tp;
+    __syncthreads();
+    if (epi.mode == 2) {
+      for (long idx = tid; idx < 128 * tp; idx += 128) {
+        const long rr = idx / tp, c = idx - rr * tp;
+        epi.Lw[(r0 + rr) * tp + c] = lws[rr * kLd + c];
+      }
+    } else {
+      // R tile in, Z = Dinv (R - Lw) and Lw out, row-major tiles are contiguous in HBM
+      for (long idx = tid; idx < 128 * tp; idx += 128) {
+        const long rr = idx / tp, c = idx - rr * tp;
+        const double x = epi.R[(r0 + rr) * tp + c];
+        const double lw = lws[rr * kLd + c];
+        const double z = (x - lw) * epi.Dinv[r0 + rr];
+        epi.Lw[(r0 + rr) * tp + c] = lw;
+        epi.Z[(r0 + rr) * tp + c] = z;
+        rzs[rr * kLd + c] = x * z;
+      }
+      __syncthreads();
+      if (tid < tp) {  // fixed-order column sums of R.Z over the tile's rows
+        double sacc = 0.0;
+        for (int rr = 0; rr < 128; ++rr) sacc += rzs[rr * kLd + tid];
+        epi.part[static_cast<long>(tile) * tp + tid] = sacc;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Persistent, warp-specialized expansion Y = U^T W (+ Woodbury epilogue): one CTA per SM loops
+// over 128-point tiles; warp 0 streams A/B stages (bulk copies), warp 1 issues the MMAs, warps
+// 2-5 drain TMEM (one lane quadrant each) and write the outputs. The producer runs ahead across
+// tile boundaries and the next tile's MMAs start as soon as TMEM is drained, so loads and the
+// output writes of tile t overlap the MMAs of tile t + 1.
+constexpr int kXStages = 3;
+constexpr int kXLd = kOzCols + 1;  // odd stride: conflict-free row-per-lane access
+constexpr int kXSmem = kXStages * (kATile + kBTile) + 128 * kXLd * 8;
+__global__ void __launch_bounds__(192, 1)
+    k_oz_expand(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int tiles, int mkb, OzEpi epi) {
+  constexpr int kStages = kXStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull, tempty;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kATile;
+  double* tileY = reinterpret_cast<double*>(smem + kStages * (kATile + kBTile));  // [128][kXLd]
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      long g = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int8_t* At = A + static_cast<long>(t) * mkb * kATile;
+        for (int kb = 0; kb < mkb; ++kb, ++g) {
+          const int st = static_cast<int>(g % kStages);
+          if (g >= kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g / kStages - 1) & 1));
+          mbar_expect_tx(&full[st], kATile + kBTile);
+          bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
+          bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * kBTile, kBTile, &full[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      long g = 0;
+      int lt = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+        if (lt > 0) {
+          mbar_wait(&tempty, static_cast<uint32_t>((lt - 1) & 1));
+          tc_fence_after();
+        }
+        for (int kb = 0; kb < mkb; ++kb, ++g) {
+          const int st = static_cast<int>(g % kStages);
+          mbar_wait(&full[st], static_cast<uint32_t>((g / kStages) & 1));
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+#pragma unroll
+          for (int a = 1; a <= kOzSlices; ++a) {
+#pragma unroll
+            for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
+              const int nb = min(4, kOzSlices + 2 - a - bs);
+              mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * kOzCols), umma_desc(a0 + (a - 1) * 4096, 2048, 128),
+                     umma_desc(b0 + (bs - 1) * 1024, 8192, 128), idesc_i8(128, nb * kOzCols),
+                     (kb > 0 || a > 1) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&tfull);
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue warps 2..5: TMEM lane quadrant q = warp % 4
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const long tp = epi.tp;
+    int lt = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      mbar_wait(&tfull, static_cast<uint32_t>(lt & 1));
+      tc_fence_after();
+      const long r0 = static_cast<long>(t) * 128;
+      const int ei = epi.erow[r0 + row];
+#pragma unroll 1
+      for (int g = 0; g < kOzCols / 16; ++g) {  // stage the tile's rows in shared memory
+        double y[16];
+        drain16(trow, g * 16, y);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) tileY[row * kXLd + g * 16 + c] = y[c] * pow2(ei + epi.ecol[g * 16 + c]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty)) : "memory");
+      // TMEM is free for the next tile already; coalesced copies of the staged rows
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // thread (column c, row parity h): rows h, h + 2, ..., coalesced across c
+      const int et = tid - 64, c = et & 63, h = et >> 6;
+      if (c < tp) {
+        double sacc = 0.0;
+        const long base = r0 * tp + c;
+#pragma unroll 8
+        for (int rr = h; rr < 128; rr += 2) {
+          const double lw = tileY[rr * kXLd + c];
+          const long off = base + static_cast<long>(rr) * tp;
+          epi.Lw[off] = lw;
+          if (epi.mode == 1) {
+            const double x = epi.R[off];
+            const double z = (x - lw) * epi.Dinv[r0 + rr];
+            epi.Z[off] = z;
+            sacc = fma(x, z, sacc);
+          }
+        }
+        if (epi.mode == 1) tileY[h * kXLd + c] = sacc;  // (row h, column c) was read only by this thread
+      }
+      if (epi.mode == 1) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (h == 0 && c < tp)  // fixed order: even rows + odd rows
+          epi.part[static_cast<long>(t) * tp + c] = tileY[c] + tileY[kXLd + c];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // tileY reused by the next tile
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---- digit planes ---------------------------------------------------------------------------------
+// project A: exponent per (chunk, inducing row) over the chunk's points
+__global__ void __launch_bounds__(256) k_oz_exp_rows(const double* __restrict__ U, long mp, long n_pad,
+                                                     int kb_per_chunk, int* __restrict__ er) {
+  __shared__ double red[256];
+  const int chunk = blockIdx.x, tile = blockIdx.y;
+  const int r = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const long i0 = static_cast<long>(chunk) * kb_per_chunk * kKb;
+  const long i1 = min(n_pad, i0 + static_cast<long>(kb_per_chunk) * kKb);
+  double mx = 0.0;
+  for (long i = i0 + half; i < i1; i += 2) mx = fmax(mx, fabs(U[i * mp + tile * 128 + r]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  if (half == 0) er[static_cast<long>(chunk) * mp + tile * 128 + r] = group_exp(fmax(mx, red[threadIdx.x + 128]));
+}
+__global__ void __launch_bounds__(256) k_oz_planes_rows(const double* __restrict__ U, long mp, int nkb,
+                                                        int kb_per_chunk, const int* __restrict__ er,
+                                                        int8_t* __restrict__ Ar) {
+  __shared__ double tileU[kKb][129];
+  const int kb = blockIdx.x, tile = blockIdx.y;
+  for (int idx = threadIdx.x; idx < kKb * 128; idx += 256) {
+    const int p = idx >> 7, r = idx & 127;
+    tileU[p][r] = U[(static_cast<long>(kb) * kKb + p) * mp + tile * 128 + r];
+  }
+  __syncthreads();
+  const int r = threadIdx.x & 127, kc = threadIdx.x >> 7;
+  const int e = er[static_cast<long>(kb / kb_per_chunk) * mp + tile * 128 + r];
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = tileU[kc * 16 + q][r];
+  int4 out[kOzSlices];
+  digits16(v, e, out);
+  int8_t* base = Ar + (static_cast<long>(tile) * nkb + kb) * kATile + kc * 2048 + (r >> 3) * 128 + (r & 7) * 16;
+#pragma unroll
+  for (int a = 0; a < kOzSlices; ++a) *reinterpret_cast<int4*>(base + a * 4096) = out[a];
+}
+// expand A: exponent per point over the inducing rows
+__global__ void k_oz_exp_points(const double* __restrict__ U, long mp, long n_pad, int* __restrict__ ec) {
+  const long i = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_pad) return;
+  double mx = 0.0;
+  for (long r = lane; r < mp; r += 32) mx = fmax(mx, fabs(U[i * mp + r]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) ec[i] = group_exp(mx);
+}
+__global__ void __launch_bounds__(256) k_oz_planes_points(const double* __restrict__ U, long mp, int mkb,
+                                                          const int* __restrict__ ec, int8_t* __restrict__ Ac) {
+  const int kb = blockIdx.x, tile = blockIdx.y;
+  const int il = threadIdx.x & 127, kc = threadIdx.x >> 7;
+  const long i = static_cast<long>(tile) * 128 + il;
+  const double* src = U + i * mp + kb * kKb + kc * 16;
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; q += 2) {
+    const double2 x = *reinterpret_cast<const double2*>(src + q);
+    v[q] = x.x;
+    v[q + 1] = x.y;
+  }
+  int4 out[kOzSlices];
+  digits16(v, ec[i], out);
+  int8_t* base = Ac + (static_cast<long>(tile) * mkb + kb) * kATile + kc * 2048 + (il >> 3) * 128 + (il & 7) * 16;
+#pragma unroll
+  for (int a = 0; a < kOzSlices; ++a) *reinterpret_cast<int4*>(base + a * 4096) = out[a];
+}
+
+// per-sweep B planes of Y = diag(scale) V (project): column max per chunk, then digits
+__global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, long tp, const double* __restrict__ scale,
+                                                 long n_pad, int kb_per_chunk, int parts,
+                                                 unsigned long long* __restrict__ ymax) {
+  __shared__ double red[256];
+  const int chunk = blockIdx.x, part = blockIdx.y;
+  const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
+  const long i0 = static_cast<long>(chunk) * kb_per_chunk * kKb;
+  const long i1 = min(n_pad, i0 + static_cast<long>(kb_per_chunk) * kKb);
+  const long len = i1 - i0, per = (len + parts - 1) / parts;
+  const long a0 = i0 + part * per, a1 = min(i1, a0 + per);
+  double mx = 0.0;
+  if (c < tp)
+    for (long i = a0 + ph; i < a1; i += 4) mx = fmax(mx, fabs(scale ? V[i * tp + c] * scale[i] : V[i * tp + c]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  if (ph == 0) {
+    mx = fmax(fmax(mx, red[threadIdx.x + 64]), fmax(red[threadIdx.x + 128], red[threadIdx.x + 192]));
+    if (mx > 0.0) atomicMax(ymax + static_cast<long>(chunk) * kOzCols + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
+}
+__global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ V, long tp,
+                                                     const double* __restrict__ scale, int kb_per_chunk,
+                                                     const unsigned long long* __restrict__ ymax,
+                                                     int* __restrict__ f, int8_t* __restrict__ Ys) {
+  const int kb = blockIdx.x;
+  const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
+  const int chunk = kb / kb_per_chunk;
+  const int e = group_exp(__longlong_as_double(static_cast<long long>(ymax[static_cast<long>(chunk) * kOzCols + c])));
+  if (kb % kb_per_chunk == 0 && kc == 0) f[static_cast<long>(chunk) * kOzCols + c] = e;
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const long i = static_cast<long>(kb) * kKb + kc * 16 + q;
+    v[q] = c < tp ? (scale ? V[i * tp + c] * scale[i] : V[i * tp + c]) : 0.0;
+  }
+  int4 out[kOzSlices];
+  digits16(v, e, out);
+  int8_t* base = Ys + static_cast<long>(kb) * kBTile + kc * 8192 + c * 16;
+#pragma unroll
+  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
+}
+// per-sweep B planes of W (expand): column exponents over all rows, then digits
+__global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long tp, long mp, int* __restrict__ h) {
+  __shared__ double red[1024];
+  const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;  // 16 row phases
+  double mx = 0.0;
+  if (c < tp)
+    for (long r = ph; r < mp; r += 16) mx = fmax(mx, fabs(W[r * tp + c]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  if (ph == 0) {
+    for (int q = 1; q < 16; ++q) mx = fmax(mx, red[q * 64 + c]);
+    h[c] = group_exp(mx);
+  }
+}
+__global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long tp, const int* __restrict__ h,
+                                                     int8_t* __restrict__ Ws) {
+  const int kb = blockIdx.x;
+  const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
+  const int e = h[c];
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * tp + c] : 0.0;
+  int4 out[kOzSlices];
+  digits16(v, e, out);
+  int8_t* base = Ws + static_cast<long>(kb) * kBTile + kc * 8192 + c * 16;
+#pragma unroll
+  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
+}
+// S[r][c] = sum_chunk part[chunk][r][c] (fixed order)
+__global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long tp, double* __restrict__ S) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= mp * tp) return;
+  const long r = idx / tp, c = idx % tp;
+  double sacc = 0.0;
+  for (int q = 0; q < nchunks; ++q) sacc += part[(static_cast<long>(q) * mp + r) * kOzCols + c];
+  S[idx] = sacc;
+}
+
+void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nkb_all, int kb_per_chunk,
+                 const OzEpi& epi, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  k_oz_gemm<<<dim3(tiles, chunks), 128, kSmem, s>>>(A, B, nkb_all, kb_per_chunk, epi);
+  FSA_LAUNCH_CHECK();
+}
+
+void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
+    attr = true;
+  }
+  const int grid = std::min(p.ptiles, kNumSMs);
+  k_oz_expand<<<grid, 192, kXSmem, s>>>(p.Ac.get(), p.Ws.get(), p.ptiles, p.mkb, epi);
+  FSA_LAUNCH_CHECK();
+}
+
+void project_impl(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s) {
+  require(p.ready && tp <= kOzCols, "ozaki: plan not prepared or too many columns");
+  FSA_CUDA(cudaMemsetAsync(p.ymax.get(), 0, p.ymax.bytes(), s));
+  k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
+  FSA_LAUNCH_CHECK();
+  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, tp, scale, p.kb_per_chunk, p.ymax.get(), p.f.get(), p.Ys.get());
+  FSA_LAUNCH_CHECK();
+  OzEpi epi{0, p.m_pad, tp, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
+  launch_gemm(p.Ar.get(), p.Ys.get(), p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, epi, s);
+  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * tp, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, tp, S);
+  FSA_LAUNCH_CHECK();
+}
+
+void slice_w(OzakiPlan& p, const double* W, long tp, cudaStream_t s) {
+  require(p.ready && tp <= kOzCols, "ozaki: plan not prepared or too many columns");
+  k_oz_wexp<<<1, 1024, 0, s>>>(W, tp, p.m_pad, p.h.get());
+  FSA_LAUNCH_CHECK();
+  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, tp, p.h.get(), p.Ws.get());
+  FSA_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaStream_t s) {
+  require(m_pad % 128 == 0 && n_pad % 128 == 0, "ozaki: padded sizes must be multiples of 128");
+  p.m_pad = m_pad;
+  p.n_pad = n_pad;
+  p.mtiles = static_cast<int>(m_pad / 128);
+  p.ptiles = static_cast<int>(n_pad / 128);
+  p.nkb = static_cast<int>(n_pad / kKb);
+  p.mkb = static_cast<int>(m_pad / kKb);
+  // split-K chunks: whole waves of CTAs (one per SM), chunk <= kMaxChunk points
+  for (int waves = 1;; ++waves) {
+    const int chunks = std::max(1, kNumSMs * waves / p.mtiles);
+    const int kbpc = static_cast<int>(cdiv(p.nkb, chunks));
+    if (static_cast<long>(kbpc) * kKb <= kMaxChunk) {
+      p.kb_per_chunk = kbpc;
+      p.nchunks = static_cast<int>(cdiv(p.nkb, kbpc));
+      break;
+    }
+  }
+  p.U = U;
+  p.Ar.alloc(static_cast<size_t>(m_pad * n_pad * kOzSlices));
+  p.Ac.alloc(static_cast<size_t>(m_pad * n_pad * kOzSlices));
+  p.er.alloc(static_cast<size_t>(p.nchunks * m_pad));
+  p.ec.alloc(static_cast<size_t>(n_pad));
+  p.Ys.alloc(static_cast<size_t>(p.nkb) * kBTile);
+  p.Ws.alloc(static_cast<size_t>(p.mkb) * kBTile);
+  p.ymax.alloc(static_cast<size_t>(p.nchunks * kOzCols));
+  p.f.alloc(static_cast<size_t>(p.nchunks * kOzCols));
+  p.h.alloc(kOzCols);
+  p.part.alloc(static_cast<size_t>(p.nchunks * m_pad * kOzCols));
+  k_oz_exp_rows<<<dim3(p.nchunks, p.mtiles), 256, 0, s>>>(U, m_pad, n_pad, p.kb_per_chunk, p.er.get());
+  FSA_LAUNCH_CHECK();
+  k_oz_planes_rows<<<dim3(p.nkb, p.mtiles), 256, 0, s>>>(U, m_pad, p.nkb, p.kb_per_chunk, p.er.get(), p.Ar.get());
+  FSA_LAUNCH_CHECK();
+  k_oz_exp_points<<<static_cast<unsigned>(cdiv(n_pad * 32, 256)), 256, 0, s>>>(U, m_pad, n_pad, p.ec.get());
+  FSA_LAUNCH_CHECK();
+  k_oz_planes_points<<<dim3(p.mkb, p.ptiles), 256, 0, s>>>(U, m_pad, p.mkb, p.ec.get(), p.Ac.get());
+  FSA_LAUNCH_CHECK();
+  p.ready = true;
+}
+
+void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s) {
+  project_impl(p, R, tp, Dinv, S, s);
+}
+void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s) {
+  project_impl(p, V, tp, scale, S, s);
+}
+
+void ozaki_expand_keep(OzakiPlan& p, const double* W, long tp, double* Z, double* Lw, const double* R,
+                       const double* Dinv, double* rz, double* partial, cudaStream_t s) {
+  slice_w(p, W, tp, s);
+  OzEpi epi{1, p.m_pad, tp, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
+  launch_expand(p, epi, s);
+  colsum_partials(partial, p.ptiles, tp, tp, rz, s);
+}
+void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s) {
+  slice_w(p, W, tp, s);
+  OzEpi epi{2, p.m_pad, tp, p.ec.get(), p.h.get(), nullptr, nullptr, Y, nullptr, nullptr};
+  launch_expand(p, epi, s);
+}
+
+}  // namespace fsa

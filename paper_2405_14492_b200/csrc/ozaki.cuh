@@ -1,0 +1,65 @@
+// FP64-accurate skinny GEMMs on the INT8 tensor cores (tcgen05.mma kind::i8).
+//
+// The two dense passes of a fused FITC-PCG sweep (fsa_core.cu) are
+//   project  S  = U diag(D^{-1}) R      (m x t, K = n points)
+//   expand   Lw = U^T W                 (n x t, K = m)
+// with U fixed for a parameter set. On sm_100a the FP64 tensor path (DMMA) peaks
+// near 40 TF/s, so both passes are compute bound; the INT8 tensor cores run
+// ~100x faster. Each fp64 operand is split (Ozaki scheme, error-free up to the
+// last digit) into kOzSlices signed 7-bit digit planes sharing one power-of-two
+// exponent per scaling group:
+//   x = 2^e * sum_a d_a 2^{-7a} + r,   d_a in [-127, 127],   |r| < 2^{e - 7 s}
+// and the product is recovered from the exact int32 products of digit planes,
+// grouped by total weight d = a + b (a + b <= s + 1 kept):
+//   (X Y)_{ij} = 2^{e_i + f_j} sum_d 2^{-7d} C_d[i][j],  C_d = sum_{a+b=d} X_a Y_b.
+// Scaling groups: project -> U per (inducing row, K chunk), D^{-1}R per (column,
+// K chunk); expand -> U per point, W per column. With s = 8 the result agrees
+// with an fp64 GEMM to ~1e-15 of sum |x||y| (tests/test_gpu_ozaki.py).
+//
+// The U digit planes are built once per parameter set (2 x 8 bytes per entry,
+// like fp64 U); R and W are sliced every sweep. Operand tiles are stored in the
+// UMMA canonical K-major no-swizzle layout, so one bulk copy (cp.async.bulk)
+// moves a whole stage into shared memory and the MMA descriptors address it
+// directly. Accumulators live in TMEM: 8 weights x 64 columns = all 512 columns.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace fsa {
+
+constexpr int kOzSlices = 8;
+constexpr int kOzCols = 64;  // RHS columns per accumulator (t_pad <= 64)
+
+struct OzakiPlan {
+  long m_pad = 0, n_pad = 0;
+  int mtiles = 0;        // m_pad / 128
+  int ptiles = 0;        // n_pad / 128
+  int nkb = 0;           // n_pad / 32 (project K blocks)
+  int mkb = 0;           // m_pad / 32 (expand K blocks)
+  int kb_per_chunk = 0;  // project split-K chunk, in K blocks
+  int nchunks = 0;
+  const double* U = nullptr;  // the fp64 block the planes were built from
+  DBuf<int8_t> Ar, Ac;        // project / expand digit planes of U
+  DBuf<int> er, ec;           // their exponents: [nchunks][m_pad], [n_pad]
+  DBuf<int8_t> Ys, Ws;        // per-sweep planes of D^{-1} R and W
+  DBuf<unsigned long long> ymax;
+  DBuf<int> f, h;             // [nchunks][64], [64]
+  DBuf<double> part;          // project partials [nchunks][m_pad][64]
+  bool ready = false;
+};
+
+inline bool ozaki_supported(long tp) { return tp <= kOzCols; }
+// digit planes of U (m_pad x n_pad, column per point, ld m_pad); n_pad % 128 == 0, m_pad % 128 == 0
+void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaStream_t s);
+// S (m_pad x tp, ld tp) = U diag(Dinv) R over the plan's n_pad rows of R (ld tp)
+void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s);
+// same contract as gemm_expand_woodbury_keep: Lw = U^T W, Z = Dinv (R - Lw), rz = column sums of R.Z
+void ozaki_expand_keep(OzakiPlan& p, const double* W, long tp, double* Z, double* Lw, const double* R,
+                       const double* Dinv, double* rz, double* partial, cudaStream_t s);
+// plain products for tests: S = U diag(scale) V (scale may be null), Y = U^T W
+void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s);
+void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s);
+
+}  // namespace fsa

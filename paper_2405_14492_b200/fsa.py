@@ -70,6 +70,7 @@ _SIGS = {
     "fsa_ctx_group_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_vp)]),
     "fsa_ctx_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fsa_ctx_synchronize": (C.c_int, [_vp]),
+    "fsa_ctx_set_gemm_mode": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fsa_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_reset_timers": (C.c_int, [_vp]),
@@ -102,6 +103,8 @@ _SIGS = {
     "fsa_model_matmat": (C.c_int, [_vp, _dp, _i64, _dp]),
     "fsa_model_deriv_matmat": (C.c_int, [_vp, C.c_int, _dp, _i64, _dp]),
     "fsa_model_diagonals": (C.c_int, [_vp, _dp, _dp]),
+    "fsa_model_lowrank_project": (C.c_int, [_vp, _dp, _i64, _dp]),
+    "fsa_model_lowrank_expand": (C.c_int, [_vp, _dp, _i64, _dp]),
     "fsa_make_preconditioner": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
     "fsa_make_jacobi": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fsa_precond_destroy": (None, [_vp]),
@@ -269,6 +272,12 @@ class Context:
     def synchronize(self):
         _check(lib().fsa_ctx_synchronize(self.h))
 
+    GEMM_MODES = {"auto": 0, "dmma": 1, "ozaki": 2}
+
+    def set_gemm_mode(self, mode="auto"):
+        """Dense U passes: 'auto' (INT8 tensor-core Ozaki path for <= 64 RHS columns), 'dmma', 'ozaki'."""
+        _check(lib().fsa_ctx_set_gemm_mode(self.h, self.GEMM_MODES[mode]))
+
     def stream(self) -> int:
         s = _vp()
         _check(lib().fsa_ctx_stream(self.h, C.byref(s)))
@@ -407,6 +416,20 @@ class FsaModel:
         a, b = _F(np.zeros(self.n)), _F(np.zeros(self.n))
         _check(lib().fsa_model_diagonals(self.h, a, b))
         return a, b
+
+    def lowrank_project(self, V):
+        """U V with U = L^{-1} Sigma_mn (m x n), V n x k, through the context's GEMM path."""
+        V = _F(V).reshape(self.n, -1, order="F")
+        out = _F(np.zeros((self.m, V.shape[1])))
+        _check(lib().fsa_model_lowrank_project(self.h, V, V.shape[1], out))
+        return out
+
+    def lowrank_expand(self, W):
+        """U^T W for W m x k."""
+        W = _F(W).reshape(self.m, -1, order="F")
+        out = _F(np.zeros((self.n, W.shape[1])))
+        _check(lib().fsa_model_lowrank_expand(self.h, W, W.shape[1], out))
+        return out
 
     def matmat(self, V):
         V = _F(V).reshape(self.n, -1, order="F")
