@@ -42,6 +42,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+constexpr int kPrefetch = 8;  // A stages prefetched into L2 ahead of the smem pipeline
+
 // UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B,
 // lbo = byte stride between the two 16-B K halves, sbo = byte stride between 8-row groups
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -185,6 +190,7 @@ __global__ void __launch_bounds__(128, 1)
       mbar_expect_tx(&full[st], kATile + kBTile);
       bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
       bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * kBTile, kBTile, &full[st]);
+      if (j + kPrefetch < nk) prefetch_l2(Ablk + static_cast<long>(j + kPrefetch) * kATile, kATile);
     };
     const int pre = min(nk, kStages);
     for (int j = 0; j < pre; ++j) load(j);
@@ -332,6 +338,14 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(&full[st], kATile + kBTile);
           bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
           bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * kBTile, kBTile, &full[st]);
+          {  // L2 prefetch kPrefetch stages ahead (possibly in this CTA's next tile)
+            int pt = t, pk = kb + kPrefetch;
+            if (pk >= mkb) {
+              pk -= mkb;
+              pt += gridDim.x;
+            }
+            if (pt < tiles) prefetch_l2(A + (static_cast<long>(pt) * mkb + pk) * kATile, kATile);
+          }
         }
       }
     }
@@ -389,21 +403,33 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty)) : "memory");
       // TMEM is free for the next tile already; coalesced copies of the staged rows
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      // thread (column c, row parity h): rows h, h + 2, ..., coalesced across c
+      // thread (column c, row parity h): rows h, h + 2, ..., coalesced across c; loads are
+      // batched ahead of the stores (R and Dinv are read-only here)
       const int et = tid - 64, c = et & 63, h = et >> 6;
       if (c < tp) {
         double sacc = 0.0;
         const long base = r0 * tp + c;
-#pragma unroll 8
-        for (int rr = h; rr < 128; rr += 2) {
-          const double lw = tileY[rr * kXLd + c];
-          const long off = base + static_cast<long>(rr) * tp;
-          epi.Lw[off] = lw;
-          if (epi.mode == 1) {
-            const double x = epi.R[off];
-            const double z = (x - lw) * epi.Dinv[r0 + rr];
-            epi.Z[off] = z;
-            sacc = fma(x, z, sacc);
+#pragma unroll 1
+        for (int rb = h; rb < 128; rb += 16) {
+          double x[8], di[8], lw[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rr = rb + 2 * u;
+            lw[u] = tileY[rr * kXLd + c];
+            if (epi.mode == 1) {
+              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * tp);
+              di[u] = __ldg(epi.Dinv + r0 + rr);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long off = base + static_cast<long>(rb + 2 * u) * tp;
+            epi.Lw[off] = lw[u];
+            if (epi.mode == 1) {
+              const double z = (x[u] - lw[u]) * di[u];
+              epi.Z[off] = z;
+              sacc = fma(x[u], z, sacc);
+            }
           }
         }
         if (epi.mode == 1) tileY[h * kXLd + c] = sacc;  // (row h, column c) was read only by this thread
