@@ -358,6 +358,91 @@ void update_xr_dot(double* X, double* R, const double* H, const double* V, const
   rowdot_launch<1>(H, V, nullptr, n, tp, k, X, R, alpha, rr, scratch, s);
 }
 
+// update_xr_dot for t <= 64 with contiguous row ranges per block, plus the column maxima
+// of |dinv[i] R[i][c]| per chunk of chunk_rows rows (atomicMax on the bit patterns of the
+// non-negative doubles: order independent), the exponents of the Ozaki projection
+__global__ void __launch_bounds__(256) k_xr_dot_max(double* __restrict__ X, double* __restrict__ R,
+                                                    const double* __restrict__ H, const double* __restrict__ V,
+                                                    const double* __restrict__ alpha, long n, long ld, long t,
+                                                    double* __restrict__ partial, const double* __restrict__ dinv,
+                                                    unsigned long long* __restrict__ ymax, long chunk_rows) {
+  __shared__ double red[8][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long c = 2 * lane;
+  const bool on = c < t;
+  const double al0 = c < t ? alpha[c] : 0.0, al1 = c + 1 < t ? alpha[c + 1] : 0.0;
+  const long per = (n + gridDim.x - 1) / gridDim.x;
+  const long ra = static_cast<long>(blockIdx.x) * per, rb = min(n, ra + per);
+  double d0 = 0.0, d1 = 0.0, m0 = 0.0, m1 = 0.0;
+  long cur = -1;
+  auto flush = [&]() {
+    if (cur >= 0 && on) {
+      if (m0 > 0.0) atomicMax(ymax + cur * 64 + c, static_cast<unsigned long long>(__double_as_longlong(m0)));
+      if (m1 > 0.0) atomicMax(ymax + cur * 64 + c + 1, static_cast<unsigned long long>(__double_as_longlong(m1)));
+    }
+    m0 = m1 = 0.0;
+  };
+  long next = 0;  // first row of the chunk after `cur`
+  constexpr int kU = 4;  // rows per batch (loads of the batch are issued together)
+  for (long rbase = ra + warp; rbase < rb; rbase += 8 * kU) {
+    double2 x[kU], rr[kU], h[kU], v[kU];
+    double di[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long r = rbase + 8 * u;
+      if (r < rb && on) {
+        x[u] = *reinterpret_cast<const double2*>(X + r * ld + c);
+        rr[u] = *reinterpret_cast<const double2*>(R + r * ld + c);
+        h[u] = *reinterpret_cast<const double2*>(H + r * ld + c);
+        v[u] = *reinterpret_cast<const double2*>(V + r * ld + c);
+        di[u] = dinv[r];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long r = rbase + 8 * u;
+      if (r >= rb) break;
+      if (r >= next) {  // entering a new chunk (rows only grow)
+        flush();
+        cur = r / chunk_rows;
+        next = (cur + 1) * chunk_rows;
+      }
+      if (!on) continue;
+      if (al0 != 0.0 || al1 != 0.0) {
+        x[u].x += al0 * h[u].x;
+        x[u].y += al1 * h[u].y;
+        rr[u].x -= al0 * v[u].x;
+        rr[u].y -= al1 * v[u].y;
+        *reinterpret_cast<double2*>(X + r * ld + c) = x[u];
+        *reinterpret_cast<double2*>(R + r * ld + c) = rr[u];
+      }
+      d0 = fma(rr[u].x, rr[u].x, d0);
+      d1 = fma(rr[u].y, rr[u].y, d1);
+      m0 = fmax(m0, fabs(rr[u].x * di[u]));
+      m1 = fmax(m1, fabs(rr[u].y * di[u]));
+    }
+  }
+  flush();
+  red[warp][2 * lane] = d0;
+  red[warp][2 * lane + 1] = d1;
+  __syncthreads();
+  if (threadIdx.x < t && threadIdx.x < 64) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += red[w][threadIdx.x];
+    partial[static_cast<long>(blockIdx.x) * t + threadIdx.x] = sacc;
+  }
+}
+void update_xr_dot_max(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
+                       long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
+                       long chunk_rows, cudaStream_t s) {
+  require(tp <= 64, "update_xr_dot_max: at most 64 columns");
+  const long nb = rowdot_blocks(n);
+  k_xr_dot_max<<<static_cast<unsigned>(nb), 256, 0, s>>>(X, R, H, V, alpha, n, tp, k, scratch, dinv, ymax, chunk_rows);
+  FSA_LAUNCH_CHECK();
+  colsum_partials(scratch, nb, k, k, rr, s);
+}
+
 void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
                bool init, cudaStream_t s) {
   k_update_uh<<<nblk(mpad * tp), 256, 0, s>>>(UH, W, active, beta, mpad * tp, tp, k, init ? 1 : 0);

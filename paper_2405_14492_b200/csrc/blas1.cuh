@@ -59,6 +59,11 @@ void update_xr(double* X, double* R, const double* H, const double* V, const dou
 // fused: X += alpha H, R -= alpha V (columns with alpha != 0) and rr[c] = |R_c|^2 (c < k)
 void update_xr_dot(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
                    long k, double* rr, double* scratch, cudaStream_t s);
+// same for t_pad <= 64, also leaving the per-chunk column maxima of |dinv R| in ymax
+// (atomicMax into [chunk][64], zeroed by the caller) for the Ozaki projection of R
+void update_xr_dot_max(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
+                       long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
+                       long chunk_rows, cudaStream_t s);
 // m-space recurrence of U H for the active columns: UH = W + beta UH (init: UH = active ? W : 0)
 void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
                bool init, cudaStream_t s);

@@ -127,7 +127,8 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
     build_pattern(g->pts, g->pts, gamma, true, full, ctx->stream);
     shard_pattern(full, g->pts, rank, world, g->shard, g->pat, ctx->stream);
   }
-  build_row_blocks(g->pat, ctx->stream);
+  static const bool groups = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "group") == 0;
+  if (groups) build_groups(g->pat, ctx->stream);  // experimental grouped SpMM (sparse.cu)
   ctx->sync();
   return g;
 }
@@ -269,6 +270,11 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   {
     KTimer t(ctx, "setup_sddmm", 2.0 * mp * pat.nnz);
     sddmm_sigma_s(M.U.get(), mp, pat, M.lowrank.get(), sp, M.sval.get(), M.info.get() + 1, s);
+  }
+  if (pat.gnnz > 0) {  // value blocks of the row groups (grouped SpMM of the PCG sweeps)
+    KTimer t(ctx, "setup_group_values", 16.0 * pat.nnz + 8.0 * kGroup * pat.gnnz);
+    M.gval.alloc(static_cast<size_t>(pat.gnnz * kGroup));
+    group_values(pat, M.sval.get(), M.gval.get(), s);
   }
   M.D.alloc(np);
   M.Dinv.alloc(np);
@@ -642,12 +648,28 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   const double flops_mn = 2.0 * md->m * n * k;
   md->cols_hint = k;
 
+  // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
+  const bool oz = fused && md->use_ozaki(tp);
+  if (oz) md->ensure_ozaki();
+  bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
   auto precond = [&](double* rzout) {
     if (fused) {
       double* S = md->mt_buf(0, tp);
       double* W = md->mt_buf(1, tp);
-      md->project(md->U.get(), w.R.get(), tp, S, md->Dinv.get());
+      if (oz) {
+        {
+          KTimer t(ctx, "lowrank_project", 2.0 * md->m * n * k);
+          ozaki_project(md->oz, w.R.get(), tp, md->Dinv.get(), S, s, ymax_ready);
+        }
+        if (md->world() > 1) {
+          KTimer t(ctx, "allreduce");
+          comm.allreduce(S, mp * tp, s);
+        }
+        ymax_ready = false;
+      } else {
+        md->project(md->U.get(), w.R.get(), tp, S, md->Dinv.get());
+      }
       {
         KTimer t(ctx, "core_solve", 2.0 * md->m * md->m * k);
         const size_t need = gemm_reduce_scratch(mp, tp, mp);
@@ -695,10 +717,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-      static const int staged = std::getenv("FSA_SPMM") ? std::atoi(std::getenv("FSA_SPMM")) : 0;
-      if (staged && tp <= 128 && md->geo->pat.nblk > 0)
-        spmm_staged(md->geo->pat, md->sval.get(), w.H.get(), tp, w.V.get(), tp, tp, 1.0, 1.0, hv, part, s,
-                    w.Vlr.get());
+      if (md->geo->pat.gnnz > 0)
+        spmm_group_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, 1.0, 1.0, hv, part, s,
+                       w.Vlr.get());
       else
         spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
                  tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
@@ -711,7 +732,14 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     {
       KTimer t(ctx, "cg_blas1");
       cg_alpha(hv, k, it, maxit, st, s);
-      update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
+      if (oz) {
+        FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
+        update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
+                          md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s);
+        ymax_ready = true;
+      } else {
+        update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
+      }
       comm.allreduce(rr, k, s);
       cg_check(rr, k, opts.tol, st, s);
     }

@@ -616,11 +616,14 @@ void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
   FSA_LAUNCH_CHECK();
 }
 
-void project_impl(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s) {
+void project_impl(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s,
+                  bool ymax_ready) {
   require(p.ready && tp <= kOzCols, "ozaki: plan not prepared or too many columns");
-  FSA_CUDA(cudaMemsetAsync(p.ymax.get(), 0, p.ymax.bytes(), s));
-  k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
-  FSA_LAUNCH_CHECK();
+  if (!ymax_ready) {
+    FSA_CUDA(cudaMemsetAsync(p.ymax.get(), 0, p.ymax.bytes(), s));
+    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
+    FSA_LAUNCH_CHECK();
+  }
   k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, tp, scale, p.kb_per_chunk, p.ymax.get(), p.f.get(), p.Ys.get());
   FSA_LAUNCH_CHECK();
   OzEpi epi{0, p.m_pad, tp, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
@@ -679,11 +682,12 @@ void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaSt
   p.ready = true;
 }
 
-void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s) {
-  project_impl(p, R, tp, Dinv, S, s);
+void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s,
+                   bool ymax_ready) {
+  project_impl(p, R, tp, Dinv, S, s, ymax_ready);
 }
 void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s) {
-  project_impl(p, V, tp, scale, S, s);
+  project_impl(p, V, tp, scale, S, s, false);
 }
 
 void ozaki_expand_keep(OzakiPlan& p, const double* W, long tp, double* Z, double* Lw, const double* R,

@@ -2,6 +2,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -149,18 +151,18 @@ __global__ void k_count(const double* rx, long rld, long rn, const double* cx, l
   counts[i] = cnt;
 }
 
-// Union of the column indices of kRowBlock consecutive rows: bitonic sort of the
-// block's entries in shared memory, unique, then each entry's local index.
-constexpr int kUnionSort = 8192;  // max entries per row block handled by the sort
-__global__ void __launch_bounds__(512) k_row_block_union(const long* __restrict__ rowptr, const int* __restrict__ col,
-                                                         long nrows, int* __restrict__ ucols,
-                                                         int* __restrict__ ucount,
-                                                         unsigned short* __restrict__ lidx) {
-  extern __shared__ int keys[];  // [kUnionSort] + [kUnionSort] scan
-  int* flag = keys + kUnionSort;
+// Union of the column indices of kGroup consecutive rows: bitonic sort of the
+// group's entries in shared memory, unique, then each entry's union-local index.
+constexpr int kUnionSort = 2048;  // max entries per group handled by the sort
+constexpr int kUnionCap = 1024;   // max union size per group
+__global__ void __launch_bounds__(256) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
+                                                     long nrows, int* __restrict__ ucols, int* __restrict__ ucount,
+                                                     int* __restrict__ lidx) {
+  __shared__ int keys[kUnionSort];
+  __shared__ int flag[kUnionSort];
   const long b = blockIdx.x;
-  const long r0 = b * kRowBlock;
-  const long r1 = r0 + kRowBlock < nrows ? r0 + kRowBlock : nrows;
+  const long r0 = b * kGroup;
+  const long r1 = r0 + kGroup < nrows ? r0 + kGroup : nrows;
   const long p0 = rowptr[r0], p1 = rowptr[r1];
   const long cnt = p1 - p0;
   const int tid = threadIdx.x;
@@ -188,10 +190,9 @@ __global__ void __launch_bounds__(512) k_row_block_union(const long* __restrict_
       __syncthreads();
     }
   }
-  // unique: flag first occurrences, inclusive scan (single warp over the array)
   for (int i = tid; i < size; i += blockDim.x) flag[i] = (i < cnt && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
   __syncthreads();
-  if (tid < 32) {
+  if (tid < 32) {  // inclusive scan of the flags (one warp)
     int carry = 0;
     for (int base = 0; base < size; base += 32) {
       int v = flag[base + tid];
@@ -220,9 +221,30 @@ __global__ void __launch_bounds__(512) k_row_block_union(const long* __restrict_
       const int mid = (lo + hi) >> 1;
       if (out[mid] < c) lo = mid + 1; else hi = mid;
     }
-    lidx[p] = static_cast<unsigned short>(lo);
+    lidx[p] = lo;
   }
   if (tid == 0) ucount[b] = U;
+}
+__global__ void k_group_compact(const int* __restrict__ ucols, const long* __restrict__ gptr, long ngrp,
+                                int* __restrict__ gcol) {
+  const long b = blockIdx.x;
+  if (b >= ngrp) return;
+  const long o = gptr[b], u = gptr[b + 1] - o;
+  for (long i = threadIdx.x; i < u; i += blockDim.x) gcol[o + i] = ucols[b * kUnionCap + i];
+}
+__global__ void k_group_slots(const long* __restrict__ rowptr, long nrows, const long* __restrict__ gptr,
+                              int* __restrict__ lidx_to_slot) {
+  const long r = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  const long o = gptr[r / kGroup];
+  for (long p = rowptr[r]; p < rowptr[r + 1]; ++p) lidx_to_slot[p] = static_cast<int>(o + lidx_to_slot[p]);
+}
+__global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int* __restrict__ bad, long* __restrict__ sizes) {
+  const long b = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= ngrp) return;
+  const int u = ucount[b];
+  if (u < 0) atomicExch(bad, 1);
+  sizes[b] = u < 0 ? 0 : u;
 }
 
 // mirror[p] = position of (c, r) for p = (r, c): binary search of r in row c (warp per row)
@@ -327,22 +349,45 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
   FSA_CUDA(cudaStreamSynchronize(s));
 }
 
-void build_row_blocks(Csr& pat, cudaStream_t s) {
-  pat.nblk = cdiv(pat.rows, kRowBlock);
-  if (pat.nblk == 0 || pat.nnz == 0) return;
-  pat.ucols.alloc(static_cast<size_t>(pat.nblk) * kUnionCap);
-  pat.ucount.alloc(pat.nblk);
-  pat.lidx.alloc(pat.nnz);
-  const int smem = 2 * kUnionSort * static_cast<int>(sizeof(int));
-  static bool attr = false;
-  if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_row_block_union, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_row_block_union<<<static_cast<unsigned>(pat.nblk), 512, smem, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows,
-                                                                        pat.ucols.get(), pat.ucount.get(),
-                                                                        pat.lidx.get());
+void build_groups(Csr& pat, cudaStream_t s) {
+  pat.gnnz = 0;
+  pat.ngrp = cdiv(pat.rows, kGroup);
+  if (pat.ngrp == 0 || pat.nnz == 0) return;
+  DBuf<int> ucols(static_cast<size_t>(pat.ngrp) * kUnionCap), ucount(pat.ngrp), bad(1);
+  DBuf<long> sizes(pat.ngrp + 1);
+  pat.gslot.alloc(pat.nnz);
+  k_group_union<<<static_cast<unsigned>(pat.ngrp), 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, ucols.get(),
+                                                               ucount.get(), pat.gslot.get());
   FSA_LAUNCH_CHECK();
+  bad.zero(s);
+  FSA_CUDA(cudaMemsetAsync(sizes.get() + pat.ngrp, 0, sizeof(long), s));
+  k_group_ok<<<static_cast<unsigned>(cdiv(pat.ngrp, 256)), 256, 0, s>>>(ucount.get(), pat.ngrp, bad.get(), sizes.get());
+  FSA_LAUNCH_CHECK();
+  int hbad = 0;
+  FSA_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  if (hbad) {  // a group too wide for the union kernel: keep the plain CSR path
+    pat.gslot.release();
+    return;
+  }
+  pat.gptr.alloc(pat.ngrp + 1);
+  size_t tmp_bytes = 0;
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes.get(), pat.gptr.get(), pat.ngrp + 1, s));
+  DBuf<unsigned char> tmp(tmp_bytes);
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, sizes.get(), pat.gptr.get(), pat.ngrp + 1, s));
+  FSA_CUDA(cudaMemcpyAsync(&pat.gnnz, pat.gptr.get() + pat.ngrp, sizeof(long), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  pat.gcol.alloc(pat.gnnz > 0 ? pat.gnnz : 1);
+  if (std::getenv("FSA_DEBUG"))
+    std::fprintf(stderr, "[fsa] row groups: %ld groups, union %ld (%.1f per group), nnz %ld (%.2f x)\n", pat.ngrp,
+                 pat.gnnz, static_cast<double>(pat.gnnz) / pat.ngrp, pat.nnz,
+                 static_cast<double>(pat.nnz) / std::max<long>(pat.gnnz, 1));
+  k_group_compact<<<static_cast<unsigned>(pat.ngrp), 128, 0, s>>>(ucols.get(), pat.gptr.get(), pat.ngrp, pat.gcol.get());
+  FSA_LAUNCH_CHECK();
+  k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
+                                                                          pat.gslot.get());
+  FSA_LAUNCH_CHECK();
+  FSA_CUDA(cudaStreamSynchronize(s));
 }
 
 void build_pattern(const SortedPoints& rows, const SortedPoints& cols, double gamma, bool force_diag, Csr& out,

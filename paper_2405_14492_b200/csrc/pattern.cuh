@@ -40,17 +40,20 @@ struct Csr {
   DBuf<double> dist;   // stored distances (parameter independent)
   DBuf<long> diagpos;  // position of (i,i) (square patterns only)
   DBuf<long> mirror;   // position of (c,r) for the entry (r,c) (square patterns only)
-  // Row blocks of kRowBlock consecutive rows with the union of their columns:
-  // the SpMM stages those RHS rows in shared memory once per block.
-  long nblk = 0;
-  DBuf<int> ucols;             // [nblk][kUnionCap] sorted union of the block's columns
-  DBuf<int> ucount;            // union size per block (-1: exceeds kUnionCap)
-  DBuf<unsigned short> lidx;   // per entry: index of its column in the block's union
+  // Row groups: kGroup consecutive rows share one column list, the union of their
+  // columns (parameter independent, built once). Values then live in a [slot][kGroup]
+  // block (zeros where a row lacks the column), so the SpMM gathers each RHS row once per
+  // group instead of once per nonzero. Hilbert order makes neighbouring rows share most
+  // of their neighbours: the union is several times smaller than the group's nonzeros.
+  long ngrp = 0, gnnz = 0;     // gnnz = total union size (0: groups not built)
+  DBuf<long> gptr;             // ngrp + 1
+  DBuf<int> gcol;              // gnnz union columns, ascending per group
+  DBuf<int> gslot;             // per entry: its slot in [0, gnnz)
 };
-constexpr int kRowBlock = 32;
-constexpr int kUnionCap = 1024;
-// builds nblk / ucols / ucount / lidx for an existing pattern
-void build_row_blocks(Csr& pat, cudaStream_t s);
+constexpr int kGroup = 8;
+// builds ngrp / gnnz / gptr / gcol / gslot (leaves gnnz = 0 if a group's entries exceed
+// the union kernel's capacity: the plain CSR kernels are used then)
+void build_groups(Csr& pat, cudaStream_t s);
 
 // grid covering both point sets (cross patterns use one grid for rows and cols)
 CellGrid make_grid(const double* coords, long n, int d, double gamma, const double* coords2, long n2);

@@ -197,6 +197,7 @@ __global__ void k_spmm(const long* __restrict__ rowptr, const int* __restrict__ 
 // (the PCG's h.v, krylov.cpp:66). Fixed grid: warp w of block b owns rows
 // b*8+w, +8*gridDim.x, ...; each lane owns columns 2*lane(+1) of every 64-column chunk,
 // so the per-column partials reduce in a fixed order (bitwise reproducible).
+constexpr bool kGatherL2 = false;  // RHS gathers through L2 only (the L1 data path bounds them otherwise)
 template <int NCH>
 __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowptr, const int* __restrict__ col,
                                                  const double* __restrict__ val, long nrows,
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
       double a0 = 0.0, a1 = 0.0;
       for (long p = pb; p < pe; ++p) {
         const double v = val[p];
-        const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
+        const double2 x = kGatherL2 ? __ldcg(reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c))
+                                    : *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
         a0 = fma(v, x.x, a0);
         a1 = fma(v, x.y, a1);
       }
@@ -252,137 +254,121 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
   }
 }
 
-// Staged SpMM + dot: one CTA (8 warps, 2 rows each) per row block of kRowBlock
-// consecutive rows. The RHS rows of the block's column union (precomputed once per
-// geometry, build_row_blocks) are copied into shared memory with cp.async, together
-// with the block's column-local indices and values; every nonzero then reads its RHS
-// row from smem. Row blocks are contiguous in the Hilbert order, so the union is
-// several times smaller than the block's nonzero count (that factor comes off the
-// L2 gather traffic). Two CTAs per SM overlap one block's copy with the other's
-// arithmetic. Blocks whose union or nonzero count exceeds the smem budget read the
-// RHS from global memory instead.
-constexpr int kStagedNnz = 4096;  // nonzeros of one row block staged in smem
-constexpr int kStagedWarps = 16;
+// Grouped SpMM + dot (Csr row groups, build_groups). Each union column of a group of
+// kGroup consecutive rows is gathered ONCE and multiplied into the kGroup row accumulators
+// by the group's value block (zero where a row lacks the column): the L1/L2 gather traffic,
+// which bounds the SpMM, drops by the group's nonzeros / union size (~4x at 80 nnz/row in
+// Hilbert order). kSplit warps share a group (interleaved union entries) so that the
+// dependent gather chains stay short; their partial sums are combined in shared memory in
+// a fixed order. Lanes own column pairs (double2); 64-column chunks.
+constexpr int kSplit = 4;
+constexpr int kGroupsPerBlock = 8 / kSplit;
 template <int NCH>
-__global__ void __launch_bounds__(32 * kStagedWarps, 1) k_spmm_staged(const long* __restrict__ rowptr, const int* __restrict__ col,
-                                                       const unsigned short* __restrict__ lidx,
-                                                       const double* __restrict__ val, const int* __restrict__ ucols,
-                                                       const int* __restrict__ ucount, long nrows,
-                                                       const double* __restrict__ X, long ldx, double* Y,
-                                                       long ldy, long ncols, double alpha, double beta,
-                                                       double* __restrict__ partial, int cap, const double* Y0) {
-  extern __shared__ __align__(16) double sx[];  // [cap][ldx] then vals[kStagedNnz], idx[kStagedNnz]
-  __shared__ double red[kStagedWarps][64 * NCH];
-  double* sv = sx + static_cast<long>(cap) * ldx;
-  unsigned short* si = reinterpret_cast<unsigned short*>(sv + kStagedNnz);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long b = blockIdx.x;
-  const long r0 = b * kRowBlock;
-  const long r1 = r0 + kRowBlock < nrows ? r0 + kRowBlock : nrows;
-  const long p0 = rowptr[r0];
-  const int U = ucount[b];
-  const bool staged = U >= 0 && U <= cap && rowptr[r1] - p0 <= kStagedNnz;
-  if (staged) {
-    const int half = static_cast<int>(ldx / 2);
-    const int* uc = ucols + b * kUnionCap;
-    for (int q = tid; q < U * half; q += blockDim.x) {
-      const int rr = q / half, c2 = (q - rr * half) * 2;
-      cp_async16(sx + rr * ldx + c2, X + static_cast<long>(uc[rr]) * ldx + c2);
-    }
-    cp_async_commit();
-    const long cnt = rowptr[r1] - p0;
-    for (long q = tid; q < cnt; q += blockDim.x) {
-      sv[q] = val[p0 + q];
-      si[q] = lidx[p0 + q];
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-  }
-  double d0[NCH], d1[NCH];
+__global__ void __launch_bounds__(256, 3) k_spmm_group(const long* __restrict__ gptr, const int* __restrict__ gcol,
+                                                   const double* __restrict__ gval, long nrows, long ngrp,
+                                                   const double* __restrict__ X, long ldx, double* Y, long ldy,
+                                                   long ncols, double alpha, double beta,
+                                                   double* __restrict__ partial, const double* Y0) {
+  __shared__ double2 acc_s[8][kGroup][32];  // [warp][row][lane]; reused for the column dots
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gl = warp / kSplit, part = warp % kSplit;
+  const long g = static_cast<long>(blockIdx.x) * kGroupsPerBlock + gl;
+  const bool live = g < ngrp;
+  const long u0 = live ? gptr[g] : 0, u1 = live ? gptr[g + 1] : 0;
+  const long r0 = g * kGroup;
+  double dsum[NCH][2];
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) d0[q] = d1[q] = 0.0;
-  for (long r = r0 + warp; r < r1; r += kStagedWarps) {
-    const long pb = rowptr[r], pe = rowptr[r + 1];
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const long c = q * 64 + 2 * lane;
-      if (c >= ncols) break;
-      double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;  // chains: even / odd nonzeros
-      long p = pb;
-      if (staged) {
-        double f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
-        long l = pb - p0;
-        const long le = pe - p0;
-        for (; l + 3 < le; l += 4) {
-          const double2 x = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l]) * ldx + c);
-          const double2 y = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 1]) * ldx + c);
-          const double2 z = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 2]) * ldx + c);
-          const double2 u = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l + 3]) * ldx + c);
-          a0 = fma(sv[l], x.x, a0);
-          a1 = fma(sv[l], x.y, a1);
-          e0 = fma(sv[l + 1], y.x, e0);
-          e1 = fma(sv[l + 1], y.y, e1);
-          f0 = fma(sv[l + 2], z.x, f0);
-          f1 = fma(sv[l + 2], z.y, f1);
-          g0 = fma(sv[l + 3], u.x, g0);
-          g1 = fma(sv[l + 3], u.y, g1);
-        }
-        for (; l < le; ++l) {
-          const double2 x = *reinterpret_cast<const double2*>(sx + static_cast<long>(si[l]) * ldx + c);
-          a0 = fma(sv[l], x.x, a0);
-          a1 = fma(sv[l], x.y, a1);
-        }
-        a0 += f0;
-        a1 += f1;
-        e0 += g0;
-        e1 += g1;
-      } else {
-        for (; p + 1 < pe; p += 2) {
-          const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
-          const double2 y = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p + 1]) * ldx + c);
-          a0 = fma(val[p], x.x, a0);
-          a1 = fma(val[p], x.y, a1);
-          e0 = fma(val[p + 1], y.x, e0);
-          e1 = fma(val[p + 1], y.y, e1);
-        }
-        if (p < pe) {
-          const double2 x = *reinterpret_cast<const double2*>(X + static_cast<long>(col[p]) * ldx + c);
-          a0 = fma(val[p], x.x, a0);
-          a1 = fma(val[p], x.y, a1);
-        }
-      }
-      a0 += e0;
-      a1 += e1;
-      double2* y = reinterpret_cast<double2*>(Y + r * ldy + c);
-      double2 o;
-      if (beta == 0.0) {
-        o = make_double2(alpha * a0, alpha * a1);
-      } else {
-        o = *reinterpret_cast<const double2*>(Y0 + r * ldy + c);
-        o.x = alpha * a0 + beta * o.x;
-        o.y = alpha * a1 + beta * o.y;
-      }
-      *y = o;
-      if (partial != nullptr) {
-        const double2 h = *reinterpret_cast<const double2*>(X + r * ldx + c);
-        d0[q] = fma(h.x, o.x, d0[q]);
-        d1[q] = fma(h.y, o.y, d1[q]);
-      }
-    }
-  }
-  if (partial == nullptr) return;
+  for (int q = 0; q < NCH; ++q) dsum[q][0] = dsum[q][1] = 0.0;
 #pragma unroll
   for (int q = 0; q < NCH; ++q) {
-    red[warp][q * 64 + 2 * lane] = d0[q];
-    red[warp][q * 64 + 2 * lane + 1] = d1[q];
+    if (q * 64 >= ncols) break;  // block-uniform
+    const long c = q * 64 + 2 * lane;
+    const bool on = c < ncols;
+    double a0[kGroup], a1[kGroup];
+#pragma unroll
+    for (int r = 0; r < kGroup; ++r) a0[r] = a1[r] = 0.0;
+    // this warp's union entries u0 + part + kSplit k: column indices fetched 32 at a time
+    // (one per lane) and broadcast by shuffle, so the gathers of a batch are independent
+    for (long ub = u0 + part; ub < u1; ub += 32L * kSplit) {
+      const long ul = ub + static_cast<long>(lane) * kSplit;
+      const int jl = ul < u1 ? gcol[ul] : 0;
+      const int cnt = static_cast<int>(min(32L, (u1 - ub + kSplit - 1) / kSplit));
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const long j = __shfl_sync(0xffffffffu, jl, k);
+        const long u = ub + static_cast<long>(k) * kSplit;
+        const double4* vp = reinterpret_cast<const double4*>(gval + u * kGroup);
+        double2 x = make_double2(0.0, 0.0);
+        if (on) x = *reinterpret_cast<const double2*>(X + j * ldx + c);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double4 va = vp[h];
+          a0[4 * h + 0] = fma(va.x, x.x, a0[4 * h + 0]);
+          a1[4 * h + 0] = fma(va.x, x.y, a1[4 * h + 0]);
+          a0[4 * h + 1] = fma(va.y, x.x, a0[4 * h + 1]);
+          a1[4 * h + 1] = fma(va.y, x.y, a1[4 * h + 1]);
+          a0[4 * h + 2] = fma(va.z, x.x, a0[4 * h + 2]);
+          a1[4 * h + 2] = fma(va.z, x.y, a1[4 * h + 2]);
+          a0[4 * h + 3] = fma(va.w, x.x, a0[4 * h + 3]);
+          a1[4 * h + 3] = fma(va.w, x.y, a1[4 * h + 3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kGroup; ++r) acc_s[warp][r][lane] = make_double2(a0[r], a1[r]);
+    __syncthreads();
+    // warp `part` of the group finishes rows part, part + kSplit, ... (fixed-order sum of the splits)
+    if (live && on) {
+#pragma unroll
+      for (int r = part; r < kGroup; r += kSplit) {
+        const long row = r0 + r;
+        if (row >= nrows) break;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int w = 0; w < kSplit; ++w) {
+          const double2 t = acc_s[gl * kSplit + w][r][lane];
+          s0 += t.x;
+          s1 += t.y;
+        }
+        double2 o;
+        if (beta == 0.0) {
+          o = make_double2(alpha * s0, alpha * s1);
+        } else {
+          o = *reinterpret_cast<const double2*>(Y0 + row * ldy + c);
+          o.x = alpha * s0 + beta * o.x;
+          o.y = alpha * s1 + beta * o.y;
+        }
+        *reinterpret_cast<double2*>(Y + row * ldy + c) = o;
+        const double2 h = *reinterpret_cast<const double2*>(X + row * ldx + c);
+        dsum[q][0] = fma(h.x, o.x, dsum[q][0]);
+        dsum[q][1] = fma(h.y, o.y, dsum[q][1]);
+      }
+    }
+    __syncthreads();
+  }
+  // column dots: fixed order over the block's warps (rows of every warp are disjoint)
+  double(*dred)[64 * NCH] = reinterpret_cast<double(*)[64 * NCH]>(&acc_s[0][0][0]);
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    dred[warp][q * 64 + 2 * lane] = dsum[q][0];
+    dred[warp][q * 64 + 2 * lane + 1] = dsum[q][1];
   }
   __syncthreads();
-  for (int c = tid; c < 64 * NCH && c < ncols; c += blockDim.x) {
+  for (int c = threadIdx.x; c < 64 * NCH && c < ncols; c += blockDim.x) {
     double sacc = 0.0;
 #pragma unroll
-    for (int w = 0; w < kStagedWarps; ++w) sacc += red[w][c];
-    partial[b * ncols + c] = sacc;
+    for (int w = 0; w < 8; ++w) sacc += dred[w][c];
+    partial[static_cast<long>(blockIdx.x) * ncols + c] = sacc;
   }
+}
+// gval[slot * kGroup + row % kGroup] = val[p] (gval zeroed first)
+__global__ void k_group_scatter(const long* __restrict__ rowptr, const int* __restrict__ gslot, long nrows,
+                                const double* __restrict__ val, double* __restrict__ gval) {
+  const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nrows) return;
+  const int rg = static_cast<int>(r % kGroup);
+  for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) gval[static_cast<long>(gslot[p]) * kGroup + rg] = val[p];
 }
 
 #define FSA_DISPATCH_MQ(KERNEL, mpad, grid, s, ...)                                      \
@@ -439,33 +425,34 @@ void extract_diag(const double* val, const long* diagpos, long n, long n_pad, do
   FSA_LAUNCH_CHECK();
 }
 
-constexpr int kStagedSmem = 184 * 1024;  // one 16-warp CTA per SM
-
-void spmm_staged(const Csr& pat, const double* val, const double* X, long ldx, double* Y, long ldy, long ncols,
-                 double alpha, double beta, double* dot, double* partial, cudaStream_t s, const double* Y0) {
-  require(ncols <= 128 && ldx % 2 == 0, "spmm_staged: at most 128 columns");
-  if (Y0 == nullptr) Y0 = Y;
-  if (pat.rows == 0) return;
-  const long nz_bytes = kStagedNnz * static_cast<long>(sizeof(double) + sizeof(unsigned short));
-  const int cap = static_cast<int>((kStagedSmem - nz_bytes) / (ldx * static_cast<long>(sizeof(double))));
-  static bool attr = false;
-  if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_spmm_staged<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmem));
-    FSA_CUDA(cudaFuncSetAttribute(k_spmm_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmem));
-    attr = true;
-  }
-  const unsigned g = static_cast<unsigned>(pat.nblk);
-  double* part = dot != nullptr ? partial : nullptr;
-  if (ncols <= 64)
-    k_spmm_staged<1><<<g, 32 * kStagedWarps, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
-                                                 pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
-                                                 alpha, beta, part, cap, Y0);
-  else
-    k_spmm_staged<2><<<g, 32 * kStagedWarps, kStagedSmem, s>>>(pat.rowptr.get(), pat.col.get(), pat.lidx.get(), val,
-                                                 pat.ucols.get(), pat.ucount.get(), pat.rows, X, ldx, Y, ldy, ncols,
-                                                 alpha, beta, part, cap, Y0);
+void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t s) {
+  if (pat.gnnz == 0) return;
+  FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
+  k_group_scatter<<<static_cast<unsigned>(cdiv(pat.rows * 32, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.gslot.get(),
+                                                                                 pat.rows, val, gval);
   FSA_LAUNCH_CHECK();
-  if (dot != nullptr) colsum_partials(partial, pat.nblk, ncols, ncols, dot, s);
+}
+
+long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : cdiv(ngrp, kGroupsPerBlock); }
+
+void spmm_group_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
+                    double alpha, double beta, double* dot, double* partial, cudaStream_t s, const double* Y0) {
+  if (pat.rows == 0) return;
+  const long nb = spmm_group_blocks(pat.ngrp);
+  const unsigned g = static_cast<unsigned>(nb);
+  const double* y0 = Y0 != nullptr ? Y0 : Y;
+  for (long c0 = 0; c0 < ncols; c0 += 256) {
+    const long w = ncols - c0 < 256 ? ncols - c0 : 256;
+    const int nch = static_cast<int>(cdiv(w, 64));
+    double* part = partial + c0 * nb;
+    switch (nch) {
+      case 1: k_spmm_group<1><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+      case 2: k_spmm_group<2><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+      default: k_spmm_group<4><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
+    }
+    FSA_LAUNCH_CHECK();
+    colsum_partials(part, nb, w, w, dot + c0, s);
+  }
 }
 
 long spmm_dot_blocks(long nrows) {  // one row per warp (the L1-friendly geometry of k_spmm)
