@@ -127,8 +127,9 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
     build_pattern(g->pts, g->pts, gamma, true, full, ctx->stream);
     shard_pattern(full, g->pts, rank, world, g->shard, g->pat, ctx->stream);
   }
-  static const bool groups = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "group") == 0;
-  if (groups) build_groups(g->pat, ctx->stream);  // experimental grouped SpMM (sparse.cu)
+  // row groups of the block SpMM (FSA_SPMM=csr keeps the per-row gather kernel)
+  static const bool csr_only = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "csr") == 0;
+  if (!csr_only) build_groups(g->pat, ctx->stream);
   ctx->sync();
   return g;
 }
@@ -717,9 +718,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-      if (md->geo->pat.gnnz > 0)
-        spmm_group_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, 1.0, 1.0, hv, part, s,
-                       w.Vlr.get());
+      if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
+        spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, w.Vlr.get(), s);
       else
         spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
                  tp, 1.0, 1.0, hv, part, s, w.Vlr.get());

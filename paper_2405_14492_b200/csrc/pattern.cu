@@ -153,9 +153,9 @@ __global__ void k_count(const double* rx, long rld, long rn, const double* cx, l
 
 // Union of the column indices of kGroup consecutive rows: bitonic sort of the
 // group's entries in shared memory, unique, then each entry's union-local index.
-constexpr int kUnionSort = 2048;  // max entries per group handled by the sort
+constexpr int kUnionSort = 4096;  // max entries per group handled by the sort
 constexpr int kUnionCap = 1024;   // max union size per group
-__global__ void __launch_bounds__(256) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
+__global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
                                                      long nrows, int* __restrict__ ucols, int* __restrict__ ucount,
                                                      int* __restrict__ lidx) {
   __shared__ int keys[kUnionSort];
@@ -225,26 +225,33 @@ __global__ void __launch_bounds__(256) k_group_union(const long* __restrict__ ro
   }
   if (tid == 0) ucount[b] = U;
 }
-__global__ void k_group_compact(const int* __restrict__ ucols, const long* __restrict__ gptr, long ngrp,
-                                int* __restrict__ gcol) {
+__global__ void k_group_compact(const int* __restrict__ ucols, const int* __restrict__ ucount,
+                                const long* __restrict__ gptr, long ngrp, int* __restrict__ gcol) {
   const long b = blockIdx.x;
   if (b >= ngrp) return;
-  const long o = gptr[b], u = gptr[b + 1] - o;
-  for (long i = threadIdx.x; i < u; i += blockDim.x) gcol[o + i] = ucols[b * kUnionCap + i];
+  const long o = gptr[b], up = gptr[b + 1] - o;
+  const int u = ucount[b];
+  for (long i = threadIdx.x; i < up; i += blockDim.x) gcol[o + i] = ucols[b * kUnionCap + (i < u ? i : 0)];
 }
+// value index of entry p (row r, union slot u of group g): A-fragment order of the
+// 8 x 4 DMMA tiles: [k-step u/4][warp (r%32)/8][lane ((r%8)*4 + u%4)]
 __global__ void k_group_slots(const long* __restrict__ rowptr, long nrows, const long* __restrict__ gptr,
                               int* __restrict__ lidx_to_slot) {
   const long r = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   const long o = gptr[r / kGroup];
-  for (long p = rowptr[r]; p < rowptr[r + 1]; ++p) lidx_to_slot[p] = static_cast<int>(o + lidx_to_slot[p]);
+  const int rr = static_cast<int>(r % kGroup);
+  for (long p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+    const int u = lidx_to_slot[p];
+    lidx_to_slot[p] = static_cast<int>(kGroup * o + ((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3));
+  }
 }
 __global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int* __restrict__ bad, long* __restrict__ sizes) {
   const long b = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= ngrp) return;
   const int u = ucount[b];
   if (u < 0) atomicExch(bad, 1);
-  sizes[b] = u < 0 ? 0 : u;
+  sizes[b] = u < 0 ? 0 : (u + 3) / 4 * 4;
 }
 
 // mirror[p] = position of (c, r) for p = (r, c): binary search of r in row c (warp per row)
@@ -356,7 +363,7 @@ void build_groups(Csr& pat, cudaStream_t s) {
   DBuf<int> ucols(static_cast<size_t>(pat.ngrp) * kUnionCap), ucount(pat.ngrp), bad(1);
   DBuf<long> sizes(pat.ngrp + 1);
   pat.gslot.alloc(pat.nnz);
-  k_group_union<<<static_cast<unsigned>(pat.ngrp), 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, ucols.get(),
+  k_group_union<<<static_cast<unsigned>(pat.ngrp), 512, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, ucols.get(),
                                                                ucount.get(), pat.gslot.get());
   FSA_LAUNCH_CHECK();
   bad.zero(s);
@@ -382,7 +389,16 @@ void build_groups(Csr& pat, cudaStream_t s) {
     std::fprintf(stderr, "[fsa] row groups: %ld groups, union %ld (%.1f per group), nnz %ld (%.2f x)\n", pat.ngrp,
                  pat.gnnz, static_cast<double>(pat.gnnz) / pat.ngrp, pat.nnz,
                  static_cast<double>(pat.nnz) / std::max<long>(pat.gnnz, 1));
-  k_group_compact<<<static_cast<unsigned>(pat.ngrp), 128, 0, s>>>(ucols.get(), pat.gptr.get(), pat.ngrp, pat.gcol.get());
+  k_group_compact<<<static_cast<unsigned>(pat.ngrp), 128, 0, s>>>(ucols.get(), ucount.get(), pat.gptr.get(), pat.ngrp,
+                                                                  pat.gcol.get());
+  {  // largest padded union (smem budget of the block SpMM)
+    std::vector<long> gp(static_cast<size_t>(pat.ngrp + 1));
+    FSA_CUDA(cudaMemcpyAsync(gp.data(), pat.gptr.get(), sizeof(long) * (pat.ngrp + 1), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    long mx = 0;
+    for (long g = 0; g < pat.ngrp; ++g) mx = std::max(mx, gp[static_cast<size_t>(g + 1)] - gp[static_cast<size_t>(g)]);
+    pat.gmax = static_cast<int>(mx);
+  }
   FSA_LAUNCH_CHECK();
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());

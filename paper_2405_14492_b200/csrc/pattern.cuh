@@ -40,19 +40,20 @@ struct Csr {
   DBuf<double> dist;   // stored distances (parameter independent)
   DBuf<long> diagpos;  // position of (i,i) (square patterns only)
   DBuf<long> mirror;   // position of (c,r) for the entry (r,c) (square patterns only)
-  // Row groups: kGroup consecutive rows share one column list, the union of their
-  // columns (parameter independent, built once). Values then live in a [slot][kGroup]
-  // block (zeros where a row lacks the column), so the SpMM gathers each RHS row once per
-  // group instead of once per nonzero. Hilbert order makes neighbouring rows share most
-  // of their neighbours: the union is several times smaller than the group's nonzeros.
-  long ngrp = 0, gnnz = 0;     // gnnz = total union size (0: groups not built)
-  DBuf<long> gptr;             // ngrp + 1
-  DBuf<int> gcol;              // gnnz union columns, ascending per group
-  DBuf<int> gslot;             // per entry: its slot in [0, gnnz)
+  // Row groups: kGroup consecutive rows (Hilbert order) share one column list, the
+  // union of their columns, padded to a multiple of 4 (parameter independent, built
+  // once). The group's values form a dense kGroup x union block (zeros where a row lacks
+  // the column), stored in DMMA m8n8k4 A-fragment order, so the SpMM is a dense block
+  // product on the FP64 tensor cores with every RHS row of the union staged in shared
+  // memory once per group (sparse.cu, spmm_block_dot).
+  long ngrp = 0, gnnz = 0;     // gnnz = total padded union size (0: groups not built)
+  DBuf<long> gptr;             // ngrp + 1 offsets into gcol (multiples of 4)
+  DBuf<int> gcol;              // union columns (ascending; padding repeats a valid column)
+  DBuf<int> gslot;             // per entry: its index in the value blocks (kGroup * gnnz)
+  int gmax = 0;                // largest padded union
 };
-constexpr int kGroup = 8;
-// builds ngrp / gnnz / gptr / gcol / gslot (leaves gnnz = 0 if a group's entries exceed
-// the union kernel's capacity: the plain CSR kernels are used then)
+constexpr int kGroup = 32;
+// builds the row groups (leaves gnnz = 0 if some group has more than 4096 entries)
 void build_groups(Csr& pat, cudaStream_t s);
 
 // grid covering both point sets (cross patterns use one grid for rows and cols)

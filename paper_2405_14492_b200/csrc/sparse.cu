@@ -254,121 +254,109 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
   }
 }
 
-// Grouped SpMM + dot (Csr row groups, build_groups). Each union column of a group of
-// kGroup consecutive rows is gathered ONCE and multiplied into the kGroup row accumulators
-// by the group's value block (zero where a row lacks the column): the L1/L2 gather traffic,
-// which bounds the SpMM, drops by the group's nonzeros / union size (~4x at 80 nnz/row in
-// Hilbert order). kSplit warps share a group (interleaved union entries) so that the
-// dependent gather chains stay short; their partial sums are combined in shared memory in
-// a fixed order. Lanes own column pairs (double2); 64-column chunks.
-constexpr int kSplit = 4;
-constexpr int kGroupsPerBlock = 8 / kSplit;
-template <int NCH>
-__global__ void __launch_bounds__(256, 3) k_spmm_group(const long* __restrict__ gptr, const int* __restrict__ gcol,
-                                                   const double* __restrict__ gval, long nrows, long ngrp,
-                                                   const double* __restrict__ X, long ldx, double* Y, long ldy,
-                                                   long ncols, double alpha, double beta,
-                                                   double* __restrict__ partial, const double* Y0) {
-  __shared__ double2 acc_s[8][kGroup][32];  // [warp][row][lane]; reused for the column dots
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gl = warp / kSplit, part = warp % kSplit;
-  const long g = static_cast<long>(blockIdx.x) * kGroupsPerBlock + gl;
-  const bool live = g < ngrp;
-  const long u0 = live ? gptr[g] : 0, u1 = live ? gptr[g + 1] : 0;
-  const long r0 = g * kGroup;
-  double dsum[NCH][2];
+// Block SpMM + dot on the FP64 tensor cores (Csr row groups, build_groups). A group of
+// kGroup = 32 consecutive rows (Hilbert order) and the union of their columns form a dense
+// 32 x u value block (zeros where a row lacks the column; ~1/3 dense at 80 nnz/row). The
+// union is consumed in pieces of kPiece rows: the piece's RHS rows (gathered) and value
+// fragments (contiguous) are copied into shared memory with cp.async, double-buffered, and
+// the block product runs as DMMA m8n8k4 tiles. Against the CSR kernel every RHS row is
+// fetched once per group instead of once per nonzero (~10x fewer bytes through L1/L2) and
+// the arithmetic moves onto the tensor pipe. 8 warps: warp w owns row tile w % 4 and every
+// other 8-column tile.
+constexpr int kPiece = 64;  // union rows per pipeline stage (16 DMMA k-steps)
+template <int NT>
+__global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ gptr, const int* __restrict__ gcol,
+                                                      const double* __restrict__ gval, long nrows,
+                                                      const double* __restrict__ X, long ldx, double* Y, long ldy,
+                                                      long ncols, const double* Y0, double* __restrict__ partial) {
+  constexpr int LDH = NT * 8 + (20 - (NT * 8) % 16) % 16;  // == 4 (mod 16): conflict-free B fragments
+  constexpr int CH = NT * 4;                               // 16-byte chunks per staged row
+  constexpr int HS = kPiece * LDH, AS = kPiece * kGroup;   // doubles per buffer
+  extern __shared__ __align__(16) double sm[];             // [2][HS] then [2][AS]
+  __shared__ double dred[4][64];
+  const long g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rt = warp & 3, half = warp >> 2;
+  const long u0 = gptr[g];
+  const int up = static_cast<int>(gptr[g + 1] - u0);
+  const int npc = (up + kPiece - 1) / kPiece;
+  const double* gv = gval + kGroup * u0;
+  auto issue = [&](int pc) {
+    double* hs = sm + (pc & 1) * HS;
+    double* as = sm + 2 * HS + (pc & 1) * AS;
+    const int ua = pc * kPiece, nr = min(kPiece, up - ua);
+    for (int idx = tid; idx < nr * CH; idx += 256) {
+      const int u = idx / CH, ch = idx - u * CH;
+      cp_async16(hs + u * LDH + ch * 2, X + static_cast<long>(gcol[u0 + ua + u]) * ldx + ch * 2);
+    }
+    const double* src = gv + static_cast<long>(ua) * kGroup;
+    for (int idx = tid; idx < nr * kGroup / 2; idx += 256) cp_async16(as + idx * 2, src + idx * 2);
+    cp_async_commit();
+  };
+  double c[NT][2];
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) dsum[q][0] = dsum[q][1] = 0.0;
-#pragma unroll
-  for (int q = 0; q < NCH; ++q) {
-    if (q * 64 >= ncols) break;  // block-uniform
-    const long c = q * 64 + 2 * lane;
-    const bool on = c < ncols;
-    double a0[kGroup], a1[kGroup];
-#pragma unroll
-    for (int r = 0; r < kGroup; ++r) a0[r] = a1[r] = 0.0;
-    // this warp's union entries u0 + part + kSplit k: column indices fetched 32 at a time
-    // (one per lane) and broadcast by shuffle, so the gathers of a batch are independent
-    for (long ub = u0 + part; ub < u1; ub += 32L * kSplit) {
-      const long ul = ub + static_cast<long>(lane) * kSplit;
-      const int jl = ul < u1 ? gcol[ul] : 0;
-      const int cnt = static_cast<int>(min(32L, (u1 - ub + kSplit - 1) / kSplit));
+  for (int q = 0; q < NT; ++q) c[q][0] = c[q][1] = 0.0;
+  if (npc > 0) issue(0);
+  for (int pc = 0; pc < npc; ++pc) {
+    if (pc + 1 < npc) {
+      issue(pc + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* hs = sm + (pc & 1) * HS;
+    const double* as = sm + 2 * HS + (pc & 1) * AS + rt * 32 + lane;
+    const int nks = min(kPiece, up - pc * kPiece) / 4;
 #pragma unroll 4
-      for (int k = 0; k < cnt; ++k) {
-        const long j = __shfl_sync(0xffffffffu, jl, k);
-        const long u = ub + static_cast<long>(k) * kSplit;
-        const double4* vp = reinterpret_cast<const double4*>(gval + u * kGroup);
-        double2 x = make_double2(0.0, 0.0);
-        if (on) x = *reinterpret_cast<const double2*>(X + j * ldx + c);
+    for (int ks = 0; ks < nks; ++ks) {
+      const double a = as[ks * kGroup * 4];
+      const double* hb = hs + (ks * 4 + (lane & 3)) * LDH + (lane >> 2);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double4 va = vp[h];
-          a0[4 * h + 0] = fma(va.x, x.x, a0[4 * h + 0]);
-          a1[4 * h + 0] = fma(va.x, x.y, a1[4 * h + 0]);
-          a0[4 * h + 1] = fma(va.y, x.x, a0[4 * h + 1]);
-          a1[4 * h + 1] = fma(va.y, x.y, a1[4 * h + 1]);
-          a0[4 * h + 2] = fma(va.z, x.x, a0[4 * h + 2]);
-          a1[4 * h + 2] = fma(va.z, x.y, a1[4 * h + 2]);
-          a0[4 * h + 3] = fma(va.w, x.x, a0[4 * h + 3]);
-          a1[4 * h + 3] = fma(va.w, x.y, a1[4 * h + 3]);
-        }
-      }
+      for (int q = 0; q < NT; ++q)
+        if ((q & 1) == half) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
     }
-#pragma unroll
-    for (int r = 0; r < kGroup; ++r) acc_s[warp][r][lane] = make_double2(a0[r], a1[r]);
-    __syncthreads();
-    // warp `part` of the group finishes rows part, part + kSplit, ... (fixed-order sum of the splits)
-    if (live && on) {
-#pragma unroll
-      for (int r = part; r < kGroup; r += kSplit) {
-        const long row = r0 + r;
-        if (row >= nrows) break;
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int w = 0; w < kSplit; ++w) {
-          const double2 t = acc_s[gl * kSplit + w][r][lane];
-          s0 += t.x;
-          s1 += t.y;
-        }
-        double2 o;
-        if (beta == 0.0) {
-          o = make_double2(alpha * s0, alpha * s1);
-        } else {
-          o = *reinterpret_cast<const double2*>(Y0 + row * ldy + c);
-          o.x = alpha * s0 + beta * o.x;
-          o.y = alpha * s1 + beta * o.y;
-        }
-        *reinterpret_cast<double2*>(Y + row * ldy + c) = o;
-        const double2 h = *reinterpret_cast<const double2*>(X + row * ldx + c);
-        dsum[q][0] = fma(h.x, o.x, dsum[q][0]);
-        dsum[q][1] = fma(h.y, o.y, dsum[q][1]);
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // the buffer is refilled by issue(pc + 2)
   }
-  // column dots: fixed order over the block's warps (rows of every warp are disjoint)
-  double(*dred)[64 * NCH] = reinterpret_cast<double(*)[64 * NCH]>(&acc_s[0][0][0]);
+  // epilogue: Y = Y0 + S X on this lane's fragment; h.v column partials
+  const long row = g * kGroup + rt * 8 + (lane >> 2);
+  double d[NT][2];
 #pragma unroll
-  for (int q = 0; q < NCH; ++q) {
-    dred[warp][q * 64 + 2 * lane] = dsum[q][0];
-    dred[warp][q * 64 + 2 * lane + 1] = dsum[q][1];
+  for (int q = 0; q < NT; ++q) {
+    d[q][0] = d[q][1] = 0.0;
+    if ((q & 1) != half) continue;
+    const long cc = q * 8 + 2 * (lane & 3);
+    if (row < nrows && cc < ncols) {
+      double2 o = *reinterpret_cast<const double2*>(Y0 + row * ldy + cc);
+      o.x += c[q][0];
+      o.y += c[q][1];
+      *reinterpret_cast<double2*>(Y + row * ldy + cc) = o;
+      const double2 h = *reinterpret_cast<const double2*>(X + row * ldx + cc);
+      d[q][0] = h.x * o.x;
+      d[q][1] = h.y * o.y;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    if ((q & 1) != half) continue;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      d[q][0] += __shfl_xor_sync(0xffffffffu, d[q][0], o);
+      d[q][1] += __shfl_xor_sync(0xffffffffu, d[q][1], o);
+    }
+    if (lane < 4) {
+      dred[rt][q * 8 + 2 * lane] = d[q][0];
+      dred[rt][q * 8 + 2 * lane + 1] = d[q][1];
+    }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < 64 * NCH && c < ncols; c += blockDim.x) {
-    double sacc = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sacc += dred[w][c];
-    partial[static_cast<long>(blockIdx.x) * ncols + c] = sacc;
-  }
+  if (tid < ncols) partial[g * ncols + tid] = ((dred[0][tid] + dred[1][tid]) + dred[2][tid]) + dred[3][tid];
 }
-// gval[slot * kGroup + row % kGroup] = val[p] (gval zeroed first)
-__global__ void k_group_scatter(const long* __restrict__ rowptr, const int* __restrict__ gslot, long nrows,
-                                const double* __restrict__ val, double* __restrict__ gval) {
-  const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= nrows) return;
-  const int rg = static_cast<int>(r % kGroup);
-  for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) gval[static_cast<long>(gslot[p]) * kGroup + rg] = val[p];
+// gval[gslot[p]] = val[p] (gval zeroed first)
+__global__ void k_group_scatter(const int* __restrict__ gslot, long nnz, const double* __restrict__ val,
+                                double* __restrict__ gval) {
+  const long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < nnz) gval[gslot[p]] = val[p];
 }
 
 #define FSA_DISPATCH_MQ(KERNEL, mpad, grid, s, ...)                                      \
@@ -428,31 +416,38 @@ void extract_diag(const double* val, const long* diagpos, long n, long n_pad, do
 void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t s) {
   if (pat.gnnz == 0) return;
   FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
-  k_group_scatter<<<static_cast<unsigned>(cdiv(pat.rows * 32, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.gslot.get(),
-                                                                                 pat.rows, val, gval);
+  k_group_scatter<<<static_cast<unsigned>(cdiv(pat.nnz, 256)), 256, 0, s>>>(pat.gslot.get(), pat.nnz, val, gval);
   FSA_LAUNCH_CHECK();
 }
 
-long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : cdiv(ngrp, kGroupsPerBlock); }
+long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
-void spmm_group_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
-                    double alpha, double beta, double* dot, double* partial, cudaStream_t s, const double* Y0) {
+bool spmm_block_supported(long ncols) { return ncols <= 64 && ncols % 8 == 0; }
+
+void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
+                    double* dot, double* partial, const double* Y0, cudaStream_t s) {
+  require(spmm_block_supported(ncols) && ldx == ncols && ldy == ncols, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
-  const long nb = spmm_group_blocks(pat.ngrp);
-  const unsigned g = static_cast<unsigned>(nb);
-  const double* y0 = Y0 != nullptr ? Y0 : Y;
-  for (long c0 = 0; c0 < ncols; c0 += 256) {
-    const long w = ncols - c0 < 256 ? ncols - c0 : 256;
-    const int nch = static_cast<int>(cdiv(w, 64));
-    double* part = partial + c0 * nb;
-    switch (nch) {
-      case 1: k_spmm_group<1><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
-      case 2: k_spmm_group<2><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
-      default: k_spmm_group<4><<<g, 256, 0, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, pat.ngrp, X + c0, ldx, Y + c0, ldy, w, alpha, beta, part, y0 + c0); break;
-    }
-    FSA_LAUNCH_CHECK();
-    colsum_partials(part, nb, w, w, dot + c0, s);
+  const int nt = static_cast<int>(ncols / 8);
+  const long ldh = ncols + (20 - ncols % 16) % 16;
+  const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
+  auto go = [&](auto kern) {
+    FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<static_cast<unsigned>(pat.ngrp), 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, X, ldx, Y,
+                                                          ldy, ncols, Y0 != nullptr ? Y0 : Y, partial);
+  };
+  switch (nt) {
+    case 1: go(k_spmm_block<1>); break;
+    case 2: go(k_spmm_block<2>); break;
+    case 3: go(k_spmm_block<3>); break;
+    case 4: go(k_spmm_block<4>); break;
+    case 5: go(k_spmm_block<5>); break;
+    case 6: go(k_spmm_block<6>); break;
+    case 7: go(k_spmm_block<7>); break;
+    default: go(k_spmm_block<8>); break;
   }
+  FSA_LAUNCH_CHECK();
+  colsum_partials(partial, pat.ngrp, ncols, ncols, dot, s);
 }
 
 long spmm_dot_blocks(long nrows) {  // one row per warp (the L1-friendly geometry of k_spmm)

@@ -20,13 +20,14 @@ void sddmm_cross(const double* Rm, long ldr, const double* Cm, long ldc, const C
 // Y = alpha S X + beta Y (first ncols <= 256 columns) fused with dot[c] = sum_r X[r][c] Y[r][c];
 // partial must hold spmm_dot_blocks(nrows) * ncols doubles
 long spmm_dot_blocks(long nrows);
-// grouped variant (pat.gnnz > 0, build_groups): same contract as spmm_dot with the value
-// blocks gval = group_values(pat, val); partial holds spmm_group_blocks(pat.ngrp) * ncols doubles
+// block variant on the row groups (pat.gnnz > 0, build_groups): Y = Y0 + S X and
+// dot[c] = sum_r X[r][c] Y[r][c] for ncols <= 64 (multiple of 8, ldx == ldy == ncols);
+// gval = group_values(pat, val); partial holds spmm_group_blocks(pat.ngrp) * ncols doubles
 void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t s);
 long spmm_group_blocks(long ngrp);
-void spmm_group_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
-                    double alpha, double beta, double* dot, double* partial, cudaStream_t s,
-                    const double* Y0 = nullptr);
+bool spmm_block_supported(long ncols);
+void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
+                    double* dot, double* partial, const double* Y0, cudaStream_t s);
 // (Y0, when given, replaces Y as the beta term: Y = alpha S X + beta Y0)
 void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
               long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
