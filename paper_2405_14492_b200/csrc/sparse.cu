@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
   __shared__ double dred[4][64];
   const long g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rt = warp & 3, half = warp >> 2;
+  constexpr int kRT = kGroup / 8, kSub = 8 / kRT;  // row tiles; warps per row tile (column subsets)
+  const int rt = warp % kRT, half = warp / kRT;
   const long u0 = gptr[g];
   const int up = static_cast<int>(gptr[g + 1] - u0);
   const int npc = (up + kPiece - 1) / kPiece;
@@ -307,14 +308,15 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     __syncthreads();
     const double* hs = sm + (pc & 1) * HS;
     const double* as = sm + 2 * HS + (pc & 1) * AS + rt * 32 + lane;
+    static_assert(kGroup % 8 == 0 && 8 % (kGroup / 8) == 0, "row tiles must divide the 8 warps");
     const int nks = min(kPiece, up - pc * kPiece) / 4;
 #pragma unroll 4
     for (int ks = 0; ks < nks; ++ks) {
-      const double a = as[ks * kGroup * 4];
+      const double a = as[ks * kRT * 32];
       const double* hb = hs + (ks * 4 + (lane & 3)) * LDH + (lane >> 2);
 #pragma unroll
       for (int q = 0; q < NT; ++q)
-        if ((q & 1) == half) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
+        if (q % kSub == half) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
     }
     __syncthreads();  // the buffer is refilled by issue(pc + 2)
   }
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
     d[q][0] = d[q][1] = 0.0;
-    if ((q & 1) != half) continue;
+    if (q % kSub != half) continue;
     const long cc = q * 8 + 2 * (lane & 3);
     if (row < nrows && cc < ncols) {
       double2 o = *reinterpret_cast<const double2*>(Y0 + row * ldy + cc);
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
   }
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
-    if ((q & 1) != half) continue;
+    if (q % kSub != half) continue;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
       d[q][0] += __shfl_xor_sync(0xffffffffu, d[q][0], o);
@@ -350,7 +352,12 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     }
   }
   __syncthreads();
-  if (tid < ncols) partial[g * ncols + tid] = ((dred[0][tid] + dred[1][tid]) + dred[2][tid]) + dred[3][tid];
+  if (tid < ncols) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) sacc += dred[r][tid];
+    partial[g * ncols + tid] = sacc;
+  }
 }
 // gval[gslot[p]] = val[p] (gval zeroed first)
 __global__ void k_group_scatter(const int* __restrict__ gslot, long nnz, const double* __restrict__ val,
