@@ -13,9 +13,11 @@ def main(path, out=None, title=""):
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in data:
-        if len(r) <= vi or "fsa::" not in r[ki]:
+        if len(r) <= vi:
             continue
-        name = re.sub(r"\(.*", "", r[ki]).replace("fsa::<unnamed>::", "").replace("fsa::", "")
+        name = re.sub(r"\(.*", "", r[ki])
+        for pre in ("fsa::<unnamed>::", "fsa::", "void ", "unnamed>::"):
+            name = name.replace(pre, "")
         v = float(r[vi].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3}[r[ui]]
         tot[name] += v
         cnt[name] += 1
