@@ -358,6 +358,87 @@ void update_xr_dot(double* X, double* R, const double* H, const double* V, const
   rowdot_launch<1>(H, V, nullptr, n, tp, k, X, R, alpha, rr, scratch, s);
 }
 
+// Jacobi-preconditioned PCG without a Z block: X += alpha H, R -= alpha V, rr = |R|^2 and
+// rz = R' D^{-1} R per column in one pass (64-column slabs, fixed-order partials)
+__global__ void __launch_bounds__(256) k_xr_dot_jacobi(double* __restrict__ X, double* __restrict__ R,
+                                                       const double* __restrict__ H, const double* __restrict__ V,
+                                                       const double* __restrict__ alpha,
+                                                       const double* __restrict__ dinv, long n, long ld, long t,
+                                                       double* __restrict__ prr, double* __restrict__ prz) {
+  __shared__ double red[2][8][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long c0 = 64L * blockIdx.y;
+  const long c = c0 + 2 * lane;
+  const bool on = c < t;
+  const double al0 = c < t ? alpha[c] : 0.0, al1 = c + 1 < t ? alpha[c + 1] : 0.0;
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  if (on) {
+    for (long r = static_cast<long>(blockIdx.x) * 8 + warp; r < n; r += 8L * gridDim.x) {
+      double2 rr = *reinterpret_cast<const double2*>(R + r * ld + c);
+      if (al0 != 0.0 || al1 != 0.0) {
+        double2 x = *reinterpret_cast<const double2*>(X + r * ld + c);
+        const double2 h = *reinterpret_cast<const double2*>(H + r * ld + c);
+        const double2 v = *reinterpret_cast<const double2*>(V + r * ld + c);
+        x.x += al0 * h.x;
+        x.y += al1 * h.y;
+        rr.x -= al0 * v.x;
+        rr.y -= al1 * v.y;
+        *reinterpret_cast<double2*>(X + r * ld + c) = x;
+        *reinterpret_cast<double2*>(R + r * ld + c) = rr;
+      }
+      const double w = dinv[r];
+      d0 = fma(rr.x, rr.x, d0);
+      d1 = fma(rr.y, rr.y, d1);
+      e0 = fma(rr.x * w, rr.x, e0);
+      e1 = fma(rr.y * w, rr.y, e1);
+    }
+  }
+  red[0][warp][2 * lane] = d0;
+  red[0][warp][2 * lane + 1] = d1;
+  red[1][warp][2 * lane] = e0;
+  red[1][warp][2 * lane + 1] = e1;
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int q = threadIdx.x >> 6, cc = threadIdx.x & 63;
+    if (c0 + cc < t) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[q][w][cc];
+      (q == 0 ? prr : prz)[static_cast<long>(blockIdx.x) * t + c0 + cc] = sacc;
+    }
+  }
+}
+void update_xr_dot_jacobi(double* X, double* R, const double* H, const double* V, const double* alpha,
+                          const double* dinv, long n, long tp, long k, double* rr, double* rz, double* scratch,
+                          cudaStream_t s) {
+  const long nb = rowdot_blocks(n);
+  const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(cdiv(k, 64)));
+  k_xr_dot_jacobi<<<grid, 256, 0, s>>>(X, R, H, V, alpha, dinv, n, tp, k, scratch, scratch + nb * k);
+  FSA_LAUNCH_CHECK();
+  colsum_partials(scratch, nb, k, k, rr, s);
+  colsum_partials(scratch + nb * k, nb, k, k, rz, s);
+}
+// H = D^{-1} R + beta H on the active columns (init: H = active ? D^{-1} R : 0)
+__global__ void k_update_h_jacobi(double* __restrict__ H, const double* __restrict__ R,
+                                  const double* __restrict__ dinv, const int* __restrict__ active,
+                                  const double* __restrict__ beta, long n, long tp, long k, int init) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n * tp) return;
+  const long i = idx / tp, j = idx - i * tp;
+  if (j >= k) return;
+  if (!active[j]) {
+    if (init) H[idx] = 0.0;
+    return;
+  }
+  const double z = R[idx] * dinv[i];
+  H[idx] = init ? z : z + beta[j] * H[idx];
+}
+void update_h_jacobi(double* H, const double* R, const double* dinv, const int* active, const double* beta, long n,
+                     long tp, long k, bool init, cudaStream_t s) {
+  k_update_h_jacobi<<<nblk(n * tp), 256, 0, s>>>(H, R, dinv, active, beta, n, tp, k, init ? 1 : 0);
+  FSA_LAUNCH_CHECK();
+}
+
 // update_xr_dot for t <= 64 with contiguous row ranges per block, plus the column maxima
 // of |dinv[i] R[i][c]| per chunk of chunk_rows rows (atomicMax on the bit patterns of the
 // non-negative doubles: order independent), the exponents of the Ozaki projection

@@ -64,6 +64,14 @@ void update_xr_dot(double* X, double* R, const double* H, const double* V, const
 void update_xr_dot_max(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
                        long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
                        long chunk_rows, cudaStream_t s);
+// Jacobi PCG without a Z block: X += alpha H, R -= alpha V, rr = |R|^2, rz = R' diag(dinv) R;
+// scratch holds 2 * coldot_scratch(n, k) doubles
+void update_xr_dot_jacobi(double* X, double* R, const double* H, const double* V, const double* alpha,
+                          const double* dinv, long n, long tp, long k, double* rr, double* rz, double* scratch,
+                          cudaStream_t s);
+// H = diag(dinv) R + beta H on the active columns (init: H = active ? diag(dinv) R : 0)
+void update_h_jacobi(double* H, const double* R, const double* dinv, const int* active, const double* beta, long n,
+                     long tp, long k, bool init, cudaStream_t s);
 // m-space recurrence of U H for the active columns: UH = W + beta UH (init: UH = active ? W : 0)
 void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
                bool init, cudaStream_t s);

@@ -604,6 +604,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   FitcPrecond* fitc = dynamic_cast<FitcPrecond*>(&P);
   const bool fused = fop != nullptr && fitc != nullptr;
   require(fused || md->world() == 1, "row-sharded solves need the FSA operator with the FITC preconditioner");
+  // Jacobi on Sigma_s (prediction solves, prediction.cpp:90-93): no Z block, r.z fused into the update
+  const bool jfused = !fused && dynamic_cast<DiagPrecond*>(&P) != nullptr && dynamic_cast<SigmaSOp*>(&A) != nullptr;
   Comm& comm = *ctx->comm;
   CgWork& w = *ctx->cgw;
   if (w.R.n < blk) {
@@ -618,7 +620,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     w.Vlr.alloc(blk);
   }
   const size_t npart = std::max(static_cast<size_t>(std::max(np / 64, spmm_dot_blocks(n)) * tp),
-                                coldot_scratch(n, tp));
+                                2 * coldot_scratch(n, tp));
   if (w.part.n < npart) w.part.alloc(npart);
   w.dots.alloc(static_cast<size_t>(4 * tp));
   w.dbl.alloc(static_cast<size_t>(6 * k));
@@ -684,6 +686,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
                                   md->Dinv.get(), rzout, part, s);
       comm.allreduce(rzout, tp, s);
+    } else if (jfused) {
+      KTimer t(ctx, "cg_blas1");
+      launch_coldot_weighted(w.R.get(), w.R.get(), md->Dinv.get(), n, tp, k, rzout, part, s);
     } else {
       P.solve(w.R.get(), w.Z.get(), tp);
       KTimer t(ctx, "cg_blas1");
@@ -701,7 +706,10 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   {
     KTimer t(ctx, "cg_blas1");
     cg_start_rz(rz, k, st, s);
-    init_h(w.H.get(), w.Z.get(), st.active, np, tp, k, s);
+    if (jfused)
+      update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, true, s);
+    else
+      init_h(w.H.get(), w.Z.get(), st.active, np, tp, k, s);
     if (fused) init_h(w.Vlr.get(), w.Lw.get(), st.active, np, tp, k, s);  // U^T U H_0 = U^T w_0
     cg_count(k, st, s);
   }
@@ -724,6 +732,13 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
                  tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
       comm.allreduce(hv, tp, s);
+    } else if (jfused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp)) {  // V = Sigma_s H; h.v
+      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
+      spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, nullptr, s);
+    } else if (jfused) {
+      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
+      spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
+               tp, 1.0, 0.0, hv, part, s);
     } else {
       A.apply(w.H.get(), w.V.get(), tp);
       KTimer t(ctx, "cg_blas1");
@@ -737,18 +752,23 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
                           md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s);
         ymax_ready = true;
+      } else if (jfused) {
+        update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
+                             s);
       } else {
         update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
       }
       comm.allreduce(rr, k, s);
       cg_check(rr, k, opts.tol, st, s);
     }
-    precond(rz);
+    if (!jfused) precond(rz);
     {
       KTimer t(ctx, "cg_blas1");
       cg_beta(rz, k, st, s);
       if (fused)  // H = Z + beta H, Vlr = U^T w + beta Vlr
         update_h2(w.H.get(), w.Z.get(), w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);
+      else if (jfused)  // H = D^{-1} R + beta H
+        update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, false, s);
       else
         update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
       cg_count(k, st, s);

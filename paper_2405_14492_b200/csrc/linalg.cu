@@ -64,26 +64,34 @@ __global__ void __launch_bounds__(256) k_potrf_panel(double* A, long ld, long k0
     Lk[r][c] = A[(k0 + c) * ld + k0 + r];
   }
   __syncthreads();
-  for (int j = 0; j < 64; ++j) {
-    if (tid == 0) {
+  if (tid < 32) {  // one warp factors the 64 x 64 diagonal block (lane owns rows lane, lane + 32)
+    const int r0 = tid, r1 = tid + 32;
+    int badj = 0;
+    for (int j = 0; j < 64; ++j) {
       double dj = Lk[j][j];
       if (!(dj > 0.0) || !isfinite(dj)) {
-        if (!bad) bad = j + 1;
+        if (!badj) badj = j + 1;
         dj = 1.0;
       }
-      Lk[j][j] = sqrt(dj);
+      const double ljj = sqrt(dj);
+      const double inv = 1.0 / ljj;
+      __syncwarp();
+      if (r0 > j) Lk[r0][j] *= inv;
+      if (r1 > j) Lk[r1][j] *= inv;
+      if (r0 == j) Lk[j][j] = ljj;
+      if (r1 == j) Lk[j][j] = ljj;
+      __syncwarp();
+      const double a0 = r0 > j ? Lk[r0][j] : 0.0, a1 = r1 > j ? Lk[r1][j] : 0.0;
+      for (int c = j + 1; c < 64; ++c) {
+        const double lc = Lk[c][j];
+        if (r0 >= c) Lk[r0][c] = fma(-a0, lc, Lk[r0][c]);
+        if (r1 >= c) Lk[r1][c] = fma(-a1, lc, Lk[r1][c]);
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    const double ljj = Lk[j][j];
-    for (int r = j + 1 + tid; r < 64; r += blockDim.x) Lk[r][j] /= ljj;
-    __syncthreads();
-    const int w = 63 - j;
-    for (int idx = tid; idx < w * w; idx += blockDim.x) {
-      const int r = j + 1 + idx % w, c = j + 1 + idx / w;
-      if (r >= c) Lk[r][c] -= Lk[r][j] * Lk[c][j];
-    }
-    __syncthreads();
+    if (tid == 0) bad = badj;
   }
+  __syncthreads();
   if (blockIdx.x == 0) {
     // the factored diagonal block goes to scratch: the other blocks of this launch
     // still read the unfactored block from A (copied back by k_copy_diag_blocks)

@@ -268,7 +268,17 @@ template <int NT>
 __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ gptr, const int* __restrict__ gcol,
                                                       const double* __restrict__ gval, long nrows,
                                                       const double* __restrict__ X, long ldx, double* Y, long ldy,
-                                                      long ncols, const double* Y0, double* __restrict__ partial) {
+                                                      long ncols, const double* Y0, double* __restrict__ partial,
+                                                      long ldp) {
+  // column tile blockIdx.y: columns [64 y, 64 y + 8 NT) of X / Y / Y0 (Y0 null: Y = S X)
+  {
+    const long c0 = 64L * blockIdx.y;
+    X += c0;
+    Y += c0;
+    if (Y0 != nullptr) Y0 += c0;
+    partial += c0;
+    ncols -= c0;
+  }
   constexpr int LDH = NT * 8 + (20 - (NT * 8) % 16) % 16;  // == 4 (mod 16): conflict-free B fragments
   constexpr int CH = NT * 4;                               // 16-byte chunks per staged row
   constexpr int HS = kPiece * LDH, AS = kPiece * kGroup;   // doubles per buffer
@@ -329,9 +339,12 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     if (q % kSub != half) continue;
     const long cc = q * 8 + 2 * (lane & 3);
     if (row < nrows && cc < ncols) {
-      double2 o = *reinterpret_cast<const double2*>(Y0 + row * ldy + cc);
-      o.x += c[q][0];
-      o.y += c[q][1];
+      double2 o = make_double2(c[q][0], c[q][1]);
+      if (Y0 != nullptr) {
+        const double2 y0 = *reinterpret_cast<const double2*>(Y0 + row * ldy + cc);
+        o.x += y0.x;
+        o.y += y0.y;
+      }
       *reinterpret_cast<double2*>(Y + row * ldy + cc) = o;
       const double2 h = *reinterpret_cast<const double2*>(X + row * ldx + cc);
       d[q][0] = h.x * o.x;
@@ -352,11 +365,11 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     }
   }
   __syncthreads();
-  if (tid < ncols) {
+  if (tid < NT * 8 && tid < ncols) {
     double sacc = 0.0;
 #pragma unroll
     for (int r = 0; r < kRT; ++r) sacc += dred[r][tid];
-    partial[g * ncols + tid] = sacc;
+    partial[g * ldp + tid] = sacc;
   }
 }
 // gval[gslot[p]] = val[p] (gval zeroed first)
@@ -429,31 +442,41 @@ void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t 
 
 long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
-bool spmm_block_supported(long ncols) { return ncols <= 64 && ncols % 8 == 0; }
+bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
 
+// Y = S X (+ Y0) over ncols (multiple of 8) columns in 64-column tiles; dot[c] = sum_r X[r][c] Y[r][c]
 void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                     double* dot, double* partial, const double* Y0, cudaStream_t s) {
-  require(spmm_block_supported(ncols) && ldx == ncols && ldy == ncols, "spmm_block_dot: unsupported block");
+  require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
-  const int nt = static_cast<int>(ncols / 8);
-  const long ldh = ncols + (20 - ncols % 16) % 16;
-  const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
-  auto go = [&](auto kern) {
-    FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<static_cast<unsigned>(pat.ngrp), 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, X, ldx, Y,
-                                                          ldy, ncols, Y0 != nullptr ? Y0 : Y, partial);
+  auto launch = [&](int nt, long c_first, long tiles) {
+    const long ldh = 8L * nt + (20 - (8L * nt) % 16) % 16;
+    const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
+    const double* x = X + c_first;
+    double* y = Y + c_first;
+    const double* y0 = Y0 != nullptr ? Y0 + c_first : nullptr;
+    double* part = partial + c_first;
+    const long nc = ncols - c_first;
+    const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
+    auto go = [&](auto kern) {
+      FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, x, ldx, y, ldy, nc, y0, part, ncols);
+    };
+    switch (nt) {
+      case 1: go(k_spmm_block<1>); break;
+      case 2: go(k_spmm_block<2>); break;
+      case 3: go(k_spmm_block<3>); break;
+      case 4: go(k_spmm_block<4>); break;
+      case 5: go(k_spmm_block<5>); break;
+      case 6: go(k_spmm_block<6>); break;
+      case 7: go(k_spmm_block<7>); break;
+      default: go(k_spmm_block<8>); break;
+    }
+    FSA_LAUNCH_CHECK();
   };
-  switch (nt) {
-    case 1: go(k_spmm_block<1>); break;
-    case 2: go(k_spmm_block<2>); break;
-    case 3: go(k_spmm_block<3>); break;
-    case 4: go(k_spmm_block<4>); break;
-    case 5: go(k_spmm_block<5>); break;
-    case 6: go(k_spmm_block<6>); break;
-    case 7: go(k_spmm_block<7>); break;
-    default: go(k_spmm_block<8>); break;
-  }
-  FSA_LAUNCH_CHECK();
+  const long full = ncols / 64, rem = ncols % 64;
+  if (full > 0) launch(8, 0, full);
+  if (rem > 0) launch(static_cast<int>(rem / 8), full * 64, 1);
   colsum_partials(partial, pat.ngrp, ncols, ncols, dot, s);
 }
 
