@@ -264,6 +264,19 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 // the arithmetic moves onto the tensor pipe. 8 warps: warp w owns row tile w % 4 and every
 // other 8-column tile.
 constexpr int kPiece = 64;  // union rows per pipeline stage (16 DMMA k-steps)
+// the k-steps of one staged piece for the n-tiles q = H, H + SUB, ... (compile-time: no
+// predicated mma.sync, which would need a warp sync per instruction)
+template <int NT, int SUB, int H>
+__device__ __forceinline__ void block_ksteps(double (&c)[NT][2], const double* as, const double* hs, int nks,
+                                             int lane, int ldh, int astride) {
+#pragma unroll 4
+  for (int ks = 0; ks < nks; ++ks) {
+    const double a = as[ks * astride];
+    const double* hb = hs + (ks * 4 + (lane & 3)) * ldh + (lane >> 2);
+#pragma unroll
+    for (int q = H; q < NT; q += SUB) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
+  }
+}
 template <int NT>
 __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ gptr, const int* __restrict__ gcol,
                                                       const double* __restrict__ gval, long nrows,
@@ -320,13 +333,12 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     const double* as = sm + 2 * HS + (pc & 1) * AS + rt * 32 + lane;
     static_assert(kGroup % 8 == 0 && 8 % (kGroup / 8) == 0, "row tiles must divide the 8 warps");
     const int nks = min(kPiece, up - pc * kPiece) / 4;
-#pragma unroll 4
-    for (int ks = 0; ks < nks; ++ks) {
-      const double a = as[ks * kRT * 32];
-      const double* hb = hs + (ks * 4 + (lane & 3)) * LDH + (lane >> 2);
-#pragma unroll
-      for (int q = 0; q < NT; ++q)
-        if (q % kSub == half) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
+    static_assert(kSub <= 4, "at most four column subsets");
+    switch (half) {
+      case 0: block_ksteps<NT, kSub, 0>(c, as, hs, nks, lane, LDH, kRT * 32); break;
+      case 1: block_ksteps<NT, kSub, 1 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
+      case 2: block_ksteps<NT, kSub, 2 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
+      default: block_ksteps<NT, kSub, 3 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
     }
     __syncthreads();  // the buffer is refilled by issue(pc + 2)
   }
