@@ -62,6 +62,17 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + " is null");
 }
 
+// Stream-ordered temporaries (DBuf) are allocated and freed on the calling thread's
+// alloc_stream(): bind it (and the device) to the handle's context on every entry, so that a
+// context driven from any host thread keeps its temporaries ordered on its own stream.
+struct Bind {
+  explicit Bind(Context* c) {
+    if (c == nullptr) return;
+    alloc_stream() = c->stream;
+    cudaSetDevice(c->device);
+  }
+};
+
 // entry points whose host buffers hold every point (caller order) exist on one rank only;
 // a row-sharded context runs the fit path (iterative_nll_grad) alone
 void single_rank(const Context* c, const char* what) {
@@ -158,7 +169,11 @@ int fsa_ctx_create(int device, fsa_ctx** out) {
     *out = c.release();
   });
 }
-void fsa_ctx_destroy(fsa_ctx* ctx) { delete ctx; }
+void fsa_ctx_destroy(fsa_ctx* ctx) {
+  if (ctx == nullptr) return;
+  Bind bind_(ctx->c.get());
+  delete ctx;
+}
 int fsa_nccl_unique_id(void* id_out) {
   return guard([&] {
     need(id_out, "id_out");
@@ -194,6 +209,7 @@ int fsa_ctx_group_create(int device, int world, fsa_ctx** out) {
 int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     if (rank) *rank = ctx->c->comm->rank();
     if (world) *world = ctx->c->comm->size();
   });
@@ -201,6 +217,7 @@ int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world) {
 int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     require(mode >= 0 && mode <= 2, "gemm mode must be 0 (auto), 1 (dmma) or 2 (ozaki)");
     ctx->c->gemm_mode = mode;
   });
@@ -208,18 +225,21 @@ int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode) {
 int fsa_ctx_synchronize(fsa_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     ctx->c->sync();
   });
 }
 int fsa_ctx_stream(fsa_ctx* ctx, void** stream) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     *stream = ctx->c->stream;
   });
 }
 int fsa_ctx_set_profiling(fsa_ctx* ctx, int on) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     ctx->c->flush_timers();
     ctx->c->profile = on != 0;
   });
@@ -227,6 +247,7 @@ int fsa_ctx_set_profiling(fsa_ctx* ctx, int on) {
 int fsa_ctx_reset_timers(fsa_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     ctx->c->flush_timers();
     ctx->c->totals.clear();
   });
@@ -234,6 +255,7 @@ int fsa_ctx_reset_timers(fsa_ctx* ctx) {
 int fsa_ctx_timer_names(fsa_ctx* ctx, char* buf, size_t len) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     ctx->c->flush_timers();
     std::string s;
     for (const auto& kv : ctx->c->totals) s += kv.first + "\n";
@@ -246,6 +268,7 @@ int fsa_ctx_timer_names(fsa_ctx* ctx, char* buf, size_t len) {
 int fsa_ctx_timer(fsa_ctx* ctx, const char* name, double* ms, int64_t* count, double* units) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     need(name, "name");
     ctx->c->flush_timers();
     auto it = ctx->c->totals.find(name);
@@ -288,6 +311,7 @@ int fsa_probe_rademacher(uint64_t seed, uint64_t index, int64_t n, double* z) {
 int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, double gamma, fsa_geometry** out) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     need(coords, "coords");
     auto g = std::make_unique<fsa_geometry>();
     g->ctx = ctx;
@@ -295,10 +319,16 @@ int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, do
     *out = g.release();
   });
 }
-void fsa_geometry_destroy(fsa_geometry* g) { delete g; }
+void fsa_geometry_destroy(fsa_geometry* g) {
+  if (g == nullptr) return;
+  Bind bind_(g->ctx->c.get());
+  cudaStreamSynchronize(g->ctx->c->stream);
+  delete g;
+}
 int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     if (n) *n = g->g->pts.n;
     if (nnz) *nnz = g->g->pat.nnz;
   });
@@ -306,6 +336,7 @@ int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz) {
 int fsa_geometry_shard_info(fsa_geometry* g, int64_t* r0, int64_t* r1, int64_t* n_halo) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     const ShardPlan& sp = g->g->shard;
     const bool one = sp.world <= 1;
     if (r0) *r0 = one ? 0 : sp.r0;
@@ -316,6 +347,7 @@ int fsa_geometry_shard_info(fsa_geometry* g, int64_t* r0, int64_t* r1, int64_t* 
 int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double* dist) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     single_rank(g->ctx->c.get(), "taper_pattern export");
     export_csr(g->g->pat, g->g->pat.dist.get(), g->g->pts, g->g->pts, g->ctx->c->stream, rowptr, col, dist);
   });
@@ -323,6 +355,7 @@ int fsa_geometry_pattern(fsa_geometry* g, int64_t* rowptr, int32_t* col, double*
 int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     std::copy(g->g->pts.perm.begin(), g->g->pts.perm.end(), perm);
   });
 }
@@ -330,6 +363,7 @@ int fsa_geometry_permutation(fsa_geometry* g, int32_t* perm) {
 int fsa_geometry_set_response(fsa_geometry* g, const double* y, const double* X, int64_t pcols) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     need(y, "y");
     require(pcols >= 0 && (pcols == 0 || X != nullptr), "nll: shape mismatch");
     Geometry& G = *g->g;
@@ -346,6 +380,7 @@ int fsa_geometry_set_response(fsa_geometry* g, const double* y, const double* X,
 int fsa_geometry_cache_probes(fsa_geometry* g, int on) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     g->g->cache_probes = on != 0;
     if (!on) {
       g->g->probes.valid = false;
@@ -360,6 +395,7 @@ int fsa_model_assemble(fsa_ctx* ctx, const double* coords, int64_t n, int d, con
                        const fsa_params* params, fsa_model** out) {
   return guard([&] {
     need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
     need(coords, "coords");
     need(inducing, "inducing");
     const Params p = to_params(params);
@@ -375,6 +411,7 @@ int fsa_model_assemble_geo(fsa_geometry* g, const double* inducing, int64_t m, c
                            fsa_model** out) {
   return guard([&] {
     need(g, "geometry");
+    Bind bind_(g->ctx->c.get());
     need(inducing, "inducing");
     auto md = std::make_unique<fsa_model>();
     md->ctx = g->ctx;
@@ -382,10 +419,16 @@ int fsa_model_assemble_geo(fsa_geometry* g, const double* inducing, int64_t m, c
     *out = md.release();
   });
 }
-void fsa_model_destroy(fsa_model* md) { delete md; }
+void fsa_model_destroy(fsa_model* md) {
+  if (md == nullptr) return;
+  Bind bind_(md->m->ctx);
+  cudaStreamSynchronize(md->m->ctx->stream);
+  delete md;
+}
 int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t* n_clamped, double* ldsm) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     Model& M = *md->m;
     if (n) *n = M.geo->pts.n;  // all points (a sharded rank owns a row block of them)
     if (m) *m = M.m;
@@ -397,6 +440,7 @@ int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t*
 int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, double* val) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     Model& M = *md->m;
     single_rank(M.ctx, "Sigma_s export");
     require(which == 0 || which == 1, "which must be 0 (sigma_s) or 1 (d sigma_s / d rho)");
@@ -408,6 +452,7 @@ int fsa_model_sigma_s(fsa_model* md, int which, int64_t* rowptr, int32_t* col, d
 int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     Model* M = md->m.get();
     single_rank(M->ctx, "matmat");
     require(k >= 1, "matrix row mismatch");
@@ -421,6 +466,7 @@ int fsa_model_matmat(fsa_model* md, const double* V, int64_t k, double* out) {
 int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k, double* out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     Model* M = md->m.get();
     single_rank(M->ctx, "matmat");
     require(k >= 1, "matrix row mismatch");
@@ -434,6 +480,7 @@ int fsa_model_deriv_matmat(fsa_model* md, int which, const double* V, int64_t k,
 int fsa_model_lowrank_project(fsa_model* md, const double* V, int64_t k, double* out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     need(V, "V");
     need(out, "out");
     Model* M = md->m.get();
@@ -453,6 +500,7 @@ int fsa_model_lowrank_project(fsa_model* md, const double* V, int64_t k, double*
 int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     need(W, "W");
     need(out, "out");
     Model* M = md->m.get();
@@ -472,6 +520,7 @@ int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* 
 int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     Model* M = md->m.get();
     single_rank(M->ctx, "diagonals");
     cudaStream_t s = M->ctx->stream;
@@ -492,6 +541,7 @@ int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {
 int fsa_make_preconditioner(fsa_model* md, int type, fsa_precond** out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     auto p = std::make_unique<fsa_precond>();
     p->md = md;
     p->p = make_preconditioner(md->m.get(), type);
@@ -501,6 +551,7 @@ int fsa_make_preconditioner(fsa_model* md, int type, fsa_precond** out) {
 int fsa_make_jacobi(fsa_model* md, fsa_precond** out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     auto p = std::make_unique<fsa_precond>();
     p->md = md;
     single_rank(md->m->ctx, "the Jacobi preconditioner");
@@ -508,16 +559,23 @@ int fsa_make_jacobi(fsa_model* md, fsa_precond** out) {
     *out = p.release();
   });
 }
-void fsa_precond_destroy(fsa_precond* p) { delete p; }
+void fsa_precond_destroy(fsa_precond* p) {
+  if (p == nullptr) return;
+  Bind bind_(p->md->m->ctx);
+  cudaStreamSynchronize(p->md->m->ctx->stream);
+  delete p;
+}
 int fsa_precond_logdet(fsa_precond* p, double* out) {
   return guard([&] {
     need(p, "preconditioner");
+    Bind bind_(p->md->m->ctx);
     *out = p->p->logdet();
   });
 }
 int fsa_precond_solve_mat(fsa_precond* p, const double* R, int64_t k, double* out) {
   return guard([&] {
     need(p, "preconditioner");
+    Bind bind_(p->md->m->ctx);
     Model* M = p->md->m.get();
     single_rank(M->ctx, "solve_mat");
     const long tp = pad_cols(k);
@@ -530,6 +588,7 @@ int fsa_precond_solve_mat(fsa_precond* p, const double* R, int64_t k, double* ou
 int fsa_precond_sample_probes(fsa_precond* p, int L, uint64_t seed, double* Z) {
   return guard([&] {
     need(p, "preconditioner");
+    Bind bind_(p->md->m->ctx);
     require(L > 0, "need at least one probe");
     Model* M = p->md->m.get();
     single_rank(M->ctx, "sample_probes");
@@ -542,6 +601,7 @@ int fsa_precond_sample_probes(fsa_precond* p, int L, uint64_t seed, double* Z) {
 int fsa_precond_deriv_trace(fsa_precond* p, int which, double* out) {
   return guard([&] {
     need(p, "preconditioner");
+    Bind bind_(p->md->m->ctx);
     require(which >= 0 && which < 3, "parameter index out of range");
     require(p->p->kind() == 2, "deriv_trace is implemented for the FITC preconditioner");
     *out = static_cast<FitcPrecond*>(p->p.get())->deriv_trace(which);
@@ -553,6 +613,7 @@ int fsa_pcg_solve_multi(fsa_model* md, fsa_precond* p, int op_kind, const double
                         double* toff, int* sweeps) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     need(p, "preconditioner");
     Model* M = md->m.get();
     single_rank(M->ctx, "pcg_solve_multi on host blocks");
@@ -586,6 +647,7 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
                            double* beta) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     need(p, "preconditioner");
     need(out, "out");
     require(pcols == 0 || X != nullptr, "nll: shape mismatch");
@@ -607,6 +669,7 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
 int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** out) {
   return guard([&] {
     need(md, "model");
+    Bind bind_(md->m->ctx);
     need(pcoords, "pcoords");
     single_rank(md->m->ctx, "prediction");
     auto pr = std::make_unique<fsa_pred>();
@@ -615,10 +678,16 @@ int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** 
     *out = pr.release();
   });
 }
-void fsa_pred_destroy(fsa_pred* pr) { delete pr; }
+void fsa_pred_destroy(fsa_pred* pr) {
+  if (pr == nullptr) return;
+  Bind bind_(pr->md->m->ctx);
+  cudaStreamSynchronize(pr->md->m->ctx->stream);
+  delete pr;
+}
 int fsa_pred_info(fsa_pred* pr, int64_t* np, int64_t* nnz) {
   return guard([&] {
     need(pr, "prediction set");
+    Bind bind_(pr->md->m->ctx);
     if (np) *np = pr->p->np;
     if (nnz) *nnz = pr->p->rows.nnz;
   });
@@ -626,6 +695,7 @@ int fsa_pred_info(fsa_pred* pr, int64_t* np, int64_t* nnz) {
 int fsa_cross_apply_t(fsa_pred* pr, const double* u, double* out) {
   return guard([&] {
     need(pr, "prediction set");
+    Bind bind_(pr->md->m->ctx);
     cross_apply_t(*pr->p, u, out);
   });
 }
@@ -633,6 +703,7 @@ int fsa_predict_mean_iterative(fsa_pred* pr, const double* resid, fsa_precond* p
                                double* mean_out) {
   return guard([&] {
     need(pr, "prediction set");
+    Bind bind_(pr->md->m->ctx);
     need(p, "preconditioner");
     predict_mean_iterative(*pr->p, resid, *p->p, to_cg(cg), mean_out);
   });
@@ -642,6 +713,7 @@ int fsa_predict_var_sim(fsa_pred* pr, int num_probes, uint64_t seed, const fsa_c
                         fsa_predvar_info* info) {
   return guard([&] {
     need(pr, "prediction set");
+    Bind bind_(pr->md->m->ctx);
     PredVarInfo pi = predict_var_sim(*pr->p, num_probes, seed, to_cg(cg), to_cg(cg_s), control_variate != 0,
                                      floor_rel, var, se);
     if (info) {
@@ -656,6 +728,7 @@ int fsa_pred_det_pieces(fsa_pred* pr, const fsa_cg_options* cg, const fsa_cg_opt
                         double* d3, int* cg_iterations) {
   return guard([&] {
     need(pr, "prediction set");
+    Bind bind_(pr->md->m->ctx);
     int it = 0;
     deterministic_pieces_host(*pr->p, to_cg(cg), to_cg(cg_s), d1, d2, d3, &it);
     if (cg_iterations) *cg_iterations = it;

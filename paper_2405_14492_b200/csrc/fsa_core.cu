@@ -270,9 +270,16 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   SddmmParams sp{p.nu, p.family, p.sigma2, p.sigma1_2, p.rho, p.gamma};
   {
     KTimer t(ctx, "setup_sddmm", 2.0 * mp * pat.nnz);
-    sddmm_sigma_s(M.U.get(), mp, pat, M.lowrank.get(), sp, M.sval.get(), M.info.get() + 1, s);
+    if (pat.gnnz > 0 && mp % 32 == 0) {  // dense Gram blocks on DMMA; fills the SpMM value blocks too
+      M.gval.alloc(static_cast<size_t>(pat.gnnz * kGroup));
+      DBuf<double> gtmp(static_cast<size_t>(pat.gnnz * kGroup));
+      sddmm_block(0, M.U.get(), nullptr, nullptr, mp, mp, pat, M.lowrank.get(), sp, M.sval.get(), M.gval.get(),
+                  M.info.get() + 1, gtmp.get(), s);
+    } else {
+      sddmm_sigma_s(M.U.get(), mp, pat, M.lowrank.get(), sp, M.sval.get(), M.info.get() + 1, s);
+    }
   }
-  if (pat.gnnz > 0) {  // value blocks of the row groups (grouped SpMM of the PCG sweeps)
+  if (pat.gnnz > 0 && !(mp % 32 == 0)) {  // value blocks of the row groups (block SpMM of the PCG sweeps)
     KTimer t(ctx, "setup_group_values", 16.0 * pat.nnz + 8.0 * kGroup * pat.gnnz);
     M.gval.alloc(static_cast<size_t>(pat.gnnz * kGroup));
     group_values(pat, M.sval.get(), M.gval.get(), s);
@@ -323,7 +330,13 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   SddmmParams sp{P.nu, P.family, P.sigma2, P.sigma1_2, P.rho, P.gamma};
   {
     KTimer t3(ctx, "rho_sddmm", 4.0 * m * pat.nnz / 2);
-    sddmm_drho(U.get(), U1.get(), T.get(), mp, pat, lowrank.get(), sp, dsval.get(), s);
+    if (pat.gnnz > 0 && mp % 32 == 0) {  // dense Gram blocks of the row groups on DMMA
+      DBuf<double> gtmp(static_cast<size_t>(pat.gnnz * kGroup));
+      sddmm_block(1, U.get(), U1.get(), T.get(), mp, mp, pat, lowrank.get(), sp, dsval.get(), nullptr, nullptr,
+                  gtmp.get(), s);
+    } else {
+      sddmm_drho(U.get(), U1.get(), T.get(), mp, pat, lowrank.get(), sp, dsval.get(), s);
+    }
   }
   dD.alloc(np);
   extract_diag(dsval.get(), pat.diagpos.get(), n, np, dD.get(), nullptr, nullptr, s);

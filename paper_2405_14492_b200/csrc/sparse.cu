@@ -384,6 +384,138 @@ __global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ 
     partial[g * ldp + tid] = sacc;
   }
 }
+// ---- block SDDMM: dense Gram blocks of the row groups on DMMA ----------------------------------
+// G = A_R^T B_C for a group's 32 rows R and a 64-column tile C of its union, over K (the
+// inducing dimension): MODE 0 A = B = U (Sigma_s); MODE 1 [U1; U]_R^T [U; T]_C (d Sigma_s /
+// d rho, K = 2 m). K pieces of 32 are staged by cp.async (double-buffered) and the block
+// product runs as DMMA m8n8k4 tiles; the result is stored in the value-block layout of the
+// block SpMM (gslot order), from which k_sddmm_finish picks the pattern's entries.
+// Evaluating full blocks costs ~6x the pattern's dot products but turns the L1-bound
+// per-nonzero gathers of m-vectors into tensor-core work on staged tiles.
+constexpr int kGK = 32;                // K per staged piece
+constexpr int kGLd = kGK + 4;          // smem row stride (== 4 mod 16: conflict-free fragments)
+template <int SUB, int H>
+__device__ __forceinline__ void gram_ksteps(double (&c)[8][2], const double* As, const double* Bs, int rt, int lane) {
+#pragma unroll
+  for (int ks = 0; ks < kGK / 4; ++ks) {
+    const double a = As[(rt * 8 + (lane >> 2)) * kGLd + ks * 4 + (lane & 3)];
+#pragma unroll
+    for (int q = H; q < 8; q += SUB) {
+      const double b = Bs[(q * 8 + (lane >> 2)) * kGLd + ks * 4 + (lane & 3)];
+      dmma8x8x4(c[q][0], c[q][1], a, b);
+    }
+  }
+}
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ gptr, const int* __restrict__ gcol,
+                                                      long nrows, const double* __restrict__ A0,
+                                                      const double* __restrict__ B0, const double* __restrict__ A1,
+                                                      const double* __restrict__ B1, long ldu, long mp,
+                                                      double* __restrict__ G) {
+  extern __shared__ __align__(16) double gsm[];
+  double(*As)[kGroup * kGLd] = reinterpret_cast<double(*)[kGroup * kGLd]>(gsm);
+  double(*Bs)[64 * kGLd] = reinterpret_cast<double(*)[64 * kGLd]>(gsm + 2 * kGroup * kGLd);
+  const long g = blockIdx.x;
+  const int jt = blockIdx.y;
+  const long u0 = gptr[g];
+  const int up = static_cast<int>(gptr[g + 1] - u0);
+  const int j0 = jt * 64;
+  if (j0 >= up) return;
+  const int nc = min(64, up - j0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rt = warp & 3, half = warp >> 2;
+  const long r0 = g * kGroup;
+  const long K = MODE == 0 ? mp : 2 * mp;
+  const int npc = static_cast<int>(K / kGK);
+  // columns beyond the tile's union and rows beyond nrows stay zero in smem
+  for (int i = tid; i < 2 * 64 * kGLd; i += 256) (&Bs[0][0])[i] = 0.0;
+  for (int i = tid; i < 2 * kGroup * kGLd; i += 256) (&As[0][0])[i] = 0.0;
+  __syncthreads();
+  auto issue = [&](int pc) {
+    const long k0 = static_cast<long>(pc) * kGK;
+    const bool second = MODE == 1 && k0 >= mp;
+    const double* A = second ? A1 : A0;
+    const double* B = second ? B1 : B0;
+    const long kk = second ? k0 - mp : k0;
+    double* as = As[pc & 1];
+    double* bs = Bs[pc & 1];
+    for (int idx = tid; idx < kGroup * (kGK / 2); idx += 256) {
+      const int r = idx / (kGK / 2), ch = idx % (kGK / 2);
+      if (r0 + r < nrows) cp_async16(as + r * kGLd + ch * 2, A + (r0 + r) * ldu + kk + ch * 2);
+    }
+    for (int idx = tid; idx < nc * (kGK / 2); idx += 256) {
+      const int j = idx / (kGK / 2), ch = idx % (kGK / 2);
+      cp_async16(bs + j * kGLd + ch * 2, B + static_cast<long>(gcol[u0 + j0 + j]) * ldu + kk + ch * 2);
+    }
+    cp_async_commit();
+  };
+  double c[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+  issue(0);
+  for (int pc = 0; pc < npc; ++pc) {
+    if (pc + 1 < npc) {
+      issue(pc + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (half == 0) gram_ksteps<2, 0>(c, As[pc & 1], Bs[pc & 1], rt, lane);
+    else gram_ksteps<2, 1>(c, As[pc & 1], Bs[pc & 1], rt, lane);
+    __syncthreads();
+  }
+  const int rr = rt * 8 + (lane >> 2);
+  double* gb = G + static_cast<long>(kGroup) * u0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if ((q & 1) != half) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int u = j0 + q * 8 + 2 * (lane & 3) + e;
+      if (u < up) gb[((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3)] = c[q][e];
+    }
+  }
+}
+// pattern entries from the Gram blocks: Sigma_s (MODE 0) or d Sigma_s / d rho (MODE 1);
+// each unordered pair is evaluated once (from the row with c > r) and mirrored, so the
+// result is exactly symmetric; MODE 0 also fills the SpMM value blocks gval
+template <int MODE>
+__global__ void k_sddmm_finish(const long* __restrict__ rowptr, const int* __restrict__ col,
+                               const long* __restrict__ mirror, const int* __restrict__ gslot,
+                               const double* __restrict__ dist, const double* __restrict__ lowrank_diag,
+                               const double* __restrict__ G, long n, SddmmParams P, double* __restrict__ val,
+                               double* __restrict__ gval, int* __restrict__ n_clamped) {
+  const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) {
+    const long c = col[p];
+    if (c < r) continue;  // written from the mirror entry
+    double v;
+    if (c == r) {
+      const double resid = P.sigma1_2 - lowrank_diag[r];
+      if (MODE == 0) {
+        if (resid < 0.0) atomicAdd(n_clamped, 1);
+        v = (resid < 0.0 ? 0.0 : resid) + P.sigma2;
+      } else {
+        v = resid < 0.0 ? 0.0 : -G[gslot[p]];
+      }
+    } else {
+      const double d = dist[p];
+      const double k = MODE == 0 ? matern_d(d, P.nu, P.sigma1_2, P.rho) : matern_drho_d(d, P.nu, P.sigma1_2, P.rho);
+      v = (k - G[gslot[p]]) * taper_d(d, P.family, P.gamma);
+    }
+    val[p] = v;
+    if (MODE == 0) gval[gslot[p]] = v;
+    const long q = mirror[p];
+    if (c != r && q >= 0) {
+      val[q] = v;
+      if (MODE == 0) gval[gslot[q]] = v;
+    }
+  }
+}
+
 // gval[gslot[p]] = val[p] (gval zeroed first)
 __global__ void k_group_scatter(const int* __restrict__ gslot, long nnz, const double* __restrict__ val,
                                 double* __restrict__ gval) {
@@ -424,6 +556,34 @@ void sddmm_drho(const double* U, const double* U1, const double* T, long ldu, co
   if (grid == 0) return;
   FSA_DISPATCH_MQ(k_sddmm_drho, ldu, grid, s, U, U1, T, ldu, pat.rowptr.get(), pat.col.get(), pat.mirror.get(),
                   pat.dist.get(), lowrank_diag, pat.rows, P, val);
+}
+
+void sddmm_block(int mode, const double* U, const double* U1, const double* T, long ldu, long mp, const Csr& pat,
+                 const double* lowrank_diag, const SddmmParams& P, double* val, double* gval, int* n_clamped_dev,
+                 double* gtmp, cudaStream_t s) {
+  require(pat.gnnz > 0 && mp % kGK == 0, "sddmm_block: row groups missing");
+  const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(cdiv(pat.gmax, 64)));
+  const int smem = static_cast<int>(2 * (kGroup + 64) * kGLd * sizeof(double));
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_block_gram<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FSA_CUDA(cudaFuncSetAttribute(k_block_gram<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  if (mode == 0)
+    k_block_gram<0><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U, U, U, U, ldu, mp, gtmp);
+  else
+    k_block_gram<1><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U1, U, U, T, ldu, mp, gtmp);
+  FSA_LAUNCH_CHECK();
+  if (mode == 0 && gval != nullptr) FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
+  const unsigned g2 = static_cast<unsigned>(cdiv(pat.rows * 32, 256));
+  if (mode == 0)
+    k_sddmm_finish<0><<<g2, 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.mirror.get(), pat.gslot.get(),
+                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, gval, n_clamped_dev);
+  else
+    k_sddmm_finish<1><<<g2, 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.mirror.get(), pat.gslot.get(),
+                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, nullptr, nullptr);
+  FSA_LAUNCH_CHECK();
 }
 
 void sddmm_cross(const double* Rm, long ldr, const double* Cm, long ldc, const Csr& pat, const SddmmParams& P,

@@ -15,6 +15,12 @@ void sddmm_sigma_s(const double* U, long ldu, const Csr& pat, const double* lowr
                    double* val, int* n_clamped_dev, cudaStream_t s);
 void sddmm_drho(const double* U, const double* U1, const double* T, long ldu, const Csr& pat,
                 const double* lowrank_diag, const SddmmParams& P, double* val, cudaStream_t s);
+// the same on the row groups (pat.gnnz > 0) through dense DMMA Gram blocks: mode 0 Sigma_s
+// (also fills the SpMM value blocks gval when non-null), mode 1 d Sigma_s / d rho;
+// gtmp holds kGroup * pat.gnnz doubles
+void sddmm_block(int mode, const double* U, const double* U1, const double* T, long ldu, long mp, const Csr& pat,
+                 const double* lowrank_diag, const SddmmParams& P, double* val, double* gval, int* n_clamped_dev,
+                 double* gtmp, cudaStream_t s);
 void sddmm_cross(const double* Rm, long ldr, const double* Cm, long ldc, const Csr& pat, const SddmmParams& P,
                  double* val, cudaStream_t s);
 // Y = alpha S X + beta Y (first ncols <= 256 columns) fused with dot[c] = sum_r X[r][c] Y[r][c];
