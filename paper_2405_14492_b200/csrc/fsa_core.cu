@@ -185,6 +185,17 @@ void Model::ensure_ozaki() {
   ozaki_prepare(oz, U.get(), m_pad, n_pad, ctx->stream);
 }
 
+bool Model::use_ozaki_spmm(long tp) const {
+  static const char* env = std::getenv("FSA_SPMM");
+  static const bool off = env && (std::strcmp(env, "csr") == 0 || std::strcmp(env, "dmma") == 0);
+  return !off && use_ozaki(tp) && geo->pat.g128.gnnz > 0;
+}
+void Model::ensure_ozaki_spmm() {
+  if (ozs.ready) return;
+  KTimer t(ctx, "ozaki_spmm_prepare", 8.0 * 128 * geo->pat.g128.gnnz);
+  ozaki_spmm_prepare(ozs, geo->pat, sval.get(), ctx->stream);
+}
+
 void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
   const double flops = 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp);
   if (M == U.get() && use_ozaki(tp)) {  // INT8 tensor cores, fp64-accurate (ozaki.cuh)
@@ -667,6 +678,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
   const bool oz = fused && md->use_ozaki(tp);
   if (oz) md->ensure_ozaki();
+  const bool oz_spmm = oz && md->use_ozaki_spmm(tp);
+  if (oz_spmm) md->ensure_ozaki_spmm();
   bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
   auto precond = [&](double* rzout) {
@@ -739,7 +752,11 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-      if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
+      if (oz_spmm)
+        // valid rows of H: owned (padded) + halo; the tail up to n_ext_pad is never written
+        ozaki_spmm_dot(md->ozs, md->geo->pat, w.H.get(), md->n_pad + (md->world() > 1 ? md->geo->shard.n_halo : 0),
+                       tp, w.V.get(), w.Vlr.get(), hv, part, s);
+      else if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
         spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, w.Vlr.get(), s);
       else
         spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,

@@ -169,6 +169,10 @@ class Model {
   OzakiPlan oz;
   bool use_ozaki(long tp) const { return ctx->gemm_mode != 1 && ozaki_supported(tp); }
   void ensure_ozaki();
+  // INT8 tensor-core SpMM planes of Sigma_s (built lazily per parameter set)
+  OzakiSpmm ozs;
+  bool use_ozaki_spmm(long tp) const;
+  void ensure_ozaki_spmm();
 };
 
 // ---- preconditioners (preconditioners.h:16-115) ------------------------------------------

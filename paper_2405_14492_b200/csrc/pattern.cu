@@ -153,20 +153,23 @@ __global__ void k_count(const double* rx, long rld, long rn, const double* cx, l
 
 // Union of the column indices of kGroup consecutive rows: bitonic sort of the
 // group's entries in shared memory, unique, then each entry's union-local index.
-constexpr int kUnionSort = 4096;  // max entries per group handled by the sort
-constexpr int kUnionCap = 1024;   // max union size per group
+constexpr int kUnionSort = 4096;  // max entries per 32-row group handled by the sort
+constexpr int kUnionCap = 1024;   // max union size per 32-row group
+// (G, sort capacity, union capacity) are runtime: dynamic smem holds 2 x kSortCap ints
 __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
-                                                     long nrows, int* __restrict__ ucols, int* __restrict__ ucount,
+                                                     long nrows, int G, int kSortCap, int kCap,
+                                                     int* __restrict__ ucols, int* __restrict__ ucount,
                                                      int* __restrict__ lidx) {
-  __shared__ int keys[kUnionSort];
-  __shared__ int flag[kUnionSort];
+  extern __shared__ int ush[];
+  int* keys = ush;
+  int* flag = ush + kSortCap;
   const long b = blockIdx.x;
-  const long r0 = b * kGroup;
-  const long r1 = r0 + kGroup < nrows ? r0 + kGroup : nrows;
+  const long r0 = b * G;
+  const long r1 = r0 + G < nrows ? r0 + G : nrows;
   const long p0 = rowptr[r0], p1 = rowptr[r1];
   const long cnt = p1 - p0;
   const int tid = threadIdx.x;
-  if (cnt > kUnionSort) {
+  if (cnt > kSortCap) {
     if (tid == 0) ucount[b] = -1;
     return;
   }
@@ -206,11 +209,11 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
   }
   __syncthreads();
   const int U = cnt > 0 ? flag[cnt - 1] : 0;
-  if (U > kUnionCap) {
+  if (U > kCap) {
     if (tid == 0) ucount[b] = -1;
     return;
   }
-  int* out = ucols + b * kUnionCap;
+  int* out = ucols + b * kCap;
   for (int i = tid; i < cnt; i += blockDim.x)
     if (i == 0 || keys[i] != keys[i - 1]) out[flag[i] - 1] = keys[i];
   __syncthreads();
@@ -225,13 +228,13 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
   }
   if (tid == 0) ucount[b] = U;
 }
-__global__ void k_group_compact(const int* __restrict__ ucols, const int* __restrict__ ucount,
+__global__ void k_group_compact(const int* __restrict__ ucols, int kCap, const int* __restrict__ ucount,
                                 const long* __restrict__ gptr, long ngrp, int* __restrict__ gcol) {
   const long b = blockIdx.x;
   if (b >= ngrp) return;
   const long o = gptr[b], up = gptr[b + 1] - o;
   const int u = ucount[b];
-  for (long i = threadIdx.x; i < up; i += blockDim.x) gcol[o + i] = ucols[b * kUnionCap + (i < u ? i : 0)];
+  for (long i = threadIdx.x; i < up; i += blockDim.x) gcol[o + i] = ucols[b * kCap + (i < u ? i : 0)];
 }
 // value index of entry p (row r, union slot u of group g): A-fragment order of the
 // 8 x 4 DMMA tiles: [k-step u/4][warp (r%32)/8][lane ((r%8)*4 + u%4)]
@@ -246,12 +249,61 @@ __global__ void k_group_slots(const long* __restrict__ rowptr, long nrows, const
     lidx_to_slot[p] = static_cast<int>(kGroup * o + ((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3));
   }
 }
-__global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int* __restrict__ bad, long* __restrict__ sizes) {
+__global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int pad, int* __restrict__ bad,
+                           long* __restrict__ sizes) {
   const long b = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= ngrp) return;
   const int u = ucount[b];
   if (u < 0) atomicExch(bad, 1);
-  sizes[b] = u < 0 ? 0 : (u + 3) / 4 * 4;
+  sizes[b] = u < 0 ? 0 : (u + pad - 1) / pad * pad;
+}
+// unions of G consecutive rows, padded to `pad`; false if a group exceeds the capacities
+bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& ngrp, long& gnnz, int& gmax,
+                  DBuf<long>& gptr, DBuf<int>& gcol, DBuf<int>& lidx, cudaStream_t s) {
+  gnnz = 0;
+  ngrp = cdiv(pat.rows, G);
+  if (ngrp == 0 || pat.nnz == 0) return false;
+  DBuf<int> ucols(static_cast<size_t>(ngrp) * cap), ucount(ngrp), bad(1);
+  DBuf<long> sizes(ngrp + 1);
+  lidx.alloc(pat.nnz);
+  const int smem = 2 * sort_cap * static_cast<int>(sizeof(int));
+  FSA_CUDA(cudaFuncSetAttribute(k_group_union, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_group_union<<<static_cast<unsigned>(ngrp), 512, smem, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap,
+                                                              cap, ucols.get(), ucount.get(), lidx.get());
+  FSA_LAUNCH_CHECK();
+  bad.zero(s);
+  FSA_CUDA(cudaMemsetAsync(sizes.get() + ngrp, 0, sizeof(long), s));
+  k_group_ok<<<static_cast<unsigned>(cdiv(ngrp, 256)), 256, 0, s>>>(ucount.get(), ngrp, pad, bad.get(), sizes.get());
+  FSA_LAUNCH_CHECK();
+  int hbad = 0;
+  FSA_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  if (hbad) {
+    lidx.release();
+    return false;
+  }
+  gptr.alloc(ngrp + 1);
+  size_t tmp_bytes = 0;
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes.get(), gptr.get(), ngrp + 1, s));
+  DBuf<unsigned char> tmp(tmp_bytes);
+  FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, sizes.get(), gptr.get(), ngrp + 1, s));
+  FSA_CUDA(cudaMemcpyAsync(&gnnz, gptr.get() + ngrp, sizeof(long), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  gcol.alloc(gnnz > 0 ? gnnz : 1);
+  k_group_compact<<<static_cast<unsigned>(ngrp), 128, 0, s>>>(ucols.get(), cap, ucount.get(), gptr.get(), ngrp,
+                                                              gcol.get());
+  FSA_LAUNCH_CHECK();
+  std::vector<long> gp(static_cast<size_t>(ngrp + 1));
+  FSA_CUDA(cudaMemcpyAsync(gp.data(), gptr.get(), sizeof(long) * (ngrp + 1), cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  long mx = 0;
+  for (long g = 0; g < ngrp; ++g) mx = std::max(mx, gp[static_cast<size_t>(g + 1)] - gp[static_cast<size_t>(g)]);
+  gmax = static_cast<int>(mx);
+  if (std::getenv("FSA_DEBUG"))
+    std::fprintf(stderr, "[fsa] row groups of %d: %ld groups, union %ld (%.1f per group, max %d), nnz %ld (%.2f x)\n",
+                 G, ngrp, gnnz, static_cast<double>(gnnz) / ngrp, gmax, pat.nnz,
+                 static_cast<double>(pat.nnz) / std::max<long>(gnnz, 1));
+  return true;
 }
 
 // mirror[p] = position of (c, r) for p = (r, c): binary search of r in row c (warp per row)
@@ -357,52 +409,18 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
 }
 
 void build_groups(Csr& pat, cudaStream_t s) {
-  pat.gnnz = 0;
-  pat.ngrp = cdiv(pat.rows, kGroup);
-  if (pat.ngrp == 0 || pat.nnz == 0) return;
-  DBuf<int> ucols(static_cast<size_t>(pat.ngrp) * kUnionCap), ucount(pat.ngrp), bad(1);
-  DBuf<long> sizes(pat.ngrp + 1);
-  pat.gslot.alloc(pat.nnz);
-  k_group_union<<<static_cast<unsigned>(pat.ngrp), 512, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, ucols.get(),
-                                                               ucount.get(), pat.gslot.get());
-  FSA_LAUNCH_CHECK();
-  bad.zero(s);
-  FSA_CUDA(cudaMemsetAsync(sizes.get() + pat.ngrp, 0, sizeof(long), s));
-  k_group_ok<<<static_cast<unsigned>(cdiv(pat.ngrp, 256)), 256, 0, s>>>(ucount.get(), pat.ngrp, bad.get(), sizes.get());
-  FSA_LAUNCH_CHECK();
-  int hbad = 0;
-  FSA_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  FSA_CUDA(cudaStreamSynchronize(s));
-  if (hbad) {  // a group too wide for the union kernel: keep the plain CSR path
-    pat.gslot.release();
+  if (!build_unions(pat, kGroup, 4, kUnionSort, kUnionCap, pat.ngrp, pat.gnnz, pat.gmax, pat.gptr, pat.gcol, pat.gslot,
+                    s)) {
+    pat.gnnz = 0;
     return;
   }
-  pat.gptr.alloc(pat.ngrp + 1);
-  size_t tmp_bytes = 0;
-  FSA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes.get(), pat.gptr.get(), pat.ngrp + 1, s));
-  DBuf<unsigned char> tmp(tmp_bytes);
-  FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, sizes.get(), pat.gptr.get(), pat.ngrp + 1, s));
-  FSA_CUDA(cudaMemcpyAsync(&pat.gnnz, pat.gptr.get() + pat.ngrp, sizeof(long), cudaMemcpyDeviceToHost, s));
-  FSA_CUDA(cudaStreamSynchronize(s));
-  pat.gcol.alloc(pat.gnnz > 0 ? pat.gnnz : 1);
-  if (std::getenv("FSA_DEBUG"))
-    std::fprintf(stderr, "[fsa] row groups: %ld groups, union %ld (%.1f per group), nnz %ld (%.2f x)\n", pat.ngrp,
-                 pat.gnnz, static_cast<double>(pat.gnnz) / pat.ngrp, pat.nnz,
-                 static_cast<double>(pat.nnz) / std::max<long>(pat.gnnz, 1));
-  k_group_compact<<<static_cast<unsigned>(pat.ngrp), 128, 0, s>>>(ucols.get(), ucount.get(), pat.gptr.get(), pat.ngrp,
-                                                                  pat.gcol.get());
-  {  // largest padded union (smem budget of the block SpMM)
-    std::vector<long> gp(static_cast<size_t>(pat.ngrp + 1));
-    FSA_CUDA(cudaMemcpyAsync(gp.data(), pat.gptr.get(), sizeof(long) * (pat.ngrp + 1), cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaStreamSynchronize(s));
-    long mx = 0;
-    for (long g = 0; g < pat.ngrp; ++g) mx = std::max(mx, gp[static_cast<size_t>(g + 1)] - gp[static_cast<size_t>(g)]);
-    pat.gmax = static_cast<int>(mx);
-  }
-  FSA_LAUNCH_CHECK();
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());
   FSA_LAUNCH_CHECK();
+  // 128-row groups of the INT8 tensor-core SpMM (unions padded to its 32-row K blocks)
+  RowGroups& q = pat.g128;
+  q.G = 128;
+  if (!build_unions(pat, 128, 32, 16384, 2048, q.ngrp, q.gnnz, q.gmax, q.gptr, q.gcol, q.gslot, s)) q.gnnz = 0;
   FSA_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -33,6 +33,16 @@ struct SortedPoints {
   DBuf<unsigned long long> keys;  // sorted cell keys, length n
 };
 
+// unions of the columns of G consecutive rows (see Csr::gptr below)
+struct RowGroups {
+  int G = 0;
+  long ngrp = 0, gnnz = 0;  // gnnz = total padded union size (0: not built)
+  int gmax = 0;
+  DBuf<long> gptr;          // ngrp + 1
+  DBuf<int> gcol;           // union columns (ascending; padding repeats a valid column)
+  DBuf<int> gslot;          // per entry: its union-local index
+};
+
 struct Csr {
   long rows = 0, cols = 0, nnz = 0;
   DBuf<long> rowptr;   // rows + 1
@@ -51,6 +61,7 @@ struct Csr {
   DBuf<int> gcol;              // union columns (ascending; padding repeats a valid column)
   DBuf<int> gslot;             // per entry: its index in the value blocks (kGroup * gnnz)
   int gmax = 0;                // largest padded union
+  RowGroups g128;              // 128-row groups of the INT8 tensor-core SpMM (ozaki.cu)
 };
 constexpr int kGroup = 32;
 // builds the row groups (leaves gnnz = 0 if some group has more than 4096 entries)
