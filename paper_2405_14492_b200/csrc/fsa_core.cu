@@ -186,9 +186,11 @@ void Model::ensure_ozaki() {
 }
 
 bool Model::use_ozaki_spmm(long tp) const {
+  // opt-in (FSA_SPMM=int8): at config 2 the INT8 SpMM (plus its per-sweep H slicing) is not
+  // yet faster than the DMMA block SpMM
   static const char* env = std::getenv("FSA_SPMM");
-  static const bool off = env && (std::strcmp(env, "csr") == 0 || std::strcmp(env, "dmma") == 0);
-  return !off && use_ozaki(tp) && geo->pat.g128.gnnz > 0;
+  static const bool on = env && std::strcmp(env, "int8") == 0;
+  return on && use_ozaki(tp) && geo->pat.g128.gnnz > 0;
 }
 void Model::ensure_ozaki_spmm() {
   if (ozs.ready) return;

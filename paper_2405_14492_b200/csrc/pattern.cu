@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -417,10 +418,13 @@ void build_groups(Csr& pat, cudaStream_t s) {
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());
   FSA_LAUNCH_CHECK();
-  // 128-row groups of the INT8 tensor-core SpMM (unions padded to its 32-row K blocks)
+  // 128-row groups of the INT8 tensor-core SpMM (opt-in, FSA_SPMM=int8; unions padded to its
+  // 32-row K blocks)
+  static const bool int8 = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "int8") == 0;
   RowGroups& q = pat.g128;
   q.G = 128;
-  if (!build_unions(pat, 128, 32, 16384, 2048, q.ngrp, q.gnnz, q.gmax, q.gptr, q.gcol, q.gslot, s)) q.gnnz = 0;
+  q.gnnz = 0;
+  if (int8 && !build_unions(pat, 128, 32, 16384, 2048, q.ngrp, q.gnnz, q.gmax, q.gptr, q.gcol, q.gslot, s)) q.gnnz = 0;
   FSA_CUDA(cudaStreamSynchronize(s));
 }
 

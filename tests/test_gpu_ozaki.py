@@ -108,3 +108,32 @@ def test_ozaki_pcg_solution_matches_oracle():
     want = O.pcg_solve_multi(om, O.Precond(om, "fitc"), B2, tol=1e-1)
     assert np.array_equal(got["iterations"], want["iterations"])
     assert np.abs(got["X"] - want["X"]).max() <= 1e-8 * np.abs(want["X"]).max()
+
+
+def test_int8_spmm_path_matches_default():
+    """Opt-in INT8 tensor-core SpMM (FSA_SPMM=int8) vs the default path, single rank and sharded."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys
+sys.path.insert(0, %r)
+from tests import test_gpu_sharded as T
+from paper_2405_14492_b200 import fsa
+locs, ind, kw, y, X = T.problem(6000, 80, 0.05, 11, p=2)
+one = T.nll_on(fsa.Context(0), locs, ind, kw, y, X)
+outs = T.run_ranks(fsa.Context.group(0, 3), lambda r, c: T.nll_on(c, locs, ind, kw, y, X))
+print(json.dumps([one["nll"], list(one["grad"]), one["cg_iterations"], outs[0]["nll"], outs[0]["cg_iterations"]]))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("dmma", "int8"):
+        env = dict(os.environ, FSA_SPMM=mode)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
+    a, b = res["int8"], res["dmma"]
+    assert a[2] == b[2] and a[4] == b[4]
+    assert a[0] == pytest.approx(b[0], rel=1e-10) and a[3] == pytest.approx(b[3], rel=1e-10)
+    np.testing.assert_allclose(a[1], b[1], rtol=1e-7, atol=1e-8)
