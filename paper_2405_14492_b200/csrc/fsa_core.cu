@@ -691,7 +691,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       if (oz) {
         {
           KTimer t(ctx, "lowrank_project", 2.0 * md->m * n * k);
-          ozaki_project(md->oz, w.R.get(), tp, md->Dinv.get(), S, s, ymax_ready);
+          ozaki_project(md->oz, w.R.get(), tp, tp, md->Dinv.get(), S, s, ymax_ready);
         }
         if (md->world() > 1) {
           KTimer t(ctx, "allreduce");
@@ -709,7 +709,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
       if (md->use_ozaki(tp))
-        ozaki_expand_keep(md->oz, W, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
+        ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
       else
         gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
                                   md->Dinv.get(), rzout, part, s);

@@ -150,6 +150,7 @@ struct OzEpi {
   int mode;
   long m_pad;   // mode 0: rows of the partial blocks
   long tp;      // real columns to write (modes 1, 2)
+  long ld;      // row stride of R / Z / Lw (modes 1, 2)
   const int* erow;  // exponents of A rows: mode 0 [nchunks][m_pad], else [n_pad]
   const int* ecol;  // exponents of B columns: mode 0 [nchunks][64], else [64]
   double* part;     // mode 0 partials / mode 1 rz partials [tiles][tp]
@@ -271,17 +272,17 @@ __global__ void __launch_bounds__(128, 1)
     if (epi.mode == 2) {
       for (long idx = tid; idx < 128 * tp; idx += 128) {
         const long rr = idx / tp, c = idx - rr * tp;
-        epi.Lw[(r0 + rr) * tp + c] = lws[rr * kLd + c];
+        epi.Lw[(r0 + rr) * epi.ld + c] = lws[rr * kLd + c];
       }
     } else {
       // R tile in, Z = Dinv (R - Lw) and Lw out, row-major tiles are contiguous in HBM
       for (long idx = tid; idx < 128 * tp; idx += 128) {
         const long rr = idx / tp, c = idx - rr * tp;
-        const double x = epi.R[(r0 + rr) * tp + c];
+        const double x = epi.R[(r0 + rr) * epi.ld + c];
         const double lw = lws[rr * kLd + c];
         const double z = (x - lw) * epi.Dinv[r0 + rr];
-        epi.Lw[(r0 + rr) * tp + c] = lw;
-        epi.Z[(r0 + rr) * tp + c] = z;
+        epi.Lw[(r0 + rr) * epi.ld + c] = lw;
+        epi.Z[(r0 + rr) * epi.ld + c] = z;
         rzs[rr * kLd + c] = x * z;
       }
       __syncthreads();
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(192, 1)
       const int et = tid - 64, c = et & 63, h = et >> 6;
       if (c < tp) {
         double sacc = 0.0;
-        const long base = r0 * tp + c;
+        const long base = r0 * epi.ld + c;
 #pragma unroll 1
         for (int rb = h; rb < 128; rb += 16) {
           double x[8], di[8], lw[8];
@@ -423,13 +424,13 @@ __global__ void __launch_bounds__(192, 1)
             const int rr = rb + 2 * u;
             lw[u] = tileY[rr * kXLd + c];
             if (epi.mode == 1) {
-              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * tp);
+              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
               di[u] = __ldg(epi.Dinv + r0 + rr);
             }
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const long off = base + static_cast<long>(rb + 2 * u) * tp;
+            const long off = base + static_cast<long>(rb + 2 * u) * epi.ld;
             epi.Lw[off] = lw[u];
             if (epi.mode == 1) {
               const double z = (x[u] - lw[u]) * di[u];
@@ -788,7 +789,8 @@ __global__ void __launch_bounds__(256) k_oz_planes_points(const double* __restri
 }
 
 // per-sweep B planes of Y = diag(scale) V (project): column max per chunk, then digits
-__global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, long tp, const double* __restrict__ scale,
+__global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, long ld, long tp,
+                                                 const double* __restrict__ scale,
                                                  long n_pad, int kb_per_chunk, int parts,
                                                  unsigned long long* __restrict__ ymax) {
   __shared__ double red[256];
@@ -800,7 +802,7 @@ __global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, l
   const long a0 = i0 + part * per, a1 = min(i1, a0 + per);
   double mx = 0.0;
   if (c < tp)
-    for (long i = a0 + ph; i < a1; i += 4) mx = fmax(mx, fabs(scale ? V[i * tp + c] * scale[i] : V[i * tp + c]));
+    for (long i = a0 + ph; i < a1; i += 4) mx = fmax(mx, fabs(scale ? V[i * ld + c] * scale[i] : V[i * ld + c]));
   red[threadIdx.x] = mx;
   __syncthreads();
   if (ph == 0) {
@@ -808,7 +810,7 @@ __global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, l
     if (mx > 0.0) atomicMax(ymax + static_cast<long>(chunk) * kOzCols + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
   }
 }
-__global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ V, long tp,
+__global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ V, long ld, long tp,
                                                      const double* __restrict__ scale, int kb_per_chunk,
                                                      const unsigned long long* __restrict__ ymax,
                                                      int* __restrict__ f, int8_t* __restrict__ Ys) {
@@ -821,7 +823,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const long i = static_cast<long>(kb) * kKb + kc * 16 + q;
-    v[q] = c < tp ? (scale ? V[i * tp + c] * scale[i] : V[i * tp + c]) : 0.0;
+    v[q] = c < tp ? (scale ? V[i * ld + c] * scale[i] : V[i * ld + c]) : 0.0;
   }
   int4 out[kOzSlices];
   digits16(v, e, out);
@@ -830,12 +832,13 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
   for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
 }
 // per-sweep B planes of W (expand): column exponents over all rows, then digits
-__global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long tp, long mp, int* __restrict__ h) {
+__global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long ld, long tp, long mp,
+                                                  int* __restrict__ h) {
   __shared__ double red[1024];
   const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;  // 16 row phases
   double mx = 0.0;
   if (c < tp)
-    for (long r = ph; r < mp; r += 16) mx = fmax(mx, fabs(W[r * tp + c]));
+    for (long r = ph; r < mp; r += 16) mx = fmax(mx, fabs(W[r * ld + c]));
   red[threadIdx.x] = mx;
   __syncthreads();
   if (ph == 0) {
@@ -843,14 +846,15 @@ __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, 
     h[c] = group_exp(mx);
   }
 }
-__global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long tp, const int* __restrict__ h,
+__global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long ld, long tp,
+                                                     const int* __restrict__ h,
                                                      int8_t* __restrict__ Ws) {
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
   const int e = h[c];
   double v[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * tp + c] : 0.0;
+  for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * ld + c] : 0.0;
   int4 out[kOzSlices];
   digits16(v, e, out);
   int8_t* base = Ws + static_cast<long>(kb) * kBTile + kc * 8192 + c * 16;
@@ -858,13 +862,14 @@ __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ 
   for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
 }
 // S[r][c] = sum_chunk part[chunk][r][c] (fixed order)
-__global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long tp, double* __restrict__ S) {
+__global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long ld, long tp,
+                            double* __restrict__ S) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= mp * tp) return;
   const long r = idx / tp, c = idx % tp;
   double sacc = 0.0;
   for (int q = 0; q < nchunks; ++q) sacc += part[(static_cast<long>(q) * mp + r) * kOzCols + c];
-  S[idx] = sacc;
+  S[r * ld + c] = sacc;
 }
 
 void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nkb_all, int kb_per_chunk,
@@ -889,27 +894,28 @@ void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
   FSA_LAUNCH_CHECK();
 }
 
-void project_impl(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s,
+void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double* scale, double* S, cudaStream_t s,
                   bool ymax_ready) {
-  require(p.ready && tp <= kOzCols, "ozaki: plan not prepared or too many columns");
+  require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
   if (!ymax_ready) {
     FSA_CUDA(cudaMemsetAsync(p.ymax.get(), 0, p.ymax.bytes(), s));
-    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
+    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, ld, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
     FSA_LAUNCH_CHECK();
   }
-  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, tp, scale, p.kb_per_chunk, p.ymax.get(), p.f.get(), p.Ys.get());
+  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, ld, tp, scale, p.kb_per_chunk, p.ymax.get(), p.f.get(), p.Ys.get());
   FSA_LAUNCH_CHECK();
-  OzEpi epi{0, p.m_pad, tp, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
+  OzEpi epi{0, p.m_pad, tp, ld, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
   launch_gemm(p.Ar.get(), p.Ys.get(), p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, epi, s);
-  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * tp, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, tp, S);
+  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * tp, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, ld, tp,
+                                                                             S);
   FSA_LAUNCH_CHECK();
 }
 
-void slice_w(OzakiPlan& p, const double* W, long tp, cudaStream_t s) {
-  require(p.ready && tp <= kOzCols, "ozaki: plan not prepared or too many columns");
-  k_oz_wexp<<<1, 1024, 0, s>>>(W, tp, p.m_pad, p.h.get());
+void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
+  require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
+  k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, p.h.get());
   FSA_LAUNCH_CHECK();
-  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, tp, p.h.get(), p.Ws.get());
+  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, p.h.get(), p.Ws.get());
   FSA_LAUNCH_CHECK();
 }
 
@@ -955,24 +961,24 @@ void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaSt
   p.ready = true;
 }
 
-void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s,
+void ozaki_project(OzakiPlan& p, const double* R, long ld, long ncols, const double* Dinv, double* S, cudaStream_t s,
                    bool ymax_ready) {
-  project_impl(p, R, tp, Dinv, S, s, ymax_ready);
+  project_impl(p, R, ld, ncols, Dinv, S, s, ymax_ready);
 }
 void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s) {
-  project_impl(p, V, tp, scale, S, s, false);
+  project_impl(p, V, tp, tp, scale, S, s, false);
 }
 
-void ozaki_expand_keep(OzakiPlan& p, const double* W, long tp, double* Z, double* Lw, const double* R,
+void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
                        const double* Dinv, double* rz, double* partial, cudaStream_t s) {
-  slice_w(p, W, tp, s);
-  OzEpi epi{1, p.m_pad, tp, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
+  slice_w(p, W, ld, ncols, s);
+  OzEpi epi{1, p.m_pad, ncols, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
   launch_expand(p, epi, s);
-  colsum_partials(partial, p.ptiles, tp, tp, rz, s);
+  colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);
 }
 void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s) {
-  slice_w(p, W, tp, s);
-  OzEpi epi{2, p.m_pad, tp, p.ec.get(), p.h.get(), nullptr, nullptr, Y, nullptr, nullptr};
+  slice_w(p, W, tp, tp, s);
+  OzEpi epi{2, p.m_pad, tp, tp, p.ec.get(), p.h.get(), nullptr, nullptr, Y, nullptr, nullptr};
   launch_expand(p, epi, s);
 }
 

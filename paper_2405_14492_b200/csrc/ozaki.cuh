@@ -63,13 +63,15 @@ struct OzakiSpmm {
 };
 // digit planes of U (m_pad x n_pad, column per point, ld m_pad); n_pad % 128 == 0, m_pad % 128 == 0
 void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaStream_t s);
-// S (m_pad x tp, ld tp) = U diag(Dinv) R over the plan's n_pad rows of R (ld tp). With
-// ymax_ready the per-chunk column maxima of |Dinv R| are already in p.ymax (update_xr_dot_max)
-void ozaki_project(OzakiPlan& p, const double* R, long tp, const double* Dinv, double* S, cudaStream_t s,
+// S (m_pad x ncols, row stride ld) = U diag(Dinv) R over the plan's n_pad rows of R (row stride
+// ld, columns [0, ncols), ncols <= 64). With ymax_ready the per-chunk column maxima of
+// |Dinv R| are already in p.ymax (update_xr_dot_max)
+void ozaki_project(OzakiPlan& p, const double* R, long ld, long ncols, const double* Dinv, double* S, cudaStream_t s,
                    bool ymax_ready = false);
 inline long ozaki_chunk_rows(const OzakiPlan& p) { return static_cast<long>(p.kb_per_chunk) * 32; }
-// same contract as gemm_expand_woodbury_keep: Lw = U^T W, Z = Dinv (R - Lw), rz = column sums of R.Z
-void ozaki_expand_keep(OzakiPlan& p, const double* W, long tp, double* Z, double* Lw, const double* R,
+// same contract as gemm_expand_woodbury_keep on columns [0, ncols) of row-stride-ld blocks:
+// Lw = U^T W, Z = Dinv (R - Lw), rz = column sums of R.Z
+void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
                        const double* Dinv, double* rz, double* partial, cudaStream_t s);
 // plain products for tests: S = U diag(scale) V (scale may be null), Y = U^T W
 void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s);
