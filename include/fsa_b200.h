@@ -109,6 +109,11 @@ int fsa_ctx_create_nccl(int device, int rank, int world, const void* unique_id, 
  * sharded decomposition on a single GPU) */
 int fsa_ctx_group_create(int device, int world, fsa_ctx** out /* array of world handles */);
 int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world);
+/* replicated mode (on != 0, before creating geometries): every rank holds the whole model and
+ * the communicator shards independent work instead of rows — fsa_predict_var_sim then splits
+ * its probe batches over the ranks and sums the moment accumulators; all
+ * single-GPU entry points are available. Default: row-sharded. */
+int fsa_ctx_set_replicated(fsa_ctx* ctx, int on);
 
 /* ---- input generators (host; same RNG streams as the reference) -------------------- */
 /* uniform_locations (locations.cpp:9-17) */

@@ -76,7 +76,7 @@ struct Bind {
 // entry points whose host buffers hold every point (caller order) exist on one rank only;
 // a row-sharded context runs the fit path (iterative_nll_grad) alone
 void single_rank(const Context* c, const char* what) {
-  if (c->comm->size() != 1)
+  if (c->row_sharded())
     throw std::invalid_argument(std::string(what) + " is not available on a row-sharded context");
 }
 
@@ -204,6 +204,12 @@ int fsa_ctx_group_create(int device, int world, fsa_ctx** out) {
       made.push_back(std::move(c));
     }
     for (int r = 0; r < world; ++r) out[r] = made[static_cast<size_t>(r)].release();
+  });
+}
+int fsa_ctx_set_replicated(fsa_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->shard_rows = on == 0;
   });
 }
 int fsa_ctx_rank(fsa_ctx* ctx, int* rank, int* world) {

@@ -116,7 +116,7 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
   g->coords_host.assign(coords, coords + n * d);
   const CellGrid grid = make_grid(coords, n, d, gamma, nullptr, 0);
   sort_points(coords, n, d, grid, round_up(n, 128), g->pts, ctx->stream);
-  const int world = ctx->comm->size(), rank = ctx->comm->rank();
+  const int world = ctx->row_sharded() ? ctx->comm->size() : 1, rank = ctx->row_sharded() ? ctx->comm->rank() : 0;
   if (world == 1) {
     build_pattern(g->pts, g->pts, gamma, true, g->pat, ctx->stream);
     g->shard.n = g->shard.n_loc = g->shard.r1 = n;
@@ -159,7 +159,7 @@ void Model::halo_exchange(double* X, long tp) {
   for (size_t q = 0; q < sp.peer.size(); ++q)
     peers.push_back(HaloPeer{sp.peer[q], halo_send.get() + sp.send_off[q] * tp, sp.send_cnt[q] * tp,
                              X + (n_pad + sp.recv_off[q]) * tp, sp.recv_cnt[q] * tp});
-  ctx->comm->exchange(peers, s);
+  rcomm->exchange(peers, s);
 }
 
 // ---- model --------------------------------------------------------------------------------------
@@ -212,7 +212,7 @@ void Model::project(const double* M, const double* V, long tp, double* out, cons
   }
   if (world() > 1) {  // m x t partials of the row blocks
     KTimer t(ctx, "allreduce");
-    ctx->comm->allreduce(out, m_pad * tp, ctx->stream);
+    rcomm->allreduce(out, m_pad * tp, ctx->stream);
   }
 }
 
@@ -238,7 +238,8 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   M.ctx = ctx;
   M.geo = geo;
   M.P = p;
-  require(geo->shard.world == ctx->comm->size(), "geometry built for another communicator");
+  require(geo->shard.world == (ctx->row_sharded() ? ctx->comm->size() : 1), "geometry built for another communicator");
+  M.rcomm = geo->shard.world > 1 ? ctx->comm.get() : &ctx->self_comm;
   M.n = geo->shard.n_loc;
   M.n_pad = geo->shard.n_loc_pad;
   M.n_ext_pad = geo->shard.n_ext_pad;
@@ -456,7 +457,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     if (md->red_scratch.n < need) md->red_scratch.alloc(need);
     KTimer tq(md->ctx, "setup_fitc_syrk", 1.0 * mp * mp * np);
     gemm_syrk(md->U.get(), mp, mp, np, md->Dinv.get(), Q.get(), mp, 1.0, md->red_scratch.get(), s);
-    md->ctx->comm->allreduce(Q.get(), mp * mp, s);  // sum of the row blocks' U_i D_i^{-1} U_i^T
+    md->rcomm->allreduce(Q.get(), mp * mp, s);  // sum of the row blocks' U_i D_i^{-1} U_i^T
   }
   add_identity(Q.get(), mp, mp, s);
   FSA_CUDA(cudaMemcpyAsync(LQ.get(), Q.get(), sizeof(double) * mp * mp, cudaMemcpyDeviceToDevice, s));
@@ -480,7 +481,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     FSA_CUDA(cudaMemcpyAsync(hs, scal.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
     if (hinfo != 0) throw NumericalError("preconditioner core matrix is not positive definite");
-    md->ctx->comm->allreduce_host(hs + 1, 1, s);  // sum log d over all rows
+    md->rcomm->allreduce_host(hs + 1, 1, s);  // sum log d over all rows
     logdetQ = hs[0];
     ld = hs[0] + hs[1];  // logdet(core) - logdet(Sigma_m) + sum log d   (preconditioners.cpp:53-55)
   }
@@ -577,7 +578,7 @@ double FitcPrecond::deriv_trace(int k) {
     double hs[7];
     FSA_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
-    md->ctx->comm->allreduce_host(hs, 4, s);  // sums over rows; the m x m sums are replicated
+    md->rcomm->allreduce_host(hs, 4, s);  // sums over rows; the m x m sums are replicated
     const double s0 = hs[0], s1 = hs[1], s2 = hs[2], qf = hs[3], trQi = hs[4], trK2 = hs[5], k2q = hs[6];
     trace[0] = s0;
     trace[1] = s1 + (static_cast<double>(mp) - trQi) / md->P.sigma1_2;
@@ -632,7 +633,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   require(fused || md->world() == 1, "row-sharded solves need the FSA operator with the FITC preconditioner");
   // Jacobi on Sigma_s (prediction solves, prediction.cpp:90-93): no Z block, r.z fused into the update
   const bool jfused = !fused && dynamic_cast<DiagPrecond*>(&P) != nullptr && dynamic_cast<SigmaSOp*>(&A) != nullptr;
-  Comm& comm = *ctx->comm;
+  Comm& comm = *md->rcomm;
   CgWork& w = *ctx->cgw;
   if (w.R.n < blk) {
     w.R.alloc(blk);
@@ -939,7 +940,7 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   cudaStream_t s = ctx->stream;
   // Row sharding: this rank holds rows [r0, r0 + n) of the N sorted points; every
   // global scalar (dots, Gram, traces) is a sum of rank partials.
-  Comm& comm = *ctx->comm;
+  Comm& comm = *md->rcomm;
   const long N = md->geo->pts.n, r0 = md->world() > 1 ? md->geo->shard.r0 : 0;
   const long n = md->n, np = md->n_pad, mp = md->m_pad;
   const long k = L + 1 + p;

@@ -50,7 +50,13 @@ struct PinnedBuf {
 struct Context {
   std::unique_ptr<CgWork> cgw{new CgWork()};
   PinnedBuf pin1, pin2;
-  std::unique_ptr<Comm> comm{new SelfComm()};  // rank / world of the row sharding
+  std::unique_ptr<Comm> comm{new SelfComm()};  // ranks of a multi-GPU job
+  // true: geometries built on this context are row-sharded over `comm`; false (replicated):
+  // every rank holds the whole model and `comm` shards independent work units (the
+  // predictive-variance probe batches)
+  bool shard_rows = true;
+  SelfComm self_comm;
+  bool row_sharded() const { return shard_rows && comm->size() > 1; }
   int device = 0;
   cudaStream_t stream = nullptr;
   int* host_flags = nullptr;  // pinned, mapped
@@ -163,7 +169,8 @@ class Model {
   // refresh the halo rows [n_pad, n_pad + n_halo) of an extended block (no-op on one rank)
   void halo_exchange(double* X, long tp);
   void cross_cov_ext(int mode, double* out);
-  int world() const { return ctx->comm->size(); }
+  int world() const { return rcomm->size(); }
+  Comm* rcomm = nullptr;  // sums over the row blocks: ctx->comm when row-sharded, else a no-op
   DBuf<double> halo_send;
   // INT8 digit planes of U for the tensor-core projection / expansion (built lazily)
   OzakiPlan oz;

@@ -275,9 +275,18 @@ PredVarInfo predict_var_sim(PredictionSet& pr, int L, unsigned long long seed, c
                                           cdiag.get());
     FSA_LAUNCH_CHECK();
   }
+  // replicated multi-GPU mode: probe batch bi runs on rank bi % world; the moment
+  // sums are added over ranks below
+  Comm& comm = *ctx->comm;
+  const bool shard_batches = !ctx->shard_rows && comm.size() > 1;
+  const int rank = shard_batches ? comm.rank() : 0, nranks = shard_batches ? comm.size() : 1;
   int done = 0;
-  while (done < L) {
+  for (int bi = 0; done < L; ++bi) {
     const int b = std::min(batch, L - done);
+    if (bi % nranks != rank) {
+      done += b;
+      continue;
+    }
 #pragma omp parallel for schedule(dynamic, 1)
     for (int j = 0; j < b; ++j)
       probe_rademacher(seed, static_cast<unsigned long long>(done + j), np, zh.data() + static_cast<long>(j) * np);
@@ -304,6 +313,13 @@ PredVarInfo predict_var_sim(PredictionSet& pr, int L, unsigned long long seed, c
       FSA_LAUNCH_CHECK();
     }
     done += b;
+  }
+  if (shard_batches) {
+    comm.allreduce(acc.get(), 5 * np, s);
+    std::vector<double> its(static_cast<size_t>(nranks), 0.0);
+    its[static_cast<size_t>(rank)] = max_it;
+    comm.allreduce_host(its.data(), nranks, s);
+    for (double v : its) max_it = std::max(max_it, static_cast<int>(v));
   }
   FSA_CUDA(cudaEventRecord(e2, s));
   // finish moments + combine_pieces (krylov.cpp:215-226,273-290; prediction.cpp:112-127), internal order

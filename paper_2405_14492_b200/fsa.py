@@ -69,6 +69,7 @@ _SIGS = {
     "fsa_ctx_create_nccl": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
     "fsa_ctx_group_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_vp)]),
     "fsa_ctx_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "fsa_ctx_set_replicated": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_synchronize": (C.c_int, [_vp]),
     "fsa_ctx_set_gemm_mode": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
@@ -258,6 +259,10 @@ class Context:
         hs = (_vp * world)()
         _check(lib().fsa_ctx_group_create(device, world, hs))
         return [cls(_handle=_vp(hs[r])) for r in range(world)]
+
+    def set_replicated(self, on=True):
+        """Replicated mode: whole model per rank; predict_var_sim shards its probe batches."""
+        _check(lib().fsa_ctx_set_replicated(self.h, 1 if on else 0))
 
     def rank_world(self):
         r, w = C.c_int(), C.c_int()

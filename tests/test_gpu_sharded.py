@@ -146,3 +146,28 @@ def test_nccl_context_single_rank():
     assert c.rank_world() == (0, 1)
     r = nll_on(c, locs, ind, kw, y, X, L=6)
     assert r["nll"] == one["nll"] and np.array_equal(r["grad"], one["grad"])
+
+
+@pytest.mark.parametrize("cv", [False, True])
+def test_replicated_prediction_shards_probe_batches(cv):
+    """Replicated mode: whole model per rank, predict_var_sim's probe batches split over ranks."""
+    locs, ind, kw, y, X = problem(4000, 60, 0.06, 61, p=0)
+    plocs = O.uniform_locations(500, 2, 62)
+
+    def run(c):
+        md = fsa.FsaModel.assemble(locs, ind, ctx=c, **kw)
+        pr = fsa.make_prediction_set(md, plocs)
+        out = pr.predict_var_sim(num_probes=600, seed=3, tol=1e-6, tol_s=1e-6, control_variate=cv)
+        out["mean"] = pr.predict_mean_iterative(y, fsa.make_preconditioner(md, "fitc"), tol=1e-6)
+        return out
+
+    one = run(fsa.Context(0))
+    ctxs = fsa.Context.group(0, 3)
+    for c in ctxs:
+        c.set_replicated(True)
+    outs = run_ranks(ctxs, lambda r, c: run(c))
+    for o in outs:  # 3 batches of <= 256 probes, one per rank; sums in another order
+        np.testing.assert_allclose(o["var"], one["var"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(o["se"], one["se"], rtol=1e-9, atol=1e-14)
+        np.testing.assert_allclose(o["mean"], one["mean"], rtol=1e-13, atol=1e-14)
+        assert o["cg_iterations"] == one["cg_iterations"]
