@@ -203,6 +203,45 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
                            int num_probes, uint64_t seed, const fsa_cg_options* cg, int cv_mode, int want_grad,
                            fsa_nll_result* out, double* beta);
 
+/* ---- maximum-likelihood fit (fit_fsa, estimation.cpp:229-303) -------
+ * L-BFGS over log(sigma2, sigma1_2, rho) (lbfgs_minimize, estimation.cpp:10-132: two-loop
+ * recursion, Armijo + curvature bracketing, NumericalError = +inf), each evaluation
+ * FsaModel::assemble + make_preconditioner + iterative_nll_grad on the device with fit-loop
+ * residency (pattern, [y | X] and probe draws kept in HBM). Inducing points: kmeans++. */
+typedef struct {
+  int nu_code;
+  int taper_family;
+  int64_t num_inducing;
+  double taper_range;    /* 0: gamma_for_avg_row_nnz(n, target_row_nnz) */
+  double target_row_nnz;
+  int precond;           /* 0 none, 1 diagonal, 2 fitc */
+  int num_probes;
+  int cv_mode;           /* 0 none, 1 one, 2 optimal */
+  uint64_t seed;
+  double cg_tol;
+  int cg_max_iter;
+  double jitter_rel;
+  int max_evals;
+  int lbfgs_memory;
+  double armijo_c1;
+  int max_backtracks;
+  double f_rel_tol;
+  double grad_tol_per_n; /* stopping tolerance = grad_tol_per_n * n (infinity norm, log space) */
+} fsa_fit_options;
+typedef struct {
+  double sigma2, sigma1_2, rho, nll, gamma;
+  double grad_log[3]; /* gradient at the returned point, log-parameter space */
+  int evals;
+  int converged;
+  int64_t n_trace;    /* entries of the nll trace (one per evaluation) */
+} fsa_fit_result;
+/* the reference's FitOptions defaults */
+void fsa_fit_options_default(fsa_fit_options* opts);
+/* beta: pcols values; inducing: num_inducing x d (column-major); nll_trace: up to trace_cap values */
+int fsa_fit(fsa_ctx* ctx, const double* coords, int64_t n, int d, const double* y, const double* X, int64_t pcols,
+            const fsa_fit_options* opts, fsa_fit_result* out, double* beta, double* inducing, double* nll_trace,
+            int64_t trace_cap);
+
 /* ---- prediction (prediction.h:21-56) ------------------------------------------------- */
 /* make_prediction_set (prediction.cpp:7-27) */
 int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** out);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "blas1.cuh"
+#include "fit.h"
 #include "fsa_core.cuh"
 #include "inputs.h"
 #include "predict.cuh"
@@ -669,6 +670,78 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
     out->total_ms = r.total_ms;
     for (long a = 0; a < pcols; ++a)
       if (beta) beta[a] = r.beta[static_cast<size_t>(a)];
+  });
+}
+
+void fsa_fit_options_default(fsa_fit_options* o) {
+  if (o == nullptr) return;
+  FitOptions d;
+  o->nu_code = d.nu;
+  o->taper_family = d.family;
+  o->num_inducing = d.num_inducing;
+  o->taper_range = d.taper_range;
+  o->target_row_nnz = d.target_row_nnz;
+  o->precond = d.precond;
+  o->num_probes = d.num_probes;
+  o->cv_mode = d.cv_mode;
+  o->seed = d.seed;
+  o->cg_tol = d.cg_tol;
+  o->cg_max_iter = d.cg_max_iter;
+  o->jitter_rel = d.jitter_rel;
+  o->max_evals = d.lbfgs.max_evals;
+  o->lbfgs_memory = d.lbfgs.memory;
+  o->armijo_c1 = d.lbfgs.armijo_c1;
+  o->max_backtracks = d.lbfgs.max_backtracks;
+  o->f_rel_tol = d.lbfgs.f_rel_tol;
+  o->grad_tol_per_n = d.grad_tol_per_n;
+}
+int fsa_fit(fsa_ctx* ctx, const double* coords, int64_t n, int d, const double* y, const double* X, int64_t pcols,
+            const fsa_fit_options* opts, fsa_fit_result* out, double* beta, double* inducing, double* nll_trace,
+            int64_t trace_cap) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Bind bind_(ctx->c.get());
+    need(coords, "coords");
+    need(y, "y");
+    need(opts, "opts");
+    need(out, "out");
+    single_rank(ctx->c.get(), "fit");
+    FitOptions o;
+    o.nu = opts->nu_code;
+    o.family = opts->taper_family;
+    o.num_inducing = opts->num_inducing;
+    o.taper_range = opts->taper_range;
+    o.target_row_nnz = opts->target_row_nnz;
+    o.precond = opts->precond;
+    o.num_probes = opts->num_probes;
+    o.cv_mode = opts->cv_mode;
+    o.seed = opts->seed;
+    o.cg_tol = opts->cg_tol;
+    o.cg_max_iter = opts->cg_max_iter;
+    o.jitter_rel = opts->jitter_rel;
+    o.lbfgs.max_evals = opts->max_evals;
+    o.lbfgs.memory = opts->lbfgs_memory;
+    o.lbfgs.armijo_c1 = opts->armijo_c1;
+    o.lbfgs.max_backtracks = opts->max_backtracks;
+    o.lbfgs.f_rel_tol = opts->f_rel_tol;
+    o.grad_tol_per_n = opts->grad_tol_per_n;
+    require(o.nu >= 0 && o.nu <= 2 && (o.family == 1 || o.family == 2), "fit: invalid kernel or taper");
+    require(o.precond >= 0 && o.precond <= 2 && o.cv_mode >= 0 && o.cv_mode <= 2, "fit: invalid options");
+    FitOutput r = fit_fsa(ctx->c.get(), coords, n, d, y, X, pcols, o);
+    out->sigma2 = r.sigma2;
+    out->sigma1_2 = r.sigma1_2;
+    out->rho = r.rho;
+    out->nll = r.nll;
+    out->gamma = r.gamma;
+    for (int k = 0; k < 3; ++k) out->grad_log[k] = k < static_cast<int>(r.grad_log.size()) ? r.grad_log[k] : 0.0;
+    out->evals = r.evals;
+    out->converged = r.converged ? 1 : 0;
+    out->n_trace = static_cast<int64_t>(r.nll_trace.size());
+    if (beta)
+      for (int64_t a = 0; a < pcols; ++a) beta[a] = r.beta[static_cast<size_t>(a)];
+    if (inducing) std::copy(r.inducing.begin(), r.inducing.end(), inducing);
+    if (nll_trace)
+      for (int64_t i = 0; i < std::min<int64_t>(trace_cap, out->n_trace); ++i) nll_trace[i] = r.nll_trace[static_cast<size_t>(i)];
   });
 }
 

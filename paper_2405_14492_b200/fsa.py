@@ -56,6 +56,21 @@ class NllResult(C.Structure):
                 ("total_ms", C.c_double)]
 
 
+class FitOptions(C.Structure):
+    _fields_ = [("nu_code", C.c_int), ("taper_family", C.c_int), ("num_inducing", C.c_int64),
+                ("taper_range", C.c_double), ("target_row_nnz", C.c_double), ("precond", C.c_int),
+                ("num_probes", C.c_int), ("cv_mode", C.c_int), ("seed", C.c_uint64), ("cg_tol", C.c_double),
+                ("cg_max_iter", C.c_int), ("jitter_rel", C.c_double), ("max_evals", C.c_int),
+                ("lbfgs_memory", C.c_int), ("armijo_c1", C.c_double), ("max_backtracks", C.c_int),
+                ("f_rel_tol", C.c_double), ("grad_tol_per_n", C.c_double)]
+
+
+class FitResult(C.Structure):
+    _fields_ = [("sigma2", C.c_double), ("sigma1_2", C.c_double), ("rho", C.c_double), ("nll", C.c_double),
+                ("gamma", C.c_double), ("grad_log", C.c_double * 3), ("evals", C.c_int), ("converged", C.c_int),
+                ("n_trace", C.c_int64)]
+
+
 class PredVarInfo(C.Structure):
     _fields_ = [("clamped", C.c_int), ("cg_iterations", C.c_int), ("det_ms", C.c_double), ("sim_ms", C.c_double)]
 
@@ -119,6 +134,9 @@ _SIGS = {
     "fsa_iterative_nll_grad": (C.c_int, [_vp, _vp, _vp, _vp, _i64, C.c_int, _u64, C.POINTER(CgOptions), C.c_int,
                                          C.c_int, C.POINTER(NllResult), _vp]),
     "fsa_pred_setup": (C.c_int, [_vp, _dp, _i64, C.POINTER(_vp)]),
+    "fsa_fit_options_default": (None, [C.POINTER(FitOptions)]),
+    "fsa_fit": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _vp, _i64, C.POINTER(FitOptions), C.POINTER(FitResult),
+                          _vp, _dp, _dp, _i64]),
     "fsa_pred_destroy": (None, [_vp]),
     "fsa_pred_info": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
     "fsa_cross_apply_t": (C.c_int, [_vp, _dp, _dp]),
@@ -587,3 +605,34 @@ class PredictionSet:
 
 def make_prediction_set(model: FsaModel, pcoords) -> PredictionSet:
     return PredictionSet(model, pcoords)
+
+
+def fit_fsa(coords, y, X=None, nu=1.5, taper_family=1, num_inducing=200, taper_range=0.0, target_row_nnz=40.0,
+            precond="fitc", num_probes=50, cv="optimal", seed=0, cg_tol=1e-3, cg_max_iter=1000, max_evals=200,
+            grad_tol_per_n=1e-3, ctx: Context | None = None, **lbfgs):
+    """fit_fsa (estimation.cpp:229-303), iterative backend, with fit-loop residency on the device."""
+    ctx = ctx or default_context()
+    c = _F(coords)
+    n, d = c.shape
+    y = _F(y)
+    p = 0 if X is None else np.asarray(X).reshape(n, -1).shape[1]
+    Xf = None if p == 0 else _F(np.asarray(X).reshape(n, p))
+    o = FitOptions()
+    lib().fsa_fit_options_default(C.byref(o))
+    o.nu_code, o.taper_family, o.num_inducing = NU_CODE[nu], FAMILY_CODE[taper_family], int(num_inducing)
+    o.taper_range, o.target_row_nnz = float(taper_range), float(target_row_nnz)
+    o.precond, o.num_probes, o.cv_mode, o.seed = PRECOND_CODE[precond], int(num_probes), CV_CODE[cv], int(seed)
+    o.cg_tol, o.cg_max_iter, o.max_evals, o.grad_tol_per_n = float(cg_tol), int(cg_max_iter), int(max_evals), float(grad_tol_per_n)
+    for k, v in lbfgs.items():
+        setattr(o, k, v)
+    res = FitResult()
+    beta = _F(np.zeros(max(p, 1)))
+    ind = _F(np.zeros((int(num_inducing), d)))
+    cap = int(max_evals) + 8
+    trace = _F(np.zeros(cap))
+    _check(lib().fsa_fit(ctx.h, c, n, d, y, None if Xf is None else Xf.ctypes.data, p, C.byref(o), C.byref(res),
+                         beta.ctypes.data, ind, trace, cap))
+    return {"sigma2": res.sigma2, "sigma1_2": res.sigma1_2, "rho": res.rho, "nll": res.nll, "gamma": res.gamma,
+            "beta": beta[:p].copy(), "evals": res.evals, "converged": bool(res.converged),
+            "grad_log": np.array(res.grad_log[:]), "inducing": ind,
+            "nll_trace": trace[:min(cap, res.n_trace)].copy()}
