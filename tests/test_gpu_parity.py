@@ -265,3 +265,21 @@ def test_config1_scale_matches_oracle():
     assert got["cg_iterations"] == want["cg_iterations"]
     assert got["nll"] == pytest.approx(want["nll"], rel=1e-6)
     np.testing.assert_allclose(got["grad"], want["grad"], rtol=1e-6, atol=1e-6 * np.abs(want["grad"]).max())
+
+
+@pytest.mark.parametrize("d,n,m,L", [(1, 3000, 40, 20), (3, 3000, 80, 30), (2, 4000, 100, 64), (2, 2000, 130, 5)])
+def test_nll_dimensions_and_widths_match_oracle(d, n, m, L):
+    """d = 1 and 3 geometries, t_pad = 72 (DMMA dense passes, 64 + 8 column SpMM tiles),
+    m_pad = 256 with a ragged m, tiny t."""
+    locs = O.uniform_locations(n, d, 41 + d)
+    ind = O.select_kmeanspp(locs, m, 42 + d)
+    gamma = {1: 0.01, 2: 0.06, 3: 0.15}[d]
+    kw = dict(nu=1.5, taper_family=1, gamma=gamma, sigma2=0.1, sigma1_2=1.0, rho=0.1)
+    y = np.random.default_rng(d).standard_normal(n)
+    md = fsa.FsaModel.assemble(locs, ind, **kw)
+    om = O.Model(locs, ind, **kw)
+    got = fsa.iterative_nll_grad(md, fsa.make_preconditioner(md, "fitc"), y, num_probes=L, seed=2, tol=1e-3)
+    want = O.iterative_nll_grad(om, O.Precond(om, "fitc"), y, num_probes=L, seed=2, tol=1e-3)
+    assert got["cg_iterations"] == want["cg_iterations"]
+    assert got["nll"] == pytest.approx(want["nll"], rel=1e-6)
+    np.testing.assert_allclose(got["grad"], want["grad"], rtol=1e-6, atol=1e-6 * np.abs(want["grad"]).max())
