@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <random>
 
 #include "blas1.cuh"
@@ -51,6 +52,24 @@ Context::Context(int dev) : device(dev) {
   FSA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   unsigned long long keep = ~0ULL;  // keep freed blocks for reuse across evaluations
   FSA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  {  // prime the device pool once per process: later per-evaluation temporaries are carved
+     // from retained memory instead of mapping new pages mid-evaluation
+    static bool primed = false;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!primed) {
+      size_t free_b = 0, total_b = 0;
+      FSA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t want = std::min<size_t>(free_b / 4, size_t(16) << 30);
+      void* p = nullptr;
+      if (want > 0 && cudaMallocAsync(&p, want, stream) == cudaSuccess) {
+        cudaFreeAsync(p, stream);
+        cudaStreamSynchronize(stream);
+      }
+      cudaGetLastError();
+      primed = true;
+    }
+  }
   FSA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags), 4 * sizeof(int), cudaHostAllocMapped));
   FSA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_flags_dev), host_flags, 0));
   if (const char* g = std::getenv("FSA_GEMM")) gemm_mode = std::strcmp(g, "dmma") == 0 ? 1 : (std::strcmp(g, "ozaki") == 0 ? 2 : 0);
@@ -252,6 +271,7 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   M.ind.alloc(m * M.d);
   FSA_CUDA(cudaMemcpyAsync(M.ind.get(), inducing, sizeof(double) * m * M.d, cudaMemcpyHostToDevice, s));
   M.info.alloc(4);
+  M.info.zero(s);  // [0] Cholesky status, [1] clamped residual diagonals
   M.dinv_scratch.alloc(mp * 64);
   M.dot_scratch.alloc(coldot_scratch(np, 128));
   DBuf<double> scal(4);
@@ -336,8 +356,13 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   }
   {
     KTimer t2(ctx, "rho_T_gemm", 2.0 * m * m * n);
-    FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * ne, cudaMemcpyDeviceToDevice, s));
-    gemm_expand_store(U.get(), mp, ne, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+    if (ctx->gemm_mode != 1 && ne == np) {  // INT8 tensor cores, 64-column tiles of K2
+      ensure_ozaki();
+      ozaki_expand_sub(oz, K2.get(), mp, U1.get(), T.get(), mp, s);
+    } else {
+      FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * ne, cudaMemcpyDeviceToDevice, s));
+      gemm_expand_store(U.get(), mp, ne, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);
+    }
   }
   const Csr& pat = geo->pat;
   dsval.alloc(pat.nnz > 0 ? pat.nnz : 1);
@@ -456,6 +481,8 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     const size_t need = gemm_reduce_scratch(mp, mp, np);
     if (md->red_scratch.n < need) md->red_scratch.alloc(need);
     KTimer tq(md->ctx, "setup_fitc_syrk", 1.0 * mp * mp * np);
+    // DMMA SYRK (lower half + mirror): the full-matrix INT8 alternative (ozaki_project_wide over
+    // 64-column tiles, 2.1 ms at config 2) does not beat it (1.7 ms)
     gemm_syrk(md->U.get(), mp, mp, np, md->Dinv.get(), Q.get(), mp, 1.0, md->red_scratch.get(), s);
     md->rcomm->allreduce(Q.get(), mp * mp, s);  // sum of the row blocks' U_i D_i^{-1} U_i^T
   }
@@ -561,15 +588,21 @@ double FitcPrecond::deriv_trace(int k) {
     const long mp = md->m_pad, np = md->n_pad, n = md->n;
     md->ensure_rho_derivs();
     KTimer tt(md->ctx, "grad_exact_traces", 2.0 * mp * mp * np);
-    // V = LQ^{-1} U, W1 = LQ^{-1} U1: q_i = |V_i|^2 (diag P^{-1}), and
-    // <Q^{-1}, U D^{-1} U1^T> = sum_i (V_i . W1_i) / D_i
-    DBuf<double> V(mp * np), W1(mp * np), q(np), f(np), pinv(np), d1(np);
-    FSA_CUDA(cudaMemcpyAsync(V.get(), md->U.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
-    FSA_CUDA(cudaMemcpyAsync(W1.get(), md->U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
-    trsm_lower_cols(LQ.get(), mp, V.get(), mp, np, md->dinv_scratch.get(), s);
-    trsm_lower_cols(LQ.get(), mp, W1.get(), mp, np, md->dinv_scratch.get(), s);
-    colnorm2(V.get(), mp, mp, n, np, q.get(), s);
-    row_dots(V.get(), W1.get(), mp, mp, n, np, f.get(), s);
+    // q_i = U_i' Q^{-1} U_i (diag P^{-1} = 1/D - q/D^2) and
+    // <Q^{-1}, U D^{-1} U1^T> = sum_i (U_i' Q^{-1} U1_i) / D_i
+    DBuf<double> q(np), f(np), pinv(np), d1(np);
+    if (md->ctx->gemm_mode != 1) {  // row dots of U^T Q^{-1} (INT8 tensor cores, 64-column tiles)
+      md->ensure_ozaki();
+      ozaki_expand_rowdots(md->oz, Qinv.get(), mp, md->U.get(), md->U1.get(), mp, q.get(), f.get(), s);
+    } else {  // V = LQ^{-1} U, W1 = LQ^{-1} U1: q_i = |V_i|^2, f_i = V_i . W1_i
+      DBuf<double> V(mp * np), W1(mp * np);
+      FSA_CUDA(cudaMemcpyAsync(V.get(), md->U.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+      FSA_CUDA(cudaMemcpyAsync(W1.get(), md->U1.get(), sizeof(double) * mp * np, cudaMemcpyDeviceToDevice, s));
+      trsm_lower_cols(LQ.get(), mp, V.get(), mp, np, md->dinv_scratch.get(), s);
+      trsm_lower_cols(LQ.get(), mp, W1.get(), mp, np, md->dinv_scratch.get(), s);
+      colnorm2(V.get(), mp, mp, n, np, q.get(), s);
+      row_dots(V.get(), W1.get(), mp, mp, n, np, f.get(), s);
+    }
     pinv_diag(pinv.get(), md->D.get(), q.get(), n, np, s);
     affine_vec(d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, s);
     DBuf<double> sums(8);

@@ -158,7 +158,11 @@ struct OzEpi {
   double* Lw;       // modes 1, 2 (Y)
   const double* R;
   const double* Dinv;
+  const double* A2 = nullptr;  // mode 4: second row operand
 };
+// expansion epilogue modes (k_oz_expand): 1 Woodbury keep, 2 plain Y = acc,
+// 3 Y = R - acc (R, Y with row stride ld), 4 row dots of acc with R and A2 (row stride ld):
+//   Z[i] = sum_c acc[i][c] R[i][c], Lw[i] = sum_c acc[i][c] A2[i][c]
 
 __global__ void __launch_bounds__(128, 1)
     k_oz_gemm(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int nkb_all, int kb_per_chunk, OzEpi epi) {
@@ -410,6 +414,20 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty)) : "memory");
       // TMEM is free for the next tile already; coalesced copies of the staged rows
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (epi.mode == 4) {  // one thread per row: dots of the staged row with R and A2 rows
+        const int rr = tid - 64;
+        const long i = r0 + rr;
+        double s1 = 0.0, s2 = 0.0;
+        for (int c = 0; c < tp; ++c) {
+          const double yv = tileY[rr * kXLd + c];
+          s1 = fma(yv, __ldg(epi.R + i * epi.ld + c), s1);
+          s2 = fma(yv, __ldg(epi.A2 + i * epi.ld + c), s2);
+        }
+        epi.Z[i] = s1;
+        epi.Lw[i] = s2;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // tileY reused by the next tile
+        continue;
+      }
       // thread (column c, row parity h): rows h, h + 2, ..., coalesced across c; loads are
       // batched ahead of the stores (R and Dinv are read-only here)
       const int et = tid - 64, c = et & 63, h = et >> 6;
@@ -426,12 +444,14 @@ __global__ void __launch_bounds__(192, 1)
             if (epi.mode == 1) {
               x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
               di[u] = __ldg(epi.Dinv + r0 + rr);
+            } else if (epi.mode == 3) {
+              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
             }
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const long off = base + static_cast<long>(rb + 2 * u) * epi.ld;
-            epi.Lw[off] = lw[u];
+            epi.Lw[off] = epi.mode == 3 ? x[u] - lw[u] : lw[u];
             if (epi.mode == 1) {
               const double z = (x[u] - lw[u]) * di[u];
               epi.Z[off] = z;
@@ -883,6 +903,20 @@ void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nk
   FSA_LAUNCH_CHECK();
 }
 
+// q[i] = sum_j qp[j][i], f likewise (fixed order)
+__global__ void k_sum_tiles(const double* __restrict__ qp, const double* __restrict__ fp, long tiles, long n,
+                            double* __restrict__ q, double* __restrict__ f) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a = 0.0, b = 0.0;
+  for (long j = 0; j < tiles; ++j) {
+    a += qp[j * n + i];
+    b += fp[j * n + i];
+  }
+  q[i] = a;
+  f[i] = b;
+}
+
 void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -975,6 +1009,34 @@ void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, doubl
   OzEpi epi{1, p.m_pad, ncols, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
   launch_expand(p, epi, s);
   colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);
+}
+void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s) {
+  require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
+  for (long j = 0; j < ldw; j += kOzCols) {
+    slice_w(p, W + j, ldw, kOzCols, s);
+    OzEpi epi{3, p.m_pad, kOzCols, ld, p.ec.get(), p.h.get(), nullptr, nullptr, Y + j, A + j, nullptr};
+    launch_expand(p, epi, s);
+  }
+}
+void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
+                          double* q, double* f, cudaStream_t s) {
+  require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
+  const long tiles = ldw / kOzCols;
+  DBuf<double> qp(static_cast<size_t>(tiles * p.n_pad)), fp(static_cast<size_t>(tiles * p.n_pad));
+  for (long j = 0; j < tiles; ++j) {
+    slice_w(p, W + j * kOzCols, ldw, kOzCols, s);
+    OzEpi epi{4, p.m_pad, kOzCols, ld, p.ec.get(), p.h.get(), nullptr, qp.get() + j * p.n_pad,
+              fp.get() + j * p.n_pad, B1 + j * kOzCols, nullptr};
+    epi.A2 = B2 + j * kOzCols;
+    launch_expand(p, epi, s);
+  }
+  k_sum_tiles<<<static_cast<unsigned>(cdiv(p.n_pad, 256)), 256, 0, s>>>(qp.get(), fp.get(), tiles, p.n_pad, q, f);
+  FSA_LAUNCH_CHECK();
+}
+void ozaki_project_wide(OzakiPlan& p, const double* V, long ldv, const double* scale, double* S, long lds,
+                        cudaStream_t s) {
+  require(ldv % kOzCols == 0 && lds >= ldv, "ozaki: wide passes need 64-column tiles");
+  for (long j = 0; j < ldv; j += kOzCols) project_impl(p, V + j, ldv, kOzCols, scale, S + j, s, false);
 }
 void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s) {
   slice_w(p, W, tp, tp, s);

@@ -73,6 +73,15 @@ inline long ozaki_chunk_rows(const OzakiPlan& p) { return static_cast<long>(p.kb
 // Lw = U^T W, Z = Dinv (R - Lw), rz = column sums of R.Z
 void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
                        const double* Dinv, double* rz, double* partial, cudaStream_t s);
+// wide passes (64-column tiles of row-major operands whose widths are multiples of 64):
+//   Y = A - U^T W            (W m_pad x ldw, A / Y n_pad x ld)
+//   q[i] = (U^T W)_i . B1_i, f[i] = (U^T W)_i . B2_i   (row dots, B1 / B2 n_pad x ld)
+//   S = U diag(scale) V      (V n_pad x ldv, S m_pad x lds)
+void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s);
+void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
+                          double* q, double* f, cudaStream_t s);
+void ozaki_project_wide(OzakiPlan& p, const double* V, long ldv, const double* scale, double* S, long lds,
+                        cudaStream_t s);
 // plain products for tests: S = U diag(scale) V (scale may be null), Y = U^T W
 void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s);
 void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s);

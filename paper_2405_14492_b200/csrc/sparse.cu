@@ -576,6 +576,7 @@ void sddmm_block(int mode, const double* U, const double* U1, const double* T, l
     k_block_gram<1><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U1, U, U, T, ldu, mp, gtmp);
   FSA_LAUNCH_CHECK();
   if (mode == 0 && gval != nullptr) FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
+  if (mode == 0 && n_clamped_dev != nullptr) FSA_CUDA(cudaMemsetAsync(n_clamped_dev, 0, sizeof(int), s));
   const unsigned g2 = static_cast<unsigned>(cdiv(pat.rows * 32, 256));
   if (mode == 0)
     k_sddmm_finish<0><<<g2, 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.mirror.get(), pat.gslot.get(),
