@@ -305,7 +305,7 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   {
     KTimer t(ctx, "setup_sddmm", 2.0 * mp * pat.nnz);
     if (pat.gnnz > 0 && mp % 32 == 0) {  // dense Gram blocks on DMMA; fills the SpMM value blocks too
-      M.gval.alloc(static_cast<size_t>(pat.gnnz * kGroup));
+      M.gval.alloc(static_cast<size_t>(32 * pat.ntiles));
       DBuf<double> gtmp(static_cast<size_t>(pat.gnnz * kGroup));
       sddmm_block(0, M.U.get(), nullptr, nullptr, mp, mp, pat, M.lowrank.get(), sp, M.sval.get(), M.gval.get(),
                   M.info.get() + 1, gtmp.get(), s);
@@ -314,8 +314,8 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
     }
   }
   if (pat.gnnz > 0 && !(mp % 32 == 0)) {  // value blocks of the row groups (block SpMM of the PCG sweeps)
-    KTimer t(ctx, "setup_group_values", 16.0 * pat.nnz + 8.0 * kGroup * pat.gnnz);
-    M.gval.alloc(static_cast<size_t>(pat.gnnz * kGroup));
+    KTimer t(ctx, "setup_group_values", 16.0 * pat.nnz + 8.0 * 32 * pat.ntiles);
+    M.gval.alloc(static_cast<size_t>(32 * pat.ntiles));
     group_values(pat, M.sval.get(), M.gval.get(), s);
   }
   M.D.alloc(np);

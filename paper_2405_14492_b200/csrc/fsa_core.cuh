@@ -144,7 +144,7 @@ class Model {
   DBuf<double> U;                // m_pad x n_pad, one column per point
   DBuf<double> lowrank;          // |U_i|^2
   DBuf<double> sval;             // Sigma_s values on geo->pat
-  DBuf<double> gval;             // the same in row-group blocks (Csr::gnnz x kGroup)
+  DBuf<double> gval;             // the same as the stored value tiles of the row groups (32 x Csr::ntiles)
   DBuf<double> D, Dinv, sqrtD;   // diag(Sigma_s) (FITC / Jacobi diagonal)
   long n_clamped = 0;
   // rho derivative blocks (lazy, fsa.cpp:101-124)

@@ -63,34 +63,33 @@ __global__ void __launch_bounds__(256) k_potrf_panel(double* A, long ld, long k0
     const int r = idx % 64, c = idx / 64;
     Lk[r][c] = A[(k0 + c) * ld + k0 + r];
   }
+  __shared__ double Ld[64];
   __syncthreads();
-  if (tid < 32) {  // one warp factors the 64 x 64 diagonal block (lane owns rows lane, lane + 32)
-    const int r0 = tid, r1 = tid + 32;
-    int badj = 0;
-    for (int j = 0; j < 64; ++j) {
-      double dj = Lk[j][j];
-      if (!(dj > 0.0) || !isfinite(dj)) {
-        if (!badj) badj = j + 1;
-        dj = 1.0;
-      }
-      const double ljj = sqrt(dj);
-      const double inv = 1.0 / ljj;
-      __syncwarp();
-      if (r0 > j) Lk[r0][j] *= inv;
-      if (r1 > j) Lk[r1][j] *= inv;
-      if (r0 == j) Lk[j][j] = ljj;
-      if (r1 == j) Lk[j][j] = ljj;
-      __syncwarp();
-      const double a0 = r0 > j ? Lk[r0][j] : 0.0, a1 = r1 > j ? Lk[r1][j] : 0.0;
-      for (int c = j + 1; c < 64; ++c) {
-        const double lc = Lk[c][j];
-        if (r0 >= c) Lk[r0][c] = fma(-a0, lc, Lk[r0][c]);
-        if (r1 >= c) Lk[r1][c] = fma(-a1, lc, Lk[r1][c]);
-      }
-      __syncwarp();
+  // right-looking factorisation of the 64 x 64 diagonal block by the whole block: column j
+  // is scaled, then the trailing lower triangle updated (two barriers per column)
+  for (int j = 0; j < 64; ++j) {
+    double dj = Lk[j][j];
+    if (!(dj > 0.0) || !isfinite(dj)) {
+      if (tid == 0 && !bad) bad = j + 1;
+      dj = 1.0;
     }
-    if (tid == 0) bad = badj;
+    const double ljj = sqrt(dj);
+    const double inv = 1.0 / ljj;
+    if (tid > j && tid < 64) Lk[tid][j] *= inv;
+    if (tid == j) Ld[j] = ljj;
+    __syncthreads();
+    {  // thread (r, c0) updates row r, columns c0, c0 + 4, ...: 16 independent predicated FMAs
+      const int r = tid & 63, c0 = tid >> 6;
+      const double lr = Lk[r][j];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = c0 + 4 * i;
+        if (c > j && r >= c) Lk[r][c] = fma(-lr, Lk[c][j], Lk[r][c]);
+      }
+    }
+    __syncthreads();
   }
+  if (tid < 64) Lk[tid][tid] = Ld[tid];
   __syncthreads();
   if (blockIdx.x == 0) {
     // the factored diagonal block goes to scratch: the other blocks of this launch
@@ -110,11 +109,22 @@ __global__ void __launch_bounds__(256) k_potrf_panel(double* A, long ld, long k0
     X[r][c] = A[(k0 + c) * ld + rb + r];
   }
   __syncthreads();
-  if (tid < 64) {
+  {  // right-looking substitution: thread (r, c0) owns row r, columns c0, c0 + 4, ... in registers
+    const int r = tid & 63, c0 = tid >> 6;
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = X[r][c0 + 4 * i];
+#pragma unroll
     for (int c = 0; c < 64; ++c) {
-      double t = X[tid][c];
-      for (int k = 0; k < c; ++k) t -= X[tid][k] * Lk[c][k];
-      X[tid][c] = t / Lk[c][c];
+      if (c0 == (c & 3)) {
+        x[c >> 2] /= Lk[c][c];
+        X[r][c] = x[c >> 2];
+      }
+      __syncthreads();
+      const double xc = X[r][c];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (c0 + 4 * i > c) x[i] = fma(-xc, Lk[c0 + 4 * i][c], x[i]);
     }
   }
   __syncthreads();
@@ -142,23 +152,33 @@ __global__ void k_zero_upper(double* A, long ld, long n) {
 
 // inverse of each 64x64 diagonal block of a lower-triangular L (col-major):
 // Dinv[kb][c*64 + r] = (L_kk^{-1})(r, c)
-__global__ void __launch_bounds__(64) k_trinv_blocks(const double* L, long ld, double* Dinv) {
+__global__ void __launch_bounds__(256) k_trinv_blocks(const double* L, long ld, double* Dinv) {
   extern __shared__ double tsm[];
   double(*Lk)[65] = reinterpret_cast<double(*)[65]>(tsm);
   double(*Xs)[65] = reinterpret_cast<double(*)[65]>(tsm + 64 * 65);
   const long k0 = 64 * static_cast<long>(blockIdx.x);
   const int tid = threadIdx.x;
-  for (int c = 0; c < 64; ++c) Lk[tid][c] = L[(k0 + c) * ld + k0 + tid];
+  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
+    const int r = idx & 63, c = idx >> 6;
+    Lk[r][c] = L[(k0 + c) * ld + k0 + r];
+  }
   __syncthreads();
-  // column tid of the inverse: forward substitution on e_tid
+  // column col of the inverse: forward substitution on e_col, four lanes per column
+  const int col = tid >> 2, part = tid & 3;
   for (int r = 0; r < 64; ++r) {
-    double t = r == tid ? 1.0 : 0.0;
-    for (int k = tid; k < r; ++k) t -= Lk[r][k] * Xs[k][tid];
-    Xs[r][tid] = r < tid ? 0.0 : t / Lk[r][r];
+    double t = 0.0;
+    for (int k = col + part; k < r; k += 4) t = fma(Lk[r][k], Xs[k][col], t);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    if (part == 0) Xs[r][col] = r < col ? 0.0 : ((r == col ? 1.0 : 0.0) - t) / Lk[r][r];
+    __syncwarp();
   }
   __syncthreads();
   double* out = Dinv + blockIdx.x * 4096L;
-  for (int c = 0; c < 64; ++c) out[c * 64 + tid] = Xs[tid][c];
+  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
+    const int r = idx & 63, c = idx >> 6;
+    out[c * 64 + r] = Xs[r][c];
+  }
 }
 
 __global__ void k_transpose(const double* __restrict__ A, long lda, long rows, long cols, double* __restrict__ B,
@@ -248,7 +268,7 @@ void trsm_lower_cols(const double* L, long mpad, double* B, long ldb, long npts,
   require(mpad % 64 == 0 && npts % 128 == 0, "trsm: unpadded shape");
   if (npts == 0) return;
   set_smem_attrs();
-  k_trinv_blocks<<<static_cast<unsigned>(mpad / 64), 64, kPanelSmem, s>>>(L, mpad, dinv);
+  k_trinv_blocks<<<static_cast<unsigned>(mpad / 64), 256, kPanelSmem, s>>>(L, mpad, dinv);
   FSA_LAUNCH_CHECK();
   for (long k0 = 0; k0 < mpad; k0 += 64) {
     // B[:, k0:k0+64] = L_kk^{-1} B[:, k0:k0+64]   (in place; rows are points)

@@ -1,6 +1,7 @@
 // INT8 tensor-core (tcgen05) emulation of the fp64 skinny GEMMs; see ozaki.cuh.
 #include <algorithm>
 
+#include "bulk.cuh"
 #include "dgemm.cuh"
 #include "ozaki.cuh"
 
@@ -15,36 +16,6 @@ constexpr int kSmem = kStages * (kATile + kBTile);
 constexpr long kMaxChunk = 16384;  // int32 exactness: 8 pairs x K x 127^2 < 2^31
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "OZ_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra OZ_DONE;\n\t"
-      "bra OZ_WAIT;\n\t"
-      "OZ_DONE:\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 constexpr int kPrefetch = 8;  // A stages prefetched into L2 ahead of the smem pipeline
 
 // UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B,
@@ -186,7 +157,7 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(&done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   tc_fence_before();
   __syncthreads();
@@ -331,7 +302,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   tc_fence_before();
   __syncthreads();
@@ -518,7 +489,7 @@ __global__ void __launch_bounds__(288, 1) k_oz_spmm(OzSpmmArgs q) {
     }
     mbar_init(&tfull, 1);
     mbar_init(&tempty, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   tc_fence_before();
   __syncthreads();

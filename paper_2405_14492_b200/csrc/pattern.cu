@@ -62,6 +62,30 @@ __device__ inline void cell_of(const double* x, long ld, long i, const GridArgs&
   }
 }
 
+// Points are sorted by (cell key, position inside the cell): the cell key keeps every cell
+// contiguous for the neighbour search, and the second level (a 2^8 x 2^8 Hilbert curve inside
+// the cell for d = 2, the 16-bit offset for d = 1) makes any run of consecutive points
+// spatially compact, which is what the 32-row groups of the block SpMM need (smaller column
+// unions, fewer stored value tiles). d = 3 keys have no spare bits and keep the cell order.
+template <int D>
+constexpr int kSubBits = D == 3 ? 0 : 16;
+__host__ __device__ inline unsigned hilbert8(unsigned x, unsigned y) {
+  unsigned d = 0;
+  for (unsigned s = 128; s > 0; s >>= 1) {
+    const unsigned rx = (x & s) ? 1 : 0, ry = (y & s) ? 1 : 0;
+    d += s * s * ((3 * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = 255 - x;
+        y = 255 - y;
+      }
+      const unsigned t = x;
+      x = y;
+      y = t;
+    }
+  }
+  return d;
+}
 template <int D>
 __global__ void k_point_keys(const double* __restrict__ xs, long n, GridArgs g, unsigned long long* keys,
                              int* idx) {
@@ -69,8 +93,24 @@ __global__ void k_point_keys(const double* __restrict__ xs, long n, GridArgs g, 
   if (i >= n) return;
   long c[3] = {0, 0, 0};
   cell_of<D>(xs, n, i, g, c);
-  keys[i] = cell_key<D>(c);
+  unsigned long long key = cell_key<D>(c);
+  if (kSubBits<D> > 0) {
+    const double o[2] = {g.o0, g.o1};
+    unsigned f[2] = {0, 0};
+    const double res = D == 1 ? 65536.0 : 256.0;
+#pragma unroll
+    for (int k = 0; k < (D < 2 ? D : 2); ++k) {
+      const double t = ((xs[i + k * n] - o[k]) / g.h - static_cast<double>(c[k])) * res;
+      f[k] = t <= 0.0 ? 0u : (t >= res - 1.0 ? static_cast<unsigned>(res - 1.0) : static_cast<unsigned>(t));
+    }
+    key = (key << kSubBits<D>) | (D == 1 ? f[0] : hilbert8(f[0], f[1]));
+  }
+  keys[i] = key;
   idx[i] = static_cast<int>(i);
+}
+__global__ void k_cell_keys(unsigned long long* keys, long n, int shift) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] >>= shift;
 }
 
 __global__ void k_gather_coords(const double* __restrict__ xs, long n, int d, const int* __restrict__ perm,
@@ -250,6 +290,25 @@ __global__ void k_group_slots(const long* __restrict__ rowptr, long nrows, const
     lidx_to_slot[p] = static_cast<int>(kGroup * o + ((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3));
   }
 }
+// kmask[kb] |= 1 << rt for every entry (dense slot = kb * 128 + rt * 32 + lane)
+__global__ void k_tile_mask(const int* __restrict__ gslot, long nnz, int* __restrict__ kmask) {
+  const long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const int d = gslot[p];
+  atomicOr(kmask + (d >> 7), 1 << ((d >> 5) & 3));
+}
+__global__ void k_tile_count(const int* __restrict__ kmask, long nkb, int* __restrict__ cnt) {
+  const long k = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k <= nkb) cnt[k] = k < nkb ? __popc(kmask[k]) : 0;
+}
+__global__ void k_piece_meta(const int* __restrict__ kmask, const int* __restrict__ koff, long nkb,
+                             int2* __restrict__ pmeta) {
+  const long k = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nkb) return;
+  int m = 0;
+  for (int i = 0; i < 8 && k + i < nkb; ++i) m |= kmask[k + i] << (4 * i);
+  pmeta[k] = make_int2(koff[k], m);
+}
 __global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int pad, int* __restrict__ bad,
                            long* __restrict__ sizes) {
   const long b = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -399,6 +458,11 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
   DBuf<unsigned char> tmp(tmp_bytes);
   FSA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys_in.get(), out.keys.get(), idx_in.get(),
                                            out.perm_d.get(), static_cast<int>(n), 0, 64, s));
+  const int sub = d == 1 ? kSubBits<1> : (d == 2 ? kSubBits<2> : kSubBits<3>);
+  if (sub > 0) {  // back to the cell keys of the neighbour search
+    k_cell_keys<<<nb, 256, 0, s>>>(out.keys.get(), n, sub);
+    FSA_LAUNCH_CHECK();
+  }
   k_gather_coords<<<static_cast<unsigned>(cdiv(n_pad, 256)), 256, 0, s>>>(raw.get(), n, d, out.perm_d.get(), n_pad,
                                                                          out.coords.get(), out.iperm_d.get());
   FSA_LAUNCH_CHECK();
@@ -418,6 +482,33 @@ void build_groups(Csr& pat, cudaStream_t s) {
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());
   FSA_LAUNCH_CHECK();
+  {  // compact tiles of the value blocks
+    pat.nkb = pat.gnnz / 4;
+    pat.kmask.alloc(pat.nkb);
+    pat.kmask.zero(s);
+    pat.koff.alloc(pat.nkb + 1);
+    k_tile_mask<<<static_cast<unsigned>(cdiv(pat.nnz, 256)), 256, 0, s>>>(pat.gslot.get(), pat.nnz, pat.kmask.get());
+    FSA_LAUNCH_CHECK();
+    DBuf<int> cnt(pat.nkb + 1);
+    k_tile_count<<<static_cast<unsigned>(cdiv(pat.nkb + 1, 256)), 256, 0, s>>>(pat.kmask.get(), pat.nkb, cnt.get());
+    FSA_LAUNCH_CHECK();
+    size_t tb = 0;
+    FSA_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), pat.koff.get(), static_cast<int>(pat.nkb + 1), s));
+    DBuf<unsigned char> tmp(tb);
+    FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), pat.koff.get(), static_cast<int>(pat.nkb + 1), s));
+    int nt = 0;
+    FSA_CUDA(cudaMemcpyAsync(&nt, pat.koff.get() + pat.nkb, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    pat.ntiles = nt;
+    pat.pmeta.alloc(2 * std::max<long>(pat.nkb, 1));
+    k_piece_meta<<<static_cast<unsigned>(cdiv(pat.nkb, 256)), 256, 0, s>>>(
+        pat.kmask.get(), pat.koff.get(), pat.nkb, reinterpret_cast<int2*>(pat.pmeta.get()));
+    FSA_LAUNCH_CHECK();
+    if (std::getenv("FSA_DEBUG"))
+      std::fprintf(stderr, "[fsa] value tiles: %ld of %ld (%.3f), %.2f entries per tile\n", pat.ntiles, pat.nkb * 4,
+                   static_cast<double>(pat.ntiles) / std::max<long>(1, pat.nkb * 4),
+                   static_cast<double>(pat.nnz) / std::max<long>(1, pat.ntiles));
+  }
   // 128-row groups of the INT8 tensor-core SpMM (opt-in, FSA_SPMM=int8; unions padded to its
   // 32-row K blocks)
   static const bool int8 = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "int8") == 0;

@@ -61,6 +61,12 @@ struct Csr {
   DBuf<int> gcol;              // union columns (ascending; padding repeats a valid column)
   DBuf<int> gslot;             // per entry: its index in the value blocks (kGroup * gnnz)
   int gmax = 0;                // largest padded union
+  // Compact value tiles: of the dense block only the 8 x 4 DMMA A tiles (row tile rt of the
+  // group, k-step kb = union slot / 4) that hold an entry are stored (~2/3 of them at 80
+  // entries per row). kmask[kb] bit rt marks them; koff[kb] = stored tiles before k-step kb.
+  long nkb = 0, ntiles = 0;    // k-steps (gnnz / 4) and stored tiles
+  DBuf<int> kmask, koff;       // nkb, nkb + 1
+  DBuf<int> pmeta;             // per k-step (int2): {koff[kb], kmask[kb + i] << 4 i for i < 8}
   RowGroups g128;              // 128-row groups of the INT8 tensor-core SpMM (ozaki.cu)
 };
 constexpr int kGroup = 32;

@@ -10,6 +10,8 @@
 #include "kernels.cuh"
 #include "sparse.cuh"
 
+#include <cstdlib>
+
 namespace fsa {
 
 namespace {
@@ -255,133 +257,179 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 }
 
 // Block SpMM + dot on the FP64 tensor cores (Csr row groups, build_groups). A group of
-// kGroup = 32 consecutive rows (Hilbert order) and the union of their columns form a dense
-// 32 x u value block (zeros where a row lacks the column; ~1/3 dense at 80 nnz/row). The
-// union is consumed in pieces of kPiece rows: the piece's RHS rows (gathered) and value
-// fragments (contiguous) are copied into shared memory with cp.async, double-buffered, and
-// the block product runs as DMMA m8n8k4 tiles. Against the CSR kernel every RHS row is
-// fetched once per group instead of once per nonzero (~10x fewer bytes through L1/L2) and
-// the arithmetic moves onto the tensor pipe. 8 warps: warp w owns row tile w % 4 and every
-// other 8-column tile.
-constexpr int kPiece = 64;  // union rows per pipeline stage (16 DMMA k-steps)
-// the k-steps of one staged piece for the n-tiles q = H, H + SUB, ... (compile-time: no
-// predicated mma.sync, which would need a warp sync per instruction)
-template <int NT, int SUB, int H>
-__device__ __forceinline__ void block_ksteps(double (&c)[NT][2], const double* as, const double* hs, int nks,
-                                             int lane, int ldh, int astride) {
-#pragma unroll 4
-  for (int ks = 0; ks < nks; ++ks) {
-    const double a = as[ks * astride];
-    const double* hb = hs + (ks * 4 + (lane & 3)) * ldh + (lane >> 2);
+// kGroup = 32 consecutive rows (Hilbert order) and the union of their columns form a
+// 32 x u value block, cut into 8 x 4 DMMA A tiles (row tile rt, k-step kb); only the tiles
+// holding an entry are stored (Csr::kmask / koff, ~2/3 of them), in A-fragment order. The
+// union is consumed in pieces of kPiece rows: the piece's RHS rows (gathered) and stored
+// tiles (contiguous) are copied into shared memory with cp.async, double-buffered, and each
+// k-step runs the DMMAs of its stored tiles only (a warp-uniform switch on the 4-bit mask;
+// skipped tiles are all-zero, so the sums are those of the dense block). Every warp covers
+// all four row tiles on its own n-tiles q = H, H + WN, ..., so each staged B fragment feeds
+// up to four DMMAs. Against the CSR kernel every RHS row is fetched once per group instead of
+// once per nonzero and the arithmetic runs on the tensor pipe.
+constexpr int kPiece = 16;  // union rows per pipeline stage (4 DMMA k-steps)
+constexpr int kSpmmWarps = 4;
+constexpr int kSpmmMinBlocks = 8;  // 64 registers: eight 4-warp blocks per SM (smem ~26 KB each)
+// one k-step of a warp: the DMMAs of the stored tiles in MASK on the warp's NQ n-tiles
+// (hb points at the warp's first n-tile, n-tiles WN * 8 columns apart)
+template <int NQ, int WN, int MASK>
+__device__ __forceinline__ void tile_kstep(double (&c)[4][NQ][2], const double* at, const double* hb) {
+  double a[4];
+  int t = 0;
 #pragma unroll
-    for (int q = H; q < NT; q += SUB) dmma8x8x4(c[q][0], c[q][1], a, hb[q * 8]);
+  for (int rt = 0; rt < 4; ++rt)
+    if ((MASK >> rt) & 1) a[rt] = at[32 * t++];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const double b = hb[j * WN * 8];
+#pragma unroll
+    for (int rt = 0; rt < 4; ++rt)
+      if ((MASK >> rt) & 1) dmma8x8x4(c[rt][j][0], c[rt][j][1], a[rt], b);
   }
 }
-template <int NT>
-__global__ void __launch_bounds__(256, 2) k_spmm_block(const long* __restrict__ gptr, const int* __restrict__ gcol,
-                                                      const double* __restrict__ gval, long nrows,
-                                                      const double* __restrict__ X, long ldx, double* Y, long ldy,
-                                                      long ncols, const double* Y0, double* __restrict__ partial,
-                                                      long ldp) {
-  // column tile blockIdx.y: columns [64 y, 64 y + 8 NT) of X / Y / Y0 (Y0 null: Y = S X)
-  {
-    const long c0 = 64L * blockIdx.y;
-    X += c0;
-    Y += c0;
-    if (Y0 != nullptr) Y0 += c0;
-    partial += c0;
-    ncols -= c0;
+// the k-steps of one staged piece (a warp-uniform switch on each k-step's tile mask; one
+// compiled body per mask keeps the kernel small enough for the instruction cache)
+template <int NQ, int WN>
+__device__ __forceinline__ void tile_ksteps(double (&c)[4][NQ][2], const double* as, const double* hs,
+                                            int masks, int nks, int lane, int ldh, int h) {
+  int t = 0;
+#pragma unroll 1
+  for (int ks = 0; ks < nks; ++ks) {
+    const int m = (masks >> (4 * ks)) & 15;
+    const double* at = as + t * 32 + lane;
+    const double* hb = hs + (ks * 4 + (lane & 3)) * ldh + (lane >> 2) + h * 8;
+    switch (m) {
+#define FSA_TILE_CASE(M) \
+  case M: tile_kstep<NQ, WN, M>(c, at, hb); break;
+      FSA_TILE_CASE(1) FSA_TILE_CASE(2) FSA_TILE_CASE(3) FSA_TILE_CASE(4) FSA_TILE_CASE(5)
+      FSA_TILE_CASE(6) FSA_TILE_CASE(7) FSA_TILE_CASE(8) FSA_TILE_CASE(9) FSA_TILE_CASE(10)
+      FSA_TILE_CASE(11) FSA_TILE_CASE(12) FSA_TILE_CASE(13) FSA_TILE_CASE(14) FSA_TILE_CASE(15)
+#undef FSA_TILE_CASE
+      default: break;
+    }
+    t += __popc(m);
   }
-  constexpr int LDH = NT * 8 + (20 - (NT * 8) % 16) % 16;  // == 4 (mod 16): conflict-free B fragments
-  constexpr int CH = NT * 4;                               // 16-byte chunks per staged row
-  constexpr int HS = kPiece * LDH, AS = kPiece * kGroup;   // doubles per buffer
-  extern __shared__ __align__(16) double sm[];             // [2][HS] then [2][AS]
-  __shared__ double dred[4][64];
+}
+struct TileSpmmArgs {
+  const long* gptr;
+  const int* gcol;
+  const int2* pmeta;   // Csr::pmeta: per k-step {stored tiles before it, masks of it and the next three}
+  const double* tval;  // stored tiles, 32 doubles each
+  long nrows;
+  const double* X;
+  long ldx;
+  double* Y;
+  long ldy;
+  long ncols;
+  const double* Y0;
+  double* partial;
+  long ldp;
+};
+template <int NT, int WN, int MINB, int P>
+__global__ void __launch_bounds__(32 * WN, MINB) k_spmm_tiles(TileSpmmArgs q) {
+  static_assert(kGroup == 32 && WN == 4 && P % WN == 0, "four row tiles per group");
+  const long c0 = 64L * blockIdx.y;  // column tile: columns [c0, c0 + 8 NT)
+  const double* X = q.X + c0;
+  double* Y = q.Y + c0;
+  const double* Y0 = q.Y0 != nullptr ? q.Y0 + c0 : nullptr;
+  const long ncols = q.ncols - c0;
+  constexpr int NTH = 32 * WN;
+  constexpr int NQ = (NT + WN - 1) / WN;  // n-tiles per warp: q = warp + WN j (q >= NT: discarded)
+  constexpr int LDH = NQ * WN * 8 + 4;     // == 4 (mod 16): conflict-free B fragments
+  constexpr int CH = NT * 4;               // 16-byte chunks per staged row (one per lane)
+  constexpr int HS = P * LDH, AS = P * kGroup;  // doubles per buffer
+  constexpr int RW = P / WN;                          // staged rows per warp and piece
+  extern __shared__ __align__(16) double sm[];            // [2][HS], [2][AS]
   const long g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kRT = kGroup / 8, kSub = 8 / kRT;  // row tiles; warps per row tile (column subsets)
-  const int rt = warp % kRT, half = warp / kRT;
-  const long u0 = gptr[g];
-  const int up = static_cast<int>(gptr[g + 1] - u0);
-  const int npc = (up + kPiece - 1) / kPiece;
-  const double* gv = gval + kGroup * u0;
-  auto issue = [&](int pc) {
+  const long u0 = q.gptr[g];
+  const int up = static_cast<int>(q.gptr[g + 1] - u0);
+  const int npc = (up + P - 1) / P;
+  const long kb0 = u0 / 4;
+  // the piece metadata and the warp's gathered row indices are loaded one piece ahead of
+  // their copies, so their latency hides behind a piece of DMMAs
+  auto load_meta = [&](int pc, int2& pm, int (&gc)[RW]) {
+    pm = q.pmeta[kb0 + pc * (P / 4)];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) {
+      const int u = pc * P + warp + WN * i;
+      gc[i] = q.gcol[u0 + (u < up ? u : 0)];
+    }
+  };
+  auto issue = [&](int pc, const int2& pm, const int (&gc)[RW]) {
     double* hs = sm + (pc & 1) * HS;
     double* as = sm + 2 * HS + (pc & 1) * AS;
-    const int ua = pc * kPiece, nr = min(kPiece, up - ua);
-    for (int idx = tid; idx < nr * CH; idx += 256) {
-      const int u = idx / CH, ch = idx - u * CH;
-      cp_async16(hs + u * LDH + ch * 2, X + static_cast<long>(gcol[u0 + ua + u]) * ldx + ch * 2);
+    const int ua = pc * P, nr = min(P, up - ua);
+    if (lane < CH) {
+#pragma unroll
+      for (int i = 0; i < RW; ++i) {
+        const int u = warp + WN * i;
+        if (u < nr) cp_async16(hs + u * LDH + lane * 2, X + static_cast<long>(gc[i]) * q.ldx + lane * 2);
+      }
     }
-    const double* src = gv + static_cast<long>(ua) * kGroup;
-    for (int idx = tid; idx < nr * kGroup / 2; idx += 256) cp_async16(as + idx * 2, src + idx * 2);
+    const int nt = __popc(pm.y & static_cast<int>((1ull << nr) - 1ull));  // nr / 4 k-steps x 4 mask bits
+    const double* src = q.tval + 32L * pm.x;
+    for (int idx = tid; idx < nt * 16; idx += NTH) cp_async16(as + idx * 2, src + idx * 2);
     cp_async_commit();
   };
-  double c[NT][2];
+  double c[4][NQ][2];
 #pragma unroll
-  for (int q = 0; q < NT; ++q) c[q][0] = c[q][1] = 0.0;
-  if (npc > 0) issue(0);
+  for (int rt = 0; rt < 4; ++rt)
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) c[rt][j][0] = c[rt][j][1] = 0.0;
+  int2 cur{0, 0}, nxt{0, 0};
+  int gc[RW];
+  if (npc > 0) {
+    load_meta(0, cur, gc);
+    issue(0, cur, gc);
+  }
+  if (npc > 1) load_meta(1, nxt, gc);
   for (int pc = 0; pc < npc; ++pc) {
-    if (pc + 1 < npc) {
-      issue(pc + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    if (pc + 1 < npc) issue(pc + 1, nxt, gc);
+    int2 after{0, 0};
+    if (pc + 2 < npc) load_meta(pc + 2, after, gc);
+    if (pc + 1 < npc) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
     const double* hs = sm + (pc & 1) * HS;
-    const double* as = sm + 2 * HS + (pc & 1) * AS + rt * 32 + lane;
-    static_assert(kGroup % 8 == 0 && 8 % (kGroup / 8) == 0, "row tiles must divide the 8 warps");
-    const int nks = min(kPiece, up - pc * kPiece) / 4;
-    static_assert(kSub <= 4, "at most four column subsets");
-    switch (half) {
-      case 0: block_ksteps<NT, kSub, 0>(c, as, hs, nks, lane, LDH, kRT * 32); break;
-      case 1: block_ksteps<NT, kSub, 1 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
-      case 2: block_ksteps<NT, kSub, 2 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
-      default: block_ksteps<NT, kSub, 3 % kSub>(c, as, hs, nks, lane, LDH, kRT * 32); break;
-    }
+    const double* as = sm + 2 * HS + (pc & 1) * AS;
+    const int nks = min(P, up - pc * P) / 4;
+    tile_ksteps<NQ, WN>(c, as, hs, cur.y, nks, lane, LDH, warp);
     __syncthreads();  // the buffer is refilled by issue(pc + 2)
+    cur = nxt;
+    nxt = after;
   }
-  // epilogue: Y = Y0 + S X on this lane's fragment; h.v column partials
-  const long row = g * kGroup + rt * 8 + (lane >> 2);
-  double d[NT][2];
+  // epilogue: Y = Y0 + S X on this lane's fragments; h.v column partials (one warp per column)
+  double* partial = q.partial + c0;
 #pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    d[q][0] = d[q][1] = 0.0;
-    if (q % kSub != half) continue;
-    const long cc = q * 8 + 2 * (lane & 3);
-    if (row < nrows && cc < ncols) {
-      double2 o = make_double2(c[q][0], c[q][1]);
-      if (Y0 != nullptr) {
-        const double2 y0 = *reinterpret_cast<const double2*>(Y0 + row * ldy + cc);
-        o.x += y0.x;
-        o.y += y0.y;
+  for (int j = 0; j < NQ; ++j) {
+    const long cc = (warp + j * WN) * 8 + 2 * (lane & 3);
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int rt = 0; rt < 4; ++rt) {
+      const long row = g * kGroup + rt * 8 + (lane >> 2);
+      if (row < q.nrows && cc < ncols) {
+        double2 o = make_double2(c[rt][j][0], c[rt][j][1]);
+        if (Y0 != nullptr) {
+          const double2 y0 = *reinterpret_cast<const double2*>(Y0 + row * q.ldy + cc);
+          o.x += y0.x;
+          o.y += y0.y;
+        }
+        *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
+        const double2 h = *reinterpret_cast<const double2*>(X + row * q.ldx + cc);
+        d0 = fma(h.x, o.x, d0);
+        d1 = fma(h.y, o.y, d1);
       }
-      *reinterpret_cast<double2*>(Y + row * ldy + cc) = o;
-      const double2 h = *reinterpret_cast<const double2*>(X + row * ldx + cc);
-      d[q][0] = h.x * o.x;
-      d[q][1] = h.y * o.y;
     }
-  }
-#pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    if (q % kSub != half) continue;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
-      d[q][0] += __shfl_xor_sync(0xffffffffu, d[q][0], o);
-      d[q][1] += __shfl_xor_sync(0xffffffffu, d[q][1], o);
+      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
     }
-    if (lane < 4) {
-      dred[rt][q * 8 + 2 * lane] = d[q][0];
-      dred[rt][q * 8 + 2 * lane + 1] = d[q][1];
+    if (lane < 4 && cc < ncols) {
+      partial[g * q.ldp + cc] = d0;
+      partial[g * q.ldp + cc + 1] = d1;
     }
-  }
-  __syncthreads();
-  if (tid < NT * 8 && tid < ncols) {
-    double sacc = 0.0;
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) sacc += dred[r][tid];
-    partial[g * ldp + tid] = sacc;
   }
 }
 // ---- block SDDMM: dense Gram blocks of the row groups on DMMA ----------------------------------
@@ -480,12 +528,18 @@ __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ 
 // pattern entries from the Gram blocks: Sigma_s (MODE 0) or d Sigma_s / d rho (MODE 1);
 // each unordered pair is evaluated once (from the row with c > r) and mirrored, so the
 // result is exactly symmetric; MODE 0 also fills the SpMM value blocks gval
+// stored-tile index of dense value-block slot d (Csr::kmask / koff)
+__device__ __forceinline__ long tile_slot(int d, const int* __restrict__ kmask, const int* __restrict__ koff) {
+  const int kb = d >> 7, rt = (d >> 5) & 3;
+  return 32L * (koff[kb] + __popc(kmask[kb] & ((1 << rt) - 1))) + (d & 31);
+}
 template <int MODE>
 __global__ void k_sddmm_finish(const long* __restrict__ rowptr, const int* __restrict__ col,
                                const long* __restrict__ mirror, const int* __restrict__ gslot,
                                const double* __restrict__ dist, const double* __restrict__ lowrank_diag,
                                const double* __restrict__ G, long n, SddmmParams P, double* __restrict__ val,
-                               double* __restrict__ gval, int* __restrict__ n_clamped) {
+                               double* __restrict__ gval, const int* __restrict__ kmask,
+                               const int* __restrict__ koff, int* __restrict__ n_clamped) {
   const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
@@ -507,20 +561,21 @@ __global__ void k_sddmm_finish(const long* __restrict__ rowptr, const int* __res
       v = (k - G[gslot[p]]) * taper_d(d, P.family, P.gamma);
     }
     val[p] = v;
-    if (MODE == 0) gval[gslot[p]] = v;
+    if (MODE == 0 && gval != nullptr) gval[tile_slot(gslot[p], kmask, koff)] = v;
     const long q = mirror[p];
     if (c != r && q >= 0) {
       val[q] = v;
-      if (MODE == 0) gval[gslot[q]] = v;
+      if (MODE == 0 && gval != nullptr) gval[tile_slot(gslot[q], kmask, koff)] = v;
     }
   }
 }
 
-// gval[gslot[p]] = val[p] (gval zeroed first)
-__global__ void k_group_scatter(const int* __restrict__ gslot, long nnz, const double* __restrict__ val,
+// stored tiles from the CSR values (gval zeroed first)
+__global__ void k_group_scatter(const int* __restrict__ gslot, const int* __restrict__ kmask,
+                                const int* __restrict__ koff, long nnz, const double* __restrict__ val,
                                 double* __restrict__ gval) {
   const long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p < nnz) gval[gslot[p]] = val[p];
+  if (p < nnz) gval[tile_slot(gslot[p], kmask, koff)] = val[p];
 }
 
 #define FSA_DISPATCH_MQ(KERNEL, mpad, grid, s, ...)                                      \
@@ -575,15 +630,17 @@ void sddmm_block(int mode, const double* U, const double* U1, const double* T, l
   else
     k_block_gram<1><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U1, U, U, T, ldu, mp, gtmp);
   FSA_LAUNCH_CHECK();
-  if (mode == 0 && gval != nullptr) FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
+  if (mode == 0 && gval != nullptr) FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * 32 * pat.ntiles, s));
   if (mode == 0 && n_clamped_dev != nullptr) FSA_CUDA(cudaMemsetAsync(n_clamped_dev, 0, sizeof(int), s));
   const unsigned g2 = static_cast<unsigned>(cdiv(pat.rows * 32, 256));
   if (mode == 0)
     k_sddmm_finish<0><<<g2, 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.mirror.get(), pat.gslot.get(),
-                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, gval, n_clamped_dev);
+                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, gval, pat.kmask.get(),
+                                        pat.koff.get(), n_clamped_dev);
   else
     k_sddmm_finish<1><<<g2, 256, 0, s>>>(pat.rowptr.get(), pat.col.get(), pat.mirror.get(), pat.gslot.get(),
-                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, nullptr, nullptr);
+                                        pat.dist.get(), lowrank_diag, gtmp, pat.rows, P, val, nullptr, nullptr, nullptr,
+                                        nullptr);
   FSA_LAUNCH_CHECK();
 }
 
@@ -608,8 +665,9 @@ void extract_diag(const double* val, const long* diagpos, long n, long n_pad, do
 
 void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t s) {
   if (pat.gnnz == 0) return;
-  FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * pat.gnnz * kGroup, s));
-  k_group_scatter<<<static_cast<unsigned>(cdiv(pat.nnz, 256)), 256, 0, s>>>(pat.gslot.get(), pat.nnz, val, gval);
+  FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * 32 * pat.ntiles, s));
+  k_group_scatter<<<static_cast<unsigned>(cdiv(pat.nnz, 256)), 256, 0, s>>>(pat.gslot.get(), pat.kmask.get(),
+                                                                            pat.koff.get(), pat.nnz, val, gval);
   FSA_LAUNCH_CHECK();
 }
 
@@ -623,27 +681,25 @@ void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ld
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
   auto launch = [&](int nt, long c_first, long tiles) {
-    const long ldh = 8L * nt + (20 - (8L * nt) % 16) % 16;
+    const long ldh = cdiv(nt, kSpmmWarps) * kSpmmWarps * 8 + 4;  // k_spmm_tiles' LDH
     const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
-    const double* x = X + c_first;
-    double* y = Y + c_first;
-    const double* y0 = Y0 != nullptr ? Y0 + c_first : nullptr;
-    double* part = partial + c_first;
-    const long nc = ncols - c_first;
+    TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
+                   X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
+                   partial + c_first, ncols};
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      kern<<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), gval, pat.rows, x, ldx, y, ldy, nc, y0, part, ncols);
+      kern<<<grid, 32 * kSpmmWarps, smem, s>>>(a);
     };
     switch (nt) {
-      case 1: go(k_spmm_block<1>); break;
-      case 2: go(k_spmm_block<2>); break;
-      case 3: go(k_spmm_block<3>); break;
-      case 4: go(k_spmm_block<4>); break;
-      case 5: go(k_spmm_block<5>); break;
-      case 6: go(k_spmm_block<6>); break;
-      case 7: go(k_spmm_block<7>); break;
-      default: go(k_spmm_block<8>); break;
+      case 1: go(k_spmm_tiles<1, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 2: go(k_spmm_tiles<2, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 3: go(k_spmm_tiles<3, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 4: go(k_spmm_tiles<4, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 5: go(k_spmm_tiles<5, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 6: go(k_spmm_tiles<6, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      case 7: go(k_spmm_tiles<7, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
+      default: go(k_spmm_tiles<8, kSpmmWarps, kSpmmMinBlocks, kPiece>); break;
     }
     FSA_LAUNCH_CHECK();
   };
