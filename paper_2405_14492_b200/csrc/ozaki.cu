@@ -16,7 +16,7 @@ constexpr int kSmem = kStages * (kATile + kBTile);
 constexpr long kMaxChunk = 16384;  // int32 exactness: 8 pairs x K x 127^2 < 2^31
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
-constexpr int kPrefetch = 8;  // A stages prefetched into L2 ahead of the smem pipeline
+// (no L2 prefetch ahead of the bulk copies: measured slower, it competes with the copies)
 
 // UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B,
 // lbo = byte stride between the two 16-B K halves, sbo = byte stride between 8-row groups
@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(128, 1)
       mbar_expect_tx(&full[st], kATile + kBTile);
       bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
       bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * kBTile, kBTile, &full[st]);
-      if (j + kPrefetch < nk) prefetch_l2(Ablk + static_cast<long>(j + kPrefetch) * kATile, kATile);
     };
     const int pre = min(nk, kStages);
     for (int j = 0; j < pre; ++j) load(j);
@@ -320,14 +319,6 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(&full[st], kATile + kBTile);
           bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
           bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * kBTile, kBTile, &full[st]);
-          {  // L2 prefetch kPrefetch stages ahead (possibly in this CTA's next tile)
-            int pt = t, pk = kb + kPrefetch;
-            if (pk >= mkb) {
-              pk -= mkb;
-              pt += gridDim.x;
-            }
-            if (pt < tiles) prefetch_l2(A + (static_cast<long>(pt) * mkb + pk) * kATile, kATile);
-          }
         }
       }
     }
