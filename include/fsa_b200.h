@@ -123,6 +123,11 @@ int fsa_select_random(const double* coords, int64_t n, int d, int64_t m, uint64_
 /* select_kmeanspp (inducing.cpp:48-139), KmeansOptions{max_iter, rel_tol} */
 int fsa_select_kmeanspp(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, int max_iter,
                         double rel_tol, double* out);
+/* select_kmeanspp on the device (inducing.cpp:48-139): same distinct pool,
+ * RNG draws, Lloyd stop rule and greedy snapping as fsa_select_kmeanspp; the seeding rounds,
+ * Lloyd assignments / centroids and snapping searches run as kernels on ctx's stream. */
+int fsa_select_kmeanspp_device(fsa_ctx* ctx, const double* coords, int64_t n, int d, int64_t m, uint64_t seed,
+                               int max_iter, double rel_tol, double* out);
 /* gamma_for_avg_row_nnz (locations.cpp:192-195) */
 double fsa_gamma_for_avg_row_nnz(int64_t n, double target_row_nnz);
 /* synthetic response: random-Fourier-feature Matern draw + N(0, nugget) noise */
@@ -202,6 +207,15 @@ int fsa_tridiag_log_quadrature(const double* diag, const double* off, int64_t le
 int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const double* X, int64_t pcols,
                            int num_probes, uint64_t seed, const fsa_cg_options* cg, int cv_mode, int want_grad,
                            fsa_nll_result* out, double* beta);
+
+/* fisher_ste (fsa.cpp:284-301, FisherOptions fsa.h:107-111): stochastic expected Fisher
+ * information of (sigma2, sigma1_2, rho) from num_probes keyed probes (Gaussian, or Rademacher
+ * when rademacher != 0). The reference solves with its exact backend (FsaModel::solve); here the
+ * L and 3L solves are batched PCG runs with preconditioner p and tolerance cg (pass a tight
+ * tolerance for exact-solve agreement). F_out: 3 x 3 column-major, exactly symmetric.
+ * cg_iterations (may be NULL): max over both solves. */
+int fsa_fisher_ste(fsa_model* md, fsa_precond* p, int num_probes, uint64_t seed, int rademacher,
+                   const fsa_cg_options* cg, double* F_out, int* cg_iterations);
 
 /* ---- maximum-likelihood fit (fit_fsa, estimation.cpp:229-303) -------
  * L-BFGS over log(sigma2, sigma1_2, rho) (lbfgs_minimize, estimation.cpp:10-132: two-loop

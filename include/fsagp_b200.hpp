@@ -154,6 +154,23 @@ inline IterativeNll iterative_nll_grad(FsaModel& md, const Preconditioner& P, co
   return out;
 }
 
+// fisher_ste (fsa.h:106-112): the reference's exact solves become FITC-PCG runs to `solve_tol`
+struct FisherOptions {  // fsa.h:107-111
+  int num_probes = 50;
+  std::uint64_t seed = 0;
+  bool rademacher = false;
+  double solve_tol = 1e-8;  // (device build only) PCG tolerance standing in for the exact solve
+  int solve_max_iter = 1000;
+};
+// returns F (3 x 3, column-major)
+inline std::array<double, 9> fisher_ste(FsaModel& md, const FisherOptions& o) {
+  Preconditioner P(md, PrecondType::fitc);
+  fsa_cg_options cg{o.solve_tol, o.solve_max_iter, 0};
+  std::array<double, 9> F{};
+  check(fsa_fisher_ste(md.get(), P.get(), o.num_probes, o.seed, o.rademacher ? 1 : 0, &cg, F.data(), nullptr));
+  return F;
+}
+
 // PredictionSet / make_prediction_set (prediction.h:16-25)
 class PredictionSet {
  public:

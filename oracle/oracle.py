@@ -408,3 +408,25 @@ class PredictionSet:
         _check(lib().orc_predict_var_sim(self.model.h, self.h, num_probes, seed, tol, max_iter, tol_s, max_iter_s,
                                          1 if control_variate else 0, floor_rel, var, se, C.byref(cl), C.byref(it)))
         return {"var": var, "se": se, "clamped": cl.value, "cg_iterations": it.value}
+
+
+def fisher_ste(model: Model, num_probes=50, seed=0, rademacher=False):
+    """fisher_ste (fsa.cpp:284-301) restated in numpy. FsaModel::solve is the reference's exact
+    backend (sparse LDLT of Sigma_s + Woodbury, fsa.cpp:196-223); for the small sizes the oracle
+    serves, a dense Cholesky of the same Sigma (= matmat of the identity) is that solve."""
+    import scipy.linalg as sla
+
+    if num_probes <= 0:
+        raise ValueError("need at least one probe")  # fsa.cpp:285
+    n = model.n
+    S = model.matmat(np.eye(n))
+    cf = sla.cho_factor(0.5 * (S + S.T), lower=True)
+    F_ = np.zeros((3, 3))
+    for i in range(num_probes):
+        z = probe_rademacher(seed, i, n) if rademacher else probe_gaussian(seed, i, 0, n)[1]
+        w = sla.cho_solve(cf, z)
+        a = np.column_stack([model.deriv_matmat(k, w)[:, 0] for k in range(3)])
+        t = np.column_stack([sla.cho_solve(cf, model.deriv_matmat(k, z)[:, 0]) for k in range(3)])
+        F_ += a.T @ t
+    F_ /= 2.0 * num_probes
+    return 0.5 * (F_ + F_.T)

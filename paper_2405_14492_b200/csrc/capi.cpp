@@ -12,6 +12,7 @@
 #include "fit.h"
 #include "fsa_core.cuh"
 #include "inputs.h"
+#include "kmeans.cuh"
 #include "predict.cuh"
 
 using namespace fsa;
@@ -295,6 +296,16 @@ int fsa_select_random(const double* coords, int64_t n, int d, int64_t m, uint64_
 int fsa_select_kmeanspp(const double* coords, int64_t n, int d, int64_t m, uint64_t seed, int max_iter,
                         double rel_tol, double* out) {
   return guard([&] { select_kmeanspp(coords, n, d, m, seed, max_iter, rel_tol, out); });
+}
+int fsa_select_kmeanspp_device(fsa_ctx* ctx, const double* coords, int64_t n, int d, int64_t m, uint64_t seed,
+                               int max_iter, double rel_tol, double* out) {
+  return guard([&] {
+    need(ctx, "context");
+    need(coords, "coords");
+    need(out, "out");
+    Bind bind_(ctx->c.get());
+    select_kmeanspp_device(ctx->c->stream, coords, n, d, m, seed, max_iter, rel_tol, out);
+  });
 }
 double fsa_gamma_for_avg_row_nnz(int64_t n, double target) {
   double g = 0.0;
@@ -670,6 +681,19 @@ int fsa_iterative_nll_grad(fsa_model* md, fsa_precond* p, const double* y, const
     out->total_ms = r.total_ms;
     for (long a = 0; a < pcols; ++a)
       if (beta) beta[a] = r.beta[static_cast<size_t>(a)];
+  });
+}
+
+int fsa_fisher_ste(fsa_model* md, fsa_precond* p, int num_probes, uint64_t seed, int rademacher,
+                   const fsa_cg_options* cg, double* F_out, int* cg_iterations) {
+  return guard([&] {
+    need(md, "model");
+    Bind bind_(md->m->ctx);
+    need(p, "preconditioner");
+    need(F_out, "F_out");
+    FisherResult r = fisher_ste(md->m.get(), *p->p, num_probes, seed, rademacher != 0, to_cg(cg));
+    std::copy(r.F, r.F + 9, F_out);
+    if (cg_iterations) *cg_iterations = r.cg_iterations;
   });
 }
 

@@ -14,6 +14,7 @@
 
 #include "fsa_core.cuh"
 #include "inputs.h"
+#include "kmeans.cuh"
 
 namespace fsa {
 namespace {
@@ -219,7 +220,9 @@ FitOutput fit_fsa(Context* ctx, const double* coords, long n, int d, const doubl
   FitOutput out;
   out.gamma = o.taper_range > 0.0 ? o.taper_range : gamma_for_avg_row_nnz(n, o.target_row_nnz);
   out.inducing.resize(static_cast<size_t>(o.num_inducing * d));
-  select_kmeanspp(coords, n, d, o.num_inducing, o.seed, o.kmeans_max_iter, o.kmeans_rel_tol, out.inducing.data());
+  // inducing points by the device k-means++ (inducing.cpp:48-139; kmeans.cu)
+  select_kmeanspp_device(ctx->stream, coords, n, d, o.num_inducing, o.seed, o.kmeans_max_iter, o.kmeans_rel_tol,
+                         out.inducing.data());
   // start point (estimation.cpp:246-257): half the residual variance each, rho at which the
   // correlation is 0.05 a quarter of the bounding-box diagonal away
   const std::vector<double> r0 = ols_residual(y, X, n, p);

@@ -1175,4 +1175,84 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
   return out;
 }
 
+FisherResult fisher_ste(Model* md, Precond& P, int L, unsigned long long seed, bool rademacher, const CgOptions& cg) {
+  require(L > 0, "need at least one probe");  // fsa.cpp:285
+  Context* ctx = md->ctx;
+  cudaStream_t s = ctx->stream;
+  Comm& comm = *md->rcomm;
+  const long N = md->geo->pts.n, r0 = md->world() > 1 ? md->geo->shard.r0 : 0;
+  const long n = md->n, np = md->n_pad, ne = md->n_ext_pad;
+  const long t1 = pad_cols(L), t3 = pad_cols(3L * L);
+  // probes z_i = gaussian_vector / rademacher_vector of probe_rng(seed, i) over all N points
+  // (fsa.cpp:288-289); a rank keeps its rows. Z lives in an extended block (owned rows +
+  // halo) so that the Sigma_s products see the neighbours.
+  DBuf<double> Z(static_cast<size_t>(ne * t1));
+  {
+    std::vector<double> h(static_cast<size_t>(N * L));
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int i = 0; i < L; ++i) {
+      double* zi = h.data() + static_cast<size_t>(i) * N;
+      if (rademacher) probe_rademacher(seed, static_cast<unsigned long long>(i), N, zi);
+      else probe_gaussian(seed, static_cast<unsigned long long>(i), 0, nullptr, N, zi);
+    }
+    DBuf<double> raw(static_cast<size_t>(N * L));
+    FSA_CUDA(cudaMemcpyAsync(raw.get(), h.data(), sizeof(double) * N * L, cudaMemcpyHostToDevice, s));
+    FSA_CUDA(cudaMemsetAsync(Z.get(), 0, sizeof(double) * ne * t1, s));
+    pack_cols_ld(raw.get(), N, n, L, md->geo->pts.perm_d.get() + r0, np, t1, 0, Z.get(), s);
+    FSA_CUDA(cudaStreamSynchronize(s));
+  }
+  md->halo_exchange(Z.get(), t1);
+  FisherResult out;
+  FsaOp op(md);
+  // W = Sigma^{-1} Z (fsa.cpp:290)
+  DBuf<double> W(static_cast<size_t>(ne * t1));
+  FSA_CUDA(cudaMemsetAsync(W.get(), 0, sizeof(double) * ne * t1, s));
+  {
+    CgResult r = pcg_solve_multi(md, op, P, Z.get(), L, t1, W.get(), cg);
+    if (!r.all_converged()) throw NumericalError("fisher: cg did not converge");
+    out.cg_iterations = r.max_iterations();
+    out.sweeps += r.sweeps;
+  }
+  md->halo_exchange(W.get(), t1);
+  // B = [dSigma_0 Z | dSigma_1 Z | dSigma_2 Z] and A_k = dSigma_k W (fsa.cpp:292-295)
+  DBuf<double> B(static_cast<size_t>(np * t3)), A(static_cast<size_t>(3 * np * t1)), tmp(static_cast<size_t>(np * t1));
+  FSA_CUDA(cudaMemsetAsync(B.get(), 0, sizeof(double) * np * t3, s));
+  for (int k = 0; k < 3; ++k) {
+    md->deriv_matmat(k, Z.get(), tmp.get(), t1);
+    copy_cols(tmp.get(), t1, B.get() + k * L, t3, np, L, s);
+    md->deriv_matmat(k, W.get(), A.get() + k * np * t1, t1);
+  }
+  // T = Sigma^{-1} B, one batched solve over the 3 L columns
+  DBuf<double> T(static_cast<size_t>(ne * t3));
+  FSA_CUDA(cudaMemsetAsync(T.get(), 0, sizeof(double) * ne * t3, s));
+  {
+    CgResult r = pcg_solve_multi(md, op, P, B.get(), 3L * L, t3, T.get(), cg);
+    if (!r.all_converged()) throw NumericalError("fisher: cg did not converge");
+    out.cg_iterations = std::max(out.cg_iterations, r.max_iterations());
+    out.sweeps += r.sweeps;
+  }
+  // F_kl = sum_i a_k,i . t_l,i: column dots of A_k against the l-th slice of T
+  DBuf<double> dots(static_cast<size_t>(9 * t1));
+  FSA_CUDA(cudaMemsetAsync(dots.get(), 0, sizeof(double) * 9 * t1, s));
+  for (int l = 0; l < 3; ++l) {
+    copy_cols(T.get() + l * L, t3, tmp.get(), t1, np, L, s);
+    for (int k = 0; k < 3; ++k)
+      launch_coldot(A.get() + k * np * t1, tmp.get(), n, t1, t1, dots.get() + (k + 3 * l) * t1, md->dot_scratch.get(),
+                    s);
+  }
+  comm.allreduce(dots.get(), 9 * t1, s);
+  std::vector<double> h(static_cast<size_t>(9 * t1));
+  FSA_CUDA(cudaMemcpyAsync(h.data(), dots.get(), sizeof(double) * 9 * t1, cudaMemcpyDeviceToHost, s));
+  FSA_CUDA(cudaStreamSynchronize(s));
+  double F[9];
+  for (int c = 0; c < 9; ++c) {
+    double acc = 0.0;
+    for (long i = 0; i < L; ++i) acc += h[static_cast<size_t>(c * t1 + i)];  // probe order, as F += a^T t
+    F[c] = acc / (2.0 * L);
+  }
+  for (int k = 0; k < 3; ++k)
+    for (int l = 0; l < 3; ++l) out.F[k + 3 * l] = 0.5 * (F[k + 3 * l] + F[l + 3 * k]);  // fsa.cpp:299-300
+  return out;
+}
+
 }  // namespace fsa

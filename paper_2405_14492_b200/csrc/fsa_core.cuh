@@ -286,6 +286,17 @@ struct NllResult {
 NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* X, long p, int num_probes,
                              unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad);
 
+// fisher_ste (fsa.cpp:284-301): F = sym( sum_i A_i^T T_i ) / (2 L) with, per probe z_i,
+// A_i = [dSigma_k Sigma^{-1} z_i]_k and T_i = [Sigma^{-1} dSigma_k z_i]_k. The reference solves
+// with its exact (sparse LDLT) backend; here every solve is one batched FITC-PCG run (L, then
+// 3 L columns) to the caller's tolerance. F is 3 x 3 column-major.
+struct FisherResult {
+  double F[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int cg_iterations = 0;  // max over both solves
+  int sweeps = 0;         // sum over both solves
+};
+FisherResult fisher_ste(Model* md, Precond& P, int L, unsigned long long seed, bool rademacher, const CgOptions& cg);
+
 // ---- host RNG identical to the reference (types.h:104-129) ------------------------------------
 unsigned long long splitmix64(unsigned long long x);
 void probe_gaussian(unsigned long long seed, unsigned long long i, long n1, double* e1, long n2, double* e2);

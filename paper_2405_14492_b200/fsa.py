@@ -95,6 +95,7 @@ _SIGS = {
     "fsa_uniform_locations": (C.c_int, [_i64, C.c_int, _u64, _dp]),
     "fsa_select_random": (C.c_int, [_dp, _i64, C.c_int, _i64, _u64, _dp]),
     "fsa_select_kmeanspp": (C.c_int, [_dp, _i64, C.c_int, _i64, _u64, C.c_int, C.c_double, _dp]),
+    "fsa_select_kmeanspp_device": (C.c_int, [_vp, _dp, _i64, C.c_int, _i64, _u64, C.c_int, C.c_double, _dp]),
     "fsa_gamma_for_avg_row_nnz": (C.c_double, [_i64, C.c_double]),
     "fsa_simulate_rff": (C.c_int, [_dp, _i64, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, _u64,
                                    _dp]),
@@ -133,6 +134,8 @@ _SIGS = {
     "fsa_tridiag_log_quadrature": (C.c_int, [_dp, _dp, _i64, C.POINTER(C.c_double)]),
     "fsa_iterative_nll_grad": (C.c_int, [_vp, _vp, _vp, _vp, _i64, C.c_int, _u64, C.POINTER(CgOptions), C.c_int,
                                          C.c_int, C.POINTER(NllResult), _vp]),
+    "fsa_fisher_ste": (C.c_int, [_vp, _vp, C.c_int, _u64, C.c_int, C.POINTER(CgOptions), _dp,
+                                 C.POINTER(C.c_int)]),
     "fsa_pred_setup": (C.c_int, [_vp, _dp, _i64, C.POINTER(_vp)]),
     "fsa_fit_options_default": (None, [C.POINTER(FitOptions)]),
     "fsa_fit": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _vp, _i64, C.POINTER(FitOptions), C.POINTER(FitResult),
@@ -196,10 +199,16 @@ def select_random(coords, m, seed):
     return out
 
 
-def select_kmeanspp(coords, m, seed, max_iter=20, rel_tol=1e-4):
+def select_kmeanspp(coords, m, seed, max_iter=20, rel_tol=1e-4, device=False, ctx=None):
+    """select_kmeanspp (inducing.cpp:48-139). device=True runs the seeding, Lloyd and snapping
+    kernels on ``ctx`` (default context) instead of the host restatement."""
     c = _F(coords)
     out = _F(np.zeros((m, c.shape[1])))
-    _check(lib().fsa_select_kmeanspp(c, c.shape[0], c.shape[1], m, seed, max_iter, rel_tol, out))
+    if device or ctx is not None:
+        ctx = ctx or default_context()
+        _check(lib().fsa_select_kmeanspp_device(ctx.h, c, c.shape[0], c.shape[1], m, seed, max_iter, rel_tol, out))
+    else:
+        _check(lib().fsa_select_kmeanspp(c, c.shape[0], c.shape[1], m, seed, max_iter, rel_tol, out))
     return out
 
 
@@ -551,6 +560,20 @@ def iterative_nll_grad(model: FsaModel, P: Preconditioner, y, X=None, num_probes
     return {"nll": res.nll, "grad": np.array(res.grad[:]), "logdet": res.logdet, "cg_iterations": res.cg_iterations,
             "beta": beta[:p].copy(), "sweeps": res.sweeps, "rhs_iterations": res.rhs_iterations,
             "pcg_ms": res.pcg_ms, "total_ms": res.total_ms}
+
+
+def fisher_ste(model: FsaModel, num_probes=50, seed=0, rademacher=False, P: Preconditioner = None, tol=1e-8,
+               max_iter=1000):
+    """fisher_ste (fsa.cpp:284-301; FisherOptions fsa.h:107-111). The reference's exact solves
+    are batched PCG runs here (preconditioner P, FITC by default) to tolerance ``tol``."""
+    if P is None:
+        P = make_preconditioner(model, "fitc")
+    F = _F(np.zeros((3, 3)))
+    it = C.c_int()
+    cg = _cg(tol, max_iter)
+    _check(lib().fsa_fisher_ste(model.h, P.h, num_probes, seed, 1 if rademacher else 0, C.byref(cg), F,
+                                C.byref(it)))
+    return F
 
 
 class PredictionSet:

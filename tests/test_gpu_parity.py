@@ -283,3 +283,13 @@ def test_nll_dimensions_and_widths_match_oracle(d, n, m, L):
     assert got["cg_iterations"] == want["cg_iterations"]
     assert got["nll"] == pytest.approx(want["nll"], rel=1e-6)
     np.testing.assert_allclose(got["grad"], want["grad"], rtol=1e-6, atol=1e-6 * np.abs(want["grad"]).max())
+
+
+@pytest.mark.parametrize("rademacher,L", [(False, 24), (True, 9)])
+def test_fisher_ste_matches_oracle(rademacher, L):  # fsa.cpp:284-301 (test_fsa.cpp:182-215)
+    locs, ind, kw, md, om = setup(n=1200, m=50, seed=11)
+    want = O.fisher_ste(om, num_probes=L, seed=5, rademacher=rademacher)  # exact dense solves
+    got = fsa.fisher_ste(md, num_probes=L, seed=5, rademacher=rademacher, tol=1e-11)  # FITC-PCG solves
+    assert np.abs(got - got.T).max() <= 1e-12 * np.abs(got).max()
+    # same probes, solves to 1e-11: agreement to the north-star scalar tolerance
+    assert rel(got, want) < 1e-6, (got, want)

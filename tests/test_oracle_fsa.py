@@ -202,3 +202,17 @@ def test_ste_unbiased_and_cv_shrinks():  # test_krylov.cpp:178-205
         assert abs(plain["value"] - exact) < 4 * np.sqrt(plain["variance_of_mean"]) + 1e-8
         assert abs(cv["value"] - exact) < 4 * np.sqrt(cv["variance_of_mean"]) + 1e-8
         assert cv["variance_of_mean"] <= plain["variance_of_mean"] + 1e-12
+
+
+def test_fisher_ste_approximates_dense():  # test_fsa.cpp:182-215
+    model, dense, _, _ = small_model(100, 10, 0.2, 0.5, 1.0, 0.12, 73)
+    n = 100
+    inv = np.linalg.inv(dense)
+    dS = [model.deriv_matmat(k, np.eye(n)) for k in range(3)]
+    want = np.array([[0.5 * np.trace(inv @ dS[k] @ inv @ dS[l]) for l in range(3)] for k in range(3)])
+    got = O.fisher_ste(model, num_probes=600, seed=5)
+    assert np.abs(got - got.T).max() < 1e-10
+    assert (np.abs(got - want) / np.maximum(np.abs(want), 1.0)).max() < 0.2
+    # Rademacher probes estimate the same matrix
+    got_r = O.fisher_ste(model, num_probes=600, seed=5, rademacher=True)
+    assert (np.abs(got_r - want) / np.maximum(np.abs(want), 1.0)).max() < 0.2
