@@ -4,6 +4,8 @@
 // scalar recurrences with Lanczos-tridiagonal capture, and the host<->device
 // layout conversions (column-major original order <-> row-major internal order).
 #include "blas1.cuh"
+
+#include <algorithm>
 #include "dgemm.cuh"
 
 namespace fsa {
@@ -442,7 +444,7 @@ void update_h_jacobi(double* H, const double* R, const double* dinv, const int* 
 // update_xr_dot for t <= 64 with contiguous row ranges per block, plus the column maxima
 // of |dinv[i] R[i][c]| per chunk of chunk_rows rows (atomicMax on the bit patterns of the
 // non-negative doubles: order independent), the exponents of the Ozaki projection
-__global__ void __launch_bounds__(256) k_xr_dot_max(double* __restrict__ X, double* __restrict__ R,
+__global__ void __launch_bounds__(256, 3) k_xr_dot_max(double* __restrict__ X, double* __restrict__ R,
                                                     const double* __restrict__ H, const double* __restrict__ V,
                                                     const double* __restrict__ alpha, long n, long ld, long t,
                                                     double* __restrict__ partial, const double* __restrict__ dinv,
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(256) k_xr_dot_max(double* __restrict__ X, doub
     m0 = m1 = 0.0;
   };
   long next = 0;  // first row of the chunk after `cur`
-  constexpr int kU = 4;  // rows per batch (loads of the batch are issued together)
+  constexpr int kU = 2;  // rows per batch (loads of the batch are issued together)
   for (long rbase = ra + warp; rbase < rb; rbase += 8 * kU) {
     double2 x[kU], rr[kU], h[kU], v[kU];
     double di[kU];
@@ -518,7 +520,7 @@ void update_xr_dot_max(double* X, double* R, const double* H, const double* V, c
                        long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
                        long chunk_rows, cudaStream_t s) {
   require(tp <= 64, "update_xr_dot_max: at most 64 columns");
-  const long nb = rowdot_blocks(n);
+  const long nb = std::min(rowdot_blocks(n), 3L * kNumSMs);  // one wave at 3 resident blocks per SM
   k_xr_dot_max<<<static_cast<unsigned>(nb), 256, 0, s>>>(X, R, H, V, alpha, n, tp, k, scratch, dinv, ymax, chunk_rows);
   FSA_LAUNCH_CHECK();
   colsum_partials(scratch, nb, k, k, rr, s);

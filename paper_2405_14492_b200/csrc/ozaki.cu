@@ -72,6 +72,29 @@ __device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[1
   }
 }
 
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+// drain16 for 8 columns (half the registers)
+__device__ __forceinline__ void drain8(uint32_t trow, int col0, double (&out)[8]) {
+  uint32_t v[kOzSlices][8];
+#pragma unroll
+  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * kOzCols + col0), v[dd]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const long long hi = (static_cast<long long>(static_cast<int>(v[0][c])) << 21) +
+                         (static_cast<long long>(static_cast<int>(v[1][c])) << 14) +
+                         (static_cast<long long>(static_cast<int>(v[2][c])) << 7) + static_cast<int>(v[3][c]);
+    const long long lo = (static_cast<long long>(static_cast<int>(v[4][c])) << 21) +
+                         (static_cast<long long>(static_cast<int>(v[5][c])) << 14) +
+                         (static_cast<long long>(static_cast<int>(v[6][c])) << 7) + static_cast<int>(v[7][c]);
+    out[c] = fma(static_cast<double>(hi), 0x1p-35, static_cast<double>(lo) * 0x1p-63);
+  }
+}
+
 // exponent e with |x| < 2^e for all x of a group whose max magnitude is mx (0 -> 0)
 __device__ __forceinline__ int group_exp(double mx) {
   int e = 0;
@@ -280,7 +303,8 @@ __global__ void __launch_bounds__(128, 1)
 constexpr int kXStages = 3;
 constexpr int kXLd = kOzCols + 1;  // odd stride: conflict-free row-per-lane access
 constexpr int kXSmem = kXStages * (kATile + kBTile) + 128 * kXLd * 8;
-__global__ void __launch_bounds__(192, 1)
+constexpr int kXEpi = 512;  // epilogue threads: four warps per TMEM lane quadrant, 16 columns each
+__global__ void __launch_bounds__(64 + kXEpi, 1)
     k_oz_expand(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int tiles, int mkb, OzEpi epi) {
   constexpr int kStages = kXStages;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -300,7 +324,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(&tfull, 1);
-    mbar_init(&tempty, 4);
+    mbar_init(&tempty, kXEpi / 32);
     mbar_init_fence();
   }
   tc_fence_before();
@@ -353,55 +377,68 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     __syncwarp();
-  } else {  // epilogue warps 2..5: TMEM lane quadrant q = warp % 4
-    const int q = warp & 3;
+  } else {  // epilogue warps 2..17: TMEM lane quadrant q = warp % 4, column group (warp - 2) / 4
+    const int q = warp & 3, gq = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const long tp = epi.tp;
+    const int et = tid - 64;  // 0 .. kXEpi - 1
     int lt = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const long r0 = static_cast<long>(t) * 128;
+      if (epi.mode == 1 || epi.mode == 3 || epi.mode == 4) {
+        // pull the tile's R rows (contiguous, 128 ld doubles) into L2 while the MMAs run, so the
+        // write-out below reads them at L2 latency
+        const char* rb = reinterpret_cast<const char*>(epi.R + r0 * epi.ld);
+        const int lines = static_cast<int>((128 * epi.ld * 8) / 128);
+        for (int li = et; li < lines; li += kXEpi)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + static_cast<long>(li) * 128));
+      }
       mbar_wait(&tfull, static_cast<uint32_t>(lt & 1));
       tc_fence_after();
-      const long r0 = static_cast<long>(t) * 128;
       const int ei = epi.erow[r0 + row];
 #pragma unroll 1
-      for (int g = 0; g < kOzCols / 16; ++g) {  // stage the tile's rows in shared memory
-        double y[16];
-        drain16(trow, g * 16, y);
+      for (int h8 = 0; h8 < 2; ++h8) {  // stage this warp's 16 columns in shared memory
+        const int c0 = gq * 16 + h8 * 8;
+        if (c0 >= tp) break;
+        double y[8];
+        drain8(trow, c0, y);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) tileY[row * kXLd + g * 16 + c] = y[c] * pow2(ei + epi.ecol[g * 16 + c]);
+        for (int c = 0; c < 8; ++c) tileY[row * kXLd + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty)) : "memory");
       // TMEM is free for the next tile already; coalesced copies of the staged rows
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");
       if (epi.mode == 4) {  // one thread per row: dots of the staged row with R and A2 rows
-        const int rr = tid - 64;
-        const long i = r0 + rr;
-        double s1 = 0.0, s2 = 0.0;
-        for (int c = 0; c < tp; ++c) {
-          const double yv = tileY[rr * kXLd + c];
-          s1 = fma(yv, __ldg(epi.R + i * epi.ld + c), s1);
-          s2 = fma(yv, __ldg(epi.A2 + i * epi.ld + c), s2);
+        if (et < 128) {
+          const long i = r0 + et;
+          double s1 = 0.0, s2 = 0.0;
+          for (int c = 0; c < tp; ++c) {
+            const double yv = tileY[et * kXLd + c];
+            s1 = fma(yv, __ldg(epi.R + i * epi.ld + c), s1);
+            s2 = fma(yv, __ldg(epi.A2 + i * epi.ld + c), s2);
+          }
+          epi.Z[i] = s1;
+          epi.Lw[i] = s2;
         }
-        epi.Z[i] = s1;
-        epi.Lw[i] = s2;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // tileY reused by the next tile
+        asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");  // tileY reused by the next tile
         continue;
       }
-      // thread (column c, row parity h): rows h, h + 2, ..., coalesced across c; loads are
+      // thread (column c, row phase h): rows h, h + 4, ..., coalesced across c; loads are
       // batched ahead of the stores (R and Dinv are read-only here)
-      const int et = tid - 64, c = et & 63, h = et >> 6;
+      constexpr int kPh = kXEpi / 64;  // row phases
+      const int c = et & 63, h = et >> 6;
       if (c < tp) {
         double sacc = 0.0;
         const long base = r0 * epi.ld + c;
 #pragma unroll 1
-        for (int rb = h; rb < 128; rb += 16) {
+        for (int rb = h; rb < 128; rb += 8 * kPh) {
           double x[8], di[8], lw[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int rr = rb + 2 * u;
+            const int rr = rb + kPh * u;
             lw[u] = tileY[rr * kXLd + c];
             if (epi.mode == 1) {
               x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
@@ -412,7 +449,7 @@ __global__ void __launch_bounds__(192, 1)
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const long off = base + static_cast<long>(rb + 2 * u) * epi.ld;
+            const long off = base + static_cast<long>(rb + kPh * u) * epi.ld;
             epi.Lw[off] = epi.mode == 3 ? x[u] - lw[u] : lw[u];
             if (epi.mode == 1) {
               const double z = (x[u] - lw[u]) * di[u];
@@ -424,11 +461,14 @@ __global__ void __launch_bounds__(192, 1)
         if (epi.mode == 1) tileY[h * kXLd + c] = sacc;  // (row h, column c) was read only by this thread
       }
       if (epi.mode == 1) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (h == 0 && c < tp)  // fixed order: even rows + odd rows
-          epi.part[static_cast<long>(t) * tp + c] = tileY[c] + tileY[kXLd + c];
+        asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");
+        if (h == 0 && c < tp) {  // fixed order over the row phases
+          double sum = tileY[c];
+          for (int ph = 1; ph < kPh; ++ph) sum += tileY[ph * kXLd + c];
+          epi.part[static_cast<long>(t) * tp + c] = sum;
+        }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // tileY reused by the next tile
+      asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");  // tileY reused by the next tile
     }
   }
   tc_fence_before();
@@ -886,7 +926,7 @@ void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
     attr = true;
   }
   const int grid = std::min(p.ptiles, kNumSMs);
-  k_oz_expand<<<grid, 192, kXSmem, s>>>(p.Ac.get(), p.Ws.get(), p.ptiles, p.mkb, epi);
+  k_oz_expand<<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), p.Ws.get(), p.ptiles, p.mkb, epi);
   FSA_LAUNCH_CHECK();
 }
 
