@@ -776,15 +776,30 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     cg_count(k, st, s);
   }
   FSA_CUDA(cudaStreamSynchronize(s));
-  auto check_err = [&]() {
-    const int e = ctx->host_flags[1];
+  auto check_err = [&](const volatile int* flags) {
+    const int e = flags[1];
     if (e == kErrOperatorNotPD) throw NumericalError("cg: operator is not positive definite");
     if (e == kErrPrecondNotPD) throw NumericalError("cg: preconditioner is not positive definite");
   };
-  check_err();
+  check_err(ctx->host_flags);
   int num_active = ctx->host_flags[0];
   CgResult res;
+  // The host reads each sweep's [num_active, err] one sweep late: sweep it + 1 is queued before
+  // the flags of sweep it are inspected, so the GPU never idles on the host round trip. Sweeps
+  // queued after every column converged are no-ops (alpha = beta = 0 and no tridiagonal push
+  // for inactive columns), so results and iteration counts are those of the synchronous loop.
+  // Flags are double-buffered in the mapped slots [2 (it % 2), 2 (it % 2) + 1].
+  cudaEvent_t sweep_ev[2] = {ctx->ev(), ctx->ev()};
+  int pending = -1;  // last queued sweep whose flags are unread
+  auto read_flags = [&](int sw) {
+    FSA_CUDA(cudaEventSynchronize(sweep_ev[sw & 1]));
+    const volatile int* f = ctx->host_flags + 2 * (sw & 1);
+    check_err(f);
+    num_active = f[0];
+    res.sweeps = sw + 1;
+  };
   for (int it = 0; it < maxit && num_active > 0; ++it) {
+    st.host_flags = ctx->host_flags_dev + 2 * (it & 1);
     if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
@@ -839,11 +854,20 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
       cg_count(k, st, s);
     }
-    FSA_CUDA(cudaStreamSynchronize(s));
-    check_err();
-    num_active = ctx->host_flags[0];
-    ++res.sweeps;
+    FSA_CUDA(cudaEventRecord(sweep_ev[it & 1], s));
+    if (pending >= 0) {
+      read_flags(pending);
+      if (num_active == 0) {  // sweep `it` was queued after convergence: a no-op
+        pending = -1;
+        break;
+      }
+    }
+    pending = it;
   }
+  if (pending >= 0) read_flags(pending);
+  FSA_CUDA(cudaStreamSynchronize(s));
+  ctx->pool.push_back(sweep_ev[0]);
+  ctx->pool.push_back(sweep_ev[1]);
   md->cols_hint = 0;
   if (num_active > 0 && opts.error_on_max_iter) throw NumericalError("cg: no convergence within max_iter");
   res.iterations.resize(static_cast<size_t>(k));
