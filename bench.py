@@ -404,8 +404,8 @@ def main():
     ozaki_on = tp_ <= 64
     sp = timers.get("spmm", {"units": 0.0, "count": 1})
     kernels = [
-        entry("spmm", "k_spmm_block (32-row groups, DMMA.8x8x4 fp64 block product)", "hbm",
-              sp["units"] / max(sp["count"], 1), 1e9, hbm, "GB/s", "k_spmm_block"),
+        entry("spmm", "k_spmm_rt (32-row groups, warp per 8-row tile, DMMA.8x8x4 fp64 block product)", "hbm",
+              sp["units"] / max(sp["count"], 1), 1e9, hbm, "GB/s", "k_spmm_rt"),
         entry("lowrank_expand", "k_oz_expand (tcgen05 kind::i8, Ozaki 8 digit planes)" if ozaki_on else
               "k_dgemm expand (DMMA fp64)", "hbm", 8.0 * mp_ * np_ + 24.0 * n_ * tp_, 1e9, hbm, "GB/s",
               "k_oz_expand"),
