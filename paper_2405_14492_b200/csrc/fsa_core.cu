@@ -671,10 +671,10 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   if (w.R.n < blk) {
     w.R.alloc(blk);
     w.V.alloc(blk);
-    w.Z.alloc(blk);
   }
-  const size_t ext_blk = static_cast<size_t>(md->n_ext_pad * tp);  // H carries the halo rows
+  const size_t ext_blk = static_cast<size_t>(md->n_ext_pad * tp);  // H and Z carry the halo rows
   if (w.H.n < ext_blk) w.H.alloc(ext_blk);
+  if (w.Z.n < ext_blk) w.Z.alloc(ext_blk);
   if (fused && w.Lw.n < blk) {
     w.Lw.alloc(blk);
     w.Vlr.alloc(blk);
@@ -711,6 +711,11 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   const double flops_mn = 2.0 * md->m * n * k;
   md->cols_hint = k;
 
+  // Fused direction update (block SpMM path): the SpMM of sweep i gathers Z_{i-1} instead of
+  // H_i and forms, on its own rows, H_i = Z + beta H and V_i = (Lw + Sigma_s Z) + beta V_{i-1}
+  // (= U^T U H_i + Sigma_s H_i by linearity), so no separate H / Vlr pass runs
+  const bool fuse_h = fused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp) && !md->use_ozaki_spmm(tp);
+  bool first_sweep = true;
   // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
   const bool oz = fused && md->use_ozaki(tp);
   if (oz) md->ensure_ozaki();
@@ -770,9 +775,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     cg_start_rz(rz, k, st, s);
     if (jfused)
       update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, true, s);
-    else
+    else if (!fuse_h)
       init_h(w.H.get(), w.Z.get(), st.active, np, tp, k, s);
-    if (fused) init_h(w.Vlr.get(), w.Lw.get(), st.active, np, tp, k, s);  // U^T U H_0 = U^T w_0
+    if (fused && !fuse_h) init_h(w.Vlr.get(), w.Lw.get(), st.active, np, tp, k, s);  // U^T U H_0 = U^T w_0
     cg_count(k, st, s);
   }
   FSA_CUDA(cudaStreamSynchronize(s));
@@ -800,7 +805,14 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   };
   for (int it = 0; it < maxit && num_active > 0; ++it) {
     st.host_flags = ctx->host_flags_dev + 2 * (it & 1);
-    if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
+    if (fuse_h) {  // H = Z + beta H, V = (Lw + Sigma_s Z) + beta V; h.v
+      md->halo_exchange(w.Z.get(), tp);
+      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + Z, Lw read + V write
+      spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
+                       w.H.get(), st.beta, k, first_sweep, s);
+      first_sweep = false;
+      comm.allreduce(hv, tp, s);
+    } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
       md->halo_exchange(w.H.get(), tp);
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
       if (oz_spmm)
@@ -846,12 +858,15 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     {
       KTimer t(ctx, "cg_blas1");
       cg_beta(rz, k, st, s);
-      if (fused)  // H = Z + beta H, Vlr = U^T w + beta Vlr
+      if (fuse_h) {
+        // H and V are updated by the next sweep's SpMM
+      } else if (fused) {  // H = Z + beta H, Vlr = U^T w + beta Vlr
         update_h2(w.H.get(), w.Z.get(), w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);
-      else if (jfused)  // H = D^{-1} R + beta H
+      } else if (jfused) {  // H = D^{-1} R + beta H
         update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, false, s);
-      else
+      } else {
         update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
+      }
       cg_count(k, st, s);
     }
     FSA_CUDA(cudaEventRecord(sweep_ev[it & 1], s));

@@ -279,6 +279,12 @@ struct TileSpmmArgs {
   const double* Y0;
   double* partial;
   long ldp;
+  // fused H update (spmm_block_dot_h): X holds Z, Y0 holds Lw and, unless `first`,
+  // H = Z + beta H and V = (Lw + S Z) + beta V on the own rows (beta[j], j < kb; 0 beyond)
+  double* Hio = nullptr;
+  const double* beta = nullptr;
+  long kb = 0;
+  int first = 0;
 };
 // k_spmm_rt: warp w owns row tile w (8 rows) of the group and all NT n-tiles, so a k-step
 // costs one warp-uniform test of its mask bit, one A fragment and NT B fragments for NT
@@ -387,8 +393,21 @@ __global__ void __launch_bounds__(128, 8) k_spmm_rt(TileSpmmArgs q) {
         o.x += y0.x;
         o.y += y0.y;
       }
+      double2 h = *reinterpret_cast<const double2*>(X + row * q.ldx + cc);
+      if (q.Hio != nullptr) {  // H = Z + beta H (krylov.cpp:92), V = (Lw + S Z) + beta V
+        double2* hp = reinterpret_cast<double2*>(q.Hio + c0 + row * q.ldy + cc);
+        if (!q.first) {
+          const long gc = c0 + cc;
+          const double b0 = gc < q.kb ? q.beta[gc] : 0.0, b1 = gc + 1 < q.kb ? q.beta[gc + 1] : 0.0;
+          const double2 ho = *hp, vo = *reinterpret_cast<const double2*>(Y + row * q.ldy + cc);
+          h.x = h.x + b0 * ho.x;
+          h.y = h.y + b1 * ho.y;
+          o.x += b0 * vo.x;
+          o.y += b1 * vo.y;
+        }
+        *hp = h;
+      }
       *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
-      const double2 h = *reinterpret_cast<const double2*>(X + row * q.ldx + cc);
       d0 = h.x * o.x;
       d1 = h.y * o.y;
     }
@@ -652,6 +671,11 @@ bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
 // Y = S X (+ Y0) over ncols (multiple of 8) columns in 64-column tiles; dot[c] = sum_r X[r][c] Y[r][c]
 void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                     double* dot, double* partial, const double* Y0, cudaStream_t s) {
+  spmm_block_dot_h(pat, gval, X, ldx, Y, ldy, ncols, dot, partial, Y0, nullptr, nullptr, 0, false, s);
+}
+void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
+                      double* dot, double* partial, const double* Y0, double* H, const double* beta, long kb,
+                      bool first, cudaStream_t s) {
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
   auto launch = [&](int nt, long c_first, long tiles) {
@@ -659,7 +683,8 @@ void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ld
     const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
     TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
                    X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
-                   partial + c_first, ncols};
+                   partial + c_first, ncols, H != nullptr ? H + c_first : nullptr,
+                   beta != nullptr ? beta + c_first : nullptr, kb - c_first, first ? 1 : 0};
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

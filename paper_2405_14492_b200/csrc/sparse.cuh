@@ -34,6 +34,12 @@ long spmm_group_blocks(long ngrp);
 bool spmm_block_supported(long ncols);
 void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                     double* dot, double* partial, const double* Y0, cudaStream_t s);
+// the same with the PCG direction update folded in (fused FITC sweep): X = Z (gathered), Y0 = Lw,
+// and on the own rows H = Z + beta H, Y = (Lw + S Z) + beta Y (first sweep: H = Z, Y = Lw + S Z);
+// dot[c] = sum_r H[r][c] Y[r][c]
+void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
+                      double* dot, double* partial, const double* Y0, double* H, const double* beta, long kb,
+                      bool first, cudaStream_t s);
 // (Y0, when given, replaces Y as the beta term: Y = alpha S X + beta Y0)
 void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
               long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
