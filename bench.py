@@ -47,7 +47,7 @@ CONFIGS = {
 METRIC = "PCG RHS-iterations/s over FSA loglik+grad evaluations"
 
 
-def make_inputs(cfg, fsa):
+def make_inputs(cfg, fsa, device_kmeans=True):
     n, m = cfg["n"], cfg["m"]
     if cfg["points"] == "uniform":
         coords = fsa.uniform_locations(n, 2, 1)
@@ -58,7 +58,8 @@ def make_inputs(cfg, fsa):
     if cfg["inducing"] == "random":
         ind = fsa.select_random(coords, m, 2)
     else:
-        ind = fsa.select_kmeanspp(coords, m, 2)
+        # device k-means++ (the same inducing set as the host restatement's, which the CPU arm uses)
+        ind = fsa.select_kmeanspp(coords, m, 2, device=device_kmeans)
     y = fsa.simulate_rff(coords, cfg["nu"], cfg["s12"], cfg["rho"], cfg["s2"], 1024, 3)
     return coords, ind, gamma, y
 
@@ -188,7 +189,7 @@ def run_reference(args, cfg):
         return
     from paper_2405_14492_b200 import fsa
 
-    coords, ind, gamma, y = make_inputs(cfg, fsa)
+    coords, ind, gamma, y = make_inputs(cfg, fsa, device_kmeans=False)  # host input generators only
     if gamma is None:
         gamma = fsa.gamma_for_avg_row_nnz(cfg["n"], cfg["nnz"])
     vals = []

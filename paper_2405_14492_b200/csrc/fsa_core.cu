@@ -718,7 +718,10 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   bool first_sweep = true;
   // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
   const bool oz = fused && md->use_ozaki(tp);
-  if (oz) md->ensure_ozaki();
+  // wider blocks (config 4: t = 65 -> t_pad = 72): full 64-column blocks on the INT8 tensor
+  // cores, the remainder on DMMA; the dense passes stream the U planes once per 64 columns
+  const bool oz_split = fused && !oz && md->ctx->gemm_mode != 1 && tp > kOzCols;
+  if (oz || oz_split) md->ensure_ozaki();
   const bool oz_spmm = oz && md->use_ozaki_spmm(tp);
   if (oz_spmm) md->ensure_ozaki_spmm();
   bool ymax_ready = false;
@@ -737,6 +740,25 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
           comm.allreduce(S, mp * tp, s);
         }
         ymax_ready = false;
+      } else if (oz_split) {
+        {
+          KTimer t(ctx, "lowrank_project", 2.0 * md->m * n * k);
+          for (long c0 = 0; c0 < tp; c0 += kOzCols) {
+            const long wd = std::min<long>(kOzCols, tp - c0);
+            if (wd == kOzCols) {
+              ozaki_project(md->oz, w.R.get() + c0, tp, wd, md->Dinv.get(), S + c0, s, false);
+            } else {
+              const size_t need = gemm_reduce_scratch(mp, wd, np);
+              if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+              gemm_reduce(md->U.get(), mp, mp, np, w.R.get() + c0, tp, wd, md->Dinv.get(), S + c0, tp, 1.0, 0.0,
+                          md->red_scratch.get(), s);
+            }
+          }
+        }
+        if (md->world() > 1) {
+          KTimer t(ctx, "allreduce");
+          comm.allreduce(S, mp * tp, s);
+        }
       } else {
         md->project(md->U.get(), w.R.get(), tp, S, md->Dinv.get());
       }
@@ -747,9 +769,19 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         gemm_reduce(fitc->Qinv.get(), mp, mp, mp, S, tp, tp, nullptr, W, tp, 1.0, 0.0, md->red_scratch.get(), s);
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
-      if (md->use_ozaki(tp))
+      if (md->use_ozaki(tp)) {
         ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
-      else
+      } else if (oz_split) {
+        for (long c0 = 0; c0 < tp; c0 += kOzCols) {
+          const long wd = std::min<long>(kOzCols, tp - c0);
+          if (wd == kOzCols)
+            ozaki_expand_keep(md->oz, W + c0, tp, wd, w.Z.get() + c0, w.Lw.get() + c0, w.R.get() + c0,
+                              md->Dinv.get(), rzout + c0, part, s);
+          else
+            gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W + c0, tp, wd, w.Z.get() + c0, w.Lw.get() + c0,
+                                      w.R.get() + c0, tp, md->Dinv.get(), rzout + c0, part, s);
+        }
+      } else
         gemm_expand_woodbury_keep(md->U.get(), mp, np, mp, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), tp,
                                   md->Dinv.get(), rzout, part, s);
       comm.allreduce(rzout, tp, s);
@@ -807,7 +839,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     st.host_flags = ctx->host_flags_dev + 2 * (it & 1);
     if (fuse_h) {  // H = Z + beta H, V = (Lw + Sigma_s Z) + beta V; h.v
       md->halo_exchange(w.Z.get(), tp);
-      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + Z, Lw read + V write
+      // CSR + Z (once per row), Lw, H, V read + H, V write
+      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 48.0 * n * k);
       spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
                        w.H.get(), st.beta, k, first_sweep, s);
       first_sweep = false;
