@@ -291,8 +291,8 @@ struct TileSpmmArgs {
 // independent DMMAs (no per-mask dispatch, no discarded n-tiles: 12 % faster at config 2 than
 // warps that share the four row tiles). The h.v column partials of the four row tiles meet in
 // shared memory in a fixed order.
-template <int NT, int P>
-__global__ void __launch_bounds__(128, 8) k_spmm_rt(TileSpmmArgs q) {
+template <int NT, int P, int MINB = 8>
+__global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
   static_assert(kGroup == 32 && P % 4 == 0, "four row tiles per group");
   constexpr int WN = 4;
   const long c0 = 64L * blockIdx.y;  // column tile: columns [c0, c0 + 8 NT)
@@ -325,11 +325,12 @@ __global__ void __launch_bounds__(128, 8) k_spmm_rt(TileSpmmArgs q) {
     double* hs = sm + (pc & 1) * HS;
     double* as = sm + 2 * HS + (pc & 1) * AS;
     const int ua = pc * P, nr = min(P, up - ua);
-    if (lane < CH) {
+#pragma unroll
+    for (int ch = lane; ch < CH; ch += 32) {  // CH = 4 NT chunks of 16 bytes per row
 #pragma unroll
       for (int i = 0; i < RW; ++i) {
         const int u = warp + WN * i;
-        if (u < nr) cp_async16(hs + u * LDH + lane * 2, X + static_cast<long>(gc[i]) * q.ldx + lane * 2);
+        if (u < nr) cp_async16(hs + u * LDH + ch * 2, X + static_cast<long>(gc[i]) * q.ldx + ch * 2);
       }
     }
     const int nt = __popc(pm.y & static_cast<int>((1ull << nr) - 1ull));
@@ -698,13 +699,18 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       case 5: go(k_spmm_rt<5, kPiece>); break;
       case 6: go(k_spmm_rt<6, kPiece>); break;
       case 7: go(k_spmm_rt<7, kPiece>); break;
-      default: go(k_spmm_rt<8, kPiece>); break;
+      case 8: go(k_spmm_rt<8, kPiece>); break;
+      default: go(k_spmm_rt<9, kPiece, 6>); break;  // 72 columns (t = 65) in one pass
     }
     FSA_LAUNCH_CHECK();
   };
-  const long full = ncols / 64, rem = ncols % 64;
-  if (full > 0) launch(8, 0, full);
-  if (rem > 0) launch(static_cast<int>(rem / 8), full * 64, 1);
+  if (ncols == 72) {  // one 9-n-tile pass instead of 64 + 8 columns (the RHS rows are gathered once)
+    launch(9, 0, 1);
+  } else {
+    const long full = ncols / 64, rem = ncols % 64;
+    if (full > 0) launch(8, 0, full);
+    if (rem > 0) launch(static_cast<int>(rem / 8), full * 64, 1);
+  }
   colsum_partials(partial, pat.ngrp, ncols, ncols, dot, s);
 }
 
