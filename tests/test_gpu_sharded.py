@@ -171,3 +171,21 @@ def test_replicated_prediction_shards_probe_batches(cv):
         np.testing.assert_allclose(o["se"], one["se"], rtol=1e-9, atol=1e-14)
         np.testing.assert_allclose(o["mean"], one["mean"], rtol=1e-13, atol=1e-14)
         assert o["cg_iterations"] == one["cg_iterations"]
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_fisher_matches_single(P):
+    # fisher_ste (fsa.cpp:284-301) over row blocks: the probe rows, halo exchanges and the
+    # summed 3 x 3 dots give the single-rank matrix
+    locs, ind, kw, y, X = problem(3000, 60, 0.05, 23, p=0)
+
+    def fisher_on(ctx):
+        g = fsa.Geometry(locs, kw["gamma"], ctx=ctx)
+        md = fsa.FsaModel.assemble(None, ind, geometry=g, **kw)
+        Pc = fsa.make_preconditioner(md, "fitc")
+        return fsa.fisher_ste(md, num_probes=6, seed=3, P=Pc, tol=1e-10)
+
+    want = fisher_on(fsa.Context(0))
+    got = run_ranks(fsa.Context.group(0, P), lambda r, c: fisher_on(c))
+    for F in got:
+        assert np.abs(F - want).max() <= 1e-8 * np.abs(want).max()
