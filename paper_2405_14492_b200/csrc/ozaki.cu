@@ -387,12 +387,12 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
       const long r0 = static_cast<long>(t) * 128;
       if (epi.mode == 1 || epi.mode == 3 || epi.mode == 4) {
-        // pull the tile's R rows (contiguous, 128 ld doubles) into L2 while the MMAs run, so the
-        // write-out below reads them at L2 latency
+        // pull the tile's R entries (128 rows x tp columns, row stride ld) into L2 while the MMAs
+        // run, so the write-out below reads them at L2 latency
         const char* rb = reinterpret_cast<const char*>(epi.R + r0 * epi.ld);
-        const int lines = static_cast<int>((128 * epi.ld * 8) / 128);
-        for (int li = et; li < lines; li += kXEpi)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + static_cast<long>(li) * 128));
+        const int lpr = static_cast<int>((tp * 8 + 127) / 128);  // 128-byte lines per row
+        for (int li = et; li < 128 * lpr; li += kXEpi)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + (li / lpr) * epi.ld * 8 + (li % lpr) * 128));
       }
       mbar_wait(&tfull, static_cast<uint32_t>(lt & 1));
       tc_fence_after();
