@@ -46,7 +46,11 @@ void probe_rademacher(unsigned long long seed, unsigned long long i, long n, dou
 // ---- context ------------------------------------------------------------------------------
 Context::Context(int dev) : device(dev) {
   FSA_CUDA(cudaSetDevice(dev));
-  FSA_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {  // the main stream outranks the side stream (the rho-derivative build fills idle SMs only)
+    int least = 0, greatest = 0;
+    FSA_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    FSA_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
+  }
   alloc_stream() = stream;
   cudaMemPool_t pool = nullptr;
   FSA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -74,7 +78,16 @@ Context::Context(int dev) : device(dev) {
   FSA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_flags_dev), host_flags, 0));
   if (const char* g = std::getenv("FSA_GEMM")) gemm_mode = std::strcmp(g, "dmma") == 0 ? 1 : (std::strcmp(g, "ozaki") == 0 ? 2 : 0);
 }
+cudaStream_t Context::side_stream() {
+  if (side == nullptr) {
+    int least = 0, greatest = 0;
+    FSA_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    FSA_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
+  }
+  return side;
+}
 Context::~Context() {
+  if (side) cudaStreamSynchronize(side);
   cudaStreamSynchronize(stream);
   cgw.reset();
   cudaStreamSynchronize(stream);
@@ -85,6 +98,7 @@ Context::~Context() {
   }
   for (auto e : pool) cudaEventDestroy(e);
   if (host_flags) cudaFreeHost(host_flags);
+  if (side) cudaStreamDestroy(side);
   if (stream) cudaStreamDestroy(stream);
 }
 cudaEvent_t Context::ev() {
@@ -114,7 +128,7 @@ void Context::flush_timers() {
 void Context::sync() { FSA_CUDA(cudaStreamSynchronize(stream)); }
 
 KTimer::KTimer(Context* ctx, const char* name, double units) : c(ctx) {
-  if (!c->profile) return;
+  if (c == nullptr || !c->profile) return;
   Context::Rec r{name, c->ev(), c->ev(), units};
   FSA_CUDA(cudaEventRecord(r.a, c->stream));
   c->pending.push_back(r);
@@ -155,9 +169,9 @@ std::shared_ptr<Geometry> make_geometry(Context* ctx, const double* coords, long
 
 // Matern (mode 0) or its rho derivative (mode 1) between the inducing points and the
 // extended point set (owned rows, zero padding, halo points): column-per-point m_pad x n_ext_pad
-void Model::cross_cov_ext(int mode, double* out) {
+void Model::cross_cov_ext(int mode, double* out, cudaStream_t s) {
   const ShardPlan& sp = geo->shard;
-  cudaStream_t s = ctx->stream;
+  if (s == nullptr) s = ctx->stream;
   launch_cross_cov(ind.get(), m, m, geo->coords_ext(), n_ext_pad, n, n_pad, d, P.nu, P.sigma1_2, P.rho, mode, out,
                    m_pad, s);
   if (n_ext_pad > n_pad)
@@ -333,30 +347,77 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   return md;
 }
 
-void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
-  if (have_rho) return;
-  cudaStream_t s = ctx->stream;
-  const long mp = m_pad, np = n_pad;
+// The rho-derivative blocks (fsa.cpp:101-124 in U-form) are needed only by the gradient, so
+// make_preconditioner starts them on the context's side stream (start_rho_derivs): they run
+// during the PCG sweeps, filling the SMs the sweep kernels leave idle (wave tails, the small
+// control kernels). Every consumer calls ensure_rho_derivs, which joins the side stream. The
+// side-stream build allocates and frees on the side stream and touches no scratch shared with
+// the main stream (own TRSM scratch; the T product on DMMA rather than through the Ozaki plan's
+// W-plane buffers, which the sweep's expansions use).
+void Model::ensure_rho_derivs() {
+  if (have_rho) {
+    if (rho_pending) {
+      FSA_CUDA(cudaStreamWaitEvent(ctx->stream, rho_done, 0));
+      rho_pending = false;
+    }
+    return;
+  }
   KTimer t(ctx, "setup_rho_derivs");
+  build_rho_derivs(ctx->stream, dinv_scratch.get(), false);
+  have_rho = true;
+}
+
+void Model::start_rho_derivs() {
+  if (have_rho) return;
+  cudaStream_t side = ctx->side_stream();
+  cudaEvent_t go = ctx->ev();
+  FSA_CUDA(cudaEventRecord(go, ctx->stream));
+  FSA_CUDA(cudaStreamWaitEvent(side, go, 0));
+  ctx->pool.push_back(go);
+  cudaStream_t saved = alloc_stream();
+  alloc_stream() = side;  // allocations and frees of the build are ordered on the side stream
+  try {
+    rho_scratch.alloc(m_pad * 64);
+    build_rho_derivs(side, rho_scratch.get(), true);
+  } catch (...) {
+    alloc_stream() = saved;
+    throw;
+  }
+  alloc_stream() = saved;
+  if (rho_done == nullptr) rho_done = ctx->ev();
+  FSA_CUDA(cudaEventRecord(rho_done, side));
+  have_rho = true;
+  rho_pending = true;
+}
+
+Model::~Model() {
+  if (rho_pending) cudaStreamWaitEvent(ctx->stream, rho_done, 0);  // frees below are ordered after the build
+  if (rho_done != nullptr) ctx->pool.push_back(rho_done);
+}
+
+void Model::build_rho_derivs(cudaStream_t s, double* trsm_scratch, bool side) {
+  const long mp = m_pad, np = n_pad;
   // K2 = L^{-1} dSigma_m/drho L^{-T}
   K2.alloc(mp * mp);
-  DBuf<double> tmp(mp * mp);
-  launch_sigma_m(ind.get(), m, m, mp, d, P.nu, P.sigma1_2, P.rho, 0.0, 1, tmp.get(), s);
-  trsm_lower_cols(L.get(), mp, tmp.get(), mp, mp, dinv_scratch.get(), s);  // X = L^{-1} dSm
-  launch_transpose(tmp.get(), mp, mp, mp, K2.get(), mp, s);
-  trsm_lower_cols(L.get(), mp, K2.get(), mp, mp, dinv_scratch.get(), s);   // L^{-1} X^T
+  {
+    DBuf<double> tmp(mp * mp);
+    launch_sigma_m(ind.get(), m, m, mp, d, P.nu, P.sigma1_2, P.rho, 0.0, 1, tmp.get(), s);
+    trsm_lower_cols(L.get(), mp, tmp.get(), mp, mp, trsm_scratch, s);  // X = L^{-1} dSm
+    launch_transpose(tmp.get(), mp, mp, mp, K2.get(), mp, s);
+  }
+  trsm_lower_cols(L.get(), mp, K2.get(), mp, mp, trsm_scratch, s);   // L^{-1} X^T
   // U1 = L^{-1} dSigma_mn/drho ; T = U1 - K2 U
   const long ne = n_ext_pad;
   U1.alloc(mp * ne);
   T.alloc(mp * ne);
-  cross_cov_ext(1, U1.get());
+  cross_cov_ext(1, U1.get(), s);
   {
-    KTimer t1(ctx, "rho_trsm", 1.0 * mp * mp * ne);
-    trsm_lower_cols(L.get(), mp, U1.get(), mp, ne, dinv_scratch.get(), s);
+    KTimer t1(side ? nullptr : ctx, "rho_trsm", 1.0 * mp * mp * ne);
+    trsm_lower_cols(L.get(), mp, U1.get(), mp, ne, trsm_scratch, s);
   }
   {
-    KTimer t2(ctx, "rho_T_gemm", 2.0 * m * m * n);
-    if (ctx->gemm_mode != 1 && ne == np) {  // INT8 tensor cores, 64-column tiles of K2
+    KTimer t2(side ? nullptr : ctx, "rho_T_gemm", 2.0 * m * m * n);
+    if (!side && ctx->gemm_mode != 1 && ne == np) {  // INT8 tensor cores, 64-column tiles of K2
       ensure_ozaki();
       ozaki_expand_sub(oz, K2.get(), mp, U1.get(), T.get(), mp, s);
     } else {
@@ -368,7 +429,7 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   dsval.alloc(pat.nnz > 0 ? pat.nnz : 1);
   SddmmParams sp{P.nu, P.family, P.sigma2, P.sigma1_2, P.rho, P.gamma};
   {
-    KTimer t3(ctx, "rho_sddmm", 4.0 * m * pat.nnz / 2);
+    KTimer t3(side ? nullptr : ctx, "rho_sddmm", 4.0 * m * pat.nnz / 2);
     if (pat.gnnz > 0 && mp % 32 == 0) {  // dense Gram blocks of the row groups on DMMA
       DBuf<double> gtmp(static_cast<size_t>(pat.gnnz * kGroup));
       sddmm_block(1, U.get(), U1.get(), T.get(), mp, mp, pat, lowrank.get(), sp, dsval.get(), nullptr, nullptr,
@@ -381,7 +442,6 @@ void Model::ensure_rho_derivs() {  // fsa.cpp:101-124 in U-form
   extract_diag(dsval.get(), pat.diagpos.get(), n, np, dD.get(), nullptr, nullptr, s);
   // padding rows of dD must be zero (extract_diag writes 1)
   affine_vec(dD.get(), dD.get(), 0.0, 1.0, n, np, s);
-  have_rho = true;
 }
 
 void Model::sigma_s_mat(const double* H, double* V, long tp, double alpha, double beta) {
@@ -452,7 +512,7 @@ DiagPrecond::DiagPrecond(Model* m, bool d) : md(m), derivs(d) {
   sum_log(md->D.get(), md->n, out.get(), md->ctx->stream);
   FSA_CUDA(cudaMemcpyAsync(&ld, out.get(), sizeof(double), cudaMemcpyDeviceToHost, md->ctx->stream));
   md->ctx->sync();
-  if (derivs) md->ensure_rho_derivs();
+  if (derivs) md->start_rho_derivs();
 }
 void DiagPrecond::solve(const double* R, double* Z, long tp) {
   scale_rows(Z, R, md->Dinv.get(), md->n_pad, tp, md->ctx->stream);
@@ -512,7 +572,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     logdetQ = hs[0];
     ld = hs[0] + hs[1];  // logdet(core) - logdet(Sigma_m) + sum log d   (preconditioners.cpp:53-55)
   }
-  if (derivs) md->ensure_rho_derivs();
+  if (derivs) md->start_rho_derivs();
 }
 
 // P^{-1} R = D^{-1} R - D^{-1} U^T Q^{-1} U D^{-1} R   (preconditioners.cpp:58-67)

@@ -59,6 +59,8 @@ struct Context {
   bool row_sharded() const { return shard_rows && comm->size() > 1; }
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // second stream (rho-derivative build during the PCG), lazily created
+  cudaStream_t side_stream();
   int* host_flags = nullptr;  // pinned, mapped
   int* host_flags_dev = nullptr;
   bool profile = false;
@@ -156,7 +158,15 @@ class Model {
 
   static std::unique_ptr<Model> assemble(Context* ctx, std::shared_ptr<Geometry> geo, const double* inducing, long m,
                                          const Params& p);
+  // rho-derivative blocks: built synchronously on first use, or started on the side stream by
+  // start_rho_derivs and joined by the next ensure_rho_derivs
   void ensure_rho_derivs();
+  void start_rho_derivs();
+  void build_rho_derivs(cudaStream_t s, double* trsm_scratch, bool side);
+  bool rho_pending = false;
+  cudaEvent_t rho_done = nullptr;
+  DBuf<double> rho_scratch;
+  ~Model();
   // device, internal layout (row-major n_pad x tp)
   void matmat(const double* H, double* V, long tp);
   void sigma_s_mat(const double* H, double* V, long tp, double alpha = 1.0, double beta = 0.0);
@@ -168,7 +178,7 @@ class Model {
   double* mt_buf(int which, long tp);
   // refresh the halo rows [n_pad, n_pad + n_halo) of an extended block (no-op on one rank)
   void halo_exchange(double* X, long tp);
-  void cross_cov_ext(int mode, double* out);
+  void cross_cov_ext(int mode, double* out, cudaStream_t s = nullptr);
   int world() const { return rcomm->size(); }
   Comm* rcomm = nullptr;  // sums over the row blocks: ctx->comm when row-sharded, else a no-op
   DBuf<double> halo_send;
