@@ -213,9 +213,37 @@ double* Model::mt_buf(int which, long tp) {
 }
 
 void Model::ensure_ozaki() {
+  if (oz_pending) {
+    FSA_CUDA(cudaStreamWaitEvent(ctx->stream, oz_done, 0));
+    oz_pending = false;
+  }
   if (oz.ready && oz.U == U.get()) return;
   KTimer t(ctx, "ozaki_prepare", 16.0 * m_pad * n_pad);
   ozaki_prepare(oz, U.get(), m_pad, n_pad, ctx->stream);
+}
+
+// The digit planes depend on U only: started on the side stream as soon as U exists, they are
+// built while the main stream runs the Sigma_s SDDMM and the FITC core (SYRK, the latency-bound
+// Cholesky panels); ensure_ozaki joins. The plan's per-call B-side buffers are only allocated here.
+void Model::start_ozaki() {
+  if (ctx->gemm_mode == 1 || (oz.ready && oz.U == U.get())) return;
+  cudaStream_t side = ctx->side_stream();
+  cudaEvent_t go = ctx->ev();
+  FSA_CUDA(cudaEventRecord(go, ctx->stream));
+  FSA_CUDA(cudaStreamWaitEvent(side, go, 0));
+  ctx->pool.push_back(go);
+  cudaStream_t saved = alloc_stream();
+  alloc_stream() = side;
+  try {
+    ozaki_prepare(oz, U.get(), m_pad, n_pad, side);
+  } catch (...) {
+    alloc_stream() = saved;
+    throw;
+  }
+  alloc_stream() = saved;
+  if (oz_done == nullptr) oz_done = ctx->ev();
+  FSA_CUDA(cudaEventRecord(oz_done, side));
+  oz_pending = true;
 }
 
 bool Model::use_ozaki_spmm(long tp) const {
@@ -312,6 +340,7 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
     trsm_lower_cols(M.L.get(), mp, M.U.get(), mp, ne, M.dinv_scratch.get(), s);
   }
   colnorm2(M.U.get(), mp, mp, M.n, np, M.lowrank.get(), s);
+  M.start_ozaki();  // INT8 digit planes of U on the side stream, under the SDDMM / FITC build
   // Sigma_s on the taper pattern (fsa.cpp:37-56)
   const Csr& pat = geo->pat;
   M.sval.alloc(pat.nnz > 0 ? pat.nnz : 1);
@@ -391,8 +420,11 @@ void Model::start_rho_derivs() {
 }
 
 Model::~Model() {
-  if (rho_pending) cudaStreamWaitEvent(ctx->stream, rho_done, 0);  // frees below are ordered after the build
+  // frees below are ordered after the side-stream builds
+  if (rho_pending) cudaStreamWaitEvent(ctx->stream, rho_done, 0);
+  if (oz_pending) cudaStreamWaitEvent(ctx->stream, oz_done, 0);
   if (rho_done != nullptr) ctx->pool.push_back(rho_done);
+  if (oz_done != nullptr) ctx->pool.push_back(oz_done);
 }
 
 void Model::build_rho_derivs(cudaStream_t s, double* trsm_scratch, bool side) {

@@ -186,6 +186,9 @@ class Model {
   OzakiPlan oz;
   bool use_ozaki(long tp) const { return ctx->gemm_mode != 1 && ozaki_supported(tp); }
   void ensure_ozaki();
+  void start_ozaki();
+  bool oz_pending = false;
+  cudaEvent_t oz_done = nullptr;
   // INT8 tensor-core SpMM planes of Sigma_s (built lazily per parameter set)
   OzakiSpmm ozs;
   bool use_ozaki_spmm(long tp) const;
