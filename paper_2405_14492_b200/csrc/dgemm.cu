@@ -262,4 +262,68 @@ void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, 
   FSA_LAUNCH_CHECK();
 }
 
+
+// ---- core solve of the fused FITC sweep: W = Qinv S (Qinv symmetric m_pad x m_pad, S and W
+// m_pad x ld row-major, ld = 8 NT <= 72). One CTA per 8 rows of W, its eight warps splitting K
+// (m_pad / 8 each) on DMMA m8n8k4 with operands read through L1 (Qinv rows are its columns:
+// contiguous), then the warps' 8 x ld partials are added in a fixed order. One launch, no
+// split-K scratch in HBM.
+namespace {
+template <int NT>
+__global__ void __launch_bounds__(256) k_core_dmma(const double* __restrict__ Qinv, long mp,
+                                                  const double* __restrict__ S, long ld,
+                                                  double* __restrict__ W) {
+  __shared__ double red[8][8][NT * 8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long r0 = static_cast<long>(blockIdx.x) * 8;
+  const long kper = mp / 8, k0 = warp * kper;
+  double c[NT][2];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
+  const double* ap = Qinv + (r0 + (lane >> 2)) * mp + (lane & 3);  // A[m = lane / 4][k = lane % 4]
+  const double* bp = S + static_cast<long>(lane & 3) * ld + (lane >> 2);  // B[k = lane % 4][n = lane / 4]
+#pragma unroll 4
+  for (long k = k0; k < k0 + kper; k += 4) {
+    const double a = __ldg(ap + k);
+    double b[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) b[j] = __ldg(bp + k * ld + j * 8);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma8x8x4(c[j][0], c[j][1], a, b[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    red[warp][lane >> 2][j * 8 + 2 * (lane & 3)] = c[j][0];
+    red[warp][lane >> 2][j * 8 + 2 * (lane & 3) + 1] = c[j][1];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 8 * NT * 8; idx += blockDim.x) {
+    const int r = idx / (NT * 8), cc = idx % (NT * 8);
+    double acc = red[0][r][cc];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) acc += red[w][r][cc];
+    W[(r0 + r) * ld + cc] = acc;
+  }
+}
+}  // namespace
+
+bool core_apply_supported(long mp, long ld) { return mp % 32 == 0 && ld % 8 == 0 && ld <= 72; }
+
+void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s) {
+  require(core_apply_supported(mp, ld), "core_apply: unsupported shape");
+  const unsigned grid = static_cast<unsigned>(mp / 8);
+  switch (ld / 8) {
+    case 1: k_core_dmma<1><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 2: k_core_dmma<2><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 3: k_core_dmma<3><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 4: k_core_dmma<4><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 5: k_core_dmma<5><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 6: k_core_dmma<6><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 7: k_core_dmma<7><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 8: k_core_dmma<8><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    default: k_core_dmma<9><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+  }
+  FSA_LAUNCH_CHECK();
+}
+
 }  // namespace fsa

@@ -325,4 +325,9 @@ void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, lo
 void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, double* out, long ldo, double alpha,
                double* scratch, cudaStream_t s);
 
+// W = Qinv S for the fused FITC sweep (Qinv symmetric m_pad x m_pad; S, W m_pad x ld row-major,
+// ld a multiple of 8, <= 72): one launch of DMMA tiles with an in-CTA split of K
+bool core_apply_supported(long mp, long ld);
+void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s);
+
 }  // namespace fsa

@@ -856,9 +856,13 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       }
       {
         KTimer t(ctx, "core_solve", 2.0 * md->m * md->m * k);
-        const size_t need = gemm_reduce_scratch(mp, tp, mp);
-        if (md->red_scratch.n < need) md->red_scratch.alloc(need);
-        gemm_reduce(fitc->Qinv.get(), mp, mp, mp, S, tp, tp, nullptr, W, tp, 1.0, 0.0, md->red_scratch.get(), s);
+        if (core_apply_supported(mp, tp)) {
+          core_apply(fitc->Qinv.get(), mp, S, tp, W, s);
+        } else {
+          const size_t need = gemm_reduce_scratch(mp, tp, mp);
+          if (md->red_scratch.n < need) md->red_scratch.alloc(need);
+          gemm_reduce(fitc->Qinv.get(), mp, mp, mp, S, tp, tp, nullptr, W, tp, 1.0, 0.0, md->red_scratch.get(), s);
+        }
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
       if (md->use_ozaki(tp)) {
