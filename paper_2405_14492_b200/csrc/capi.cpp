@@ -2,6 +2,7 @@
 #include "../../include/fsa_b200.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -17,8 +18,12 @@
 
 using namespace fsa;
 
+// Handles are reference counted: a geometry or model keeps its context alive and a
+// preconditioner or prediction set keeps its model alive, so the caller may destroy them in any
+// order (a garbage collector tearing down a Python session does).
 struct fsa_ctx {
   std::unique_ptr<Context> c;
+  std::atomic<int> refs{1};
 };
 struct fsa_geometry {
   fsa_ctx* ctx;
@@ -27,6 +32,7 @@ struct fsa_geometry {
 struct fsa_model {
   fsa_ctx* ctx;
   std::unique_ptr<Model> m;
+  std::atomic<int> refs{1};
 };
 struct fsa_precond {
   fsa_model* md;
@@ -171,10 +177,34 @@ int fsa_ctx_create(int device, fsa_ctx** out) {
     *out = c.release();
   });
 }
-void fsa_ctx_destroy(fsa_ctx* ctx) {
-  if (ctx == nullptr) return;
+namespace {
+fsa_ctx* ctx_acquire(fsa_ctx* ctx) {
+  ctx->refs.fetch_add(1);
+  return ctx;
+}
+void ctx_release(fsa_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) != 1) return;
   Bind bind_(ctx->c.get());
   delete ctx;
+}
+fsa_model* model_acquire(fsa_model* md) {
+  md->refs.fetch_add(1);
+  return md;
+}
+void model_release(fsa_model* md) {
+  if (md->refs.fetch_sub(1) != 1) return;
+  fsa_ctx* ctx = md->ctx;
+  {
+    Bind bind_(md->m->ctx);
+    cudaStreamSynchronize(md->m->ctx->stream);
+    delete md;
+  }
+  ctx_release(ctx);
+}
+}  // namespace
+void fsa_ctx_destroy(fsa_ctx* ctx) {
+  if (ctx == nullptr) return;
+  ctx_release(ctx);
 }
 int fsa_nccl_unique_id(void* id_out) {
   return guard([&] {
@@ -332,16 +362,20 @@ int fsa_geometry_create(fsa_ctx* ctx, const double* coords, int64_t n, int d, do
     Bind bind_(ctx->c.get());
     need(coords, "coords");
     auto g = std::make_unique<fsa_geometry>();
-    g->ctx = ctx;
     g->g = make_geometry(ctx->c.get(), coords, n, d, gamma);
+    g->ctx = ctx_acquire(ctx);
     *out = g.release();
   });
 }
 void fsa_geometry_destroy(fsa_geometry* g) {
   if (g == nullptr) return;
-  Bind bind_(g->ctx->c.get());
-  cudaStreamSynchronize(g->ctx->c->stream);
-  delete g;
+  fsa_ctx* ctx = g->ctx;
+  {
+    Bind bind_(ctx->c.get());
+    cudaStreamSynchronize(ctx->c->stream);
+    delete g;
+  }
+  ctx_release(ctx);
 }
 int fsa_geometry_info(fsa_geometry* g, int64_t* n, int64_t* nnz) {
   return guard([&] {
@@ -420,8 +454,8 @@ int fsa_model_assemble(fsa_ctx* ctx, const double* coords, int64_t n, int d, con
     require(p.gamma > 0.0, "taper range gamma must be positive");
     auto geo = make_geometry(ctx->c.get(), coords, n, d, p.gamma);
     auto md = std::make_unique<fsa_model>();
-    md->ctx = ctx;
     md->m = Model::assemble(ctx->c.get(), geo, inducing, m, p);
+    md->ctx = ctx_acquire(ctx);
     *out = md.release();
   });
 }
@@ -432,16 +466,14 @@ int fsa_model_assemble_geo(fsa_geometry* g, const double* inducing, int64_t m, c
     Bind bind_(g->ctx->c.get());
     need(inducing, "inducing");
     auto md = std::make_unique<fsa_model>();
-    md->ctx = g->ctx;
     md->m = Model::assemble(g->ctx->c.get(), g->g, inducing, m, to_params(params));
+    md->ctx = ctx_acquire(g->ctx);
     *out = md.release();
   });
 }
 void fsa_model_destroy(fsa_model* md) {
   if (md == nullptr) return;
-  Bind bind_(md->m->ctx);
-  cudaStreamSynchronize(md->m->ctx->stream);
-  delete md;
+  model_release(md);
 }
 int fsa_model_info(fsa_model* md, int64_t* n, int64_t* m, int64_t* nnz, int64_t* n_clamped, double* ldsm) {
   return guard([&] {
@@ -561,8 +593,8 @@ int fsa_make_preconditioner(fsa_model* md, int type, fsa_precond** out) {
     need(md, "model");
     Bind bind_(md->m->ctx);
     auto p = std::make_unique<fsa_precond>();
-    p->md = md;
     p->p = make_preconditioner(md->m.get(), type);
+    p->md = model_acquire(md);
     *out = p.release();
   });
 }
@@ -571,17 +603,21 @@ int fsa_make_jacobi(fsa_model* md, fsa_precond** out) {
     need(md, "model");
     Bind bind_(md->m->ctx);
     auto p = std::make_unique<fsa_precond>();
-    p->md = md;
     single_rank(md->m->ctx, "the Jacobi preconditioner");
     p->p = std::make_unique<DiagPrecond>(md->m.get(), false);
+    p->md = model_acquire(md);
     *out = p.release();
   });
 }
 void fsa_precond_destroy(fsa_precond* p) {
   if (p == nullptr) return;
-  Bind bind_(p->md->m->ctx);
-  cudaStreamSynchronize(p->md->m->ctx->stream);
-  delete p;
+  fsa_model* md = p->md;
+  {
+    Bind bind_(md->m->ctx);
+    cudaStreamSynchronize(md->m->ctx->stream);
+    delete p;
+  }
+  model_release(md);
 }
 int fsa_precond_logdet(fsa_precond* p, double* out) {
   return guard([&] {
@@ -776,16 +812,20 @@ int fsa_pred_setup(fsa_model* md, const double* pcoords, int64_t np, fsa_pred** 
     need(pcoords, "pcoords");
     single_rank(md->m->ctx, "prediction");
     auto pr = std::make_unique<fsa_pred>();
-    pr->md = md;
     pr->p = make_prediction_set(md->m.get(), pcoords, np);
+    pr->md = model_acquire(md);
     *out = pr.release();
   });
 }
 void fsa_pred_destroy(fsa_pred* pr) {
   if (pr == nullptr) return;
-  Bind bind_(pr->md->m->ctx);
-  cudaStreamSynchronize(pr->md->m->ctx->stream);
-  delete pr;
+  fsa_model* md = pr->md;
+  {
+    Bind bind_(md->m->ctx);
+    cudaStreamSynchronize(md->m->ctx->stream);
+    delete pr;
+  }
+  model_release(md);
 }
 int fsa_pred_info(fsa_pred* pr, int64_t* np, int64_t* nnz) {
   return guard([&] {

@@ -293,3 +293,24 @@ def test_fisher_ste_matches_oracle(rademacher, L):  # fsa.cpp:284-301 (test_fsa.
     assert np.abs(got - got.T).max() <= 1e-12 * np.abs(got).max()
     # same probes, solves to 1e-11: agreement to the north-star scalar tolerance
     assert rel(got, want) < 1e-6, (got, want)
+
+
+def test_handles_outlive_their_context():
+    # handles are reference counted: destroying the context (then the model) before the
+    # preconditioner, prediction set and geometry must neither crash nor break those handles
+    locs = O.uniform_locations(2000, 2, 31)
+    ind = O.select_random(locs, 40, 32)
+    ctx = fsa.Context(0)
+    g = fsa.Geometry(locs, 0.05, ctx=ctx)
+    md = fsa.FsaModel.assemble(None, ind, geometry=g, nu=1.5, taper_family=1, gamma=0.05, sigma2=0.2,
+                               sigma1_2=1.0, rho=0.1)
+    P = fsa.make_preconditioner(md, "fitc")
+    pr = fsa.PredictionSet(md, O.uniform_locations(300, 2, 33))
+    fsa.lib().fsa_ctx_destroy(ctx.h)
+    ctx.h = None
+    z = P.sample_probes(3, 1)  # the model and its context are still alive through P
+    assert np.isfinite(z).all()
+    fsa.lib().fsa_model_destroy(md.h)
+    md.h = None
+    assert np.isfinite(P.logdet())
+    del pr, P, g
