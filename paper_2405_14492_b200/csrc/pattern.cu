@@ -197,10 +197,14 @@ __global__ void k_count(const double* rx, long rld, long rn, const double* cx, l
 constexpr int kUnionSort = 4096;  // max entries per 32-row group handled by the sort
 constexpr int kUnionCap = 1024;   // max union size per 32-row group
 // (G, sort capacity, union capacity) are runtime: dynamic smem holds 2 x kSortCap ints
+// RADIX: the group's (<= 4096) column indices are sorted by a block radix sort over key_bits
+// bits (3 to 6 passes instead of the 78 passes of the bitonic network); larger capacities
+// (the 128-row groups of the opt-in INT8 SpMM) keep the bitonic sort.
+template <bool RADIX>
 __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
                                                      long nrows, int G, int kSortCap, int kCap,
                                                      int* __restrict__ ucols, int* __restrict__ ucount,
-                                                     int* __restrict__ lidx) {
+                                                     int* __restrict__ lidx, int key_bits) {
   extern __shared__ int ush[];
   int* keys = ush;
   int* flag = ush + kSortCap;
@@ -216,6 +220,21 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
   }
   int size = 1;
   while (size < cnt) size <<= 1;
+  if constexpr (RADIX) {
+    typedef cub::BlockRadixSort<int, 512, 8> BRS;
+    __shared__ typename BRS::TempStorage rs;
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = tid * 8 + j;
+      v[j] = i < cnt ? col[p0 + i] : 0x7fffffff;
+    }
+    BRS(rs).Sort(v, 0, key_bits < 31 ? key_bits + 1 : 32);  // + 1 bit: the 0x7fffffff padding sorts last
+#pragma unroll
+    for (int j = 0; j < 8; ++j) keys[tid * 8 + j] = v[j];
+    __syncthreads();
+    size = 4096;
+  } else {
   for (int i = tid; i < size; i += blockDim.x) keys[i] = i < cnt ? col[p0 + i] : 0x7fffffff;
   __syncthreads();
   for (int k = 2; k <= size; k <<= 1) {
@@ -233,6 +252,7 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
       }
       __syncthreads();
     }
+  }
   }
   for (int i = tid; i < size; i += blockDim.x) flag[i] = (i < cnt && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
   __syncthreads();
@@ -327,9 +347,20 @@ bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& n
   DBuf<long> sizes(ngrp + 1);
   lidx.alloc(pat.nnz);
   const int smem = 2 * sort_cap * static_cast<int>(sizeof(int));
-  FSA_CUDA(cudaFuncSetAttribute(k_group_union, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_group_union<<<static_cast<unsigned>(ngrp), 512, smem, s>>>(pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap,
-                                                              cap, ucols.get(), ucount.get(), lidx.get());
+  int key_bits = 1;  // column indices (extended indexing) are < 2^key_bits
+  {
+    long maxc = pat.cols > 0 ? pat.cols : pat.rows;
+    while ((1L << key_bits) < maxc + 1 && key_bits < 31) ++key_bits;
+  }
+  if (sort_cap == 4096) {
+    FSA_CUDA(cudaFuncSetAttribute(k_group_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_group_union<true><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
+        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits);
+  } else {
+    FSA_CUDA(cudaFuncSetAttribute(k_group_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_group_union<false><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
+        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits);
+  }
   FSA_LAUNCH_CHECK();
   bad.zero(s);
   FSA_CUDA(cudaMemsetAsync(sizes.get() + ngrp, 0, sizeof(long), s));
