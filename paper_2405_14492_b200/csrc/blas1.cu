@@ -516,14 +516,15 @@ __global__ void __launch_bounds__(256, 3) k_xr_dot_max(double* __restrict__ X, d
     partial[static_cast<long>(blockIdx.x) * t + threadIdx.x] = sacc;
   }
 }
+long xr_dot_max_blocks(long n) { return std::min(rowdot_blocks(n), 3L * kNumSMs); }  // one wave at 3 blocks/SM
 void update_xr_dot_max(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
                        long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
-                       long chunk_rows, cudaStream_t s) {
+                       long chunk_rows, cudaStream_t s, bool colsum) {
   require(tp <= 64, "update_xr_dot_max: at most 64 columns");
-  const long nb = std::min(rowdot_blocks(n), 3L * kNumSMs);  // one wave at 3 resident blocks per SM
+  const long nb = xr_dot_max_blocks(n);
   k_xr_dot_max<<<static_cast<unsigned>(nb), 256, 0, s>>>(X, R, H, V, alpha, n, tp, k, scratch, dinv, ymax, chunk_rows);
   FSA_LAUNCH_CHECK();
-  colsum_partials(scratch, nb, k, k, rr, s);
+  if (colsum) colsum_partials(scratch, nb, k, k, rr, s);
 }
 
 void update_uh(double* UH, const double* W, const int* active, const double* beta, long mpad, long tp, long k,
@@ -741,6 +742,100 @@ void scale_rows(double* Y, const double* X, const double* w, long n, long tp, cu
 void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_t s) {
   if (len == 0) return;
   k_axpby<<<nblk(len), 256, 0, s>>>(Y, X, a, b, len);
+  FSA_LAUNCH_CHECK();
+}
+
+
+// ---- column sums fused with the per-column PCG control (single rank) ---------------------
+// out[c] = sum_b partial[b][c] exactly as k_colsum_partials (same strided assignment and tree),
+// then thread 0 of column c < k runs that column's control step: MODE 0 alpha (k_cg_alpha),
+// MODE 1 the residual test (k_cg_check), MODE 2 beta (k_cg_beta) followed, in the last block to
+// finish, by the active count for the host (k_cg_count; `ticket` is reset for the next call).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ partial, long nb, long ldp,
+                                                    double* __restrict__ out, long k, int it, int max_iter,
+                                                    double tol, CgState st, unsigned int* ticket) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  const long c = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double s0 = 0.0, s1 = 0.0;
+  long b = tid;
+  for (; b + 256 < nb; b += 512) {
+    s0 += partial[b * ldp + c];
+    s1 += partial[(b + 256) * ldp + c];
+  }
+  if (b < nb) s0 += partial[b * ldp + c];
+  double sacc = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if (lane == 0) red[warp] = sacc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[c] = t;
+    const long j = c;
+    if (j < k) {
+      if (MODE == 0) {  // alpha = rz / h'v, tridiagonal push (krylov.cpp:66-75)
+        if (!st.active[j]) {
+          st.alpha[j] = 0.0;
+        } else if (!(t > 0.0)) {
+          atomicCAS(st.err, 0, kErrOperatorNotPD);
+          st.alpha[j] = 0.0;
+        } else {
+          const double a = st.rz[j] / t;
+          st.alpha[j] = a;
+          st.tdiag[j * max_iter + it] = 1.0 / a + st.beta_prev[j] / st.alpha_prev[j];
+          if (it > 0) st.toff[j * max_iter + it - 1] = sqrt(st.beta_prev[j]) / st.alpha_prev[j];
+          st.iterations[j] = it + 1;
+        }
+      } else if (MODE == 1) {  // residual test (krylov.cpp:77-82)
+        if (st.active[j] && sqrt(t) < tol) {
+          st.converged[j] = 1;
+          st.active[j] = 0;
+        }
+      } else {  // beta = rz_new / rz (krylov.cpp:83-90)
+        if (!st.active[j]) {
+          st.beta[j] = 0.0;
+        } else if (!(t > 0.0)) {
+          atomicCAS(st.err, 0, kErrPrecondNotPD);
+          st.beta[j] = 0.0;
+        } else {
+          const double bb = t / st.rz[j];
+          st.beta[j] = bb;
+          st.beta_prev[j] = bb;
+          st.alpha_prev[j] = st.alpha[j];
+          st.rz[j] = t;
+        }
+      }
+    }
+    if (MODE == 2) {
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+  }
+  if (MODE == 2) {
+    __syncthreads();
+    if (last && tid == 0) {
+      __threadfence();
+      int cnt = 0;
+      for (long jj = 0; jj < k; ++jj) cnt += reinterpret_cast<volatile int*>(st.active)[jj] != 0;
+      st.host_flags[0] = cnt;
+      st.host_flags[1] = *reinterpret_cast<volatile int*>(st.err);
+      *ticket = 0u;
+    }
+  }
+}
+void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, double* out, long k, int it,
+                int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s) {
+  require(t >= k && t > 0, "colsum_ctl: fewer sums than columns");
+  const unsigned g = static_cast<unsigned>(t);
+  switch (mode) {
+    case 0: k_colsum_ctl<0><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
+    case 1: k_colsum_ctl<1><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
+    default: k_colsum_ctl<2><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
+  }
   FSA_LAUNCH_CHECK();
 }
 

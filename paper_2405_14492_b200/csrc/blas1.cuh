@@ -63,7 +63,13 @@ void update_xr_dot(double* X, double* R, const double* H, const double* V, const
 // (atomicMax into [chunk][64], zeroed by the caller) for the Ozaki projection of R
 void update_xr_dot_max(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp,
                        long k, double* rr, double* scratch, const double* dinv, unsigned long long* ymax,
-                       long chunk_rows, cudaStream_t s);
+                       long chunk_rows, cudaStream_t s, bool colsum = true);
+long xr_dot_max_blocks(long n);  // partial rows (ld k) left in scratch when colsum = false
+// column sums of partials (as colsum_partials) fused with the per-column PCG control of the
+// single-rank sweep: mode 0 alpha (cg_alpha), 1 residual test (cg_check), 2 beta + active count
+// (cg_beta, cg_count; `ticket` is a zeroed device counter, left zero)
+void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, double* out, long k, int it,
+                int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s);
 // Jacobi PCG without a Z block: X += alpha H, R -= alpha V, rr = |R|^2, rz = R' diag(dinv) R;
 // scratch holds 2 * coldot_scratch(n, k) doubles
 void update_xr_dot_jacobi(double* X, double* R, const double* H, const double* V, const double* alpha,

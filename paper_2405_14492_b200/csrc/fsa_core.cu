@@ -814,11 +814,18 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   // cores, the remainder on DMMA; the dense passes stream the U planes once per 64 columns
   const bool oz_split = fused && !oz && md->ctx->gemm_mode != 1 && tp > kOzCols;
   if (oz || oz_split) md->ensure_ozaki();
+  // single rank: the column sums of the SpMM, residual-update and expansion partials run fused
+  // with the alpha / residual-test / beta + count control kernels (no separate launches)
+  const bool ctl = fuse_h && oz && md->world() == 1;
+  if (ctl) {
+    w.tick.alloc(1);
+    w.tick.zero(s);
+  }
   const bool oz_spmm = oz && md->use_ozaki_spmm(tp);
   if (oz_spmm) md->ensure_ozaki_spmm();
   bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
-  auto precond = [&](double* rzout) {
+  auto precond = [&](double* rzout, bool sums = true) {
     if (fused) {
       double* S = md->mt_buf(0, tp);
       double* W = md->mt_buf(1, tp);
@@ -866,7 +873,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
       if (md->use_ozaki(tp)) {
-        ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
+        ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s, sums);
       } else if (oz_split) {
         for (long c0 = 0; c0 < tp; c0 += kOzCols) {
           const long wd = std::min<long>(kOzCols, tp - c0);
@@ -938,7 +945,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       // CSR + Z (once per row), Lw, H, V read + H, V write
       KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 48.0 * n * k);
       spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
-                       w.H.get(), st.beta, k, first_sweep, s);
+                       w.H.get(), st.beta, k, first_sweep, s, !ctl);
       first_sweep = false;
       comm.allreduce(hv, tp, s);
     } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
@@ -968,11 +975,14 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     }
     {
       KTimer t(ctx, "cg_blas1");
-      cg_alpha(hv, k, it, maxit, st, s);
+      if (ctl)
+        colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s);
+      else
+        cg_alpha(hv, k, it, maxit, st, s);
       if (oz) {
         FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
         update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
-                          md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s);
+                          md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl);
         ymax_ready = true;
       } else if (jfused) {
         update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
@@ -981,12 +991,18 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
       }
       comm.allreduce(rr, k, s);
-      cg_check(rr, k, opts.tol, st, s);
+      if (ctl)
+        colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s);
+      else
+        cg_check(rr, k, opts.tol, st, s);
     }
-    if (!jfused) precond(rz);
+    if (!jfused) precond(rz, !ctl);
     {
       KTimer t(ctx, "cg_blas1");
-      cg_beta(rz, k, st, s);
+      if (ctl)  // beta and the active count
+        colsum_ctl(2, part, md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st, w.tick.get(), s);
+      else
+        cg_beta(rz, k, st, s);
       if (fuse_h) {
         // H and V are updated by the next sweep's SpMM
       } else if (fused) {  // H = Z + beta H, Vlr = U^T w + beta Vlr
@@ -996,7 +1012,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       } else {
         update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
       }
-      cg_count(k, st, s);
+      if (!ctl) cg_count(k, st, s);
     }
     FSA_CUDA(cudaEventRecord(sweep_ev[it & 1], s));
     if (pending >= 0) {

@@ -30,6 +30,7 @@ struct CgWork {
   DBuf<double> R, H, V, Z, Lw, Vlr, dots, dbl, part;
   DBuf<int> ints;
   DBuf<double> tri;
+  DBuf<unsigned int> tick;  // last-block counter of the fused control kernels
 };
 
 struct PinnedBuf {

@@ -1006,11 +1006,11 @@ void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* s
 }
 
 void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
-                       const double* Dinv, double* rz, double* partial, cudaStream_t s) {
+                       const double* Dinv, double* rz, double* partial, cudaStream_t s, bool colsum) {
   slice_w(p, W, ld, ncols, s);
   OzEpi epi{1, p.m_pad, ncols, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
   launch_expand(p, epi, s);
-  colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);
+  if (colsum) colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);
 }
 void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");

@@ -676,7 +676,7 @@ void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ld
 }
 void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                       double* dot, double* partial, const double* Y0, double* H, const double* beta, long kb,
-                      bool first, cudaStream_t s) {
+                      bool first, cudaStream_t s, bool colsum) {
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
   auto launch = [&](int nt, long c_first, long tiles) {
@@ -711,7 +711,7 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
     if (full > 0) launch(8, 0, full);
     if (rem > 0) launch(static_cast<int>(rem / 8), full * 64, 1);
   }
-  colsum_partials(partial, pat.ngrp, ncols, ncols, dot, s);
+  if (colsum) colsum_partials(partial, pat.ngrp, ncols, ncols, dot, s);
 }
 
 long spmm_dot_blocks(long nrows) {  // one row per warp (the L1-friendly geometry of k_spmm)

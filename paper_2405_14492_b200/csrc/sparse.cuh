@@ -39,7 +39,7 @@ void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ld
 // dot[c] = sum_r H[r][c] Y[r][c]
 void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                       double* dot, double* partial, const double* Y0, double* H, const double* beta, long kb,
-                      bool first, cudaStream_t s);
+                      bool first, cudaStream_t s, bool colsum = true);  // colsum = false: partials [ngrp][ncols] only
 // (Y0, when given, replaces Y as the beta term: Y = alpha S X + beta Y0)
 void spmm_dot(const long* rowptr, const int* col, const double* val, long nrows, const double* X, long ldx, double* Y,
               long ldy, long ncols, double alpha, double beta, double* dot, double* partial, cudaStream_t s,
