@@ -817,13 +817,18 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
   }
   if (MODE == 2) {
     __syncthreads();
-    if (last && tid == 0) {
+    if (last) {  // block-uniform: the whole last block counts the active columns
       __threadfence();
       int cnt = 0;
-      for (long jj = 0; jj < k; ++jj) cnt += reinterpret_cast<volatile int*>(st.active)[jj] != 0;
-      st.host_flags[0] = cnt;
-      st.host_flags[1] = *reinterpret_cast<volatile int*>(st.err);
-      *ticket = 0u;
+      for (long base = 0; base < k; base += blockDim.x) {
+        const long jj = base + tid;
+        cnt += __syncthreads_count(jj < k && reinterpret_cast<volatile int*>(st.active)[jj] != 0);
+      }
+      if (tid == 0) {
+        st.host_flags[0] = cnt;
+        st.host_flags[1] = *reinterpret_cast<volatile int*>(st.err);
+        *ticket = 0u;
+      }
     }
   }
 }
