@@ -604,7 +604,61 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
     logdetQ = hs[0];
     ld = hs[0] + hs[1];  // logdet(core) - logdet(Sigma_m) + sum log d   (preconditioners.cpp:53-55)
   }
-  if (derivs) md->start_rho_derivs();
+  if (derivs) {
+    md->start_rho_derivs();
+    start_traces();
+  }
+}
+
+// The exact traces need Q^{-1}, D and the rho-derivative blocks: queued on the side stream right
+// after those (off the main stream's critical path); deriv_trace joins and finishes on the host.
+void FitcPrecond::start_traces() {
+  if (have_traces || traces_pending || md->ctx->gemm_mode == 1 || !md->rho_pending || !md->oz.ready) return;
+  Context* ctx = md->ctx;
+  cudaStream_t side = ctx->side_stream();
+  const long mp = md->m_pad, np = md->n_pad, n = md->n;
+  cudaStream_t saved = alloc_stream();
+  alloc_stream() = side;
+  try {
+    tr_q.alloc(np);
+    tr_f.alloc(np);
+    tr_pinv.alloc(np);
+    tr_d1.alloc(np);
+    tr_sums.alloc(8);
+    // rows dots of U^T Q^{-1} with U and U1 (INT8 passes, side-stream W-plane buffers)
+    ozaki_expand_rowdots(md->oz, Qinv.get(), mp, md->U.get(), md->U1.get(), mp, tr_q.get(), tr_f.get(), side, true);
+    pinv_diag(tr_pinv.get(), md->D.get(), tr_q.get(), n, np, side);
+    affine_vec(tr_d1.get(), md->D.get(), -md->P.sigma2, 1.0 / md->P.sigma1_2, n, np, side);
+    trace_sums(tr_pinv.get(), tr_d1.get(), md->dD.get(), tr_f.get(), md->D.get(), n, Qinv.get(), md->K2.get(), mp,
+               tr_sums.get(), side);
+    if (traces_host == nullptr) FSA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&traces_host), 8 * sizeof(double)));
+    FSA_CUDA(cudaMemcpyAsync(traces_host, tr_sums.get(), 7 * sizeof(double), cudaMemcpyDeviceToHost, side));
+  } catch (...) {
+    alloc_stream() = saved;
+    throw;
+  }
+  alloc_stream() = saved;
+  if (traces_done == nullptr) traces_done = ctx->ev();
+  FSA_CUDA(cudaEventRecord(traces_done, side));
+  traces_pending = true;
+}
+
+void FitcPrecond::finish_traces(const double* h) {
+  double hs[7];
+  std::copy(h, h + 7, hs);
+  md->rcomm->allreduce_host(hs, 4, md->ctx->stream);  // sums over rows; the m x m sums are replicated
+  const double s0 = hs[0], s1 = hs[1], s2 = hs[2], qf = hs[3], trQi = hs[4], trK2 = hs[5], k2q = hs[6];
+  trace[0] = s0;
+  trace[1] = s1 + (static_cast<double>(md->m_pad) - trQi) / md->P.sigma1_2;
+  trace[2] = s2 + 2.0 * qf - (trK2 - k2q);
+  have_traces = true;
+}
+
+FitcPrecond::~FitcPrecond() {
+  // frees below (stream-ordered on the main stream) come after the side-stream trace work
+  if (traces_pending) cudaStreamWaitEvent(md->ctx->stream, traces_done, 0);
+  if (traces_done != nullptr) md->ctx->pool.push_back(traces_done);
+  if (traces_host != nullptr) cudaFreeHost(traces_host);
 }
 
 // P^{-1} R = D^{-1} R - D^{-1} U^T Q^{-1} U D^{-1} R   (preconditioners.cpp:58-67)
@@ -675,6 +729,12 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
 //   k = 2: pinv . dD + 2 <Q^{-1}, F> - Tr(K2) + <K2, Q^{-1}>,  F = U D^{-1} U1^T
 double FitcPrecond::deriv_trace(int k) {
   require(derivs, "FITC preconditioner built without derivatives");
+  if (!have_traces && traces_pending) {
+    md->ensure_rho_derivs();
+    FSA_CUDA(cudaEventSynchronize(traces_done));
+    traces_pending = false;
+    finish_traces(traces_host);
+  }
   if (!have_traces) {
     cudaStream_t s = md->ctx->stream;
     const long mp = md->m_pad, np = md->n_pad, n = md->n;
@@ -703,12 +763,7 @@ double FitcPrecond::deriv_trace(int k) {
     double hs[7];
     FSA_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof(hs), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
-    md->rcomm->allreduce_host(hs, 4, s);  // sums over rows; the m x m sums are replicated
-    const double s0 = hs[0], s1 = hs[1], s2 = hs[2], qf = hs[3], trQi = hs[4], trK2 = hs[5], k2q = hs[6];
-    trace[0] = s0;
-    trace[1] = s1 + (static_cast<double>(mp) - trQi) / md->P.sigma1_2;
-    trace[2] = s2 + 2.0 * qf - (trK2 - k2q);
-    have_traces = true;
+    finish_traces(hs);
   }
   return trace[k];
 }

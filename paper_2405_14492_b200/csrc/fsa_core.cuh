@@ -247,6 +247,14 @@ class FitcPrecond final : public Precond {
   bool derivs = false;
   bool have_traces = false;
   double trace[3] = {0, 0, 0};
+  // the exact traces' device work, on the side stream after the rho-derivative build
+  void start_traces();
+  void finish_traces(const double* hs);
+  bool traces_pending = false;
+  cudaEvent_t traces_done = nullptr;
+  double* traces_host = nullptr;  // pinned [8]
+  DBuf<double> tr_q, tr_f, tr_pinv, tr_d1, tr_sums;
+  ~FitcPrecond() override;
 };
 
 std::unique_ptr<Precond> make_preconditioner(Model* md, int type);

@@ -919,14 +919,14 @@ __global__ void k_sum_tiles(const double* __restrict__ qp, const double* __restr
   f[i] = b;
 }
 
-void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s) {
+void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const int8_t* Ws = nullptr) {
   static bool attr = false;
   if (!attr) {
     FSA_CUDA(cudaFuncSetAttribute(k_oz_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
     attr = true;
   }
   const int grid = std::min(p.ptiles, kNumSMs);
-  k_oz_expand<<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), p.Ws.get(), p.ptiles, p.mkb, epi);
+  k_oz_expand<<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), Ws != nullptr ? Ws : p.Ws.get(), p.ptiles, p.mkb, epi);
   FSA_LAUNCH_CHECK();
 }
 
@@ -947,12 +947,15 @@ void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double*
   FSA_LAUNCH_CHECK();
 }
 
-void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
+void slice_w_to(OzakiPlan& p, const double* W, long ld, long tp, int8_t* Ws, int* h, cudaStream_t s) {
   require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
-  k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, p.h.get());
+  k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, h);
   FSA_LAUNCH_CHECK();
-  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, p.h.get(), p.Ws.get());
+  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws);
   FSA_LAUNCH_CHECK();
+}
+void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
+  slice_w_to(p, W, ld, tp, p.Ws.get(), p.h.get(), s);
 }
 
 }  // namespace
@@ -1021,16 +1024,22 @@ void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, 
   }
 }
 void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
-                          double* q, double* f, cudaStream_t s) {
+                          double* q, double* f, cudaStream_t s, bool side_buffers) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
   const long tiles = ldw / kOzCols;
+  if (side_buffers) {  // own W-plane buffers: the main stream's sweeps keep rewriting p.Ws / p.h
+    if (p.Ws_side.n < p.Ws.n) p.Ws_side.alloc(p.Ws.n);
+    if (p.h_side.n < p.h.n) p.h_side.alloc(p.h.n);
+  }
+  int8_t* Ws = side_buffers ? p.Ws_side.get() : p.Ws.get();
+  int* h = side_buffers ? p.h_side.get() : p.h.get();
   DBuf<double> qp(static_cast<size_t>(tiles * p.n_pad)), fp(static_cast<size_t>(tiles * p.n_pad));
   for (long j = 0; j < tiles; ++j) {
-    slice_w(p, W + j * kOzCols, ldw, kOzCols, s);
-    OzEpi epi{4, p.m_pad, kOzCols, ld, p.ec.get(), p.h.get(), nullptr, qp.get() + j * p.n_pad,
+    slice_w_to(p, W + j * kOzCols, ldw, kOzCols, Ws, h, s);
+    OzEpi epi{4, p.m_pad, kOzCols, ld, p.ec.get(), h, nullptr, qp.get() + j * p.n_pad,
               fp.get() + j * p.n_pad, B1 + j * kOzCols, nullptr};
     epi.A2 = B2 + j * kOzCols;
-    launch_expand(p, epi, s);
+    launch_expand(p, epi, s, Ws);
   }
   k_sum_tiles<<<static_cast<unsigned>(cdiv(p.n_pad, 256)), 256, 0, s>>>(qp.get(), fp.get(), tiles, p.n_pad, q, f);
   FSA_LAUNCH_CHECK();

@@ -45,6 +45,8 @@ struct OzakiPlan {
   DBuf<int8_t> Ar, Ac;        // project / expand digit planes of U
   DBuf<int> er, ec;           // their exponents: [nchunks][m_pad], [n_pad]
   DBuf<int8_t> Ys, Ws;        // per-sweep planes of D^{-1} R and W
+  DBuf<int8_t> Ws_side;       // W planes of passes run on the side stream (exact traces)
+  DBuf<int> h_side;
   DBuf<unsigned long long> ymax;
   DBuf<int> f, h;             // [nchunks][64], [64]
   DBuf<double> part;          // project partials [nchunks][m_pad][64]
@@ -80,7 +82,7 @@ void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, doubl
 //   S = U diag(scale) V      (V n_pad x ldv, S m_pad x lds)
 void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s);
 void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
-                          double* q, double* f, cudaStream_t s);
+                          double* q, double* f, cudaStream_t s, bool side_buffers = false);
 void ozaki_project_wide(OzakiPlan& p, const double* V, long ldv, const double* scale, double* S, long lds,
                         cudaStream_t s);
 // plain products for tests: S = U diag(scale) V (scale may be null), Y = U^T W
