@@ -754,11 +754,14 @@ void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_
 template <int MODE>
 __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ partial, long nb, long ldp,
                                                     double* __restrict__ out, long k, int it, int max_iter,
-                                                    double tol, CgState st, unsigned int* ticket) {
+                                                    double tol, CgState st, unsigned int* ticket,
+                                                    unsigned long long* __restrict__ zero_buf, long zero_len) {
   __shared__ double red[8];
   __shared__ bool last;
   const long c = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // (MODE 0) clear the next kernel's column-maxima accumulators on the way
+  for (long i = c * blockDim.x + tid; i < zero_len; i += static_cast<long>(gridDim.x) * blockDim.x) zero_buf[i] = 0ull;
   double s0 = 0.0, s1 = 0.0;
   long b = tid;
   for (; b + 256 < nb; b += 512) {
@@ -833,13 +836,20 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
   }
 }
 void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, double* out, long k, int it,
-                int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s) {
+                int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s,
+                unsigned long long* zero_buf, long zero_len) {
   require(t >= k && t > 0, "colsum_ctl: fewer sums than columns");
   const unsigned g = static_cast<unsigned>(t);
   switch (mode) {
-    case 0: k_colsum_ctl<0><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
-    case 1: k_colsum_ctl<1><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
-    default: k_colsum_ctl<2><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket); break;
+    case 0:
+      k_colsum_ctl<0><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      break;
+    case 1:
+      k_colsum_ctl<1><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      break;
+    default:
+      k_colsum_ctl<2><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      break;
   }
   FSA_LAUNCH_CHECK();
 }

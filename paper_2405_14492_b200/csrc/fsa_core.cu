@@ -1030,12 +1030,13 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     }
     {
       KTimer t(ctx, "cg_blas1");
-      if (ctl)
-        colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s);
+      if (ctl)  // alpha, and the ymax clear of the residual update below
+        colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s,
+                   md->oz.ymax.get(), static_cast<long>(md->oz.ymax.n));
       else
         cg_alpha(hv, k, it, maxit, st, s);
       if (oz) {
-        FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
+        if (!ctl) FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
         update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
                           md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl);
         ymax_ready = true;
