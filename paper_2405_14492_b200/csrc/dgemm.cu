@@ -272,7 +272,7 @@ namespace {
 template <int NT>
 __global__ void __launch_bounds__(256) k_core_dmma(const double* __restrict__ Qinv, long mp,
                                                   const double* __restrict__ S, long ld,
-                                                  double* __restrict__ W) {
+                                                  double* __restrict__ W, unsigned long long* __restrict__ wmax) {
   __shared__ double red[8][8][NT * 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long r0 = static_cast<long>(blockIdx.x) * 8;
@@ -303,25 +303,36 @@ __global__ void __launch_bounds__(256) k_core_dmma(const double* __restrict__ Qi
 #pragma unroll
     for (int w = 1; w < 8; ++w) acc += red[w][r][cc];
     W[(r0 + r) * ld + cc] = acc;
+    red[0][r][cc] = fabs(acc);  // (this thread alone read red[*][r][cc])
+  }
+  if (wmax != nullptr) {  // column maxima of |W| for the expansion's digit planes (non-negative bits)
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < NT * 8; cc += blockDim.x) {
+      double mx = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) mx = fmax(mx, red[0][r][cc]);
+      if (mx > 0.0) atomicMax(wmax + cc, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    }
   }
 }
 }  // namespace
 
 bool core_apply_supported(long mp, long ld) { return mp % 32 == 0 && ld % 8 == 0 && ld <= 72; }
 
-void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s) {
+void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s,
+                unsigned long long* wmax) {
   require(core_apply_supported(mp, ld), "core_apply: unsupported shape");
   const unsigned grid = static_cast<unsigned>(mp / 8);
   switch (ld / 8) {
-    case 1: k_core_dmma<1><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 2: k_core_dmma<2><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 3: k_core_dmma<3><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 4: k_core_dmma<4><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 5: k_core_dmma<5><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 6: k_core_dmma<6><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 7: k_core_dmma<7><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    case 8: k_core_dmma<8><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
-    default: k_core_dmma<9><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W); break;
+    case 1: k_core_dmma<1><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 2: k_core_dmma<2><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 3: k_core_dmma<3><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 4: k_core_dmma<4><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 5: k_core_dmma<5><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 6: k_core_dmma<6><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 7: k_core_dmma<7><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 8: k_core_dmma<8><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    default: k_core_dmma<9><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
   }
   FSA_LAUNCH_CHECK();
 }

@@ -328,6 +328,8 @@ void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, 
 // W = Qinv S for the fused FITC sweep (Qinv symmetric m_pad x m_pad; S, W m_pad x ld row-major,
 // ld a multiple of 8, <= 72): one launch of DMMA tiles with an in-CTA split of K
 bool core_apply_supported(long mp, long ld);
-void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s);
+// wmax (optional, zeroed by the caller): atomicMax of the bit patterns of |W| per column
+void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W, cudaStream_t s,
+                unsigned long long* wmax = nullptr);
 
 }  // namespace fsa

@@ -875,6 +875,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   if (ctl) {
     w.tick.alloc(1);
     w.tick.zero(s);
+    w.wmax.alloc(kOzCols);
   }
   const bool oz_spmm = oz && md->use_ozaki_spmm(tp);
   if (oz_spmm) md->ensure_ozaki_spmm();
@@ -919,7 +920,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       {
         KTimer t(ctx, "core_solve", 2.0 * md->m * md->m * k);
         if (core_apply_supported(mp, tp)) {
-          core_apply(fitc->Qinv.get(), mp, S, tp, W, s);
+          // (the fused path's sweeps also leave the column maxima the expansion slices W with)
+          core_apply(fitc->Qinv.get(), mp, S, tp, W, s, ctl && !sums ? w.wmax.get() : nullptr);
         } else {
           const size_t need = gemm_reduce_scratch(mp, tp, mp);
           if (md->red_scratch.n < need) md->red_scratch.alloc(need);
@@ -928,7 +930,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       }
       KTimer t(ctx, "lowrank_expand", flops_mn);
       if (md->use_ozaki(tp)) {
-        ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s, sums);
+        ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s, sums,
+                          ctl && !sums ? w.wmax.get() : nullptr);
       } else if (oz_split) {
         for (long c0 = 0; c0 < tp; c0 += kOzCols) {
           const long wd = std::min<long>(kOzCols, tp - c0);
@@ -1047,8 +1050,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
       }
       comm.allreduce(rr, k, s);
-      if (ctl)
-        colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s);
+      if (ctl)  // residual test, and the wmax clear of this sweep's core solve
+        colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s,
+                   w.wmax.get(), kOzCols);
       else
         cg_check(rr, k, opts.tol, st, s);
     }

@@ -31,6 +31,7 @@ struct CgWork {
   DBuf<int> ints;
   DBuf<double> tri;
   DBuf<unsigned int> tick;  // last-block counter of the fused control kernels
+  DBuf<unsigned long long> wmax;  // column maxima of |w| from the core solve (fused control path)
 };
 
 struct PinnedBuf {

@@ -869,11 +869,17 @@ __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, 
   }
 }
 __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long ld, long tp,
-                                                     const int* __restrict__ h,
-                                                     int8_t* __restrict__ Ws) {
+                                                     int* __restrict__ h, int8_t* __restrict__ Ws,
+                                                     const unsigned long long* __restrict__ wmax) {
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
-  const int e = h[c];
+  int e;
+  if (wmax != nullptr) {  // column maxima left by the producer of W (core_apply)
+    e = c < tp ? group_exp(__longlong_as_double(static_cast<long long>(wmax[c]))) : 0;
+    if (kb == 0 && kc == 0) h[c] = e;
+  } else {
+    e = h[c];
+  }
   double v[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * ld + c] : 0.0;
@@ -947,11 +953,14 @@ void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double*
   FSA_LAUNCH_CHECK();
 }
 
-void slice_w_to(OzakiPlan& p, const double* W, long ld, long tp, int8_t* Ws, int* h, cudaStream_t s) {
+void slice_w_to(OzakiPlan& p, const double* W, long ld, long tp, int8_t* Ws, int* h, cudaStream_t s,
+                const unsigned long long* wmax = nullptr) {
   require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
-  k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, h);
-  FSA_LAUNCH_CHECK();
-  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws);
+  if (wmax == nullptr) {
+    k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, h);
+    FSA_LAUNCH_CHECK();
+  }
+  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws, wmax);
   FSA_LAUNCH_CHECK();
 }
 void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
@@ -1009,8 +1018,9 @@ void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* s
 }
 
 void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
-                       const double* Dinv, double* rz, double* partial, cudaStream_t s, bool colsum) {
-  slice_w(p, W, ld, ncols, s);
+                       const double* Dinv, double* rz, double* partial, cudaStream_t s, bool colsum,
+                       const unsigned long long* wmax) {
+  slice_w_to(p, W, ld, ncols, p.Ws.get(), p.h.get(), s, wmax);
   OzEpi epi{1, p.m_pad, ncols, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
   launch_expand(p, epi, s);
   if (colsum) colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);

@@ -75,7 +75,8 @@ inline long ozaki_chunk_rows(const OzakiPlan& p) { return static_cast<long>(p.kb
 // Lw = U^T W, Z = Dinv (R - Lw), rz = column sums of R.Z
 void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
                        const double* Dinv, double* rz, double* partial, cudaStream_t s,
-                       bool colsum = true);  // colsum = false: partials [ptiles][ncols] only
+                       bool colsum = true,  // colsum = false: partials [ptiles][ncols] only
+                       const unsigned long long* wmax = nullptr);  // column maxima of |W| (core_apply)
 // wide passes (64-column tiles of row-major operands whose widths are multiples of 64):
 //   Y = A - U^T W            (W m_pad x ldw, A / Y n_pad x ld)
 //   q[i] = (U^T W)_i . B1_i, f[i] = (U^T W)_i . B2_i   (row dots, B1 / B2 n_pad x ld)
