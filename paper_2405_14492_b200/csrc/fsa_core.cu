@@ -613,7 +613,9 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
 // The exact traces need Q^{-1}, D and the rho-derivative blocks: queued on the side stream right
 // after those (off the main stream's critical path); deriv_trace joins and finishes on the host.
 void FitcPrecond::start_traces() {
-  if (have_traces || traces_pending || md->ctx->gemm_mode == 1 || !md->rho_pending || !md->oz.ready) return;
+  static const bool sync_traces = std::getenv("FSA_SYNC_TRACES") != nullptr;
+  if (sync_traces || have_traces || traces_pending || md->ctx->gemm_mode == 1 || !md->rho_pending || !md->oz.ready)
+    return;
   Context* ctx = md->ctx;
   cudaStream_t side = ctx->side_stream();
   const long mp = md->m_pad, np = md->n_pad, n = md->n;
