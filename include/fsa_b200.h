@@ -10,7 +10,9 @@
  *     columns sorted per row (sp_mat_t RowMajor, types.h:15-16);
  *   - parameter order is (sigma2 = nugget, sigma1_2 = marginal variance, rho)
  *     (types.h:72-102); gradients follow the same order.
- * The caller owns all host buffers; device state lives in the opaque handles.
+ * The caller owns all host buffers; device state lives in the opaque handles. Handles are
+ * reference counted: a geometry or model keeps its context alive and a preconditioner or
+ * prediction set keeps its model alive, so the *_destroy calls may come in any order.
  * Return codes: FSA_OK, FSA_EINVAL (std::invalid_argument in the reference,
  * types.h:27-29), FSA_ENUMERIC (fsagp::NumericalError, types.h:22-25),
  * FSA_ECUDA (device failure). fsa_last_error() gives the message (thread-local).
