@@ -88,6 +88,12 @@ int fsa_ctx_stream(fsa_ctx* ctx, void** stream); /* cudaStream_t all kernels run
 /* dense m x n passes with the low-rank factor: 0 auto (INT8 tensor-core Ozaki emulation of the fp64
  * product when the RHS block has <= 64 columns, DMMA fp64 otherwise), 1 DMMA fp64 always, 2 Ozaki */
 int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode);
+/* Diagnostics of the last PCG solve on this context (pcg_solve_multi, iterative_nll_grad, the
+ * prediction solves): *k = its column count; for columns j < cap_k, iterations[j] and the
+ * residual-norm history rnorm[j * cap_len + i] = ||r_j||_2 after iteration i + 1 (zero past the
+ * column's count). No reference counterpart: CgMultiResult (krylov.h:52-75) keeps counts only;
+ * the parity tests use the histories to tell an oracle tie from a divergence. */
+int fsa_ctx_last_cg(fsa_ctx* ctx, int64_t* k, int64_t cap_k, int64_t cap_len, int* iterations, double* rnorm);
 /* CUDA-event timers around kernel groups (name -> total ms, launches, algorithmic units) */
 int fsa_ctx_set_profiling(fsa_ctx* ctx, int on);
 int fsa_ctx_reset_timers(fsa_ctx* ctx);

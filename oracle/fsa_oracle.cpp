@@ -179,6 +179,64 @@ void uniform_locations(long n, int d, uint64_t seed, double* out) {
     for (int k = 0; k < d; ++k) out[i + k * n] = U(rng);
 }
 
+// ---- synthetic inputs of the BASELINE configs (not reference code: the reference's own
+// simulate_gp needs an exact Cholesky, estimation.cpp:330-332). Independent restatement of the
+// generator spec the product's host generators implement: a random-Fourier-feature
+// Matern draw plus nugget noise, and the config-5 Gaussian-blob mixture on [0,1]^d.
+void simulate_rff(const double* c, long n, int d, int nu_code, double sigma1_2, double rho, double nugget,
+                  int features, uint64_t seed, double* y) {
+  require(n > 0 && features > 0, "simulate_rff: invalid sizes");
+  const double nu = nu_code == 0 ? 0.5 : (nu_code == 1 ? 1.5 : 2.5);
+  rng_t rng(splitmix64(seed ^ 0x5eed5eedULL));
+  std::normal_distribution<double> N01(0.0, 1.0);
+  std::chi_squared_distribution<double> chi(2.0 * nu);  // spectral density of Matern-nu: Student-t
+  std::uniform_real_distribution<double> U(0.0, 2.0 * M_PI);
+  std::vector<double> w(static_cast<size_t>(features) * d), b(static_cast<size_t>(features));
+  for (int f = 0; f < features; ++f) {
+    const double u = chi(rng);
+    const double scale = 1.0 / (rho * std::sqrt(u / (2.0 * nu)));
+    for (int k = 0; k < d; ++k) w[static_cast<size_t>(f) * d + k] = N01(rng) * scale;
+    b[static_cast<size_t>(f)] = U(rng);
+  }
+  const double amp = std::sqrt(2.0 * sigma1_2 / features);
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int f = 0; f < features; ++f) {
+      double arg = b[static_cast<size_t>(f)];
+      for (int k = 0; k < d; ++k) arg += w[static_cast<size_t>(f) * d + k] * c[i + k * n];
+      acc += std::cos(arg);
+    }
+    y[i] = amp * acc;
+  }
+  rng_t noise(splitmix64(seed ^ 0x0153ULL));
+  std::normal_distribution<double> E(0.0, 1.0);
+  const double sd = std::sqrt(nugget);
+  for (long i = 0; i < n; ++i) y[i] += sd * E(noise);
+}
+
+void blob_locations(long n, int d, int blobs, double sd, uint64_t seed, double* out) {
+  require(n > 0 && blobs > 0 && d <= 3, "blob_locations: invalid sizes");
+  rng_t rng(splitmix64(seed));
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  std::vector<double> centre(static_cast<size_t>(blobs) * d);
+  for (double& v : centre) v = U(rng);
+  std::uniform_int_distribution<int> pick(0, blobs - 1);
+  std::normal_distribution<double> N(0.0, sd);
+  for (long i = 0; i < n;) {
+    const int bl = pick(rng);
+    double p[3];
+    bool inside = true;
+    for (int k = 0; k < d; ++k) {
+      p[k] = centre[static_cast<size_t>(bl) * d + k] + N(rng);
+      inside = inside && p[k] >= 0.0 && p[k] <= 1.0;
+    }
+    if (!inside) continue;  // rejected
+    for (int k = 0; k < d; ++k) out[i + k * n] = p[k];
+    ++i;
+  }
+}
+
 // GridIndex (locations.cpp:19-62): cells of edge h, 3^d neighbourhood scan,
 // strict ||x - q|| < h. Cells are keyed by their integer coordinates here
 // (collision-free) — the reference's splitmix-hashed keys give the same set
@@ -874,6 +932,7 @@ struct CgResult {
   std::vector<int> iterations;
   std::vector<char> converged;
   std::vector<std::vector<double>> tdiag, toff;
+  std::vector<std::vector<double>> rnorm;  // ||r||_2 after each iteration (test diagnostics: tie margins)
   int sweeps = 0;
   bool all_converged() const {
     for (char c : converged) if (!c) return false;
@@ -898,6 +957,7 @@ CgResult pcg_solve_multi(const LinOp& A, const Precond& P, const double* B, long
   res.converged.assign(static_cast<size_t>(k), 0);
   res.tdiag.resize(static_cast<size_t>(k));
   res.toff.resize(static_cast<size_t>(k));
+  res.rnorm.resize(static_cast<size_t>(k));
   std::vector<double> R(B, B + n * k), H(static_cast<size_t>(n * k), 0.0), V(static_cast<size_t>(n * k), 0.0);
   std::vector<double> rz(static_cast<size_t>(k), 0.0), ap(static_cast<size_t>(k), 1.0), bp(static_cast<size_t>(k), 0.0);
   std::vector<char> active(static_cast<size_t>(k), 1);
@@ -952,7 +1012,9 @@ CgResult pcg_solve_multi(const LinOp& A, const Precond& P, const double* B, long
       for (long i = 0; i < n; ++i) x[i] += alpha * h[i];
       for (long i = 0; i < n; ++i) r[i] -= alpha * v[i];
       res.iterations[sj] = it + 1;
-      if (std::sqrt(dot(r, r, n)) < tol) {
+      const double rn = std::sqrt(dot(r, r, n));
+      res.rnorm[sj].push_back(rn);
+      if (rn < tol) {
         res.converged[sj] = 1;
         active[sj] = 0;
         ++dropped;
@@ -1127,7 +1189,12 @@ std::vector<double> small_spd_solve(std::vector<double> G, long p, std::vector<d
   return b;
 }
 
-struct NllOut { double nll, g[3], logdet; int cg_iterations; std::vector<double> beta; };
+struct NllOut {
+  double nll, g[3], logdet;
+  int cg_iterations;
+  std::vector<double> beta;
+  CgResult sol;  // the [Z | y | X] solve (test diagnostics: per-column counts, residual norms, X)
+};
 
 // iterative_nll_grad (estimation.cpp:178-227)
 NllOut iterative_nll_grad(Model& md, const Precond& P, const double* y, const double* X, long p, int L,
@@ -1179,6 +1246,7 @@ NllOut iterative_nll_grad(Model& md, const Precond& P, const double* y, const do
       out.g[kk] = 0.5 * (tr.value - dot(u.data(), du.data(), n));
     }
   }
+  out.sol = std::move(sol);
   return out;
 }
 
@@ -1571,6 +1639,25 @@ int orc_pcg(void* mdv, int op_kind, void* p, const double* B, long k, double tol
     *sweeps = r.sweeps;
   });
 }
+// orc_pcg plus the residual-norm history (k x max_iter)
+int orc_pcg_ex(void* mdv, int op_kind, void* p, const double* B, long k, double tol, int max_iter, int batched,
+               double* X, int* iters, int* conv, double* tdiag, double* toff, double* rnorm, int* sweeps) {
+  return guard([&] {
+    Model& md = *static_cast<Model*>(mdv);
+    LinOp op = op_kind == 0 ? fsa_operator(md) : sigma_s_operator(md);
+    CgResult r = pcg_solve_multi(op, *static_cast<Precond*>(p), B, k, tol, max_iter, batched != 0);
+    std::copy(r.X.begin(), r.X.end(), X);
+    for (long j = 0; j < k; ++j) {
+      const size_t sj = static_cast<size_t>(j);
+      iters[j] = r.iterations[sj];
+      conv[j] = r.converged[sj];
+      std::copy(r.tdiag[sj].begin(), r.tdiag[sj].end(), tdiag + j * max_iter);
+      std::copy(r.toff[sj].begin(), r.toff[sj].end(), toff + j * max_iter);
+      std::copy(r.rnorm[sj].begin(), r.rnorm[sj].end(), rnorm + j * max_iter);
+    }
+    *sweeps = r.sweeps;
+  });
+}
 int orc_tridiag_log_quadrature(const double* diag, const double* off, long len, double* out) {
   return guard([&] { *out = tridiag_log_quadrature(diag, off, len); });
 }
@@ -1584,6 +1671,34 @@ int orc_iterative_nll_grad(void* mdv, void* p, const double* y, const double* X,
     out[5] = static_cast<double>(r.cg_iterations);
     for (long a = 0; a < pcols; ++a) beta[a] = r.beta[static_cast<size_t>(a)];
   });
+}
+// same plus the solve's diagnostics (tests only): per-column iterations, the residual-norm history
+// rnorm (k x max_iter, column j at j*max_iter) and X at the rows `rows` (nrows x k, column-major)
+int orc_iterative_nll_grad_ex(void* mdv, void* p, const double* y, const double* X, long pcols, int L, uint64_t seed,
+                              double tol, int max_iter, int cv, int want_grad, double* out, double* beta, int* iters,
+                              double* rnorm, const long* rows, long nrows, double* xrows) {
+  return guard([&] {
+    Model& md = *static_cast<Model*>(mdv);
+    NllOut r = iterative_nll_grad(md, *static_cast<Precond*>(p), y, X, pcols, L, seed, tol, max_iter, cv,
+                                  want_grad != 0);
+    out[0] = r.nll; out[1] = r.g[0]; out[2] = r.g[1]; out[3] = r.g[2]; out[4] = r.logdet;
+    out[5] = static_cast<double>(r.cg_iterations);
+    for (long a = 0; a < pcols; ++a) beta[a] = r.beta[static_cast<size_t>(a)];
+    const long k = static_cast<long>(r.sol.iterations.size());
+    for (long j = 0; j < k; ++j) {
+      iters[j] = r.sol.iterations[static_cast<size_t>(j)];
+      const auto& h = r.sol.rnorm[static_cast<size_t>(j)];
+      std::copy(h.begin(), h.end(), rnorm + j * max_iter);
+      for (long q = 0; q < nrows; ++q) xrows[q + j * nrows] = r.sol.X[static_cast<size_t>(rows[q] + j * md.n)];
+    }
+  });
+}
+int orc_simulate_rff(const double* c, long n, int d, int nu_code, double sigma1_2, double rho, double nugget,
+                     int features, uint64_t seed, double* y) {
+  return guard([&] { simulate_rff(c, n, d, nu_code, sigma1_2, rho, nugget, features, seed, y); });
+}
+int orc_blob_locations(long n, int d, int blobs, double sd, uint64_t seed, double* out) {
+  return guard([&] { blob_locations(n, d, blobs, sd, seed, out); });
 }
 // ste_grad_trace for a given (Z, W): out [value, c_hat, var_of_mean]
 int orc_ste_grad_trace(void* mdv, void* p, const double* Z, const double* W, long L, int which, int mode, double* out) {

@@ -49,6 +49,14 @@ int orc_pcg(void* mdv, int op_kind, void* p, const double* B, long k, double tol
 int orc_tridiag_log_quadrature(const double* diag, const double* off, long len, double* out);
 int orc_iterative_nll_grad(void* mdv, void* p, const double* y, const double* X, long pcols, int L, uint64_t seed,
                            double tol, int max_iter, int cv, int want_grad, double* out, double* beta);
+int orc_iterative_nll_grad_ex(void* mdv, void* p, const double* y, const double* X, long pcols, int L, uint64_t seed,
+                              double tol, int max_iter, int cv, int want_grad, double* out, double* beta, int* iters,
+                              double* rnorm, const long* rows, long nrows, double* xrows);
+int orc_pcg_ex(void* mdv, int op_kind, void* p, const double* B, long k, double tol, int max_iter, int batched,
+               double* X, int* iters, int* conv, double* tdiag, double* toff, double* rnorm, int* sweeps);
+int orc_simulate_rff(const double* c, long n, int d, int nu_code, double sigma1_2, double rho, double nugget,
+                     int features, uint64_t seed, double* y);
+int orc_blob_locations(long n, int d, int blobs, double sd, uint64_t seed, double* out);
 int orc_ste_grad_trace(void* mdv, void* p, const double* Z, const double* W, long L, int which, int mode, double* out);
 int orc_pred_make(void* mdv, const double* pc, long np, void** out, long* nnz);
 void orc_pred_free(void* p);

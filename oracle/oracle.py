@@ -87,6 +87,13 @@ def lib():
             "orc_tridiag_log_quadrature": (C.c_int, [dp, dp, C.c_long, C.POINTER(C.c_double)]),
             "orc_iterative_nll_grad": (C.c_int, [vp, vp, dp, dp, C.c_long, C.c_int, C.c_uint64, C.c_double, C.c_int,
                                                  C.c_int, C.c_int, dp, dp]),
+            "orc_iterative_nll_grad_ex": (C.c_int, [vp, vp, dp, dp, C.c_long, C.c_int, C.c_uint64, C.c_double,
+                                                    C.c_int, C.c_int, C.c_int, dp, dp, ip, dp, lp, C.c_long, dp]),
+            "orc_pcg_ex": (C.c_int, [vp, C.c_int, vp, dp, C.c_long, C.c_double, C.c_int, C.c_int, dp, ip, ip, dp,
+                                     dp, dp, C.POINTER(C.c_int)]),
+            "orc_simulate_rff": (C.c_int, [dp, C.c_long, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                           C.c_int, C.c_uint64, dp]),
+            "orc_blob_locations": (C.c_int, [C.c_long, C.c_int, C.c_int, C.c_double, C.c_uint64, dp]),
             "orc_ste_grad_trace": (C.c_int, [vp, vp, dp, dp, C.c_long, C.c_int, C.c_int, dp]),
             "orc_pred_make": (C.c_int, [vp, dp, C.c_long, C.POINTER(vp), C.POINTER(C.c_long)]),
             "orc_pred_free": (None, [vp]),
@@ -351,6 +358,59 @@ def iterative_nll_grad(model: Model, P: Precond, y, X=None, num_probes=50, seed=
                                         1 if want_grad else 0, out, beta))
     return {"nll": out[0], "grad": out[1:4].copy(), "logdet": out[4], "cg_iterations": int(out[5]),
             "beta": beta[:p].copy()}
+
+
+def iterative_nll_grad_ex(model: Model, P: Precond, y, X=None, num_probes=50, seed=0, tol=1e-3, max_iter=1000,
+                          cv="optimal", want_grad=True, rows=None):
+    """iterative_nll_grad plus the solve's diagnostics (tests only): per-column CG iterations,
+    residual-norm histories ``rnorm[j]`` (||r||_2 after each iteration) and X at ``rows``."""
+    y = F(y)
+    p = 0 if X is None else np.asarray(X).reshape(model.n, -1).shape[1]
+    Xf = F(np.zeros((model.n, 1))) if p == 0 else F(np.asarray(X).reshape(model.n, p))
+    k = num_probes + 1 + p
+    rows = np.zeros(0, np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    out = F(np.zeros(6))
+    beta = F(np.zeros(max(p, 1)))
+    it = np.zeros(k, np.int32)
+    rn = F(np.zeros((max_iter, k)))
+    xr = F(np.zeros((max(len(rows), 1), k)))
+    _check(lib().orc_iterative_nll_grad_ex(model.h, P.h, y, Xf, p, num_probes, seed, tol, max_iter, CV_CODE[cv],
+                                           1 if want_grad else 0, out, beta, it, rn, rows, len(rows), xr))
+    return {"nll": out[0], "grad": out[1:4].copy(), "logdet": out[4], "cg_iterations": int(out[5]),
+            "beta": beta[:p].copy(), "iterations": it, "rnorm": [rn[: it[j], j].copy() for j in range(k)],
+            "xrows": xr[: len(rows)].copy()}
+
+
+def pcg_solve_multi_ex(model: Model, P: Precond, B, tol=1e-3, max_iter=1000, op="fsa"):
+    """pcg_solve_multi plus the per-column residual-norm histories (tests only)."""
+    B = F(B).reshape(model.n, -1, order="F")
+    k = B.shape[1]
+    X = F(np.zeros_like(B))
+    it = np.zeros(k, np.int32)
+    cv = np.zeros(k, np.int32)
+    td, to, rn = (F(np.zeros((max_iter, k))) for _ in range(3))
+    sw = C.c_int()
+    _check(lib().orc_pcg_ex(model.h, 0 if op == "fsa" else 1, P.h, B, k, tol, max_iter, 1, X, it, cv, td, to, rn,
+                            C.byref(sw)))
+    tri = [(td[: it[j], j].copy(), to[: max(it[j] - 1, 0), j].copy()) for j in range(k)]
+    return {"X": X, "iterations": it, "converged": cv.astype(bool), "tridiags": tri, "sweeps": sw.value,
+            "rnorm": [rn[: it[j], j].copy() for j in range(k)]}
+
+
+def simulate_rff(coords, nu, sigma1_2, rho, nugget, features=1024, seed=0):
+    """Synthetic response of the BASELINE configs: RFF Matern draw + N(0, nugget) noise."""
+    c = F(coords)
+    n, d = c.shape
+    y = F(np.zeros(n))
+    _check(lib().orc_simulate_rff(c, n, d, NU_CODE[nu], sigma1_2, rho, nugget, features, seed, y))
+    return y
+
+
+def blob_locations(n, d, blobs, sd, seed):
+    """Config-5 locations: mixture of seeded Gaussian blobs on [0,1]^d (points outside rejected)."""
+    out = F(np.zeros((n, d)))
+    _check(lib().orc_blob_locations(n, d, blobs, sd, seed, out))
+    return out
 
 
 def ste_grad_trace(model, P, Z, W, which, mode="optimal"):

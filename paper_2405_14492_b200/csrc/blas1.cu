@@ -112,11 +112,13 @@ __global__ void k_cg_alpha(const double* __restrict__ hv, long k, int it, int ma
 }
 
 // residual test on the unpreconditioned residual (krylov.cpp:77-82)
-__global__ void k_cg_check(const double* __restrict__ rr, long k, double tol, CgState st) {
+__global__ void k_cg_check(const double* __restrict__ rr, long k, double tol, int it, int max_iter, CgState st) {
   const long j = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= k) return;
   if (!st.active[j]) return;
-  if (sqrt(rr[j]) < tol) {
+  const double rn = sqrt(rr[j]);
+  st.rnorm[j * max_iter + it] = rn;
+  if (rn < tol) {
     st.converged[j] = 1;
     st.active[j] = 0;
   }
@@ -585,8 +587,8 @@ void cg_alpha(const double* hv, long k, int it, int max_iter, const CgState& st,
   k_cg_alpha<<<nblk(k, 128), 128, 0, s>>>(hv, k, it, max_iter, st);
   FSA_LAUNCH_CHECK();
 }
-void cg_check(const double* rr, long k, double tol, const CgState& st, cudaStream_t s) {
-  k_cg_check<<<nblk(k, 128), 128, 0, s>>>(rr, k, tol, st);
+void cg_check(const double* rr, long k, double tol, int it, int max_iter, const CgState& st, cudaStream_t s) {
+  k_cg_check<<<nblk(k, 128), 128, 0, s>>>(rr, k, tol, it, max_iter, st);
   FSA_LAUNCH_CHECK();
 }
 void cg_beta(const double* rzn, long k, const CgState& st, cudaStream_t s) {
@@ -794,9 +796,13 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
           st.iterations[j] = it + 1;
         }
       } else if (MODE == 1) {  // residual test (krylov.cpp:77-82)
-        if (st.active[j] && sqrt(t) < tol) {
-          st.converged[j] = 1;
-          st.active[j] = 0;
+        if (st.active[j]) {
+          const double rn = sqrt(t);
+          st.rnorm[j * max_iter + it] = rn;
+          if (rn < tol) {
+            st.converged[j] = 1;
+            st.active[j] = 0;
+          }
         }
       } else {  // beta = rz_new / rz (krylov.cpp:83-90)
         if (!st.active[j]) {

@@ -20,6 +20,7 @@ struct CgState {
   int* iterations;
   double* tdiag;  // [k][max_iter]
   double* toff;   // [k][max_iter]
+  double* rnorm;  // [k][max_iter]: ||r||_2 after each iteration (diagnostics: tie margins vs the oracle)
   int* err;
   int* host_flags;  // mapped pinned memory: [num_active, err]
 };
@@ -51,7 +52,7 @@ void unpack_cols(const double* in, long n, long k, const int* perm_dev, long tp,
 void cg_start(const double* rr, long k, double tol, const CgState& st, cudaStream_t s);
 void cg_start_rz(const double* rz, long k, const CgState& st, cudaStream_t s);
 void cg_alpha(const double* hv, long k, int it, int max_iter, const CgState& st, cudaStream_t s);
-void cg_check(const double* rr, long k, double tol, const CgState& st, cudaStream_t s);
+void cg_check(const double* rr, long k, double tol, int it, int max_iter, const CgState& st, cudaStream_t s);
 void cg_beta(const double* rzn, long k, const CgState& st, cudaStream_t s);
 void cg_count(long k, const CgState& st, cudaStream_t s);
 void update_xr(double* X, double* R, const double* H, const double* V, const double* alpha, long n, long tp, long k,

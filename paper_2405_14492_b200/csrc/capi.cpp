@@ -260,6 +260,21 @@ int fsa_ctx_set_gemm_mode(fsa_ctx* ctx, int mode) {
     ctx->c->gemm_mode = mode;
   });
 }
+int fsa_ctx_last_cg(fsa_ctx* ctx, int64_t* k, int64_t cap_k, int64_t cap_len, int* iterations, double* rnorm) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const Context& c = *ctx->c;
+    const int64_t kk = static_cast<int64_t>(c.last_cg_iterations.size());
+    if (k) *k = kk;
+    for (int64_t j = 0; j < std::min(kk, cap_k); ++j) {
+      if (iterations) iterations[j] = c.last_cg_iterations[static_cast<size_t>(j)];
+      if (!rnorm) continue;
+      const auto& h = c.last_cg_rnorm[static_cast<size_t>(j)];
+      for (int64_t i = 0; i < cap_len; ++i)
+        rnorm[j * cap_len + i] = i < static_cast<int64_t>(h.size()) ? h[static_cast<size_t>(i)] : 0.0;
+    }
+  });
+}
 int fsa_ctx_synchronize(fsa_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");

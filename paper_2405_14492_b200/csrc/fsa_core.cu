@@ -834,7 +834,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   w.dots.alloc(static_cast<size_t>(4 * tp));
   w.dbl.alloc(static_cast<size_t>(6 * k));
   w.ints.alloc(static_cast<size_t>(3 * k + 1));
-  w.tri.alloc(static_cast<size_t>(2 * k * maxit));
+  w.tri.alloc(static_cast<size_t>(3 * k * maxit));
   CgState st;
   st.rz = w.dbl.get();
   st.alpha_prev = st.rz + k;
@@ -848,13 +848,14 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   st.err = st.active + 3 * k;
   st.tdiag = w.tri.get();
   st.toff = st.tdiag + k * maxit;
+  st.rnorm = st.toff + k * maxit;
   st.host_flags = ctx->host_flags_dev;
   double* rr = w.dots.get();
   double* hv = rr + tp;
   double* rz = rr + 2 * tp;
   double* part = w.part.get();
   FSA_CUDA(cudaMemsetAsync(st.err, 0, sizeof(int), s));
-  FSA_CUDA(cudaMemsetAsync(st.tdiag, 0, sizeof(double) * 2 * k * maxit, s));
+  FSA_CUDA(cudaMemsetAsync(st.tdiag, 0, sizeof(double) * 3 * k * maxit, s));
   FSA_CUDA(cudaMemcpyAsync(w.R.get(), B, sizeof(double) * blk, cudaMemcpyDeviceToDevice, s));
   FSA_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * blk, s));
   const double flops_mn = 2.0 * md->m * n * k;
@@ -1056,7 +1057,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s,
                    w.wmax.get(), kOzCols);
       else
-        cg_check(rr, k, opts.tol, st, s);
+        cg_check(rr, k, opts.tol, it, maxit, st, s);
     }
     if (!jfused) precond(rz, !ctl);
     {
@@ -1097,23 +1098,27 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   // only the first `sweeps` entries of each column's tridiagonal can be set: strided copy
   // into pinned staging (2 k sweeps doubles instead of 2 k max_iter)
   const long used = res.sweeps > 0 ? res.sweeps : 1;
-  ctx->pin1.ensure(static_cast<size_t>(2 * k * used + 2 * k));
+  ctx->pin1.ensure(static_cast<size_t>(3 * k * used + 2 * k));
   double* td = ctx->pin1.p;
-  int* hint = reinterpret_cast<int*>(td + 2 * k * used);
+  int* hint = reinterpret_cast<int*>(td + 3 * k * used);
   FSA_CUDA(cudaMemcpyAsync(hint, st.iterations, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
   FSA_CUDA(cudaMemcpyAsync(hint + k, st.converged, sizeof(int) * k, cudaMemcpyDeviceToHost, s));
   FSA_CUDA(cudaMemcpy2DAsync(td, sizeof(double) * used, st.tdiag, sizeof(double) * maxit, sizeof(double) * used,
-                             2 * k, cudaMemcpyDeviceToHost, s));
+                             3 * k, cudaMemcpyDeviceToHost, s));
   FSA_CUDA(cudaStreamSynchronize(s));
   res.iterations.assign(hint, hint + k);
   res.converged.assign(hint + k, hint + 2 * k);
   res.tdiag.resize(static_cast<size_t>(k));
   res.toff.resize(static_cast<size_t>(k));
+  res.rnorm.resize(static_cast<size_t>(k));
   for (long j = 0; j < k; ++j) {
     const int it = res.iterations[static_cast<size_t>(j)];
     res.tdiag[static_cast<size_t>(j)].assign(td + j * used, td + j * used + it);
     if (it > 1) res.toff[static_cast<size_t>(j)].assign(td + (k + j) * used, td + (k + j) * used + it - 1);
+    res.rnorm[static_cast<size_t>(j)].assign(td + (2 * k + j) * used, td + (2 * k + j) * used + it);
   }
+  ctx->last_cg_iterations = res.iterations;
+  ctx->last_cg_rnorm = res.rnorm;
   return res;
 }
 

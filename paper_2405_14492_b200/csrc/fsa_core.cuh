@@ -82,6 +82,10 @@ struct Context {
   long launches = 0;  // kernels issued by the library (approximate: per host call site)
   // dense m x n passes with U: 0 auto (INT8 tensor-core Ozaki path when t_pad <= 64), 1 DMMA fp64, 2 Ozaki
   int gemm_mode = 0;
+  // per-column iteration counts and residual-norm histories of the last PCG solve on this
+  // context (fsa_ctx_last_cg: parity diagnostics)
+  std::vector<int> last_cg_iterations;
+  std::vector<std::vector<double>> last_cg_rnorm;
 
   explicit Context(int dev);
   ~Context();
@@ -270,6 +274,7 @@ struct CgResult {
   std::vector<int> iterations;
   std::vector<int> converged;
   std::vector<std::vector<double>> tdiag, toff;
+  std::vector<std::vector<double>> rnorm;  // ||r||_2 after each iteration, per column
   int sweeps = 0;
   bool all_converged() const;
   int max_iterations() const;

@@ -87,6 +87,7 @@ _SIGS = {
     "fsa_ctx_set_replicated": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_synchronize": (C.c_int, [_vp]),
     "fsa_ctx_set_gemm_mode": (C.c_int, [_vp, C.c_int]),
+    "fsa_ctx_last_cg": (C.c_int, [_vp, C.POINTER(C.c_int64), C.c_int64, C.c_int64, _vp, _vp]),
     "fsa_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fsa_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_reset_timers": (C.c_int, [_vp]),
@@ -309,6 +310,17 @@ class Context:
     def set_gemm_mode(self, mode="auto"):
         """Dense U passes: 'auto' (INT8 tensor-core Ozaki path for <= 64 RHS columns), 'dmma', 'ozaki'."""
         _check(lib().fsa_ctx_set_gemm_mode(self.h, self.GEMM_MODES[mode]))
+
+    def last_cg(self):
+        """Per-column iteration counts and residual-norm histories of the last PCG solve."""
+        k = C.c_int64()
+        _check(lib().fsa_ctx_last_cg(self.h, C.byref(k), 0, 0, None, None))
+        it = np.zeros(k.value, np.int32)
+        _check(lib().fsa_ctx_last_cg(self.h, C.byref(k), k.value, 0, it.ctypes.data, None))
+        cap = max(int(it.max()) if len(it) else 0, 1)
+        rn = np.zeros((k.value, cap))
+        _check(lib().fsa_ctx_last_cg(self.h, C.byref(k), k.value, cap, it.ctypes.data, rn.ctypes.data))
+        return {"iterations": it, "rnorm": [rn[j, : it[j]].copy() for j in range(k.value)]}
 
     def stream(self) -> int:
         s = _vp()

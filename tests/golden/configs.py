@@ -1,0 +1,49 @@
+"""The BASELINE.json configurations as concrete seeded workloads.
+
+Shared by bench.py, the fixture generator (make_config_fixtures.py) and the GPU parity tests so
+that all three build identical inputs: coordinates = uniform_locations(n, 2, 1) (or the config-5
+blob mixture, seed 1), inducing points = select_random / select_kmeanspp(coords, m, 2),
+y = simulate_rff(coords, nu, sigma1_2, rho, nugget, 1024, 3), prediction points (config 3)
+= uniform_locations(n_p, 2, 101). Wendland-1 taper (the fit-path default, estimation.h:50).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+CONFIGS = {
+    1: dict(n=10_000, m=200, inducing="random", nu=0.5, s12=1.0, rho=0.1, s2=0.1, nnz=30, L=50, tol=1e-3,
+            points="uniform"),
+    2: dict(n=100_000, m=500, inducing="kmeans", nu=1.5, s12=1.0, rho=0.05, s2=0.05, nnz=80, L=50, tol=1e-3,
+            points="uniform"),
+    3: dict(n=100_000, m=500, inducing="kmeans", nu=1.5, s12=1.0, rho=0.05, s2=0.05, nnz=80, L=1000, tol=1e-3,
+            points="uniform", np=100_000),
+    4: dict(n=1_000_000, m=1000, inducing="kmeans", nu=1.5, s12=1.0, rho=0.03, s2=0.05, nnz=80, L=64, tol=1e-3,
+            points="uniform"),
+    5: dict(n=200_000, m=1000, inducing="kmeans", nu=2.5, s12=1.0, rho=0.3, s2=1e-3, nnz=120, L=50, tol=1e-4,
+            points="blobs"),
+}
+
+
+def calibrate_gamma(n, target, nnz_of):
+    """Taper range by bisection on the measured nnz/row (clustered points: the uniform-density
+    rule gamma_for_avg_row_nnz, locations.cpp:192-195, overshoots). ``nnz_of(gamma)``
+    returns the pattern's nnz; the decisions depend only on these integers, so every
+    implementation of the pattern reaches the same gamma."""
+    lo, hi = 1e-5, 0.2
+    for _ in range(30):
+        mid = math.sqrt(lo * hi)
+        avg = nnz_of(mid) / n
+        if avg < target:
+            lo = mid
+        else:
+            hi = mid
+        if abs(avg - target) / target < 0.02:
+            return mid
+    return math.sqrt(lo * hi)
+
+
+def sample_rows(n, count=512):
+    """Fixed row sample (original point order) at which solutions / variances are compared."""
+    return np.unique(np.linspace(0, n - 1, count).round().astype(np.int64))
