@@ -38,7 +38,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from tests.golden.configs import CONFIGS, calibrate_gamma  # noqa: E402
+from tests.golden.configs import CONFIGS, calibrate_gamma, model_kw  # noqa: E402
 
 METRIC = "PCG RHS-iterations/s over FSA loglik+grad evaluations"
 
@@ -183,7 +183,7 @@ def cpu_pcg_sample(cfg, coords, ind, gamma, y, sweeps=2):
     krylov.cpp:83); RHS-iterations / s."""
     from oracle import oracle as O
 
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     om = O.Model(coords, ind, **kw)
     P = O.Precond(om, "fitc", plain=True)
     Z = P.sample_probes(cfg["L"], 0)
@@ -241,7 +241,7 @@ def cpu_prediction_sample(cfg, coords, ind, gamma, plocs, probes=256, det_cols=N
     T(batch) = T(det + 1 batch) - T(det) from a second run with the deterministic pieces only."""
     from oracle import oracle as O
 
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     om = O.Model(coords, ind, **kw)
     t0 = time.perf_counter()
     pr = O.PredictionSet(om, plocs)
@@ -293,7 +293,7 @@ def run_prediction(args, cfg):
     ctx = fsa.Context(0)
     coords, ind, gamma, y = make_inputs(cfg, fsa, ctx)
     plocs = fsa.uniform_locations(cfg["np"], 2, 101)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     geo = fsa.Geometry(coords, gamma, ctx)
     nnz = geo.nnz()
     md = fsa.FsaModel.assemble(None, ind, geometry=geo, **kw)
@@ -458,7 +458,7 @@ def main():
     ctx = make_ctx()
     coords, ind, gamma, y = make_inputs(cfg, fsa, ctx)
     fp64_peak = measure_fp64_peak(torch)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     L, tol = cfg["L"], cfg["tol"]
     stream = torch.cuda.ExternalStream(ctx.stream())
 
@@ -477,14 +477,18 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    ctx.set_profiling(True)
-    ctx.reset_timers()
+    # timed pass (the headline): library timers off, so the PCG sweeps run as replayed CUDA graphs
     sampler = ClockSampler(local)
     sampler.start()
     l0 = fsa.launch_count()
     results, ms = time_steps(step, args.steps, ctx, stream, torch, barrier, max_over_ranks)
     launches = fsa.launch_count() - l0
     clocks = sampler.stop()
+    # second timed pass with the per-kernel-group CUDA-event timers (eager launches): the roofline
+    # entries' average launch durations and shares come from here
+    ctx.set_profiling(True)
+    ctx.reset_timers()
+    presults, pms = time_steps(step, args.steps, ctx, stream, torch, barrier, max_over_ranks)
     timers = ctx.timers()
     ctx.set_profiling(False)
     copies = 1 if sharded else world  # replicas each solve the whole problem
@@ -518,7 +522,7 @@ def main():
         ach = units_per_launch / (avg * 1e-3) / 1e9
         return {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": traffic.get(kernel.split()[0]), "avg_launch_ms": avg, "launches": t["count"],
-                "share_of_step": t["ms"] / ms, "units_per_launch": units_per_launch}
+                "share_of_step": t["ms"] / pms, "units_per_launch": units_per_launch}
 
     int8 = tp_ <= 64
     nnz_loc = nnz / (world if sharded else 1)
@@ -539,7 +543,7 @@ def main():
     roofline["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
     roofline["all"] = kernels
     roofline["fp64_dgemm_tflops_measured"] = fp64_peak
-    sweeps = sum(r["sweeps"] for r in results)
+    sweeps = sum(r["sweeps"] for r in presults)
     sweep_groups = ("spmm", "lowrank_project", "lowrank_expand", "core_solve", "cg_blas1", "allreduce",
                     "halo_exchange")
     t_sweep = sum(timers[k]["ms"] for k in sweep_groups if k in timers) / max(sweeps, 1)
@@ -555,6 +559,7 @@ def main():
         "vectors": (80.0 * n_ * t_, 12.0 * n_ * t_),
     }
     t_roof = sum(max(b / (hbm * 1e9), f / (fp64_peak * 1e12)) for b, f in phases.values()) * 1e3
+    roofline["profiled_pass_ms_per_step"] = pms / args.steps
     roofline["sweep"] = {"unit": "one PCG sweep", "t_measured_ms": t_sweep,
                          "own_floor": {"bytes": floor_bytes, "t_floor_ms": t_floor,
                                        "frac": t_floor / t_sweep if t_sweep else None,
@@ -676,7 +681,7 @@ def strong_record(args, fsa, torch, world, rank, local, dist, barrier, max_over_
     dist.broadcast_object_list(uid, src=0)
     ctx = fsa.Context.nccl(local, rank, world, uid[0])
     coords, ind, gamma, y = make_inputs(cfg, fsa, ctx)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     geo = fsa.Geometry(coords, gamma, ctx)
     geo.set_response(y)
     geo.cache_probes(True)

@@ -188,6 +188,11 @@ int fsa_model_lowrank_project(fsa_model* md, const double* V, int64_t k, double*
 int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* out);
 /* diag(Sigma_s) including the nugget (the FITC / Jacobi diagonal) and |U_i|^2 = lowrank diag */
 int fsa_model_diagonals(fsa_model* md, double* sigma_s_diag, double* lowrank_diag);
+/* Diagnostics (no reference counterpart): average device time of one launch group of a PCG
+ * sweep kernel on synthetic k-column blocks — which 0: block SpMM + direction update
+ * (k_spmm_rt), 1: Ozaki projection, 2: Ozaki expansion + Woodbury epilogue; flags (which = 0):
+ * 1 skip the DMMAs, 2 skip the epilogue, 4 skip the RHS-row gather, 8 skip the value tiles. */
+int fsa_debug_kernel_bench(fsa_model* md, int which, int64_t k, int reps, int flags, double* ms_out);
 
 /* ---- preconditioners (make_preconditioner, estimation.h:81-82; preconditioners.h) -- */
 /* type: 0 none (IdentityPrecond), 1 diagonal (DiagPrecond), 2 fitc (FitcPrecond::from_fsa(model, true)) */

@@ -781,6 +781,7 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
     for (int w = 0; w < 8; ++w) t += red[w];
     out[c] = t;
     const long j = c;
+    if (st.it_dev != nullptr) it = *st.it_dev;
     if (j < k) {
       if (MODE == 0) {  // alpha = rz / h'v, tridiagonal push (krylov.cpp:66-75)
         if (!st.active[j]) {
@@ -834,8 +835,14 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
         cnt += __syncthreads_count(jj < k && reinterpret_cast<volatile int*>(st.active)[jj] != 0);
       }
       if (tid == 0) {
-        st.host_flags[0] = cnt;
-        st.host_flags[1] = *reinterpret_cast<volatile int*>(st.err);
+        int* hf = st.host_flags;
+        if (st.it_dev != nullptr) {  // graph-captured sweep: slot by the device sweep index, then advance it
+          const int itv = *st.it_dev;
+          hf += 2 * (itv & 1);
+          *st.it_dev = itv + 1;
+        }
+        hf[0] = cnt;
+        hf[1] = *reinterpret_cast<volatile int*>(st.err);
         *ticket = 0u;
       }
     }

@@ -23,6 +23,10 @@ struct CgState {
   double* rnorm;  // [k][max_iter]: ||r||_2 after each iteration (diagnostics: tie margins vs the oracle)
   int* err;
   int* host_flags;  // mapped pinned memory: [num_active, err]
+  // graph-captured sweeps (fused single-rank path): the sweep index lives on the device; the
+  // control kernels read it, and the last one (k_colsum_ctl<2>) writes the flags into slot
+  // 2 (it % 2) of host_flags and advances it. nullptr: `it` comes from the host launch.
+  int* it_dev = nullptr;
 };
 
 size_t coldot_scratch(long n, long t);

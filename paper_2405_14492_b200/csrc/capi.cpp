@@ -2,6 +2,7 @@
 #include "../../include/fsa_b200.h"
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <memory>
@@ -15,6 +16,7 @@
 #include "inputs.h"
 #include "kmeans.cuh"
 #include "predict.cuh"
+#include "sparse.cuh"
 
 using namespace fsa;
 
@@ -580,6 +582,58 @@ int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* 
     FSA_CUDA(cudaMemcpyAsync(Wd.get(), h.data(), sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
     M->expand(Wd.get(), tp, Y.get());
     to_host_block(M, Y.get(), k, tp, out);
+  });
+}
+int fsa_debug_kernel_bench(fsa_model* md, int which, int64_t k, int reps, int flags, double* ms_out) {
+  return guard([&] {
+    need(md, "model");
+    Bind bind_(md->m->ctx);
+    need(ms_out, "ms_out");
+    Model* M = md->m.get();
+    single_rank(M->ctx, "debug_kernel_bench");
+    require(k >= 1 && reps >= 1, "invalid sizes");
+    cudaStream_t s = M->ctx->stream;
+    const long tp = pad_cols(k), np = M->n_pad, mp = M->m_pad;
+    const size_t blk = static_cast<size_t>(M->n_ext_pad * tp);
+    DBuf<double> Z(blk), Lw(blk), H(blk), V(blk), R(blk), part(static_cast<size_t>((np / 32 + 1) * tp * 4)),
+        dots(static_cast<size_t>(4 * tp)), beta(static_cast<size_t>(tp)), W(static_cast<size_t>(mp * tp));
+    std::vector<double> h(blk);
+    for (size_t i = 0; i < blk; ++i) h[i] = std::sin(0.37 * static_cast<double>(i)) * 0.5;
+    for (DBuf<double>* b : {&Z, &Lw, &H, &V, &R})
+      FSA_CUDA(cudaMemcpyAsync(b->get(), h.data(), sizeof(double) * blk, cudaMemcpyHostToDevice, s));
+    std::vector<double> hb(static_cast<size_t>(tp), 0.3), hw(static_cast<size_t>(mp * tp));
+    for (size_t i = 0; i < hw.size(); ++i) hw[i] = std::cos(0.11 * static_cast<double>(i));
+    FSA_CUDA(cudaMemcpyAsync(beta.get(), hb.data(), sizeof(double) * tp, cudaMemcpyHostToDevice, s));
+    FSA_CUDA(cudaMemcpyAsync(W.get(), hw.data(), sizeof(double) * mp * tp, cudaMemcpyHostToDevice, s));
+    if (which != 0) M->ensure_ozaki();
+    auto run = [&] {
+      switch (which) {
+        case 0:
+          spmm_block_dot_h(M->geo->pat, M->gval.get(), Z.get(), tp, V.get(), tp, tp, dots.get(), part.get(),
+                           Lw.get(), H.get(), beta.get(), k, false, s, false);
+          break;
+        case 1:
+          ozaki_project(M->oz, R.get(), tp, tp, M->Dinv.get(), W.get(), s, false);
+          break;
+        default:
+          ozaki_expand_keep(M->oz, W.get(), tp, tp, Z.get(), Lw.get(), R.get(), M->Dinv.get(), dots.get(),
+                            part.get(), s, false, nullptr);
+          break;
+      }
+    };
+    g_spmm_dbg = flags;
+    run();
+    cudaEvent_t a = M->ctx->ev(), b = M->ctx->ev();
+    FSA_CUDA(cudaEventRecord(a, s));
+    for (int i = 0; i < reps; ++i) run();
+    FSA_CUDA(cudaEventRecord(b, s));
+    FSA_CUDA(cudaEventSynchronize(b));
+    g_spmm_dbg = 0;
+    float ms = 0.f;
+    FSA_CUDA(cudaEventElapsedTime(&ms, a, b));
+    *ms_out = static_cast<double>(ms) / reps;
+    M->ctx->pool.push_back(a);
+    M->ctx->pool.push_back(b);
   });
 }
 int fsa_model_diagonals(fsa_model* md, double* sdiag, double* lowrank) {

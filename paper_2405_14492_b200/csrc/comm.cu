@@ -56,6 +56,14 @@ __global__ void k_sum_ptrs(PtrSet ps, int world, long count, double* __restrict_
   for (int j = 0; j < world; ++j) s += ps.p[j][i];
   out[i] = s;
 }
+// out[i] = sum_j g[j * count + i] in rank order (the gathered partials of NcclComm::allreduce)
+__global__ void k_sum_ranks(const double* __restrict__ g, int world, long count, double* __restrict__ out) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int j = 0; j < world; ++j) s += g[static_cast<long>(j) * count + i];
+  out[i] = s;
+}
 }  // namespace
 
 ThreadComm::ThreadComm(std::shared_ptr<ThreadGroup> g, int rank) : g_(std::move(g)), rank_(rank) {}
@@ -117,6 +125,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -138,6 +147,7 @@ NcclApi& nccl() {
   api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
   api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
   api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
   api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
@@ -169,11 +179,21 @@ NcclComm::NcclComm(int rank, int world, const void* unique_id) : rank_(rank), wo
 NcclComm::~NcclComm() {
   if (comm_) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
 }
+// Fixed-order sum over ranks (SURVEY §8e "determinism needs fixed-order reductions"): the rank
+// partials are all-gathered and every rank adds them in rank order, so the result is bitwise
+// identical on every rank, run to run, and equal to the in-process ThreadComm's k_sum_ptrs order
+// (whatever ring / tree / NVLS algorithm NCCL picks for the transfer). The payloads are an m x t
+// projection (<= 0.6 MB at config 4) and t-long dot vectors: at W <= 8 the W-fold gather volume
+// costs a few microseconds on NVLink, the same launch count as ncclAllReduce.
 void NcclComm::allreduce(double* dev, long count, cudaStream_t s) {
   if (world_ == 1 || count == 0) return;
-  nccl_check(nccl().AllReduce(dev, dev, static_cast<size_t>(count), ncclDouble, ncclSum,
+  const size_t need = static_cast<size_t>(count) * static_cast<size_t>(world_);
+  if (gather_.n < need) gather_.alloc(need);
+  nccl_check(nccl().AllGather(dev, gather_.get(), static_cast<size_t>(count), ncclDouble,
                               static_cast<ncclComm_t>(comm_), s),
-             "ncclAllReduce");
+             "ncclAllGather");
+  k_sum_ranks<<<static_cast<unsigned>(cdiv(count, 256)), 256, 0, s>>>(gather_.get(), world_, count, dev);
+  FSA_LAUNCH_CHECK();
 }
 void NcclComm::exchange(const std::vector<HaloPeer>& peers, cudaStream_t s) {
   if (world_ == 1) return;

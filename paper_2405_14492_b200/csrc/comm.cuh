@@ -33,7 +33,8 @@ class Comm {
   virtual int rank() const = 0;
   virtual int size() const = 0;
   virtual std::string kind() const = 0;
-  // in-place sum over ranks of a device array; identical result on every rank
+  // in-place sum over ranks of a device array, added in rank order: bitwise identical on every
+  // rank and for every implementation (thread group, NCCL)
   virtual void allreduce(double* dev, long count, cudaStream_t s) = 0;
   // point-to-point exchange with each listed peer
   virtual void exchange(const std::vector<HaloPeer>& peers, cudaStream_t s) = 0;
@@ -80,6 +81,7 @@ class NcclComm final : public Comm {
  private:
   int rank_, world_;
   void* comm_ = nullptr;  // ncclComm_t
+  DBuf<double> gather_;   // [world][count] partials of the fixed-order allreduce
 };
 // fills 128 bytes with a fresh ncclUniqueId (rank 0 calls it and broadcasts)
 void nccl_unique_id(void* out);

@@ -833,7 +833,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   if (w.part.n < npart) w.part.alloc(npart);
   w.dots.alloc(static_cast<size_t>(4 * tp));
   w.dbl.alloc(static_cast<size_t>(6 * k));
-  w.ints.alloc(static_cast<size_t>(3 * k + 1));
+  w.ints.alloc(static_cast<size_t>(3 * k + 2));
   w.tri.alloc(static_cast<size_t>(3 * k * maxit));
   CgState st;
   st.rz = w.dbl.get();
@@ -999,83 +999,121 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     num_active = f[0];
     res.sweeps = sw + 1;
   };
-  for (int it = 0; it < maxit && num_active > 0; ++it) {
-    st.host_flags = ctx->host_flags_dev + 2 * (it & 1);
+  // One sweep's kernels. On the fused single-rank path (ctl) sweeps 1, 2, ... are identical
+  // launch sequences (the sweep index is read on the device, CgState::it_dev), so they are
+  // captured once into a CUDA graph and replayed: one launch per sweep instead of eleven, and
+  // no host gaps between the kernels (profiling runs keep eager launches for the group timers).
+  auto sweep = [&](int it) {
     if (fuse_h) {  // H = Z + beta H, V = (Lw + Sigma_s Z) + beta V; h.v
-      md->halo_exchange(w.Z.get(), tp);
-      // CSR + Z (once per row), Lw, H, V read + H, V write
-      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 48.0 * n * k);
-      spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
-                       w.H.get(), st.beta, k, first_sweep, s, !ctl);
-      first_sweep = false;
-      comm.allreduce(hv, tp, s);
-    } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
-      md->halo_exchange(w.H.get(), tp);
-      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-      if (oz_spmm)
-        // valid rows of H: owned (padded) + halo; the tail up to n_ext_pad is never written
-        ozaki_spmm_dot(md->ozs, md->geo->pat, w.H.get(), md->n_pad + (md->world() > 1 ? md->geo->shard.n_halo : 0),
-                       tp, w.V.get(), w.Vlr.get(), hv, part, s);
-      else if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
-        spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, w.Vlr.get(), s);
-      else
-        spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
-                 tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
-      comm.allreduce(hv, tp, s);
-    } else if (jfused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp)) {  // V = Sigma_s H; h.v
-      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
-      spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, nullptr, s);
-    } else if (jfused) {
-      KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
-      spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
-               tp, 1.0, 0.0, hv, part, s);
-    } else {
-      A.apply(w.H.get(), w.V.get(), tp);
-      KTimer t(ctx, "cg_blas1");
-      launch_coldot(w.H.get(), w.V.get(), n, tp, k, hv, part, s);
-    }
-    {
-      KTimer t(ctx, "cg_blas1");
-      if (ctl)  // alpha, and the ymax clear of the residual update below
-        colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s,
-                   md->oz.ymax.get(), static_cast<long>(md->oz.ymax.n));
-      else
-        cg_alpha(hv, k, it, maxit, st, s);
-      if (oz) {
-        if (!ctl) FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
-        update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
-                          md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl);
-        ymax_ready = true;
+        md->halo_exchange(w.Z.get(), tp);
+        // CSR + Z (once per row), Lw, H, V read + H, V write
+        KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 48.0 * n * k);
+        spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
+                         w.H.get(), st.beta, k, first_sweep, s, !ctl);
+        first_sweep = false;
+        comm.allreduce(hv, tp, s);
+      } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
+        md->halo_exchange(w.H.get(), tp);
+        KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
+        if (oz_spmm)
+          // valid rows of H: owned (padded) + halo; the tail up to n_ext_pad is never written
+          ozaki_spmm_dot(md->ozs, md->geo->pat, w.H.get(), md->n_pad + (md->world() > 1 ? md->geo->shard.n_halo : 0),
+                         tp, w.V.get(), w.Vlr.get(), hv, part, s);
+        else if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
+          spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, w.Vlr.get(), s);
+        else
+          spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
+                   tp, 1.0, 1.0, hv, part, s, w.Vlr.get());
+        comm.allreduce(hv, tp, s);
+      } else if (jfused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp)) {  // V = Sigma_s H; h.v
+        KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
+        spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, nullptr, s);
       } else if (jfused) {
-        update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
-                             s);
+        KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 16.0 * n * k);
+        spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,
+                 tp, 1.0, 0.0, hv, part, s);
       } else {
-        update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
+        A.apply(w.H.get(), w.V.get(), tp);
+        KTimer t(ctx, "cg_blas1");
+        launch_coldot(w.H.get(), w.V.get(), n, tp, k, hv, part, s);
       }
-      comm.allreduce(rr, k, s);
-      if (ctl)  // residual test, and the wmax clear of this sweep's core solve
-        colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s,
-                   w.wmax.get(), kOzCols);
-      else
-        cg_check(rr, k, opts.tol, it, maxit, st, s);
-    }
-    if (!jfused) precond(rz, !ctl);
-    {
-      KTimer t(ctx, "cg_blas1");
-      if (ctl)  // beta and the active count
-        colsum_ctl(2, part, md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st, w.tick.get(), s);
-      else
-        cg_beta(rz, k, st, s);
-      if (fuse_h) {
-        // H and V are updated by the next sweep's SpMM
-      } else if (fused) {  // H = Z + beta H, Vlr = U^T w + beta Vlr
-        update_h2(w.H.get(), w.Z.get(), w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);
-      } else if (jfused) {  // H = D^{-1} R + beta H
-        update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, false, s);
-      } else {
-        update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
+      {
+        KTimer t(ctx, "cg_blas1");
+        if (ctl)  // alpha, and the ymax clear of the residual update below
+          colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s,
+                     md->oz.ymax.get(), static_cast<long>(md->oz.ymax.n));
+        else
+          cg_alpha(hv, k, it, maxit, st, s);
+        if (oz) {
+          if (!ctl) FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
+          update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
+                            md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl);
+          ymax_ready = true;
+        } else if (jfused) {
+          update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
+                               s);
+        } else {
+          update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
+        }
+        comm.allreduce(rr, k, s);
+        if (ctl)  // residual test, and the wmax clear of this sweep's core solve
+          colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s,
+                     w.wmax.get(), kOzCols);
+        else
+          cg_check(rr, k, opts.tol, it, maxit, st, s);
       }
-      if (!ctl) cg_count(k, st, s);
+      if (!jfused) precond(rz, !ctl);
+      {
+        KTimer t(ctx, "cg_blas1");
+        if (ctl)  // beta and the active count
+          colsum_ctl(2, part, md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st, w.tick.get(), s);
+        else
+          cg_beta(rz, k, st, s);
+        if (fuse_h) {
+          // H and V are updated by the next sweep's SpMM
+        } else if (fused) {  // H = Z + beta H, Vlr = U^T w + beta Vlr
+          update_h2(w.H.get(), w.Z.get(), w.Vlr.get(), w.Lw.get(), st.active, st.beta, np, tp, k, s);
+        } else if (jfused) {  // H = D^{-1} R + beta H
+          update_h_jacobi(w.H.get(), w.R.get(), md->Dinv.get(), st.active, st.beta, np, tp, k, false, s);
+        } else {
+          update_h(w.H.get(), w.Z.get(), st.active, st.beta, np, tp, k, s);
+        }
+        if (!ctl) cg_count(k, st, s);
+      }
+  };
+  const bool graph = ctl && !ctx->profile && std::getenv("FSA_NO_GRAPH") == nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  long graph_kernels = 0;
+  if (graph) {
+    st.it_dev = st.err + 1;
+    FSA_CUDA(cudaMemsetAsync(st.it_dev, 0, sizeof(int), s));
+  }
+  for (int it = 0; it < maxit && num_active > 0; ++it) {
+    if (graph && it > 0) {
+      if (gexec == nullptr) {
+        st.host_flags = ctx->host_flags_dev;
+        cudaGraph_t g = nullptr;
+        const long before = launch_counter().load();
+        FSA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+          sweep(it);
+        } catch (...) {
+          cudaGraph_t dead = nullptr;
+          cudaStreamEndCapture(s, &dead);
+          if (dead) cudaGraphDestroy(dead);
+          throw;
+        }
+        FSA_CUDA(cudaStreamEndCapture(s, &g));
+        graph_kernels = launch_counter().load() - before;  // captured, not yet run: counted per replay
+        launch_counter().fetch_sub(graph_kernels);
+        FSA_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+        FSA_CUDA(cudaGraphDestroy(g));
+      }
+      FSA_CUDA(cudaGraphLaunch(gexec, s));
+      launch_counter().fetch_add(graph_kernels);
+    } else {
+      st.host_flags = graph ? ctx->host_flags_dev : ctx->host_flags_dev + 2 * (it & 1);
+      sweep(it);
     }
     FSA_CUDA(cudaEventRecord(sweep_ev[it & 1], s));
     if (pending >= 0) {
@@ -1089,6 +1127,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   }
   if (pending >= 0) read_flags(pending);
   FSA_CUDA(cudaStreamSynchronize(s));
+  if (gexec != nullptr) FSA_CUDA(cudaGraphExecDestroy(gexec));
   ctx->pool.push_back(sweep_ev[0]);
   ctx->pool.push_back(sweep_ev[1]);
   md->cols_hint = 0;

@@ -200,11 +200,18 @@ constexpr int kUnionCap = 1024;   // max union size per 32-row group
 // RADIX: the group's (<= 4096) column indices are sorted by a block radix sort over key_bits
 // bits (3 to 6 passes instead of the 78 passes of the bitonic network); larger capacities
 // (the 128-row groups of the opt-in INT8 SpMM) keep the bitonic sort.
+// TILE_ORDER (32-row groups of the block SpMM): the union is then re-ordered so that columns
+// referenced by the same subset of the group's four 8-row tiles are adjacent — key = the rank of
+// the column's row-tile mask in kMaskRank (a chain 0001, 0011, 0111, 1111, 1110, 1100, 1000 in
+// which every tile's columns form one run), ties by column. A 4-column k-step then rarely mixes
+// columns of different tiles, so fewer of the 8 x 4 DMMA A tiles are stored and those stored are
+// denser (sparse.cu k_spmm_rt does one DMMA per stored tile and n-tile).
+__constant__ int kMaskRank[16] = {15, 0, 8, 1, 9, 10, 7, 2, 6, 11, 14, 12, 5, 13, 4, 3};
 template <bool RADIX>
 __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ rowptr, const int* __restrict__ col,
                                                      long nrows, int G, int kSortCap, int kCap,
                                                      int* __restrict__ ucols, int* __restrict__ ucount,
-                                                     int* __restrict__ lidx, int key_bits) {
+                                                     int* __restrict__ lidx, int key_bits, int tile_order) {
   extern __shared__ int ush[];
   int* keys = ush;
   int* flag = ush + kSortCap;
@@ -287,6 +294,32 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
     }
     lidx[p] = lo;
   }
+  if (tile_order && U > 0) {
+    __syncthreads();  // lidx (global, written by this block) and `out` complete
+    int* umask = flag;       // [U] row-tile masks
+    int* okey = keys;        // [U] order keys
+    int* oldc = keys + 2048; // [U] union columns in ascending order (U <= kCap <= 1024)
+    for (int i = tid; i < U; i += blockDim.x) {
+      umask[i] = 0;
+      oldc[i] = out[i];
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    for (long r = r0 + warp; r < r1; r += blockDim.x / 32)
+      for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) atomicOr(&umask[lidx[p]], 1 << ((r - r0) >> 3));
+    __syncthreads();
+    for (int i = tid; i < U; i += blockDim.x) okey[i] = (kMaskRank[umask[i] & 15] << 12) | i;
+    __syncthreads();
+    for (int i = tid; i < U; i += blockDim.x) {  // rank of key i (keys are distinct)
+      const int ki = okey[i];
+      int pos = 0;
+      for (int j = 0; j < U; ++j) pos += okey[j] < ki ? 1 : 0;
+      flag[i] = pos;  // new position of old slot i (umask no longer needed)
+    }
+    __syncthreads();
+    for (int i = tid; i < U; i += blockDim.x) out[flag[i]] = oldc[i];
+    for (long p = p0 + tid; p < p1; p += blockDim.x) lidx[p] = flag[lidx[p]];
+  }
   if (tid == 0) ucount[b] = U;
 }
 __global__ void k_group_compact(const int* __restrict__ ucols, int kCap, const int* __restrict__ ucount,
@@ -339,7 +372,7 @@ __global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int pad, i
 }
 // unions of G consecutive rows, padded to `pad`; false if a group exceeds the capacities
 bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& ngrp, long& gnnz, int& gmax,
-                  DBuf<long>& gptr, DBuf<int>& gcol, DBuf<int>& lidx, cudaStream_t s) {
+                  DBuf<long>& gptr, DBuf<int>& gcol, DBuf<int>& lidx, cudaStream_t s, bool tile_order = false) {
   gnnz = 0;
   ngrp = cdiv(pat.rows, G);
   if (ngrp == 0 || pat.nnz == 0) return false;
@@ -355,11 +388,13 @@ bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& n
   if (sort_cap == 4096) {
     FSA_CUDA(cudaFuncSetAttribute(k_group_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_group_union<true><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
-        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits);
+        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits,
+        tile_order ? 1 : 0);
   } else {
     FSA_CUDA(cudaFuncSetAttribute(k_group_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_group_union<false><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
-        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits);
+        pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits,
+        tile_order ? 1 : 0);
   }
   FSA_LAUNCH_CHECK();
   bad.zero(s);
@@ -505,8 +540,9 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
 }
 
 void build_groups(Csr& pat, cudaStream_t s) {
+  static const bool plain_order = std::getenv("FSA_UNION_ORDER") && std::strcmp(std::getenv("FSA_UNION_ORDER"), "plain") == 0;
   if (!build_unions(pat, kGroup, 4, kUnionSort, kUnionCap, pat.ngrp, pat.gnnz, pat.gmax, pat.gptr, pat.gcol, pat.gslot,
-                    s)) {
+                    s, !plain_order)) {
     pat.gnnz = 0;
     return;
   }

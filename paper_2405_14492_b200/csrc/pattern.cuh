@@ -58,7 +58,7 @@ struct Csr {
   // memory once per group (sparse.cu, spmm_block_dot).
   long ngrp = 0, gnnz = 0;     // gnnz = total padded union size (0: groups not built)
   DBuf<long> gptr;             // ngrp + 1 offsets into gcol (multiples of 4)
-  DBuf<int> gcol;              // union columns (ascending; padding repeats a valid column)
+  DBuf<int> gcol;              // union columns (row-tile-mask order, see k_group_union; padding repeats a valid column)
   DBuf<int> gslot;             // per entry: its index in the value blocks (kGroup * gnnz)
   int gmax = 0;                // largest padded union
   // Compact value tiles: of the dense block only the 8 x 4 DMMA A tiles (row tile rt of the

@@ -88,6 +88,7 @@ _SIGS = {
     "fsa_ctx_synchronize": (C.c_int, [_vp]),
     "fsa_ctx_set_gemm_mode": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_last_cg": (C.c_int, [_vp, C.POINTER(C.c_int64), C.c_int64, C.c_int64, _vp, _vp]),
+    "fsa_debug_kernel_bench": (C.c_int, [_vp, C.c_int, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "fsa_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fsa_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "fsa_ctx_reset_timers": (C.c_int, [_vp]),
@@ -474,6 +475,12 @@ class FsaModel:
         out = _F(np.zeros((self.n, W.shape[1])))
         _check(lib().fsa_model_lowrank_expand(self.h, W, W.shape[1], out))
         return out
+
+    def debug_kernel_bench(self, which=0, k=51, reps=20, flags=0):
+        """Average ms of one sweep-kernel launch group on synthetic blocks (diagnostics)."""
+        ms = C.c_double()
+        _check(lib().fsa_debug_kernel_bench(self.h, int(which), int(k), int(reps), int(flags), C.byref(ms)))
+        return ms.value
 
     def matmat(self, V):
         V = _F(V).reshape(self.n, -1, order="F")

@@ -21,9 +21,18 @@ CONFIGS = {
             points="uniform", np=100_000),
     4: dict(n=1_000_000, m=1000, inducing="kmeans", nu=1.5, s12=1.0, rho=0.03, s2=0.05, nnz=80, L=64, tol=1e-3,
             points="uniform"),
+    # config 5: the reference's FITC core Sigma_m + Sigma_mn D^-1 Sigma_mn^T (preconditioners.cpp:74-87) is not
+    # numerically PD at the default jitter_rel 1e-10 (nor 1e-8) on these clustered points -- the reference
+    # throws NumericalError; AssembleOptions::jitter_rel (fsa.h:16) is raised to 1e-6
     5: dict(n=200_000, m=1000, inducing="kmeans", nu=2.5, s12=1.0, rho=0.3, s2=1e-3, nnz=120, L=50, tol=1e-4,
-            points="blobs"),
+            points="blobs", jitter=1e-6),
 }
+
+
+def model_kw(cfg, gamma):
+    """FsaModel::assemble parameters of a config (Wendland-1 taper, the fit-path default)."""
+    return dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"],
+                jitter_rel=cfg.get("jitter", 1e-10))
 
 
 def calibrate_gamma(n, target, nnz_of):

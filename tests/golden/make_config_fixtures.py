@@ -34,7 +34,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
-from tests.golden.configs import CONFIGS, calibrate_gamma, sample_rows  # noqa: E402
+from tests.golden.configs import CONFIGS, calibrate_gamma, model_kw, sample_rows  # noqa: E402
 
 
 def digest(a) -> str:
@@ -56,7 +56,7 @@ def oracle_inputs(cfg):
 
 def run_nll(k, cfg, out):
     coords, ind, gamma, y = oracle_inputs(cfg)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     t0 = time.time()
     om = O.Model(coords, ind, **kw)
     P = O.Precond(om, "fitc")
@@ -125,7 +125,7 @@ def run_bench_precond(k, cfg, om, y, out, max_iter=1000):
 
 def run_prediction(k, cfg, out):
     coords, ind, gamma, y = oracle_inputs(cfg)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     plocs = O.uniform_locations(cfg["np"], 2, 101)
     t0 = time.time()
     om = O.Model(coords, ind, **kw)
@@ -141,7 +141,22 @@ def run_prediction(k, cfg, out):
           f"clamped={res['clamped']} ({dt:.0f} s)", flush=True)
 
 
+def add_spread(k):
+    """Append the ulp-perturbation self-spread to an existing fixture."""
+    path = os.path.join(HERE, f"config{k}_oracle.npz")
+    out = dict(np.load(path))
+    cfg = CONFIGS[k]
+    coords, ind, gamma, y = oracle_inputs(cfg)
+    om = O.Model(coords, ind, **model_kw(cfg, gamma))
+    run_self_spread(k, cfg, om, y, out)
+    np.savez_compressed(path, **out)
+
+
 def main(which):
+    if which and which[0] == 0:  # 0 k...: add the self-spread run to existing fixtures
+        for k in which[1:]:
+            add_spread(k)
+        return
     for k in which:
         cfg = CONFIGS[k]
         out = {"config": json.dumps(cfg, sort_keys=True)}
@@ -149,7 +164,7 @@ def main(which):
             run_prediction(k, cfg, out)
         else:
             om, coords, ind, gamma, y = run_nll(k, cfg, out)
-            if k in (1, 2):
+            if k in (1, 2, 5):
                 run_self_spread(k, cfg, om, y, out)
             if k == 5:
                 run_bench_precond(k, cfg, om, y, out)

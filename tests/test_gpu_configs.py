@@ -33,7 +33,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.golden.configs import CONFIGS, calibrate_gamma
+from tests.golden.configs import CONFIGS, calibrate_gamma, model_kw
 
 pytestmark = pytest.mark.gpu
 
@@ -128,7 +128,7 @@ def test_config_nll_grad_matches_oracle(k):
     coords, ind, gamma, y = workload(k, ctx)
     assert (digest(coords), digest(ind), digest(y)) == (str(f["coords_sha"]), str(f["ind_sha"]), str(f["y_sha"]))
     assert gamma == float(f["gamma"])
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     md = fsa.FsaModel.assemble(coords, ind, ctx=ctx, **kw)
     P = fsa.make_preconditioner(md, "fitc")
     r = fsa.iterative_nll_grad(md, P, y, num_probes=cfg["L"], seed=0, tol=cfg["tol"])
@@ -151,7 +151,7 @@ def test_config_solution_matches_oracle(k):
     cfg = CONFIGS[k]
     ctx = fsa.Context(0)
     coords, ind, gamma, y = workload(k, ctx)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     md = fsa.FsaModel.assemble(coords, ind, ctx=ctx, **kw)
     P = fsa.make_preconditioner(md, "fitc")
     B = np.column_stack([P.sample_probes(cfg["L"], 0), y])
@@ -182,7 +182,7 @@ def test_config2_ozaki_matches_dmma():
     cfg = CONFIGS[2]
     ctx = fsa.Context(0)
     coords, ind, gamma, y = workload(2, ctx)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     out = {}
     for mode in ("ozaki", "dmma"):
         ctx.set_gemm_mode(mode)
@@ -206,7 +206,7 @@ def test_config3_predictive_variance_matches_oracle():
     plocs = fsa.uniform_locations(cfg["np"], 2, 101)
     assert (digest(coords), digest(ind), digest(plocs)) == (str(f["coords_sha"]), str(f["ind_sha"]),
                                                             str(f["plocs_sha"]))
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     md = fsa.FsaModel.assemble(coords, ind, ctx=ctx, **kw)
     pr = fsa.make_prediction_set(md, plocs)
     res = pr.predict_var_sim(num_probes=cfg["L"], seed=0, tol=cfg["tol"], tol_s=cfg["tol"])
@@ -232,7 +232,7 @@ def test_config5_bench_precond_matches_oracle():
     cfg = CONFIGS[5]
     ctx = fsa.Context(0)
     coords, ind, gamma, y = workload(5, ctx)
-    kw = dict(nu=cfg["nu"], taper_family=1, gamma=gamma, sigma2=cfg["s2"], sigma1_2=cfg["s12"], rho=cfg["rho"])
+    kw = model_kw(cfg, gamma)
     md = fsa.FsaModel.assemble(coords, ind, ctx=ctx, **kw)
     for name in ("fitc", "diagonal", "none"):
         P = fsa.make_preconditioner(md, name)

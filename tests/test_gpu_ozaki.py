@@ -47,9 +47,21 @@ def test_ozaki_products_match_fp64(n, m, k):
     # amplified by the conditioning of Sigma_m)
     rp = np.max(np.abs(pd - ref_p) / scale_p)
     re = np.max(np.abs(ed - ref_e) / scale_e)
-    print(n, m, k, "ozaki-dmma project", dp, "expand", de, "| dmma-ref", rp, re)
+    # expansion: the scaling groups are a point's whole U column and a whole W column, so the
+    # error bound is normwise per group: |dY_ij| <= 2^-53 (max_k|U_ki| sum_k|W_kj| + max_k|W_kj|
+    # sum_k|U_ki|) (digit truncation at 2^-56 of each group's exponent + the dropped weight >= 10
+    # products). Relative to the componentwise sum|U||W| it is ~2e-15 typically and larger only
+    # where a W entry happens to be tiny exactly where U_i is concentrated (measured below).
+    Ua, Wa = np.abs(U), np.abs(W)
+    bound = 2.0 ** -53 * (Ua.max(axis=0)[:, None] * Wa.sum(axis=0)[None, :]
+                          + Ua.sum(axis=0)[:, None] * Wa.max(axis=0)[None, :])
+    dn = np.max(np.abs(eo - ed) / bound)
+    comp = np.abs(eo - ed) / scale_e
+    print(n, m, k, "ozaki-dmma project", dp, "expand", de, "(p99.9", np.quantile(comp, 0.999), ", normwise",
+          dn, ") | dmma-ref", rp, re)
     assert dp < 5e-15
-    assert de < 3e-11
+    assert dn < 1.0
+    assert np.quantile(comp, 0.999) < 1e-14
     assert rp < 1e-13 and re < 1e-11
 
 
