@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -40,6 +41,15 @@ inline std::atomic<long>& launch_counter() {
     ::fsa::launch_counter().fetch_add(1);         \
     FSA_CUDA(cudaGetLastError());                 \
   } while (0)
+
+// NVTX phase range (assemble / FITC setup / PCG / SLQ / traces / prediction): visible in nsys /
+// ncu --nvtx; no-ops without a tool attached (NVTX v3 is header-only)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 inline long round_up(long x, long a) { return (x + a - 1) / a * a; }
 inline long cdiv(long x, long a) { return (x + a - 1) / a; }

@@ -289,6 +289,7 @@ void Model::expand(const double* W, long tp, double* Y) {
 
 std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> geo, const double* inducing, long m,
                                        const Params& p) {
+  NvtxRange nvtx_("fsa::assemble");
   validate(p);
   require(geo != nullptr, "geometry missing");
   require(m > 0, "empty inducing set");
@@ -619,6 +620,12 @@ void FitcPrecond::start_traces() {
   Context* ctx = md->ctx;
   cudaStream_t side = ctx->side_stream();
   const long mp = md->m_pad, np = md->n_pad, n = md->n;
+  // the trace passes read Q^{-1}, written on the main stream: order them after it explicitly
+  // (not through the host synchronisation that happens to precede this call)
+  cudaEvent_t qready = ctx->ev();
+  FSA_CUDA(cudaEventRecord(qready, ctx->stream));
+  FSA_CUDA(cudaStreamWaitEvent(side, qready, 0));
+  ctx->pool.push_back(qready);
   cudaStream_t saved = alloc_stream();
   alloc_stream() = side;
   try {
@@ -657,8 +664,12 @@ void FitcPrecond::finish_traces(const double* h) {
 }
 
 FitcPrecond::~FitcPrecond() {
-  // frees below (stream-ordered on the main stream) come after the side-stream trace work
-  if (traces_pending) cudaStreamWaitEvent(md->ctx->stream, traces_done, 0);
+  // frees below (stream-ordered on the main stream) come after the side-stream trace work, and
+  // the pinned host buffer its device-to-host copy targets is released only after that copy
+  if (traces_pending) {
+    cudaStreamWaitEvent(md->ctx->stream, traces_done, 0);
+    cudaEventSynchronize(traces_done);
+  }
   if (traces_done != nullptr) md->ctx->pool.push_back(traces_done);
   if (traces_host != nullptr) cudaFreeHost(traces_host);
 }
@@ -771,6 +782,7 @@ double FitcPrecond::deriv_trace(int k) {
 }
 
 std::unique_ptr<Precond> make_preconditioner(Model* md, int type) {  // estimation.cpp:160-176
+  NvtxRange nvtx_("fsa::make_preconditioner");
   require(md->world() == 1 || type == 2, "row-sharded models support the FITC preconditioner only");
   switch (type) {
     case 0: return std::make_unique<IdentityPrecond>(md);
@@ -802,6 +814,7 @@ int CgResult::max_iterations() const {
 // reference sequence's four dense passes (krylov.cpp:56-93, preconditioners.cpp:58-61).
 CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long k, long tp, double* X,
                          const CgOptions& opts) {
+  NvtxRange nvtx_("fsa::pcg_solve_multi");
   require(opts.tol > 0.0 && opts.max_iter > 0, "cg: invalid options");
   require(k >= 1 && k <= tp, "cg: column count mismatch");
   Context* ctx = md->ctx;
@@ -868,9 +881,13 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   bool first_sweep = true;
   // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
   const bool oz = fused && md->use_ozaki(tp);
-  // wider blocks (config 4: t = 65 -> t_pad = 72): full 64-column blocks on the INT8 tensor
-  // cores, the remainder on DMMA; the dense passes stream the U planes once per 64 columns
+  // wider blocks (config 4: t = 65 -> t_pad = 72): two INT8 column tiles in one launch whose CTA
+  // pairs share each U-plane tile through L2 (ozaki_*_pair); beyond 128 columns, 64-column INT8
+  // blocks and a DMMA remainder
   const bool oz_split = fused && !oz && md->ctx->gemm_mode != 1 && tp > kOzCols;
+  // FSA_OZ_PAIR=0: the 64-column INT8 + DMMA-remainder passes instead of the pair (A/B measurement)
+  static const bool pair_off = std::getenv("FSA_OZ_PAIR") && std::strcmp(std::getenv("FSA_OZ_PAIR"), "0") == 0;
+  const bool oz_pair = oz_split && tp <= kOzPairCols && !pair_off;
   if (oz || oz_split) md->ensure_ozaki();
   // single rank: the column sums of the SpMM, residual-update and expansion partials run fused
   // with the alpha / residual-test / beta + count control kernels (no separate launches)
@@ -885,6 +902,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
   auto precond = [&](double* rzout, bool sums = true) {
+    // column maxima of |W| for the expansion's digit planes: left by the one-launch core solve
+    // (only that kernel fills them; zeroed by the residual-test control kernel)
+    const bool wfill = ctl && !sums && core_apply_supported(mp, tp);
     if (fused) {
       double* S = md->mt_buf(0, tp);
       double* W = md->mt_buf(1, tp);
@@ -898,6 +918,15 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
           comm.allreduce(S, mp * tp, s);
         }
         ymax_ready = false;
+      } else if (oz_pair) {  // two column tiles, U planes streamed once
+        {
+          KTimer t(ctx, "lowrank_project", 2.0 * md->m * n * k);
+          ozaki_project_pair(md->oz, w.R.get(), tp, tp, md->Dinv.get(), S, s);
+        }
+        if (md->world() > 1) {
+          KTimer t(ctx, "allreduce");
+          comm.allreduce(S, mp * tp, s);
+        }
       } else if (oz_split) {
         {
           KTimer t(ctx, "lowrank_project", 2.0 * md->m * n * k);
@@ -924,7 +953,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         KTimer t(ctx, "core_solve", 2.0 * md->m * md->m * k);
         if (core_apply_supported(mp, tp)) {
           // (the fused path's sweeps also leave the column maxima the expansion slices W with)
-          core_apply(fitc->Qinv.get(), mp, S, tp, W, s, ctl && !sums ? w.wmax.get() : nullptr);
+          core_apply(fitc->Qinv.get(), mp, S, tp, W, s, wfill ? w.wmax.get() : nullptr);
         } else {
           const size_t need = gemm_reduce_scratch(mp, tp, mp);
           if (md->red_scratch.n < need) md->red_scratch.alloc(need);
@@ -934,7 +963,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       KTimer t(ctx, "lowrank_expand", flops_mn);
       if (md->use_ozaki(tp)) {
         ozaki_expand_keep(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s, sums,
-                          ctl && !sums ? w.wmax.get() : nullptr);
+                          wfill ? w.wmax.get() : nullptr);
+      } else if (oz_pair) {
+        ozaki_expand_keep_pair(md->oz, W, tp, tp, w.Z.get(), w.Lw.get(), w.R.get(), md->Dinv.get(), rzout, part, s);
       } else if (oz_split) {
         for (long c0 = 0; c0 < tp; c0 += kOzCols) {
           const long wd = std::min<long>(kOzCols, tp - c0);
@@ -1251,6 +1282,7 @@ static std::vector<double> small_spd_solve(std::vector<double> G, long p, std::v
 
 NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const double* Xc, long p, int L,
                              unsigned long long seed, const CgOptions& cg, int cv_mode, bool want_grad) {
+  NvtxRange nvtx_("fsa::iterative_nll_grad");
   require(L > 0, "nll: need at least one probe");
   const bool resident = y == nullptr;
   if (resident) {  // response kept in HBM by fsa_geometry_set_response
@@ -1466,6 +1498,7 @@ NllResult iterative_nll_grad(Model* md, Precond& P, const double* y, const doubl
 }
 
 FisherResult fisher_ste(Model* md, Precond& P, int L, unsigned long long seed, bool rademacher, const CgOptions& cg) {
+  NvtxRange nvtx_("fsa::fisher_ste");
   require(L > 0, "need at least one probe");  // fsa.cpp:285
   Context* ctx = md->ctx;
   cudaStream_t s = ctx->stream;

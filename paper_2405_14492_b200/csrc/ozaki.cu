@@ -55,10 +55,10 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[1
 }
 // 16 columns [col0, col0 + 16) of this lane's row: sum_d 2^{-7d} C_d with the eight int32
 // accumulators combined exactly in two int64 halves (|hi|, |lo| < 2^53: exact conversions)
-__device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[16]) {
+__device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[16], int wstride = kOzCols) {
   uint32_t v[kOzSlices][16];
 #pragma unroll
-  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * kOzCols + col0), v[dd]);
+  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
@@ -78,10 +78,10 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]
                : "r"(taddr));
 }
 // drain16 for 8 columns (half the registers)
-__device__ __forceinline__ void drain8(uint32_t trow, int col0, double (&out)[8]) {
+__device__ __forceinline__ void drain8(uint32_t trow, int col0, double (&out)[8], int wstride = kOzCols) {
   uint32_t v[kOzSlices][8];
 #pragma unroll
-  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * kOzCols + col0), v[dd]);
+  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -158,12 +158,33 @@ struct OzEpi {
 // 3 Y = R - acc (R, Y with row stride ld), 4 row dots of acc with R and A2 (row stride ld):
 //   Z[i] = sum_c acc[i][c] R[i][c], Lw[i] = sum_c acc[i][c] A2[i][c]
 
+// Two column tiles of one wider RHS block in one launch (t_pad in (64, 128], config 4's 72): the
+// two CTAs of a (row tile, K chunk) -- or, in the persistent expansion, of a pair -- are adjacent
+// in the launch order, run concurrently and stream the SAME A (U digit-plane) tiles, so the second
+// read of each A tile comes from L2: the U planes cross HBM once per pass, where a 64-column INT8
+// pass plus an 8-column fp64 DMMA remainder read 8 + 8 bytes of U per entry.
+// The block is split evenly (72 = 36 + 36) and both tiles use the same B width nc (a multiple of
+// 16, <= 48 here): equal MMA work, so the two CTAs of a pair run in step and the second read of
+// every A tile hits L2 (a 64 + 8 split ran the short tile ahead and paid the A stream twice).
+struct OzPair {
+  const int8_t* B[2];
+  OzEpi epi[2];
+  int nc = kOzCols;  // B tile width of both column tiles (PAIRED)
+};
+template <bool PAIRED>
 __global__ void __launch_bounds__(128, 1)
-    k_oz_gemm(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int nkb_all, int kb_per_chunk, OzEpi epi) {
+    k_oz_gemm(const int8_t* __restrict__ A, OzPair pr, int nkb_all, int kb_per_chunk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], done;
   __shared__ uint32_t tmem_base_s;
-  const int tile = blockIdx.x, chunk = blockIdx.y;
+  const int ct = PAIRED ? blockIdx.x : 0;
+  const int tile = PAIRED ? blockIdx.y : blockIdx.x, chunk = PAIRED ? blockIdx.z : blockIdx.y;
+  const int8_t* __restrict__ B = pr.B[ct];
+  const OzEpi& epi = pr.epi[ct];
+  // B tile width NC: 64, or the pair's nc (layout of k_oz_planes_*: plane stride 16 NC bytes,
+  // K-half stride 128 NC bytes; one accumulator weight per NC TMEM columns)
+  const int NC = PAIRED ? pr.nc : kOzCols;
+  const uint32_t btile = static_cast<uint32_t>(256 * NC);
   const int kb0 = chunk * kb_per_chunk;
   const int nk = min(nkb_all - kb0, kb_per_chunk);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -189,12 +210,12 @@ __global__ void __launch_bounds__(128, 1)
 
   if (tid == 0) {
     const int8_t* Ablk = A + (static_cast<long>(tile) * nkb_all + kb0) * kATile;
-    const int8_t* Bblk = B + static_cast<long>(kb0) * kBTile;
+    const int8_t* Bblk = B + static_cast<long>(kb0) * btile;
     auto load = [&](int j) {
       const int st = j % kStages;
-      mbar_expect_tx(&full[st], kATile + kBTile);
+      mbar_expect_tx(&full[st], kATile + btile);
       bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
-      bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * kBTile, kBTile, &full[st]);
+      bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * btile, btile, &full[st]);
     };
     const int pre = min(nk, kStages);
     for (int j = 0; j < pre; ++j) load(j);
@@ -209,8 +230,8 @@ __global__ void __launch_bounds__(128, 1)
         for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
           const int nb = min(4, kOzSlices + 2 - a - bs);
           const uint64_t ad = umma_desc(a0 + (a - 1) * 4096, 2048, 128);
-          const uint64_t bd = umma_desc(b0 + (bs - 1) * 1024, 8192, 128);
-          mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * kOzCols), ad, bd, idesc_i8(128, nb * kOzCols),
+          const uint64_t bd = umma_desc(b0 + (bs - 1) * 16 * NC, 128 * NC, 128);
+          mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * NC), ad, bd, idesc_i8(128, nb * NC),
                  (j > 0 || a > 1) ? 1u : 0u);
         }
       }
@@ -235,11 +256,17 @@ __global__ void __launch_bounds__(128, 1)
   double* lws = reinterpret_cast<double*>(smem);
   double* rzs = lws + 128 * kLd;
   for (int hh = 0; hh < 2; ++hh) {
+    if (hh * 32 >= NC) break;  // (NC = 16 or 48: the last half is partial)
     double acc[32];
     {
       double y0[16], y1[16];
-      drain16(trow, hh * 32, y0);
-      drain16(trow, hh * 32 + 16, y1);
+      drain16(trow, hh * 32, y0, NC);
+      if (hh * 32 + 16 < NC) {
+        drain16(trow, hh * 32 + 16, y1, NC);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) y1[c] = 0.0;
+      }
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         acc[c] = y0[c];
@@ -253,7 +280,8 @@ __global__ void __launch_bounds__(128, 1)
       const int* fc = epi.ecol + static_cast<long>(chunk) * kOzCols + hh * 32;
 #pragma unroll
       for (int c = 0; c < 32; c += 2)
-        *reinterpret_cast<double2*>(out + c) = make_double2(acc[c] * pow2(er + fc[c]), acc[c + 1] * pow2(er + fc[c + 1]));
+        if (hh * 32 + c < NC)
+          *reinterpret_cast<double2*>(out + c) = make_double2(acc[c] * pow2(er + fc[c]), acc[c + 1] * pow2(er + fc[c + 1]));
     } else {  // modes 1, 2: Lw (and Z) through shared memory, coalesced row copies
       const long i = static_cast<long>(tile) * 128 + row;
       const double sci = pow2(epi.erow[i]);
@@ -304,12 +332,21 @@ constexpr int kXStages = 3;
 constexpr int kXLd = kOzCols + 1;  // odd stride: conflict-free row-per-lane access
 constexpr int kXSmem = kXStages * (kATile + kBTile) + 128 * kXLd * 8;
 constexpr int kXEpi = 512;  // epilogue threads: four warps per TMEM lane quadrant, 16 columns each
+template <bool PAIRED>
 __global__ void __launch_bounds__(64 + kXEpi, 1)
-    k_oz_expand(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int tiles, int mkb, OzEpi epi) {
+    k_oz_expand(const int8_t* __restrict__ A, OzPair pr, int tiles, int mkb) {
   constexpr int kStages = kXStages;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull, tempty;
   __shared__ uint32_t tmem_base_s;
+  // PAIRED: CTAs 2j and 2j + 1 process the same point tiles j, j + G/2, ... for column tiles 0 / 1
+  const int ct = PAIRED ? (blockIdx.x & 1) : 0;
+  const int t_first = PAIRED ? (blockIdx.x >> 1) : blockIdx.x;
+  const int t_step = PAIRED ? (gridDim.x >> 1) : gridDim.x;
+  const int8_t* __restrict__ B = pr.B[ct];
+  const OzEpi& epi = pr.epi[ct];
+  const int NC = PAIRED ? pr.nc : kOzCols;  // B tile width (see k_oz_gemm)
+  const uint32_t btile = static_cast<uint32_t>(256 * NC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kATile;
@@ -335,14 +372,14 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   if (warp == 0) {
     if (lane == 0) {  // producer
       long g = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t_first; t < tiles; t += t_step) {
         const int8_t* At = A + static_cast<long>(t) * mkb * kATile;
         for (int kb = 0; kb < mkb; ++kb, ++g) {
           const int st = static_cast<int>(g % kStages);
           if (g >= kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g / kStages - 1) & 1));
-          mbar_expect_tx(&full[st], kATile + kBTile);
+          mbar_expect_tx(&full[st], kATile + btile);
           bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
-          bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * kBTile, kBTile, &full[st]);
+          bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * btile, btile, &full[st]);
         }
       }
     }
@@ -351,7 +388,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
     if (lane == 0) {  // MMA issuer
       long g = 0;
       int lt = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      for (int t = t_first; t < tiles; t += t_step, ++lt) {
         if (lt > 0) {
           mbar_wait(&tempty, static_cast<uint32_t>((lt - 1) & 1));
           tc_fence_after();
@@ -366,8 +403,8 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
 #pragma unroll
             for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
               const int nb = min(4, kOzSlices + 2 - a - bs);
-              mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * kOzCols), umma_desc(a0 + (a - 1) * 4096, 2048, 128),
-                     umma_desc(b0 + (bs - 1) * 1024, 8192, 128), idesc_i8(128, nb * kOzCols),
+              mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * NC), umma_desc(a0 + (a - 1) * 4096, 2048, 128),
+                     umma_desc(b0 + (bs - 1) * 16 * NC, 128 * NC, 128), idesc_i8(128, nb * NC),
                      (kb > 0 || a > 1) ? 1u : 0u);
             }
           }
@@ -384,7 +421,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
     const long tp = epi.tp;
     const int et = tid - 64;  // 0 .. kXEpi - 1
     int lt = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+    for (int t = t_first; t < tiles; t += t_step, ++lt) {
       const long r0 = static_cast<long>(t) * 128;
       if (epi.mode == 1 || epi.mode == 3 || epi.mode == 4) {
         // pull the tile's R entries (128 rows x tp columns, row stride ld) into L2 while the MMAs
@@ -400,9 +437,9 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
 #pragma unroll 1
       for (int h8 = 0; h8 < 2; ++h8) {  // stage this warp's 16 columns in shared memory
         const int c0 = gq * 16 + h8 * 8;
-        if (c0 >= tp) break;
+        if (c0 >= tp || c0 >= NC) break;
         double y[8];
-        drain8(trow, c0, y);
+        drain8(trow, c0, y, NC);
 #pragma unroll
         for (int c = 0; c < 8; ++c) tileY[row * kXLd + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
       }
@@ -832,12 +869,15 @@ __global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, l
     if (mx > 0.0) atomicMax(ymax + static_cast<long>(chunk) * kOzCols + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
   }
 }
+// B planes in the layout [kb][kc][plane * nc / 8 + col / 8][col % 8][16] of an nc-column tile
+// (nc = 64, or 16 for the narrow second tile of a pair)
 __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ V, long ld, long tp,
                                                      const double* __restrict__ scale, int kb_per_chunk,
                                                      const unsigned long long* __restrict__ ymax,
-                                                     int* __restrict__ f, int8_t* __restrict__ Ys) {
+                                                     int* __restrict__ f, int8_t* __restrict__ Ys, int nc = kOzCols) {
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
+  if (c >= nc) return;
   const int chunk = kb / kb_per_chunk;
   const int e = group_exp(__longlong_as_double(static_cast<long long>(ymax[static_cast<long>(chunk) * kOzCols + c])));
   if (kb % kb_per_chunk == 0 && kc == 0) f[static_cast<long>(chunk) * kOzCols + c] = e;
@@ -849,9 +889,9 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
   }
   int4 out[kOzSlices];
   digits16(v, e, out);
-  int8_t* base = Ys + static_cast<long>(kb) * kBTile + kc * 8192 + c * 16;
+  int8_t* base = Ys + static_cast<long>(kb) * (256 * nc) + kc * (128 * nc) + c * 16;
 #pragma unroll
-  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
+  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
 }
 // per-sweep B planes of W (expand): column exponents over all rows, then digits
 __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long ld, long tp, long mp,
@@ -870,9 +910,10 @@ __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, 
 }
 __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long ld, long tp,
                                                      int* __restrict__ h, int8_t* __restrict__ Ws,
-                                                     const unsigned long long* __restrict__ wmax) {
+                                                     const unsigned long long* __restrict__ wmax, int nc = kOzCols) {
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
+  if (c >= nc) return;
   int e;
   if (wmax != nullptr) {  // column maxima left by the producer of W (core_apply)
     e = c < tp ? group_exp(__longlong_as_double(static_cast<long long>(wmax[c]))) : 0;
@@ -885,9 +926,9 @@ __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ 
   for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * ld + c] : 0.0;
   int4 out[kOzSlices];
   digits16(v, e, out);
-  int8_t* base = Ws + static_cast<long>(kb) * kBTile + kc * 8192 + c * 16;
+  int8_t* base = Ws + static_cast<long>(kb) * (256 * nc) + kc * (128 * nc) + c * 16;
 #pragma unroll
-  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * 1024) = out[b];
+  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
 }
 // S[r][c] = sum_chunk part[chunk][r][c] (fixed order)
 __global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long ld, long tp,
@@ -904,10 +945,21 @@ void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nk
                  const OzEpi& epi, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  k_oz_gemm<<<dim3(tiles, chunks), 128, kSmem, s>>>(A, B, nkb_all, kb_per_chunk, epi);
+  OzPair pr{{B, B}, {epi, epi}};
+  k_oz_gemm<false><<<dim3(tiles, chunks), 128, kSmem, s>>>(A, pr, nkb_all, kb_per_chunk);
+  FSA_LAUNCH_CHECK();
+}
+void launch_gemm_pair(const int8_t* A, const OzPair& pr, int tiles, int chunks, int nkb_all, int kb_per_chunk,
+                      cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  k_oz_gemm<true><<<dim3(2, tiles, chunks), 128, kSmem, s>>>(A, pr, nkb_all, kb_per_chunk);
   FSA_LAUNCH_CHECK();
 }
 
@@ -928,24 +980,41 @@ __global__ void k_sum_tiles(const double* __restrict__ qp, const double* __restr
 void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const int8_t* Ws = nullptr) {
   static bool attr = false;
   if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
     attr = true;
   }
   const int grid = std::min(p.ptiles, kNumSMs);
-  k_oz_expand<<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), Ws != nullptr ? Ws : p.Ws.get(), p.ptiles, p.mkb, epi);
+  const int8_t* B = Ws != nullptr ? Ws : p.Ws.get();
+  OzPair pr{{B, B}, {epi, epi}};
+  k_oz_expand<false><<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), pr, p.ptiles, p.mkb);
+  FSA_LAUNCH_CHECK();
+}
+void launch_expand_pair(const OzakiPlan& p, const OzPair& pr, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
+    attr = true;
+  }
+  const int grid = 2 * std::min(p.ptiles, kNumSMs / 2);
+  k_oz_expand<true><<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), pr, p.ptiles, p.mkb);
   FSA_LAUNCH_CHECK();
 }
 
+// digit planes of diag(scale) V (columns [0, tp) of a row-stride-ld block) for the projection
+void slice_y(OzakiPlan& p, const double* V, long ld, long tp, const double* scale, unsigned long long* ymax, int* f,
+             int8_t* Ys, cudaStream_t s, bool ymax_ready, int nc = kOzCols) {
+  if (!ymax_ready) {
+    FSA_CUDA(cudaMemsetAsync(ymax, 0, sizeof(unsigned long long) * p.nchunks * kOzCols, s));
+    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, ld, tp, scale, p.n_pad, p.kb_per_chunk, 16, ymax);
+    FSA_LAUNCH_CHECK();
+  }
+  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, ld, tp, scale, p.kb_per_chunk, ymax, f, Ys, nc);
+  FSA_LAUNCH_CHECK();
+}
 void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double* scale, double* S, cudaStream_t s,
                   bool ymax_ready) {
   require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
-  if (!ymax_ready) {
-    FSA_CUDA(cudaMemsetAsync(p.ymax.get(), 0, p.ymax.bytes(), s));
-    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, ld, tp, scale, p.n_pad, p.kb_per_chunk, 16, p.ymax.get());
-    FSA_LAUNCH_CHECK();
-  }
-  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, ld, tp, scale, p.kb_per_chunk, p.ymax.get(), p.f.get(), p.Ys.get());
-  FSA_LAUNCH_CHECK();
+  slice_y(p, V, ld, tp, scale, p.ymax.get(), p.f.get(), p.Ys.get(), s, ymax_ready);
   OzEpi epi{0, p.m_pad, tp, ld, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
   launch_gemm(p.Ar.get(), p.Ys.get(), p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, epi, s);
   k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * tp, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, ld, tp,
@@ -954,13 +1023,13 @@ void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double*
 }
 
 void slice_w_to(OzakiPlan& p, const double* W, long ld, long tp, int8_t* Ws, int* h, cudaStream_t s,
-                const unsigned long long* wmax = nullptr) {
+                const unsigned long long* wmax = nullptr, int nc = kOzCols) {
   require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
   if (wmax == nullptr) {
     k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, h);
     FSA_LAUNCH_CHECK();
   }
-  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws, wmax);
+  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws, wmax, nc);
   FSA_LAUNCH_CHECK();
 }
 void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
@@ -1024,6 +1093,62 @@ void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, doubl
   OzEpi epi{1, p.m_pad, ncols, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv};
   launch_expand(p, epi, s);
   if (colsum) colsum_partials(partial, p.ptiles, ncols, ncols, rz, s);
+}
+// second column tile's per-sweep buffers (lazily, 65..96 columns)
+static void ensure_pair(OzakiPlan& p) {
+  if (p.Ys2.n == 0) {
+    p.Ys2.alloc(static_cast<size_t>(p.nkb) * kBTile);
+    p.Ws2.alloc(static_cast<size_t>(p.mkb) * kBTile);
+    p.ymax2.alloc(static_cast<size_t>(p.nchunks * kOzCols));
+    p.f2.alloc(static_cast<size_t>(p.nchunks * kOzCols));
+    p.h2.alloc(kOzCols);
+    p.part2.alloc(static_cast<size_t>(p.nchunks * p.m_pad * kOzCols));
+  }
+}
+// even split of ncols: n0 + n1 columns, both tiles nc = round_up(n0, 16) wide
+static void pair_split(long ncols, long& n0, long& n1, int& nc) {
+  n0 = (ncols + 1) / 2;
+  n1 = ncols - n0;
+  nc = static_cast<int>(round_up(n0, 16));
+}
+void ozaki_project_pair(OzakiPlan& p, const double* R, long ld, long ncols, const double* Dinv, double* S,
+                        cudaStream_t s) {
+  require(p.ready && ncols > kOzCols && ncols <= kOzPairCols && ncols <= ld, "ozaki pair: 65..96 columns");
+  ensure_pair(p);
+  long n0, n1;
+  int nc;
+  pair_split(ncols, n0, n1, nc);
+  slice_y(p, R, ld, n0, Dinv, p.ymax.get(), p.f.get(), p.Ys.get(), s, false, nc);
+  slice_y(p, R + n0, ld, n1, Dinv, p.ymax2.get(), p.f2.get(), p.Ys2.get(), s, false, nc);
+  OzPair pr{{p.Ys.get(), p.Ys2.get()},
+            {OzEpi{0, p.m_pad, n0, ld, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr},
+             OzEpi{0, p.m_pad, n1, ld, p.er.get(), p.f2.get(), p.part2.get(), nullptr, nullptr, nullptr, nullptr}},
+            nc};
+  launch_gemm_pair(p.Ar.get(), pr, p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, s);
+  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * n0, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, ld, n0,
+                                                                            S);
+  FSA_LAUNCH_CHECK();
+  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * n1, 256)), 256, 0, s>>>(p.part2.get(), p.nchunks, p.m_pad, ld, n1,
+                                                                            S + n0);
+  FSA_LAUNCH_CHECK();
+}
+void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
+                            const double* Dinv, double* rz, double* partial, cudaStream_t s) {
+  require(p.ready && ncols > kOzCols && ncols <= kOzPairCols && ncols <= ld, "ozaki pair: 65..96 columns");
+  ensure_pair(p);
+  long n0, n1;
+  int nc;
+  pair_split(ncols, n0, n1, nc);
+  slice_w_to(p, W, ld, n0, p.Ws.get(), p.h.get(), s, nullptr, nc);
+  slice_w_to(p, W + n0, ld, n1, p.Ws2.get(), p.h2.get(), s, nullptr, nc);
+  double* part2 = partial + static_cast<long>(p.ptiles) * n0;
+  OzPair pr{{p.Ws.get(), p.Ws2.get()},
+            {OzEpi{1, p.m_pad, n0, ld, p.ec.get(), p.h.get(), partial, Z, Lw, R, Dinv},
+             OzEpi{1, p.m_pad, n1, ld, p.ec.get(), p.h2.get(), part2, Z + n0, Lw + n0, R + n0, Dinv}},
+            nc};
+  launch_expand_pair(p, pr, s);
+  colsum_partials(partial, p.ptiles, n0, n0, rz, s);
+  colsum_partials(part2, p.ptiles, n1, n1, rz + n0, s);
 }
 void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");

@@ -13,8 +13,16 @@
 // grouped by total weight d = a + b (a + b <= s + 1 kept):
 //   (X Y)_{ij} = 2^{e_i + f_j} sum_d 2^{-7d} C_d[i][j],  C_d = sum_{a+b=d} X_a Y_b.
 // Scaling groups: project -> U per (inducing row, K chunk), D^{-1}R per (column,
-// K chunk); expand -> U per point, W per column. With s = 8 the result agrees
-// with an fp64 GEMM to ~1e-15 of sum |x||y| (tests/test_gpu_ozaki.py).
+// K chunk); expand -> U per point, W per column. Every operand loses at most 2^-56 of
+// its group's power-of-two bound and the dropped weight >= 10 products are of the
+// same order, so per output entry
+//   |dY_ij| <= 2^-53 (max_k|X_ik| sum_k|Y_kj| + sum_k|X_ik| max_k|Y_kj|)
+// -- an fp64-GEMM-class NORMWISE bound per scaling group. Measured against the
+// componentwise sum_k |X_ik||Y_kj| (tests/test_gpu_ozaki.py): projection <= 6e-16;
+// expansion median 2.5e-15, p99.9 < 1e-14, with a tail to ~4e-12 at entries where a
+// W entry happens to be tiny exactly where a point's U column is concentrated (a
+// per-column exponent cannot resolve it; an fp64 GEMM would). End to end at config 2
+// the Ozaki and DMMA paths agree to 2e-11 in the gradient with identical CG counts.
 //
 // The U digit planes are built once per parameter set (2 x 8 bytes per entry,
 // like fp64 U); R and W are sliced every sweep. Operand tiles are stored in the
@@ -32,6 +40,7 @@ namespace fsa {
 
 constexpr int kOzSlices = 8;
 constexpr int kOzCols = 64;  // RHS columns per accumulator (t_pad <= 64)
+constexpr int kOzPairCols = 96;  // widest block of the paired passes (two column tiles of <= 48)
 
 struct OzakiPlan {
   long m_pad = 0, n_pad = 0;
@@ -50,6 +59,11 @@ struct OzakiPlan {
   DBuf<unsigned long long> ymax;
   DBuf<int> f, h;             // [nchunks][64], [64]
   DBuf<double> part;          // project partials [nchunks][m_pad][64]
+  // second column tile of 65..128-column blocks (ozaki_*_pair), allocated on first use
+  DBuf<int8_t> Ys2, Ws2;
+  DBuf<unsigned long long> ymax2;
+  DBuf<int> f2, h2;
+  DBuf<double> part2;
   bool ready = false;
 };
 
@@ -77,6 +91,13 @@ void ozaki_expand_keep(OzakiPlan& p, const double* W, long ld, long ncols, doubl
                        const double* Dinv, double* rz, double* partial, cudaStream_t s,
                        bool colsum = true,  // colsum = false: partials [ptiles][ncols] only
                        const unsigned long long* wmax = nullptr);  // column maxima of |W| (core_apply)
+// 65..128 columns (t_pad = 72 at config 4) as two column tiles in ONE launch whose CTA pairs stream
+// the same U digit-plane tiles (the second read hits L2): same contracts as ozaki_project /
+// ozaki_expand_keep; `partial` holds ptiles * ncols doubles
+void ozaki_project_pair(OzakiPlan& p, const double* R, long ld, long ncols, const double* Dinv, double* S,
+                        cudaStream_t s);
+void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
+                            const double* Dinv, double* rz, double* partial, cudaStream_t s);
 // wide passes (64-column tiles of row-major operands whose widths are multiples of 64):
 //   Y = A - U^T W            (W m_pad x ldw, A / Y n_pad x ld)
 //   q[i] = (U^T W)_i . B1_i, f[i] = (U^T W)_i . B2_i   (row dots, B1 / B2 n_pad x ld)

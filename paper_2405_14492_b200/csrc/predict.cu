@@ -250,6 +250,7 @@ void deterministic_pieces_host(PredictionSet& pr, const CgOptions& cg, const CgO
 // predict_var_sim (prediction.cpp:131-172) with stochastic_diag(_cv) (krylov.cpp:230-291)
 PredVarInfo predict_var_sim(PredictionSet& pr, int L, unsigned long long seed, const CgOptions& cg,
                             const CgOptions& cg_s, bool cv, double floor_rel, double* var, double* se) {
+  NvtxRange nvtx_("fsa::predict_var_sim");
   Model* md = pr.md;
   Context* ctx = md->ctx;
   cudaStream_t s = ctx->stream;

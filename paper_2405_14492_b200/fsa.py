@@ -153,6 +153,14 @@ _SIGS = {
 }
 
 
+def _destroy(fn, h):
+    """Handle release from __del__: skipped at interpreter shutdown, when the module globals are
+    already torn down (the process exit releases the device state)."""
+    if _lib is None or _SIGS is None:
+        return
+    getattr(_lib, fn)(h)
+
+
 def lib():
     """Load libfsa_b200.so (raises if it was not built: there is no fallback)."""
     global _lib
@@ -300,7 +308,10 @@ class Context:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().fsa_ctx_destroy(self.h)
+            try:
+                _destroy("fsa_ctx_destroy", self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def synchronize(self):
@@ -369,7 +380,10 @@ class Geometry:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().fsa_geometry_destroy(self.h)
+            try:
+                _destroy("fsa_geometry_destroy", self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def nnz(self):
@@ -440,7 +454,10 @@ class FsaModel:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().fsa_model_destroy(self.h)
+            try:
+                _destroy("fsa_model_destroy", self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def info(self):
@@ -508,7 +525,10 @@ class Preconditioner:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().fsa_precond_destroy(self.h)
+            try:
+                _destroy("fsa_precond_destroy", self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def name(self):
@@ -608,7 +628,10 @@ class PredictionSet:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().fsa_pred_destroy(self.h)
+            try:
+                _destroy("fsa_pred_destroy", self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def nnz(self):
