@@ -234,25 +234,23 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def cpu_prediction_sample(cfg, coords, ind, gamma, plocs, probes=256, det_cols=None):
-    """Config 3 on the oracle port: make_prediction_set + predict_var_sim with one 256-vector
-    simulation batch (the unit the reference accumulates, krylov.cpp:236-246), timed; the
-    1000-vector time is extrapolated as T(det + 1 batch) + (L/256 - 1) T(batch), with
-    T(batch) = T(det + 1 batch) - T(det) from a second run with the deterministic pieces only."""
+def cpu_prediction_sample(cfg, coords, ind, gamma, plocs, cols=16, probes=32):
+    """Config 3 on the oracle port, a bounded sample: make_prediction_set (timed), the deterministic
+    pieces' two m-RHS solves on `cols` of their m columns (independent per-column recurrences:
+    x m / cols), `probes` simulation vectors of a batch (x L / probes); the small dense remainder of the
+    deterministic pieces is not counted (the estimate is conservative)."""
     from oracle import oracle as O
 
     kw = model_kw(cfg, gamma)
     om = O.Model(coords, ind, **kw)
     t0 = time.perf_counter()
     pr = O.PredictionSet(om, plocs)
-    pr.predict_var_sim(num_probes=probes, seed=0, tol=cfg["tol"], tol_s=cfg["tol"])
-    t_one = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    pr.det_pieces(tol=cfg["tol"], tol_s=cfg["tol"])
-    t_det = time.perf_counter() - t0
-    t_batch = max(t_one - t_det, 0.0)
-    total = t_one + (cfg["L"] / probes - 1.0) * t_batch
-    return total * 1e3, t_one, t_det
+    t_set = time.perf_counter() - t0
+    t = pr.sample_timing(cols=cols, probes=probes, seed=0, tol=cfg["tol"], tol_s=cfg["tol"])
+    scale = cfg["m"] / cols
+    total = t_set + (t["x1"] + t["x2"]) * scale + t["batch"] * cfg["L"] / probes
+    sampled = t_set + t["x1"] + t["x2"] + t["batch"]
+    return total * 1e3, sampled, t
 
 
 def run_reference_prediction(args, cfg, coords, ind, gamma, y, nnz):
@@ -260,13 +258,14 @@ def run_reference_prediction(args, cfg, coords, ind, gamma, y, nnz):
 
     plocs = O.uniform_locations(cfg["np"], 2, 101)
     vals = []
-    for i in range(max(args.warmup, 0) + args.steps):
-        ms, t_one, t_det = cpu_prediction_sample(cfg, coords, ind, gamma, plocs)
-        if i >= args.warmup:
+    for i in range(min(args.warmup, 1) + max(1, min(args.steps, 3))):
+        ms, sampled, t = cpu_prediction_sample(cfg, coords, ind, gamma, plocs)
+        if i >= min(args.warmup, 1):
             vals.append(ms)
     value = statistics.median(vals)
-    sample = (f"oracle port: make_prediction_set + predict_var_sim (prediction.cpp:131-172) at n = n_p = "
-              f"{cfg['n']}, m = {cfg['m']} with one 256-vector batch, extrapolated to {cfg['L']} vectors")
+    sample = (f"oracle port (prediction.cpp:72-172) at n = n_p = {cfg['n']}, m = {cfg['m']}: make_prediction_set + "
+              f"16 of the {cfg['m']} columns of each deterministic m-RHS solve (x {cfg['m'] / 16:g}) + 32 "
+              f"simulation vectors (x {cfg['L'] / 32:g}); {sampled:.1f} s of CPU work per step")
     line = {"impl": "reference", "metric": "predictive-variance wall time (make_prediction_set + predict_var_sim)",
             "value": value, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -354,11 +353,11 @@ def run_prediction(args, cfg):
         try:
             from oracle import oracle as O  # noqa: F401
 
-            cms, t_one, t_det = cpu_prediction_sample(cfg, coords, ind, gamma, plocs)
+            cms, sampled, t = cpu_prediction_sample(cfg, coords, ind, gamma, plocs)
             cpu = {"value": cms, "unit": "ms", "cores": cpu_threads(), "kind": "port",
-                   "sample": f"oracle port, make_prediction_set + predict_var_sim with one 256-vector batch "
-                             f"({t_one:.1f} s, of which deterministic pieces {t_det:.1f} s), extrapolated to "
-                             f"{cfg['L']} vectors"}
+                   "sample": f"oracle port: make_prediction_set + 16 of {cfg['m']} columns of each deterministic "
+                             f"m-RHS solve (x {cfg['m'] / 16:g}: X1 {t['x1']:.1f} s, X2 {t['x2']:.1f} s) + 32 "
+                             f"simulation vectors ({t['batch']:.1f} s, x {cfg['L'] / 32:g}); {sampled:.1f} s sampled"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "ms", "cores": cpu_threads(), "kind": "port", "sample": f"failed: {exc}"}
     e2e_v = statistics.median(e2e_ms) if e2e_ms else None

@@ -21,6 +21,7 @@
 #include "fsa_oracle.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -1747,6 +1748,45 @@ int orc_predict_var_sim(void* mdv, void* pv, int L, uint64_t seed, double tol, i
   });
 }
 // deterministic pieces only (for parity of the GPU decomposition): d1, d2, d3 (np each)
+// Bounded CPU sample of predict_var_sim (bench.py's cpu_baseline for config 3; tests only): seconds
+// for the deterministic pieces' two m-RHS solves restricted to their first `cols` columns
+// (X1 = FITC-PCG on Sigma_mn^T, X2 = Jacobi-PCG on Sigma_s; prediction.cpp:72-110 -- the columns
+// are independent recurrences, so the full solves cost ~m / cols times these) and for one batch of
+// `probes` simulation vectors (quad_mat, prediction.cpp:142-148). out = [t_x1, t_x2, t_batch].
+int orc_pred_sample_timing(void* mdv, void* pv, long cols, int probes, uint64_t seed, double tol, int maxit,
+                           double tol_s, int maxit_s, double* out) {
+  return guard([&] {
+    Model& md = *static_cast<Model*>(mdv);
+    const Pred& P = *static_cast<Pred*>(pv);
+    const long n = md.n, m = md.m, np = P.np;
+    cols = std::max(1L, std::min(cols, m));
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    std::unique_ptr<FitcP> fitc(fitc_from_fsa(md, false));
+    Mat SmnT(n, cols);
+    for (long j = 0; j < cols; ++j)
+      for (long i = 0; i < n; ++i) SmnT(i, j) = md.sigma_mn(j, i);
+    auto t0 = now();
+    CgResult x1 = pcg_solve_multi(fsa_operator(md), *fitc, SmnT.data(), cols, tol, maxit, true);
+    auto t1 = now();
+    DiagP jacobi(csr_diag(md.sigma_s), nullptr);
+    CgResult x2 = pcg_solve_multi(sigma_s_operator(md), jacobi, SmnT.data(), cols, tol_s, maxit_s, true);
+    auto t2 = now();
+    std::vector<double> Z(static_cast<size_t>(np * probes)), G(static_cast<size_t>(n * probes)), Q(Z.size());
+    for (int j = 0; j < probes; ++j) {
+      rng_t rng = probe_rng(seed, static_cast<uint64_t>(j));
+      rademacher_fill(rng, Z.data() + static_cast<long>(j) * np, np);
+    }
+    auto t3 = now();
+    spmm(P.sigma_s_np, Z.data(), np, probes, G.data(), n);
+    CgResult sol = pcg_solve_multi(sigma_s_operator(md), jacobi, G.data(), probes, tol_s, maxit_s, true);
+    spmm_t(P.sigma_s_np, sol.X.data(), n, probes, Q.data(), np);
+    auto t4 = now();
+    out[0] = sec(t0, t1);
+    out[1] = sec(t1, t2);
+    out[2] = sec(t3, t4);
+  });
+}
 int orc_pred_det_pieces(void* mdv, void* pv, double tol, int maxit, double tol_s, int maxit_s, double* d1, double* d2,
                         double* d3, int* cg_iters) {
   return guard([&] {

@@ -65,6 +65,8 @@ int orc_cross_apply_t(void* mdv, void* pv, const double* u, double* out);
 int orc_predict_mean_iterative(void* mdv, void* pv, const double* resid, void* p, double tol, int max_iter, double* out);
 int orc_predict_var_sim(void* mdv, void* pv, int L, uint64_t seed, double tol, int maxit, double tol_s, int maxit_s,
                         int cv, double floor_rel, double* var, double* se, int* clamped, int* cg_iters);
+int orc_pred_sample_timing(void* mdv, void* pv, long cols, int probes, uint64_t seed, double tol, int maxit,
+                           double tol_s, int maxit_s, double* out);
 int orc_pred_det_pieces(void* mdv, void* pv, double tol, int maxit, double tol_s, int maxit_s, double* d1, double* d2,
                         double* d3, int* cg_iters);
 #ifdef __cplusplus

@@ -102,6 +102,8 @@ def lib():
             "orc_predict_mean_iterative": (C.c_int, [vp, vp, dp, vp, C.c_double, C.c_int, dp]),
             "orc_predict_var_sim": (C.c_int, [vp, vp, C.c_int, C.c_uint64, C.c_double, C.c_int, C.c_double, C.c_int,
                                               C.c_int, C.c_double, dp, dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+            "orc_pred_sample_timing": (C.c_int, [vp, vp, C.c_long, C.c_int, C.c_uint64, C.c_double, C.c_int,
+                                                 C.c_double, C.c_int, dp]),
             "orc_pred_det_pieces": (C.c_int, [vp, vp, C.c_double, C.c_int, C.c_double, C.c_int, dp, dp, dp,
                                               C.POINTER(C.c_int)]),
         }
@@ -460,6 +462,13 @@ class PredictionSet:
         _check(lib().orc_pred_det_pieces(self.model.h, self.h, tol, max_iter, tol_s, max_iter_s, d1, d2, d3,
                                          C.byref(it)))
         return d1, d2, d3, it.value
+
+    def sample_timing(self, cols=16, probes=256, seed=0, tol=1e-3, max_iter=1000, tol_s=1e-3, max_iter_s=1000):
+        """Seconds for cols columns of the two m-RHS solves and for one simulation batch."""
+        out = F(np.zeros(3))
+        _check(lib().orc_pred_sample_timing(self.model.h, self.h, cols, probes, seed, tol, max_iter, tol_s, max_iter_s,
+                                            out))
+        return {"x1": out[0], "x2": out[1], "batch": out[2]}
 
     def predict_var_sim(self, num_probes=1000, seed=0, tol=1e-3, max_iter=1000, tol_s=1e-3, max_iter_s=1000,
                         control_variate=False, floor_rel=1e-6):
