@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(256, 3) k_xr_dot_max(double* __restrict__ X, d
                                                     double* __restrict__ partial, const double* __restrict__ dinv,
                                                     unsigned long long* __restrict__ ymax, long chunk_rows) {
   __shared__ double red[8][64];
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long c = 2 * lane;
   const bool on = c < t;
@@ -524,7 +525,8 @@ void update_xr_dot_max(double* X, double* R, const double* H, const double* V, c
                        long chunk_rows, cudaStream_t s, bool colsum) {
   require(tp <= 64, "update_xr_dot_max: at most 64 columns");
   const long nb = xr_dot_max_blocks(n);
-  k_xr_dot_max<<<static_cast<unsigned>(nb), 256, 0, s>>>(X, R, H, V, alpha, n, tp, k, scratch, dinv, ymax, chunk_rows);
+  launch_pdl(k_xr_dot_max, dim3(static_cast<unsigned>(nb)), dim3(256), 0, s, X, R, H, V, alpha, n, tp, k, scratch, dinv,
+             ymax, chunk_rows);
   FSA_LAUNCH_CHECK();
   if (colsum) colsum_partials(scratch, nb, k, k, rr, s);
 }
@@ -760,6 +762,7 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
                                                     unsigned long long* __restrict__ zero_buf, long zero_len) {
   __shared__ double red[8];
   __shared__ bool last;
+  pdl_wait();
   const long c = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // (MODE 0) clear the next kernel's column-maxima accumulators on the way
@@ -855,13 +858,16 @@ void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, doub
   const unsigned g = static_cast<unsigned>(t);
   switch (mode) {
     case 0:
-      k_colsum_ctl<0><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      launch_pdl(k_colsum_ctl<0>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
+                 zero_buf, zero_len);
       break;
     case 1:
-      k_colsum_ctl<1><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      launch_pdl(k_colsum_ctl<1>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
+                 zero_buf, zero_len);
       break;
     default:
-      k_colsum_ctl<2><<<g, 256, 0, s>>>(partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf, zero_len);
+      launch_pdl(k_colsum_ctl<2>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
+                 zero_buf, zero_len);
       break;
   }
   FSA_LAUNCH_CHECK();

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -50,6 +51,36 @@ struct NvtxRange {
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
+
+// ---- programmatic dependent launch (PDL) -------------------------------------------------
+// The PCG sweep kernels are launched with programmatic stream serialisation: a kernel's CTAs
+// may be scheduled while its predecessor drains, and each such kernel executes pdl_wait()
+// (griddepcontrol.wait) before it touches anything the predecessor writes (setup such as TMEM
+// allocation and mbarrier initialisation goes first). Without the attribute the wait is a no-op.
+// FSA_PDL=0 disables it (A/B measurement).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FSA_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... Params, typename... Args>
+inline void launch_pdl(void (*kern)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<Params>(args)...);
+  if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
 
 inline long round_up(long x, long a) { return (x + a - 1) / a * a; }
 inline long cdiv(long x, long a) { return (x + a - 1) / a; }

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(256) k_core_dmma(const double* __restrict__ Qi
                                                   const double* __restrict__ S, long ld,
                                                   double* __restrict__ W, unsigned long long* __restrict__ wmax) {
   __shared__ double red[8][8][NT * 8];
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long r0 = static_cast<long>(blockIdx.x) * 8;
   const long kper = mp / 8, k0 = warp * kper;
@@ -324,15 +325,15 @@ void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W
   require(core_apply_supported(mp, ld), "core_apply: unsupported shape");
   const unsigned grid = static_cast<unsigned>(mp / 8);
   switch (ld / 8) {
-    case 1: k_core_dmma<1><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 2: k_core_dmma<2><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 3: k_core_dmma<3><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 4: k_core_dmma<4><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 5: k_core_dmma<5><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 6: k_core_dmma<6><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 7: k_core_dmma<7><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    case 8: k_core_dmma<8><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
-    default: k_core_dmma<9><<<grid, 256, 0, s>>>(Qinv, mp, S, ld, W, wmax); break;
+    case 1: launch_pdl(k_core_dmma<1>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 2: launch_pdl(k_core_dmma<2>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 3: launch_pdl(k_core_dmma<3>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 4: launch_pdl(k_core_dmma<4>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 5: launch_pdl(k_core_dmma<5>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 6: launch_pdl(k_core_dmma<6>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 7: launch_pdl(k_core_dmma<7>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    case 8: launch_pdl(k_core_dmma<8>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
+    default: launch_pdl(k_core_dmma<9>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
   }
   FSA_LAUNCH_CHECK();
 }

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  pdl_wait();  // (TMEM allocation and barrier setup overlap the predecessor)
 
   if (tid == 0) {
     const int8_t* Ablk = A + (static_cast<long>(tile) * nkb_all + kb0) * kATile;
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // producer
@@ -853,6 +855,7 @@ __global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, l
                                                  long n_pad, int kb_per_chunk, int parts,
                                                  unsigned long long* __restrict__ ymax) {
   __shared__ double red[256];
+  pdl_wait();
   const int chunk = blockIdx.x, part = blockIdx.y;
   const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
   const long i0 = static_cast<long>(chunk) * kb_per_chunk * kKb;
@@ -875,6 +878,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
                                                      const double* __restrict__ scale, int kb_per_chunk,
                                                      const unsigned long long* __restrict__ ymax,
                                                      int* __restrict__ f, int8_t* __restrict__ Ys, int nc = kOzCols) {
+  pdl_wait();
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
   if (c >= nc) return;
@@ -897,6 +901,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
 __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long ld, long tp, long mp,
                                                   int* __restrict__ h) {
   __shared__ double red[1024];
+  pdl_wait();
   const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;  // 16 row phases
   double mx = 0.0;
   if (c < tp)
@@ -911,6 +916,7 @@ __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, 
 __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ W, long ld, long tp,
                                                      int* __restrict__ h, int8_t* __restrict__ Ws,
                                                      const unsigned long long* __restrict__ wmax, int nc = kOzCols) {
+  pdl_wait();
   const int kb = blockIdx.x;
   const int c = threadIdx.x & 63, kc = threadIdx.x >> 6;
   if (c >= nc) return;
@@ -933,6 +939,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ 
 // S[r][c] = sum_chunk part[chunk][r][c] (fixed order)
 __global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long ld, long tp,
                             double* __restrict__ S) {
+  pdl_wait();
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= mp * tp) return;
   const long r = idx / tp, c = idx % tp;
@@ -949,7 +956,7 @@ void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nk
     attr = true;
   }
   OzPair pr{{B, B}, {epi, epi}};
-  k_oz_gemm<false><<<dim3(tiles, chunks), 128, kSmem, s>>>(A, pr, nkb_all, kb_per_chunk);
+  launch_pdl(k_oz_gemm<false>, dim3(tiles, chunks), dim3(128), kSmem, s, A, pr, nkb_all, kb_per_chunk);
   FSA_LAUNCH_CHECK();
 }
 void launch_gemm_pair(const int8_t* A, const OzPair& pr, int tiles, int chunks, int nkb_all, int kb_per_chunk,
@@ -959,7 +966,7 @@ void launch_gemm_pair(const int8_t* A, const OzPair& pr, int tiles, int chunks, 
     FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  k_oz_gemm<true><<<dim3(2, tiles, chunks), 128, kSmem, s>>>(A, pr, nkb_all, kb_per_chunk);
+  launch_pdl(k_oz_gemm<true>, dim3(2, tiles, chunks), dim3(128), kSmem, s, A, pr, nkb_all, kb_per_chunk);
   FSA_LAUNCH_CHECK();
 }
 
@@ -986,7 +993,8 @@ void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const i
   const int grid = std::min(p.ptiles, kNumSMs);
   const int8_t* B = Ws != nullptr ? Ws : p.Ws.get();
   OzPair pr{{B, B}, {epi, epi}};
-  k_oz_expand<false><<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), pr, p.ptiles, p.mkb);
+  launch_pdl(k_oz_expand<false>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()), pr,
+             p.ptiles, p.mkb);
   FSA_LAUNCH_CHECK();
 }
 void launch_expand_pair(const OzakiPlan& p, const OzPair& pr, cudaStream_t s) {
@@ -996,7 +1004,8 @@ void launch_expand_pair(const OzakiPlan& p, const OzPair& pr, cudaStream_t s) {
     attr = true;
   }
   const int grid = 2 * std::min(p.ptiles, kNumSMs / 2);
-  k_oz_expand<true><<<grid, 64 + kXEpi, kXSmem, s>>>(p.Ac.get(), pr, p.ptiles, p.mkb);
+  launch_pdl(k_oz_expand<true>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()), pr,
+             p.ptiles, p.mkb);
   FSA_LAUNCH_CHECK();
 }
 
@@ -1005,10 +1014,11 @@ void slice_y(OzakiPlan& p, const double* V, long ld, long tp, const double* scal
              int8_t* Ys, cudaStream_t s, bool ymax_ready, int nc = kOzCols) {
   if (!ymax_ready) {
     FSA_CUDA(cudaMemsetAsync(ymax, 0, sizeof(unsigned long long) * p.nchunks * kOzCols, s));
-    k_oz_ymax<<<dim3(p.nchunks, 16), 256, 0, s>>>(V, ld, tp, scale, p.n_pad, p.kb_per_chunk, 16, ymax);
+    launch_pdl(k_oz_ymax, dim3(p.nchunks, 16), dim3(256), 0, s, V, ld, tp, scale, p.n_pad, p.kb_per_chunk, 16, ymax);
     FSA_LAUNCH_CHECK();
   }
-  k_oz_planes_y<<<p.nkb, 128, 0, s>>>(V, ld, tp, scale, p.kb_per_chunk, ymax, f, Ys, nc);
+  launch_pdl(k_oz_planes_y, dim3(p.nkb), dim3(128), 0, s, V, ld, tp, scale, p.kb_per_chunk,
+             static_cast<const unsigned long long*>(ymax), f, Ys, nc);
   FSA_LAUNCH_CHECK();
 }
 void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double* scale, double* S, cudaStream_t s,
@@ -1017,8 +1027,8 @@ void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double*
   slice_y(p, V, ld, tp, scale, p.ymax.get(), p.f.get(), p.Ys.get(), s, ymax_ready);
   OzEpi epi{0, p.m_pad, tp, ld, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
   launch_gemm(p.Ar.get(), p.Ys.get(), p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, epi, s);
-  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * tp, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, ld, tp,
-                                                                             S);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * tp, 256))), dim3(256), 0, s, p.part.get(), p.nchunks, p.m_pad, ld, tp,
+             S);
   FSA_LAUNCH_CHECK();
 }
 
@@ -1026,10 +1036,10 @@ void slice_w_to(OzakiPlan& p, const double* W, long ld, long tp, int8_t* Ws, int
                 const unsigned long long* wmax = nullptr, int nc = kOzCols) {
   require(p.ready && tp <= kOzCols && tp <= ld, "ozaki: plan not prepared or too many columns");
   if (wmax == nullptr) {
-    k_oz_wexp<<<1, 1024, 0, s>>>(W, ld, tp, p.m_pad, h);
+    launch_pdl(k_oz_wexp, dim3(1), dim3(1024), 0, s, W, ld, tp, p.m_pad, h);
     FSA_LAUNCH_CHECK();
   }
-  k_oz_planes_w<<<p.mkb, 128, 0, s>>>(W, ld, tp, h, Ws, wmax, nc);
+  launch_pdl(k_oz_planes_w, dim3(p.mkb), dim3(128), 0, s, W, ld, tp, h, Ws, wmax, nc);
   FSA_LAUNCH_CHECK();
 }
 void slice_w(OzakiPlan& p, const double* W, long ld, long tp, cudaStream_t s) {
@@ -1125,11 +1135,11 @@ void ozaki_project_pair(OzakiPlan& p, const double* R, long ld, long ncols, cons
              OzEpi{0, p.m_pad, n1, ld, p.er.get(), p.f2.get(), p.part2.get(), nullptr, nullptr, nullptr, nullptr}},
             nc};
   launch_gemm_pair(p.Ar.get(), pr, p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, s);
-  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * n0, 256)), 256, 0, s>>>(p.part.get(), p.nchunks, p.m_pad, ld, n0,
-                                                                            S);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * n0, 256))), dim3(256), 0, s, p.part.get(), p.nchunks, p.m_pad, ld, n0,
+             S);
   FSA_LAUNCH_CHECK();
-  k_oz_reduce<<<static_cast<unsigned>(cdiv(p.m_pad * n1, 256)), 256, 0, s>>>(p.part2.get(), p.nchunks, p.m_pad, ld, n1,
-                                                                            S + n0);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * n1, 256))), dim3(256), 0, s, p.part2.get(), p.nchunks, p.m_pad, ld, n1,
+             S + n0);
   FSA_LAUNCH_CHECK();
 }
 void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,

@@ -359,10 +359,9 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
   const int below = (1 << warp) - 1;
   int2 cur{0, 0}, nxt{0, 0};
   int gc[RW];
-  if (npc > 0) {
-    load_meta(0, cur, gc);
-    issue(0, cur, gc);
-  }
+  if (npc > 0) load_meta(0, cur, gc);  // (static group metadata: read before the dependency wait)
+  pdl_wait();
+  if (npc > 0) issue(0, cur, gc);
   if (npc > 1) load_meta(1, nxt, gc);
   for (int pc = 0; pc < npc; ++pc) {
     if (pc + 1 < npc) issue(pc + 1, nxt, gc);
@@ -947,7 +946,7 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      kern<<<grid, 128, smem, s>>>(a);
+      launch_pdl(kern, grid, dim3(128), static_cast<size_t>(smem), s, a);
     };
     auto go_ws = [&](auto kern, int wsmem) {
       static int blocks_per_sm = 0;  // per template instance
