@@ -28,11 +28,27 @@ __global__ void k_copy_cols(const double* __restrict__ src, long lds, double* __
   dst[i * ldd + j] = src[i * lds + j];
 }
 
-__global__ void k_sum_log(const double* __restrict__ x, long n, double* out) {
+// sum_i log x_i in two fixed-order passes (block partials over fixed row ranges, then their sum):
+// deterministic, and the logs spread over every SM instead of one block (was 231 us at n = 1e5)
+constexpr int kSumLogBlocks = 2 * kNumSMs;
+__global__ void k_sum_log(const double* __restrict__ x, long n, double* __restrict__ part) {
   __shared__ double red[256];
   double s = 0.0;
-  for (long i = threadIdx.x; i < n; i += blockDim.x) s += log(x[i]);
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x)
+    s += log(x[i]);
   red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void k_sum_parts(const double* __restrict__ part, int nb, double* out) {
+  __shared__ double red[256];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) v += part[i];
+  red[threadIdx.x] = v;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
@@ -555,7 +571,10 @@ void copy_cols(const double* src, long lds, double* dst, long ldd, long n, long 
   FSA_LAUNCH_CHECK();
 }
 void sum_log(const double* x, long n, double* out_dev, cudaStream_t s) {
-  k_sum_log<<<1, 256, 0, s>>>(x, n, out_dev);
+  DBuf<double> part(kSumLogBlocks);
+  k_sum_log<<<kSumLogBlocks, 256, 0, s>>>(x, n, part.get());
+  FSA_LAUNCH_CHECK();
+  k_sum_parts<<<1, 256, 0, s>>>(part.get(), kSumLogBlocks, out_dev);
   FSA_LAUNCH_CHECK();
 }
 void affine_vec(double* y, const double* x, double a, double b, long n, long n_pad, cudaStream_t s) {

@@ -246,18 +246,6 @@ void Model::start_ozaki() {
   oz_pending = true;
 }
 
-bool Model::use_ozaki_spmm(long tp) const {
-  // opt-in (FSA_SPMM=int8): at config 2 the INT8 SpMM (plus its per-sweep H slicing) is not
-  // yet faster than the DMMA block SpMM
-  static const char* env = std::getenv("FSA_SPMM");
-  static const bool on = env && std::strcmp(env, "int8") == 0;
-  return on && use_ozaki(tp) && geo->pat.g128.gnnz > 0;
-}
-void Model::ensure_ozaki_spmm() {
-  if (ozs.ready) return;
-  KTimer t(ctx, "ozaki_spmm_prepare", 8.0 * 128 * geo->pat.g128.gnnz);
-  ozaki_spmm_prepare(ozs, geo->pat, sval.get(), ctx->stream);
-}
 
 void Model::project(const double* M, const double* V, long tp, double* out, const double* scale) {
   const double flops = 2.0 * m * n * (cols_hint > 0 && cols_hint <= tp ? cols_hint : tp);
@@ -877,7 +865,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   // Fused direction update (block SpMM path): the SpMM of sweep i gathers Z_{i-1} instead of
   // H_i and forms, on its own rows, H_i = Z + beta H and V_i = (Lw + Sigma_s Z) + beta V_{i-1}
   // (= U^T U H_i + Sigma_s H_i by linearity), so no separate H / Vlr pass runs
-  const bool fuse_h = fused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp) && !md->use_ozaki_spmm(tp);
+  const bool fuse_h = fused && md->geo->pat.gnnz > 0 && spmm_block_supported(tp);
   bool first_sweep = true;
   // Ozaki projection inputs: update_xr_dot_max leaves the chunk maxima of |D^{-1} R|
   const bool oz = fused && md->use_ozaki(tp);
@@ -897,8 +885,6 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     w.tick.zero(s);
     w.wmax.alloc(kOzCols);
   }
-  const bool oz_spmm = oz && md->use_ozaki_spmm(tp);
-  if (oz_spmm) md->ensure_ozaki_spmm();
   bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
   auto precond = [&](double* rzout, bool sums = true) {
@@ -1046,11 +1032,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
         md->halo_exchange(w.H.get(), tp);
         KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 24.0 * n * k);  // CSR + H, Vlr read + V write
-        if (oz_spmm)
-          // valid rows of H: owned (padded) + halo; the tail up to n_ext_pad is never written
-          ozaki_spmm_dot(md->ozs, md->geo->pat, w.H.get(), md->n_pad + (md->world() > 1 ? md->geo->shard.n_halo : 0),
-                         tp, w.V.get(), w.Vlr.get(), hv, part, s);
-        else if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
+        if (md->geo->pat.gnnz > 0 && spmm_block_supported(tp))
           spmm_block_dot(md->geo->pat, md->gval.get(), w.H.get(), tp, w.V.get(), tp, tp, hv, part, w.Vlr.get(), s);
         else
           spmm_dot(md->geo->pat.rowptr.get(), md->geo->pat.col.get(), md->sval.get(), n, w.H.get(), tp, w.V.get(), tp,

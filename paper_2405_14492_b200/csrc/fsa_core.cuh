@@ -195,10 +195,6 @@ class Model {
   void start_ozaki();
   bool oz_pending = false;
   cudaEvent_t oz_done = nullptr;
-  // INT8 tensor-core SpMM planes of Sigma_s (built lazily per parameter set)
-  OzakiSpmm ozs;
-  bool use_ozaki_spmm(long tp) const;
-  void ensure_ozaki_spmm();
 };
 
 // ---- preconditioners (preconditioners.h:16-115) ------------------------------------------

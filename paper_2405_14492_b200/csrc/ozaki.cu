@@ -515,273 +515,6 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// ---- SpMM V = Vlr + Sigma_s H on the INT8 tensor cores -------------------------------------
-// 128-row groups (Csr::g128): the group's 128 x union value block is split per row into 8
-// digit planes (A, K-major, precomputed per parameter set, one bulk copy per 32-slot K block);
-// H is split per column (global exponent) into 8 planes per sweep, and the K block's 32 union
-// rows of every plane are gathered with cp.async straight into the MN-major canonical layout
-// of the B operand ([K group][MN group][8 rows][16 columns]). Same MMA schedule and TMEM
-// accumulators as the expansion; the epilogue adds Vlr and forms the h.v column partials.
-struct OzSpmmArgs {
-  const long* gptr;     // 128-row group union offsets (multiples of 32)
-  const int* gcol;      // union columns
-  const int8_t* Ap;     // value planes [K block][plane][kc][rg][8][16]
-  const int* erow;      // row exponents of the value planes
-  const int8_t* Hp;     // H planes [plane][row][64]
-  long hrows;           // rows per H plane
-  const int* fcol;      // column exponents of H
-  const double* H;      // fp64 H (h.v)
-  const double* Vlr;
-  double* V;
-  double* part;         // [group][tp] h.v partials
-  long nrows, tp;
-  int ngrp;
-};
-constexpr int kSStages = 3;
-constexpr int kSSmem = kSStages * (kATile + kBTile) + 128 * kXLd * 8;
-__global__ void __launch_bounds__(288, 1) k_oz_spmm(OzSpmmArgs q) {
-  constexpr int kStages = kSStages;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull, tempty;
-  __shared__ uint32_t tmem_base_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kATile;
-  double* tileY = reinterpret_cast<double*>(smem + kStages * (kATile + kBTile));  // [128][kXLd]
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 32) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], 129);  // 128 gathering threads (cp.async arrive) + the bulk-copy arrival
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(&tfull, 1);
-    mbar_init(&tempty, 4);
-    mbar_init_fence();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_s;
-  if (warp < 4) {  // producers: thread 0 bulk-copies the A planes, all 128 gather the B planes
-    long g_stage = 0;
-    int pend = -1;  // stage whose gathers are in flight and not yet signalled
-    __shared__ int ucol[2048];
-    for (int g = blockIdx.x; g < q.ngrp; g += gridDim.x) {
-      const long u0 = q.gptr[g];
-      const int up = static_cast<int>(q.gptr[g + 1] - u0);
-      const int nkb = up / 32;
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // previous group's ucol fully consumed
-      for (int i = tid; i < up; i += 128) ucol[i] = q.gcol[u0 + i];
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      for (int kb = 0; kb < nkb; ++kb, ++g_stage) {
-        const int st = static_cast<int>(g_stage % kStages);
-        if (g_stage >= kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g_stage / kStages - 1) & 1));
-        if (tid == 0) {
-          mbar_expect_tx(&full[st], kATile);
-          bulk_g2s(sA + st * kATile, q.Ap + (u0 / 32 + kb) * static_cast<long>(kATile), kATile, &full[st]);
-        }
-        uint8_t* bs = sB + st * kBTile;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {  // 1024 16-byte chunks: (union row u, plane b, column group mg)
-          const int id = tid + 128 * i;
-          const int mg = id & 3, b = (id >> 2) & 7, u = id >> 5;
-          const long row = ucol[kb * 32 + u];
-          cp_async16(bs + ((u >> 3) * 32 + b * 4 + mg) * 128 + (u & 7) * 16,
-                     q.Hp + (static_cast<long>(b) * q.hrows + row) * 64 + mg * 16);
-        }
-        cp_async_commit();
-        // the previous stage's gathers have landed: make them visible to the tensor core
-        // (async proxy) and arrive; the current stage stays in flight meanwhile
-        if (pend >= 0) {
-          cp_async_wait<1>();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[pend])) : "memory");
-        }
-        pend = st;
-      }
-    }
-    if (pend >= 0) {
-      cp_async_wait<0>();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[pend])) : "memory");
-    }
-  } else if (warp == 4) {
-    if (lane == 0) {  // MMA issuer
-      long g_stage = 0;
-      int lt = 0;
-      for (int g = blockIdx.x; g < q.ngrp; g += gridDim.x, ++lt) {
-        const int nkb = static_cast<int>((q.gptr[g + 1] - q.gptr[g]) / 32);
-        if (lt > 0) {
-          mbar_wait(&tempty, static_cast<uint32_t>((lt - 1) & 1));
-          tc_fence_after();
-        }
-        for (int kb = 0; kb < nkb; ++kb, ++g_stage) {
-          const int st = static_cast<int>(g_stage % kStages);
-          mbar_wait(&full[st], static_cast<uint32_t>((g_stage / kStages) & 1));
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-#pragma unroll
-          for (int a = 1; a <= kOzSlices; ++a) {
-#pragma unroll
-            for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
-              const int nb = min(4, kOzSlices + 2 - a - bs);
-              // B: MN-major, MN groups of 16 columns at 128 B, K groups of 8 rows at 32 x 128 B
-              mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * kOzCols), umma_desc(a0 + (a - 1) * 4096, 2048, 128),
-                     umma_desc(b0 + (bs - 1) * 512, 4096, 128), idesc_i8(128, nb * kOzCols) | (1u << 16),
-                     (kb > 0 || a > 1) ? 1u : 0u);
-            }
-          }
-          mma_commit(&empty[st]);
-        }
-        mma_commit(&tfull);
-      }
-    }
-    __syncwarp();
-  } else {  // epilogue warps 5..8: TMEM lane quadrant warp % 4
-    const int qd = warp & 3;
-    const int row = qd * 32 + lane;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
-    const long tp = q.tp;
-    const int et = tid - 160;  // 0..127
-    int lt = 0;
-    for (int g = blockIdx.x; g < q.ngrp; g += gridDim.x, ++lt) {
-      mbar_wait(&tfull, static_cast<uint32_t>(lt & 1));
-      tc_fence_after();
-      const long r0 = static_cast<long>(g) * 128;
-      const long ri = r0 + row;
-      const int ei = ri < q.nrows ? q.erow[ri] : 0;
-#pragma unroll 1
-      for (int gq = 0; gq < kOzCols / 16; ++gq) {
-        double y[16];
-        drain16(trow, gq * 16, y);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) tileY[row * kXLd + gq * 16 + c] = y[c] * pow2(ei + q.fcol[gq * 16 + c]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty)) : "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // thread (column c, row parity h): coalesced rows; V = Vlr + S H, h.v column partials
-      const int c = et & 63, h = et >> 6;
-      double sacc = 0.0;
-      if (c < tp) {
-#pragma unroll 1
-        for (int rb = h; rb < 128; rb += 16) {
-          double vl[8], hh[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const long r = r0 + rb + 2 * u;
-            vl[u] = r < q.nrows ? __ldg(q.Vlr + r * tp + c) : 0.0;
-            hh[u] = r < q.nrows ? __ldg(q.H + r * tp + c) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const long r = r0 + rb + 2 * u;
-            if (r < q.nrows) {
-              const double v = vl[u] + tileY[(rb + 2 * u) * kXLd + c];
-              q.V[r * tp + c] = v;
-              sacc = fma(hh[u], v, sacc);
-            }
-          }
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (c < tp) tileY[h * kXLd + c] = sacc;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (h == 0 && c < tp) q.part[static_cast<long>(g) * tp + c] = tileY[c] + tileY[kXLd + c];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// value planes of the 128-row groups: dense blocks (scatter), row exponents, digits
-__global__ void k_spv_scatter(const long* __restrict__ rowptr, const int* __restrict__ lidx,
-                              const long* __restrict__ gptr, long nrows, const double* __restrict__ val,
-                              double* __restrict__ dense, int* __restrict__ erow) {
-  const long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= nrows) return;
-  const long g = r / 128, o = gptr[g], up = gptr[g + 1] - o;
-  const int rr = static_cast<int>(r % 128);
-  double mx = 0.0;
-  for (long p = rowptr[r] + lane; p < rowptr[r + 1]; p += 32) {
-    const double v = val[p];
-    dense[128 * o + rr * up + lidx[p]] = v;
-    mx = fmax(mx, fabs(v));
-  }
-#pragma unroll
-  for (int w = 16; w > 0; w >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, w));
-  if (lane == 0) erow[r] = group_exp(mx);
-}
-__global__ void __launch_bounds__(256) k_spv_planes(const double* __restrict__ dense, const long* __restrict__ gptr,
-                                                    const int* __restrict__ kbgroup, const int* __restrict__ erow,
-                                                    long nrows, int8_t* __restrict__ Ap) {
-  const long gkb = blockIdx.x;  // global K block
-  const int g = kbgroup[gkb];
-  const long o = gptr[g], up = gptr[g + 1] - o;
-  const long kb = gkb - o / 32;
-  const int rr = threadIdx.x & 127, kc = threadIdx.x >> 7;
-  const long r = static_cast<long>(g) * 128 + rr;
-  const int e = r < nrows ? erow[r] : 0;
-  double v[16];
-  const double* src = dense + 128 * o + rr * up + kb * 32 + kc * 16;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = src[i];
-  int4 out[kOzSlices];
-  digits16(v, e, out);
-  int8_t* base = Ap + gkb * kATile + kc * 2048 + (rr >> 3) * 128 + (rr & 7) * 16;
-#pragma unroll
-  for (int a = 0; a < kOzSlices; ++a) *reinterpret_cast<int4*>(base + a * 4096) = out[a];
-}
-__global__ void k_kb_group(const long* __restrict__ gptr, long ngrp, int* __restrict__ kbgroup) {
-  const long g = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g >= ngrp) return;
-  for (long kb = gptr[g] / 32; kb < gptr[g + 1] / 32; ++kb) kbgroup[kb] = static_cast<int>(g);
-}
-// per-sweep H planes: column exponents over all rows, then digits [plane][row][64]
-__global__ void __launch_bounds__(256) k_h_colmax(const double* __restrict__ H, long tp, long nrows,
-                                                  unsigned long long* __restrict__ hmax) {
-  __shared__ double red[256];
-  const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
-  double mx = 0.0;
-  if (c < tp)
-    for (long i = static_cast<long>(blockIdx.x) * 4 + ph; i < nrows; i += 4L * gridDim.x) mx = fmax(mx, fabs(H[i * tp + c]));
-  red[threadIdx.x] = mx;
-  __syncthreads();
-  if (ph == 0) {
-    mx = fmax(fmax(mx, red[threadIdx.x + 64]), fmax(red[threadIdx.x + 128], red[threadIdx.x + 192]));
-    if (mx > 0.0) atomicMax(hmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
-  }
-}
-__global__ void k_h_planes(const double* __restrict__ H, long tp, long nrows, long hrows,
-                           const unsigned long long* __restrict__ hmax, int* __restrict__ fcol,
-                           int8_t* __restrict__ Hp) {
-  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;  // (row, 16-column chunk)
-  if (idx >= hrows * 4) return;
-  const long i = idx >> 2;
-  const int ch = static_cast<int>(idx & 3);
-  double v[16];
-  int e[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int c = ch * 16 + j;
-    e[j] = group_exp(__longlong_as_double(static_cast<long long>(hmax[c])));
-    v[j] = (c < tp && i < nrows) ? H[i * tp + c] * pow2(-e[j]) : 0.0;
-  }
-  if (i == 0)
-    for (int j = 0; j < 16; ++j) fcol[ch * 16 + j] = e[j];
-  int4 out[kOzSlices];
-  digits16(v, 0, out);
-#pragma unroll
-  for (int a = 0; a < kOzSlices; ++a) *reinterpret_cast<int4*>(Hp + (a * hrows + i) * 64 + ch * 16) = out[a];
-}
-
 // ---- digit planes ---------------------------------------------------------------------------------
 // project A: exponent per (chunk, inducing row) over the chunk's points
 __global__ void __launch_bounds__(256) k_oz_exp_rows(const double* __restrict__ U, long mp, long n_pad,
@@ -1198,53 +931,6 @@ void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaS
   slice_w(p, W, tp, tp, s);
   OzEpi epi{2, p.m_pad, tp, tp, p.ec.get(), p.h.get(), nullptr, nullptr, Y, nullptr, nullptr};
   launch_expand(p, epi, s);
-}
-
-void ozaki_spmm_prepare(OzakiSpmm& z, const Csr& pat, const double* val, cudaStream_t s) {
-  const RowGroups& q = pat.g128;
-  z.ready = false;
-  if (q.gnnz == 0) return;
-  const long nkb = q.gnnz / 32;
-  z.Ap.alloc(static_cast<size_t>(nkb) * kATile);
-  z.erow.alloc(static_cast<size_t>(std::max<long>(pat.rows, 1)));
-  z.kbgroup.alloc(static_cast<size_t>(nkb));
-  DBuf<double> dense(static_cast<size_t>(128 * q.gnnz));
-  dense.zero(s);
-  k_spv_scatter<<<static_cast<unsigned>(cdiv(pat.rows * 32, 256)), 256, 0, s>>>(
-      pat.rowptr.get(), q.gslot.get(), q.gptr.get(), pat.rows, val, dense.get(), z.erow.get());
-  FSA_LAUNCH_CHECK();
-  k_kb_group<<<static_cast<unsigned>(cdiv(q.ngrp, 256)), 256, 0, s>>>(q.gptr.get(), q.ngrp, z.kbgroup.get());
-  FSA_LAUNCH_CHECK();
-  k_spv_planes<<<static_cast<unsigned>(nkb), 256, 0, s>>>(dense.get(), q.gptr.get(), z.kbgroup.get(), z.erow.get(),
-                                                         pat.rows, z.Ap.get());
-  FSA_LAUNCH_CHECK();
-  z.hmax.alloc(kOzCols);
-  z.fcol.alloc(kOzCols);
-  z.ready = true;
-}
-
-void ozaki_spmm_dot(OzakiSpmm& z, const Csr& pat, const double* H, long hrows, long tp, double* V, const double* Vlr,
-                    double* hv, double* partial, cudaStream_t s) {
-  require(z.ready && tp <= kOzCols, "ozaki_spmm: not prepared or too many columns");
-  const RowGroups& q = pat.g128;
-  const long hr = round_up(hrows, 8);
-  if (z.Hp.n < static_cast<size_t>(8 * hr * 64)) z.Hp.alloc(static_cast<size_t>(8 * hr * 64));
-  FSA_CUDA(cudaMemsetAsync(z.hmax.get(), 0, z.hmax.bytes(), s));
-  k_h_colmax<<<kNumSMs * 4, 256, 0, s>>>(H, tp, hrows, z.hmax.get());
-  FSA_LAUNCH_CHECK();
-  k_h_planes<<<static_cast<unsigned>(cdiv(hr * 4, 256)), 256, 0, s>>>(H, tp, hrows, hr, z.hmax.get(), z.fcol.get(),
-                                                                      z.Hp.get());
-  FSA_LAUNCH_CHECK();
-  static bool attr = false;
-  if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_spmm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem));
-    attr = true;
-  }
-  OzSpmmArgs a{q.gptr.get(), q.gcol.get(), z.Ap.get(), z.erow.get(), z.Hp.get(), hr, z.fcol.get(), H, Vlr, V,
-               partial, pat.rows, tp, static_cast<int>(q.ngrp)};
-  k_oz_spmm<<<static_cast<unsigned>(std::min<long>(q.ngrp, kNumSMs)), 288, kSSmem, s>>>(a);
-  FSA_LAUNCH_CHECK();
-  colsum_partials(partial, q.ngrp, tp, tp, hv, s);
 }
 
 }  // namespace fsa

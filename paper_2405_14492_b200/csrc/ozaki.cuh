@@ -69,14 +69,6 @@ struct OzakiPlan {
 
 inline bool ozaki_supported(long tp) { return tp <= kOzCols; }
 
-// INT8 tensor-core SpMM of the PCG sweep (Csr::g128 row groups): value digit planes per
-// parameter set, H digit planes per call
-struct OzakiSpmm {
-  DBuf<int8_t> Ap, Hp;
-  DBuf<int> erow, kbgroup, fcol;
-  DBuf<unsigned long long> hmax;
-  bool ready = false;
-};
 // digit planes of U (m_pad x n_pad, column per point, ld m_pad); n_pad % 128 == 0, m_pad % 128 == 0
 void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaStream_t s);
 // S (m_pad x ncols, row stride ld) = U diag(Dinv) R over the plan's n_pad rows of R (row stride
@@ -110,12 +102,5 @@ void ozaki_project_wide(OzakiPlan& p, const double* V, long ldv, const double* s
 // plain products for tests: S = U diag(scale) V (scale may be null), Y = U^T W
 void ozaki_project_plain(OzakiPlan& p, const double* V, long tp, const double* scale, double* S, cudaStream_t s);
 void ozaki_expand_plain(OzakiPlan& p, const double* W, long tp, double* Y, cudaStream_t s);
-
-// planes of the Sigma_s values on pat.g128 (no-op when the groups were not built)
-void ozaki_spmm_prepare(OzakiSpmm& z, const Csr& pat, const double* val, cudaStream_t s);
-// V = Vlr + S H (tp <= 64, ld tp) over pat.rows rows; H has hrows rows (local + halo);
-// hv[c] = sum_r H[r][c] V[r][c]; partial holds pat.g128.ngrp * tp doubles
-void ozaki_spmm_dot(OzakiSpmm& z, const Csr& pat, const double* H, long hrows, long tp, double* V, const double* Vlr,
-                    double* hv, double* partial, cudaStream_t s);
 
 }  // namespace fsa

@@ -576,13 +576,6 @@ void build_groups(Csr& pat, cudaStream_t s) {
                    static_cast<double>(pat.ntiles) / std::max<long>(1, pat.nkb * 4),
                    static_cast<double>(pat.nnz) / std::max<long>(1, pat.ntiles));
   }
-  // 128-row groups of the INT8 tensor-core SpMM (opt-in, FSA_SPMM=int8; unions padded to its
-  // 32-row K blocks)
-  static const bool int8 = std::getenv("FSA_SPMM") && std::strcmp(std::getenv("FSA_SPMM"), "int8") == 0;
-  RowGroups& q = pat.g128;
-  q.G = 128;
-  q.gnnz = 0;
-  if (int8 && !build_unions(pat, 128, 32, 16384, 2048, q.ngrp, q.gnnz, q.gmax, q.gptr, q.gcol, q.gslot, s)) q.gnnz = 0;
   FSA_CUDA(cudaStreamSynchronize(s));
 }
 

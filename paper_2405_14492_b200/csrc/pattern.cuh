@@ -33,15 +33,6 @@ struct SortedPoints {
   DBuf<unsigned long long> keys;  // sorted cell keys, length n
 };
 
-// unions of the columns of G consecutive rows (see Csr::gptr below)
-struct RowGroups {
-  int G = 0;
-  long ngrp = 0, gnnz = 0;  // gnnz = total padded union size (0: not built)
-  int gmax = 0;
-  DBuf<long> gptr;          // ngrp + 1
-  DBuf<int> gcol;           // union columns (ascending; padding repeats a valid column)
-  DBuf<int> gslot;          // per entry: its union-local index
-};
 
 struct Csr {
   long rows = 0, cols = 0, nnz = 0;
@@ -67,7 +58,6 @@ struct Csr {
   long nkb = 0, ntiles = 0;    // k-steps (gnnz / 4) and stored tiles
   DBuf<int> kmask, koff;       // nkb, nkb + 1
   DBuf<int> pmeta;             // per k-step (int2): {koff[kb], kmask[kb + i] << 4 i for i < 8}
-  RowGroups g128;              // 128-row groups of the INT8 tensor-core SpMM (ozaki.cu)
 };
 constexpr int kGroup = 32;
 // builds the row groups (leaves gnnz = 0 if some group has more than 4096 entries)

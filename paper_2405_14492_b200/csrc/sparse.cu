@@ -443,237 +443,6 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
   if (tid < NT * 8 && tid < ncols)
     q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
 }
-// k_spmm_ws: persistent, warp-specialised form of k_spmm_rt (same value tiles, same DMMA
-// schedule, same epilogue and the same fixed-order h.v partials). Measured on k_spmm_rt: with its
-// one-piece-ahead cp.async double buffer and two __syncthreads per 16-row piece, the kernel
-// skeleton alone (no gathers, no DMMA, no epilogue) took 43 of its 138 us at config 2 — every
-// piece waited out the gather latency, and 3125 short-lived CTAs paid their prologue and
-// epilogue in series. Here one producer warp streams the RHS rows and value tiles of piece after
-// piece, group after group, into an S-stage ring (cp.async with mbarrier completion, the next
-// piece's column indices prefetched into registers), and the four consumer warps (row tile w
-// each) only wait on `full` barriers: the ring keeps S pieces of gathers in flight, and while the
-// consumers run a group's epilogue (the H / V streams, HBM-bound) the producer is already
-// filling the ring with the next group.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-template <int NT>
-struct WsCfg {
-  static constexpr int P = 16;                   // union rows per stage (4 DMMA k-steps)
-  static constexpr int S = NT <= 7 ? 8 : 6;      // ring stages
-  static constexpr int LDH = NT * 8 + 4;
-  static constexpr int HS = P * LDH, AS = P * kGroup;
-  static constexpr int STAGE = HS + AS;          // doubles per stage
-  static constexpr int META = 2 * 1024 * 4 + 2 * 256 * 8;  // the producer's double-buffered group metadata
-  static constexpr int SMEM = S * STAGE * 8 + META;
-};
-template <int NT>
-__global__ void __launch_bounds__(160, 2) k_spmm_ws(TileSpmmArgs q, int ngrp) {
-  using Cfg = WsCfg<NT>;
-  constexpr int P = Cfg::P, S = Cfg::S, LDH = Cfg::LDH, HS = Cfg::HS, STAGE = Cfg::STAGE;
-  constexpr int WN = 4;
-  constexpr int CH = NT * 4;  // 16-byte chunks per staged row
-  constexpr int GI = (P * CH + 31) / 32;
-  constexpr int UCAP = 1024;  // union capacity of a 32-row group (pattern.cu kUnionCap)
-  extern __shared__ __align__(16) double sm[];  // [S][STAGE], then the producer's group metadata
-  __shared__ __align__(8) uint64_t full[S], empty[S];
-  __shared__ __align__(16) int4 meta[S];        // per stage: value-tile offset, masks, k-steps, last piece
-  int(*gbuf)[UCAP] = reinterpret_cast<int(*)[UCAP]>(sm + S * STAGE);           // [2][UCAP] union columns
-  int2(*mbuf)[UCAP / 4] = reinterpret_cast<int2(*)[UCAP / 4]>(sm + S * STAGE + UCAP);  // [2][UCAP / 4] k-step metadata
-  __shared__ double red[WN][NT * 8];
-  const long c0 = 64L * blockIdx.y;
-  const double* X = q.X + c0;
-  double* Y = q.Y + c0;
-  const double* Y0 = q.Y0 != nullptr ? q.Y0 + c0 : nullptr;
-  const long ncols = q.ncols - c0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 33);  // 32 cp.async arrivals of the producer lanes + lane 0's meta release
-      mbar_init(&empty[i], WN);
-    }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  if (warp == WN) {  // ---- producer warp ----
-    // group metadata (union columns, per-k-step tile masks) is staged into shared memory one group
-    // ahead, so no per-piece global load sits on the producer's critical path
-    auto stage_meta = [&](long g, int b) {
-      const long u0 = q.gptr[g];
-      const int up = static_cast<int>(q.gptr[g + 1] - u0);
-      for (int i = lane; i < up / 4; i += 32) cp_async16(&gbuf[b][4 * i], q.gcol + u0 + 4 * i);
-      for (int i = lane; i < up / 4; i += 32) cp_async8(&mbuf[b][i], q.pmeta + u0 / 4 + i);
-      cp_async_commit();
-    };
-    long k = 0;
-    int b = 0;
-    long g = blockIdx.x;
-    if (g < ngrp) stage_meta(g, 0);
-    for (; g < ngrp; g += gridDim.x, b ^= 1) {
-      const int up = static_cast<int>(q.gptr[g + 1] - q.gptr[g]);
-      if (lane == 0 && !(q.dbg & 16)) {  // this group's epilogue rows into L2 ahead of the consumers
-        const uint32_t rb = static_cast<uint32_t>(kGroup * q.ldy * 8);
-        if (q.Y0 != nullptr) prefetch_l2(q.Y0 + g * kGroup * q.ldy, rb);
-        prefetch_l2(q.X + g * kGroup * q.ldx, static_cast<uint32_t>(kGroup * q.ldx * 8));
-        if (q.Hio != nullptr && !q.first) {
-          prefetch_l2(q.Hio + g * kGroup * q.ldy, rb);
-          prefetch_l2(q.Y + g * kGroup * q.ldy, rb);
-        }
-      }
-      if (g + gridDim.x < ngrp) {
-        stage_meta(g + gridDim.x, b ^ 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      const int npc = (up + P - 1) / P;
-      for (int pc = 0; pc < npc; ++pc, ++k) {
-        const int ua = pc * P, nr = min(P, up - ua);
-        const int gcc = lane < nr ? gbuf[b][ua + lane] : 0;
-        const int2 pm = mbuf[b][pc * (P / 4)];
-        const int st = static_cast<int>(k % S);
-        if (k >= S) mbar_wait(&empty[st], static_cast<uint32_t>((k / S - 1) & 1));
-        double* hs = sm + st * STAGE;
-        double* as = hs + HS;
-#pragma unroll
-        for (int i = 0; i < GI; ++i) {
-          const int idx = lane + 32 * i;
-          const int r = idx / CH, ch = idx - r * CH;
-          const int col = __shfl_sync(0xffffffffu, gcc, r < P ? r : 0);
-          if (r < nr && !(q.dbg & 4)) cp_async16(hs + r * LDH + ch * 2, X + static_cast<long>(col) * q.ldx + ch * 2);
-        }
-        const int nt = __popc(pm.y & static_cast<int>((1ull << nr) - 1ull));
-        const double* src = q.tval + 32L * pm.x;
-        if (!(q.dbg & 8))
-          for (int idx = lane; idx < nt * 16; idx += 32) cp_async16(as + idx * 2, src + idx * 2);
-        cp_async_arrive_noinc(&full[st]);
-        if (lane == 0) {
-          meta[st] = make_int4(pm.x, pm.y, nr / 4, pc == npc - 1 ? 1 : 0);
-          mbar_arrive(&full[st]);  // release: meta[st] is visible to the consumers' acquire
-        }
-      }
-    }
-    return;
-  }
-  // ---- consumer warps: warp w owns row tile w of every group ----
-  const int below = (1 << warp) - 1;
-  long k = 0;
-  for (long g = blockIdx.x; g < ngrp; g += gridDim.x) {
-    double c[NT][2];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
-    for (bool last = false; !last; ++k) {
-      const int st = static_cast<int>(k % S);
-      mbar_wait(&full[st], static_cast<uint32_t>((k / S) & 1));
-      const int4 cur = meta[st];
-      last = cur.w != 0;
-      const double* hs = sm + st * STAGE + (lane & 3) * LDH + (lane >> 2);
-      const double* as = sm + st * STAGE + HS + lane;
-      const int nks = cur.z;
-      int t = 0;
-#pragma unroll
-      for (int ks = 0; ks < P / 4; ++ks) {
-        if (ks < nks) {
-          const int m = (cur.y >> (4 * ks)) & 15;
-          if (((m >> warp) & 1) && !(q.dbg & 1)) {
-            const double a = as[(t + __popc(m & below)) * 32];
-            const double* hb = hs + ks * 4 * LDH;
-            double bb[NT];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bb[j] = hb[j * 8];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) dmma8x8x4(c[j][0], c[j][1], a, bb[j]);
-          }
-          t += __popc(m);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-    }
-    // epilogue: Y = Y0 + S X on this lane's fragments (+ the direction update); h.v partials
-    const long row = g * kGroup + warp * 8 + (lane >> 2);
-    const bool rok = row < q.nrows;
-    double d[NT][2];
-    if (q.dbg & 2) {
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        d[j][0] = c[j][0];
-        d[j][1] = c[j][1];
-      }
-    } else {
-      // loads of JB n-tiles at a time first (memory-level parallelism), then updates and stores
-      constexpr int JB = 4;
-      const bool upd = q.Hio != nullptr && !q.first;
-#pragma unroll
-      for (int j0 = 0; j0 < NT; j0 += JB) {
-        double2 y0v[JB], hv[JB], ho[JB], vo[JB];
-#pragma unroll
-        for (int jj = 0; jj < JB; ++jj) {
-          const int j = j0 + jj;
-          const long cc = j * 8 + 2 * (lane & 3);
-          const bool ok = j < NT && rok && cc < ncols;
-          const double2 zero = make_double2(0.0, 0.0);
-          y0v[jj] = ok && Y0 != nullptr ? *reinterpret_cast<const double2*>(Y0 + row * q.ldy + cc) : zero;
-          hv[jj] = ok ? *reinterpret_cast<const double2*>(X + row * q.ldx + cc) : zero;
-          ho[jj] = ok && upd ? *reinterpret_cast<const double2*>(q.Hio + c0 + row * q.ldy + cc) : zero;
-          vo[jj] = ok && upd ? *reinterpret_cast<const double2*>(Y + row * q.ldy + cc) : zero;
-        }
-#pragma unroll
-        for (int jj = 0; jj < JB; ++jj) {
-          const int j = j0 + jj;
-          if (j >= NT) break;
-          const long cc = j * 8 + 2 * (lane & 3);
-          d[j][0] = d[j][1] = 0.0;
-          if (rok && cc < ncols) {
-            double2 o = make_double2(c[j][0] + y0v[jj].x, c[j][1] + y0v[jj].y);
-            double2 h = hv[jj];
-            if (q.Hio != nullptr) {  // H = Z + beta H (krylov.cpp:92), V = (Lw + S Z) + beta V
-              if (upd) {
-                const long gc = c0 + cc;
-                const double b0 = gc < q.kb ? q.beta[gc] : 0.0, b1 = gc + 1 < q.kb ? q.beta[gc + 1] : 0.0;
-                h.x = h.x + b0 * ho[jj].x;
-                h.y = h.y + b1 * ho[jj].y;
-                o.x += b0 * vo[jj].x;
-                o.y += b1 * vo[jj].y;
-              }
-              *reinterpret_cast<double2*>(q.Hio + c0 + row * q.ldy + cc) = h;
-            }
-            *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
-            d[j][0] = h.x * o.x;
-            d[j][1] = h.y * o.y;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const long cc = j * 8 + 2 * (lane & 3);
-      double d0 = d[j][0], d1 = d[j][1];
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      }
-      if (lane < 4) {
-        red[warp][cc] = d0;
-        red[warp][cc + 1] = d1;
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (tid < NT * 8 && tid < ncols)
-      q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // red is rewritten by the next group
-  }
-}
-
 // ---- block SDDMM: dense Gram blocks of the row groups on DMMA ----------------------------------
 // G = A_R^T B_C for a group's 32 rows R and a 64-column tile C of its union, over K (the
 // inducing dimension): MODE 0 A = B = U (Sigma_s); MODE 1 [U1; U]_R^T [U; T]_C (d Sigma_s /
@@ -917,12 +686,7 @@ void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t 
 
 long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
-// one-CTA-per-group k_spmm_rt (default) or the warp-specialised persistent k_spmm_ws
-// (FSA_SPMM_KERNEL=ws: measured slower at config 2, 145 vs 139 us; kept for A/B measurement)
-static bool spmm_ws() {
-  static const bool ws = std::getenv("FSA_SPMM_KERNEL") && std::strcmp(std::getenv("FSA_SPMM_KERNEL"), "ws") == 0;
-  return ws;
-}
+
 
 bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
 
@@ -948,36 +712,6 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       launch_pdl(kern, grid, dim3(128), static_cast<size_t>(smem), s, a);
     };
-    auto go_ws = [&](auto kern, int wsmem) {
-      static int blocks_per_sm = 0;  // per template instance
-      if (blocks_per_sm == 0) {
-        FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem));
-        FSA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 160, wsmem));
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-      }
-      const long ctas = std::min<long>(pat.ngrp, static_cast<long>(blocks_per_sm) * kNumSMs);
-      kern<<<dim3(static_cast<unsigned>(ctas), static_cast<unsigned>(tiles)), 160, wsmem, s>>>(a, static_cast<int>(pat.ngrp));
-      const cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess)
-        throw CudaError(std::string("k_spmm_ws launch (nt ") + std::to_string(nt) + ", grid " + std::to_string(ctas) +
-                        " x " + std::to_string(tiles) + ", smem " + std::to_string(wsmem) + ", blocks/SM " +
-                        std::to_string(blocks_per_sm) + "): " + cudaGetErrorString(e));
-    };
-    if (spmm_ws()) {
-      switch (nt) {
-        case 1: go_ws(k_spmm_ws<1>, WsCfg<1>::SMEM); break;
-        case 2: go_ws(k_spmm_ws<2>, WsCfg<2>::SMEM); break;
-        case 3: go_ws(k_spmm_ws<3>, WsCfg<3>::SMEM); break;
-        case 4: go_ws(k_spmm_ws<4>, WsCfg<4>::SMEM); break;
-        case 5: go_ws(k_spmm_ws<5>, WsCfg<5>::SMEM); break;
-        case 6: go_ws(k_spmm_ws<6>, WsCfg<6>::SMEM); break;
-        case 7: go_ws(k_spmm_ws<7>, WsCfg<7>::SMEM); break;
-        case 8: go_ws(k_spmm_ws<8>, WsCfg<8>::SMEM); break;
-        default: go_ws(k_spmm_ws<9>, WsCfg<9>::SMEM); break;
-      }
-      FSA_LAUNCH_CHECK();
-      return;
-    }
     switch (nt) {
       case 1: go(k_spmm_rt<1, kPiece>); break;
       case 2: go(k_spmm_rt<2, kPiece>); break;

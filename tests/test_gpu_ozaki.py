@@ -122,30 +122,22 @@ def test_ozaki_pcg_solution_matches_oracle():
     assert np.abs(got["X"] - want["X"]).max() <= 1e-8 * np.abs(want["X"]).max()
 
 
-def test_int8_spmm_path_matches_default():
-    """Opt-in INT8 tensor-core SpMM (FSA_SPMM=int8) vs the default path, single rank and sharded."""
-    import json
-    import os
-    import subprocess
-    import sys
-
-    code = r"""
-import json, sys
-sys.path.insert(0, %r)
-from tests import test_gpu_sharded as T
-from paper_2405_14492_b200 import fsa
-locs, ind, kw, y, X = T.problem(6000, 80, 0.05, 11, p=2)
-one = T.nll_on(fsa.Context(0), locs, ind, kw, y, X)
-outs = T.run_ranks(fsa.Context.group(0, 3), lambda r, c: T.nll_on(c, locs, ind, kw, y, X))
-print(json.dumps([one["nll"], list(one["grad"]), one["cg_iterations"], outs[0]["nll"], outs[0]["cg_iterations"]]))
-""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+def test_ozaki_pair_72_columns_matches_dmma():
+    """t = 65 -> t_pad = 72 (config 4's block): the two INT8 column tiles of ozaki_*_pair (CTA
+    pairs sharing the U planes through L2) against the all-DMMA solve."""
+    n, m = 12000, 200
+    locs = O.uniform_locations(n, 2, 21)
+    ind = O.select_kmeanspp(locs, m, 22)
+    kw = dict(nu=1.5, taper_family=1, gamma=0.03, sigma2=0.05, sigma1_2=1.0, rho=0.05)
+    y = fsa.simulate_rff(locs, 1.5, 1.0, 0.05, 0.05, 256, 23)
     res = {}
-    for mode in ("dmma", "int8"):
-        env = dict(os.environ, FSA_SPMM=mode)
-        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[mode] = json.loads(out.stdout.strip().splitlines()[-1])
-    a, b = res["int8"], res["dmma"]
-    assert a[2] == b[2] and a[4] == b[4]
-    assert a[0] == pytest.approx(b[0], rel=1e-10) and a[3] == pytest.approx(b[3], rel=1e-10)
-    np.testing.assert_allclose(a[1], b[1], rtol=1e-7, atol=1e-8)
+    for mode in ("ozaki", "dmma"):
+        ctx = fsa.Context(0)
+        ctx.set_gemm_mode(mode)
+        md = fsa.FsaModel.assemble(locs, ind, ctx=ctx, **kw)
+        P = fsa.make_preconditioner(md, "fitc")
+        res[mode] = (fsa.iterative_nll_grad(md, P, y, num_probes=64, seed=4, tol=1e-3), ctx.last_cg()["iterations"])
+    (a, ia), (b, ib) = res["ozaki"], res["dmma"]
+    assert np.array_equal(ia, ib)
+    assert a["nll"] == pytest.approx(b["nll"], rel=1e-10)
+    np.testing.assert_allclose(a["grad"], b["grad"], rtol=1e-8, atol=0)
