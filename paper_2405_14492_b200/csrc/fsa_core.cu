@@ -879,7 +879,10 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
   if (oz || oz_split) md->ensure_ozaki();
   // single rank: the column sums of the SpMM, residual-update and expansion partials run fused
   // with the alpha / residual-test / beta + count control kernels (no separate launches)
-  const bool ctl = fuse_h && oz && md->world() == 1;
+  // fused column-sum / CG-control kernels (k_colsum_ctl). On several row ranks the launchers'
+  // column sums are allreduced first and the control kernels run on those sums (one "partial")
+  const bool ctl = fuse_h && oz;
+  const bool multi = md->world() > 1;
   if (ctl) {
     w.tick.alloc(1);
     w.tick.zero(s);
@@ -1026,7 +1029,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         // CSR + Z (once per row), Lw, H, V read + H, V write
         KTimer t(ctx, "spmm", 12.0 * md->geo->pat.nnz + 48.0 * n * k);
         spmm_block_dot_h(md->geo->pat, md->gval.get(), w.Z.get(), tp, w.V.get(), tp, tp, hv, part, w.Lw.get(),
-                         w.H.get(), st.beta, k, first_sweep, s, !ctl);
+                         w.H.get(), st.beta, k, first_sweep, s, !ctl || multi);
         first_sweep = false;
         comm.allreduce(hv, tp, s);
       } else if (fused) {  // V = Vlr + Sigma_s H with Vlr = U^T U H kept by recurrence; h.v
@@ -1053,14 +1056,14 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
       {
         KTimer t(ctx, "cg_blas1");
         if (ctl)  // alpha, and the ymax clear of the residual update below
-          colsum_ctl(0, part, md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st, w.tick.get(), s,
-                     md->oz.ymax.get(), static_cast<long>(md->oz.ymax.n));
+          colsum_ctl(0, multi ? hv : part, multi ? 1 : md->geo->pat.ngrp, tp, tp, hv, k, it, maxit, 0.0, st,
+                     w.tick.get(), s, md->oz.ymax.get(), static_cast<long>(md->oz.ymax.n));
         else
           cg_alpha(hv, k, it, maxit, st, s);
         if (oz) {
           if (!ctl) FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
           update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
-                            md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl);
+                            md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl || multi);
           ymax_ready = true;
         } else if (jfused) {
           update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
@@ -1070,16 +1073,17 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         }
         comm.allreduce(rr, k, s);
         if (ctl)  // residual test, and the wmax clear of this sweep's core solve
-          colsum_ctl(1, part, xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st, w.tick.get(), s,
-                     w.wmax.get(), kOzCols);
+          colsum_ctl(1, multi ? rr : part, multi ? 1 : xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st,
+                     w.tick.get(), s, w.wmax.get(), kOzCols);
         else
           cg_check(rr, k, opts.tol, it, maxit, st, s);
       }
-      if (!jfused) precond(rz, !ctl);
+      if (!jfused) precond(rz, !ctl || multi);
       {
         KTimer t(ctx, "cg_blas1");
         if (ctl)  // beta and the active count
-          colsum_ctl(2, part, md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st, w.tick.get(), s);
+          colsum_ctl(2, multi ? rz : part, multi ? 1 : md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st,
+                     w.tick.get(), s);
         else
           cg_beta(rz, k, st, s);
         if (fuse_h) {
@@ -1094,7 +1098,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         if (!ctl) cg_count(k, st, s);
       }
   };
-  const bool graph = ctl && !ctx->profile && std::getenv("FSA_NO_GRAPH") == nullptr;
+  const bool graph = ctl && !multi && !ctx->profile && std::getenv("FSA_NO_GRAPH") == nullptr;
   cudaGraphExec_t gexec = nullptr;
   long graph_kernels = 0;
   if (graph) {

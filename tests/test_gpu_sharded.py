@@ -93,6 +93,20 @@ def test_sharded_nll_matches_single_rank(world):
         assert close(o["traces"], one["traces"], 1e-10)
 
 
+def test_sharded_72_column_pair_path_matches_single_rank():
+    """t = 65 -> t_pad = 72 (config 4's block: the paired INT8 passes, ozaki_*_pair) on 2 row
+    ranks against one rank: the pair path under sharding (projection summed over ranks after the
+    paired launch, r.z partials of both column tiles)."""
+    locs, ind, kw, y, X = problem(8000, 150, 0.04, 31, p=0)
+    one = nll_on(fsa.Context(0), locs, ind, kw, y, X, L=64, tol=1e-3)
+    outs = run_ranks(fsa.Context.group(0, 2), lambda r, c: nll_on(c, locs, ind, kw, y, X, L=64, tol=1e-3))
+    for o in outs:
+        assert o["nll"] == outs[0]["nll"]
+        assert o["cg_iterations"] == one["cg_iterations"]
+        assert close(o["nll"], one["nll"], 1e-10)
+        assert close(o["grad"], one["grad"], 1e-8)
+
+
 def test_sharded_nll_matches_oracle_host_inputs():
     locs, ind, kw, y, X = problem(4000, 64, 0.06, 23, p=1)
     ctxs = fsa.Context.group(0, 2)
