@@ -209,17 +209,21 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = tmem_base_s;
   pdl_wait();  // (TMEM allocation and barrier setup overlap the predecessor)
 
-  if (tid == 0) {
+  // warp-specialised issue: lane 0 of warp 1 streams the stages (waiting only for a stage to be
+  // released), lane 0 of warp 0 issues the MMAs (waiting only for a stage to land) -- the loads no
+  // longer queue behind the MMA thread's waits
+  if (tid == 32) {
     const int8_t* Ablk = A + (static_cast<long>(tile) * nkb_all + kb0) * kATile;
     const int8_t* Bblk = B + static_cast<long>(kb0) * btile;
-    auto load = [&](int j) {
+    for (int j = 0; j < nk; ++j) {
       const int st = j % kStages;
+      if (j >= kStages) mbar_wait(&empty[st], ((j / kStages) - 1) & 1);
       mbar_expect_tx(&full[st], kATile + btile);
       bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
       bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * btile, btile, &full[st]);
-    };
-    const int pre = min(nk, kStages);
-    for (int j = 0; j < pre; ++j) load(j);
+    }
+  }
+  if (tid == 0) {
     for (int j = 0; j < nk; ++j) {
       const int st = j % kStages;
       mbar_wait(&full[st], (j / kStages) & 1);
@@ -237,11 +241,6 @@ __global__ void __launch_bounds__(128, 1)
         }
       }
       mma_commit(&empty[st]);
-      if (j >= 1 && j - 1 + kStages < nk) {
-        const int sp = (j - 1) % kStages;
-        mbar_wait(&empty[sp], ((j - 1) / kStages) & 1);
-        load(j - 1 + kStages);
-      }
     }
     mma_commit(&done);
   }
