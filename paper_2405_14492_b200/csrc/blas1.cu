@@ -17,6 +17,7 @@ __global__ void k_pack(const double* __restrict__ in, long ld_in, long n, long k
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n_pad * k) return;
   const long i = idx / k, j = idx % k;
+  FSA_DCHECK(i >= n || (perm[i] >= 0 && perm[i] < ld_in), "pack: permutation index out of range");
   out[i * tp + col0 + j] = i < n ? in[static_cast<long>(perm[i]) + j * ld_in] : 0.0;
 }
 
@@ -82,6 +83,7 @@ __global__ void k_unpack(const double* __restrict__ in, long n, long k, const in
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n * k) return;
   const long i = idx / k, j = idx % k;
+  FSA_DCHECK(perm[i] >= 0 && perm[i] < n, "unpack: permutation index out of range");
   out[static_cast<long>(perm[i]) + j * n] = in[i * tp + col0 + j];
 }
 

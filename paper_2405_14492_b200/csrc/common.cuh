@@ -37,11 +37,20 @@ inline std::atomic<long>& launch_counter() {
   return c;
 }
 
+#ifdef FSA_CHECKED
+#define FSA_LAUNCH_CHECK()                        \
+  do {                                            \
+    ::fsa::launch_counter().fetch_add(1);         \
+    FSA_CUDA(cudaGetLastError());                 \
+    FSA_CUDA(cudaDeviceSynchronize());            \
+  } while (0)
+#else
 #define FSA_LAUNCH_CHECK()                        \
   do {                                            \
     ::fsa::launch_counter().fetch_add(1);         \
     FSA_CUDA(cudaGetLastError());                 \
   } while (0)
+#endif
 
 // NVTX phase range (assemble / FITC setup / PCG / SLQ / traces / prediction): visible in nsys /
 // ncu --nvtx; no-ops without a tool attached (NVTX v3 is header-only)
@@ -51,6 +60,27 @@ struct NvtxRange {
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
+
+// ---- checked build (make checked -> build/checked/libfsa_b200.so, FSA_LIB selects it) ----------
+// Bounds checks on the gather / scatter indices of the sweep kernels, and a stream synchronisation
+// after every launch so a fault is reported at the kernel that caused it (graph capture is then
+// off). The pool's compute-sanitizer is closed; this is the substitute.
+#ifdef FSA_CHECKED
+#define FSA_DCHECK(cond, what)                                                                     \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("FSA_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,      \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                        \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+constexpr bool kChecked = true;
+#else
+#define FSA_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+constexpr bool kChecked = false;
+#endif
 
 // ---- programmatic dependent launch (PDL) -------------------------------------------------
 // The PCG sweep kernels are launched with programmatic stream serialisation: a kernel's CTAs

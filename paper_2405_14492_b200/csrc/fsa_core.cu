@@ -1098,7 +1098,7 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
         if (!ctl) cg_count(k, st, s);
       }
   };
-  const bool graph = ctl && !multi && !ctx->profile && std::getenv("FSA_NO_GRAPH") == nullptr;
+  const bool graph = ctl && !multi && !ctx->profile && !kChecked && std::getenv("FSA_NO_GRAPH") == nullptr;
   cudaGraphExec_t gexec = nullptr;
   long graph_kernels = 0;
   if (graph) {

@@ -676,6 +676,7 @@ __global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long m
   if (idx >= mp * tp) return;
   const long r = idx / tp, c = idx % tp;
   double sacc = 0.0;
+#pragma unroll 8  // (loads of eight chunks in flight; the additions keep the fixed chunk order)
   for (int q = 0; q < nchunks; ++q) sacc += part[(static_cast<long>(q) * mp + r) * kOzCols + c];
   S[r * ld + c] = sacc;
 }

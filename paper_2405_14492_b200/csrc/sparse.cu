@@ -288,6 +288,8 @@ struct TileSpmmArgs {
   const double* beta = nullptr;
   long kb = 0;
   int first = 0;
+  long xrows = 0;    // rows of X that may be gathered (own + halo); checked builds only
+  long ntiles = 0;   // stored value tiles; checked builds only
   int dbg = 0;  // diagnostics only (fsa_debug_kernel_bench): 1 no DMMA, 2 no epilogue, 4 no RHS gather, 8 no A tiles,
                 // 16 no L2 prefetch of the epilogue rows
 };
@@ -335,10 +337,12 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
 #pragma unroll
       for (int i = 0; i < RW; ++i) {
         const int u = warp + WN * i;
+        FSA_DCHECK(u >= nr || (gc[i] >= 0 && gc[i] < q.xrows), "spmm: gathered RHS row out of range");
         if (u < nr && !(q.dbg & 4)) cp_async16(hs + u * LDH + ch * 2, X + static_cast<long>(gc[i]) * q.ldx + ch * 2);
       }
     }
     const int nt = __popc(pm.y & static_cast<int>((1ull << nr) - 1ull));
+    FSA_DCHECK(pm.x >= 0 && pm.x + nt <= q.ntiles, "spmm: value tile range out of bounds");
     const double* src = q.tval + 32L * pm.x;
     if (!(q.dbg & 8))
       for (int idx = tid; idx < nt * 16; idx += NTH) cp_async16(as + idx * 2, src + idx * 2);
@@ -504,6 +508,7 @@ __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ 
     }
     for (int idx = tid; idx < nc * (kGK / 2); idx += 256) {
       const int j = idx / (kGK / 2), ch = idx % (kGK / 2);
+      FSA_DCHECK(gcol[u0 + j0 + j] >= 0, "block gram: negative union column");
       cp_async16(bs + j * kGLd + ch * 2, B + static_cast<long>(gcol[u0 + j0 + j]) * ldu + kk + ch * 2);
     }
     cp_async_commit();
@@ -706,7 +711,8 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
     TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
                    X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
                    partial + c_first, ncols, H != nullptr ? H + c_first : nullptr,
-                   beta != nullptr ? beta + c_first : nullptr, kb - c_first, first ? 1 : 0, g_spmm_dbg};
+                   beta != nullptr ? beta + c_first : nullptr, kb - c_first, first ? 1 : 0,
+                   pat.cols > 0 ? pat.cols : pat.rows, pat.ntiles, g_spmm_dbg};
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsa_b200.so")
+# FSA_LIB selects another build of the same library (the bounds-checked one: make -C csrc checked)
+LIB_PATH = os.environ.get("FSA_LIB") or os.path.join(_HERE, "libfsa_b200.so")
 _lib = None
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="F_CONTIGUOUS")
