@@ -268,6 +268,16 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 // CSR kernel every RHS row is fetched once per group instead of once per nonzero and the
 // arithmetic runs on the tensor pipe.
 constexpr int kPiece = 16;  // union rows per pipeline stage (4 DMMA k-steps; 8 and 32 measured slower)
+// resident CTAs per SM that the ring's shared memory allows (the __launch_bounds__ minimum)
+constexpr int spmm_minb(int nt, int ns) {
+  const int b = (227 * 1024) / (ns * kPiece * (nt * 8 + 4 + kGroup) * 8 + 3 * 1024);
+  return b > 8 ? 8 : (b < 1 ? 1 : b);
+}
+// ... and the register budget of the batched epilogue (two column tiles of loads in flight)
+constexpr int spmm_minb(int nt, int ns, int jb) {
+  const int b = spmm_minb(nt, ns);
+  return jb == 2 && nt >= 6 && b > 7 ? 7 : b;
+}
 struct TileSpmmArgs {
   const long* gptr;
   const int* gcol;
@@ -292,6 +302,8 @@ struct TileSpmmArgs {
   long ntiles = 0;   // stored value tiles; checked builds only
   int dbg = 0;  // diagnostics only (fsa_debug_kernel_bench): 1 no DMMA, 2 no epilogue, 4 no RHS gather, 8 no A tiles,
                 // 16 no L2 prefetch of the epilogue rows
+  int gcap = 0;  // k_spmm_v3: union slots reserved in shared memory (gmax rounded up to whole pieces)
+  int epf = 0;   // k_spmm_v3: L2 prefetch of the group's epilogue rows this many pieces before the end (0 off)
 };
 // k_spmm_rt: warp w owns row tile w (8 rows) of the group and all NT n-tiles, so a k-step
 // costs one warp-uniform test of its mask bit, one A fragment and NT B fragments for NT
@@ -446,6 +458,194 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
   __syncthreads();
   if (tid < NT * 8 && tid < ncols)
     q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
+}
+
+// the h.v epilogue of the block SpMM kernels (Y = Y0 + S X, H / V direction update, column partials)
+template <int NT, int JB>
+__device__ __forceinline__ void spmm_epilogue(const TileSpmmArgs& q, const double (&c)[NT][2], long g, long c0,
+                                              double (&red)[4][NT * 8]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* X = q.X + c0;
+  double* Y = q.Y + c0;
+  const double* Y0 = q.Y0 != nullptr ? q.Y0 + c0 : nullptr;
+  const long ncols = q.ncols - c0;
+  const long row = g * kGroup + warp * 8 + (lane >> 2);
+  const bool rok = row < q.nrows;
+  const bool upd = q.Hio != nullptr, first = q.first != 0;
+#pragma unroll
+  for (int j0 = 0; j0 < NT; j0 += JB) {
+    // the loads of JB column tiles are issued before any of their stores (the stores may alias
+    // them as far as the compiler knows): JB DRAM round trips fewer per warp
+    double2 y0[JB], xz[JB], ho[JB], vo[JB];
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      const int j = j0 + jj;
+      const long cc = j * 8 + 2 * (lane & 3);
+      y0[jj] = xz[jj] = ho[jj] = vo[jj] = make_double2(0.0, 0.0);
+      if (j < NT && !(q.dbg & 2) && rok && cc < ncols) {
+        if (Y0 != nullptr) y0[jj] = __ldg(reinterpret_cast<const double2*>(Y0 + row * q.ldy + cc));
+        xz[jj] = __ldg(reinterpret_cast<const double2*>(X + row * q.ldx + cc));
+        if (upd && !first) {
+          ho[jj] = *reinterpret_cast<const double2*>(q.Hio + c0 + row * q.ldy + cc);
+          vo[jj] = *reinterpret_cast<const double2*>(Y + row * q.ldy + cc);
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      const int j = j0 + jj;
+      if (j >= NT) break;
+      const long cc = j * 8 + 2 * (lane & 3);
+      double d0 = 0.0, d1 = 0.0;
+      if (q.dbg & 2) {
+        d0 = c[j][0];
+        d1 = c[j][1];
+      } else if (rok && cc < ncols) {
+        double2 o = make_double2(c[j][0] + y0[jj].x, c[j][1] + y0[jj].y);
+        double2 h = xz[jj];
+        if (upd) {  // H = Z + beta H (krylov.cpp:92), V = (Lw + S Z) + beta V
+          if (!first) {
+            const long gc = c0 + cc;
+            const double b0 = gc < q.kb ? q.beta[gc] : 0.0, b1 = gc + 1 < q.kb ? q.beta[gc + 1] : 0.0;
+            h.x = h.x + b0 * ho[jj].x;
+            h.y = h.y + b1 * ho[jj].y;
+            o.x += b0 * vo[jj].x;
+            o.y += b1 * vo[jj].y;
+          }
+          *reinterpret_cast<double2*>(q.Hio + c0 + row * q.ldy + cc) = h;
+        }
+        *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
+        d0 = h.x * o.x;
+        d1 = h.y * o.y;
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+      }
+      if (lane < 4) {
+        red[warp][cc] = d0;
+        red[warp][cc + 1] = d1;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < NT * 8 && tid < ncols)
+    q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
+}
+
+// k_spmm_v3: the lean main loop. Everything a piece needs besides its data is precomputed once per
+// CTA into shared memory: the gathered rows' element offsets (padded to whole pieces with a valid
+// row), each warp's k-step word per piece (bit ks: this row tile has a stored tile in k-step ks; bits
+// 4 + 5 ks: its index among the piece's stored tiles) and the piece's {first tile, tile count}.
+// Warp w gathers piece rows 4w .. 4w + 3 (one 16-byte vector load of their offsets), so a piece
+// costs a warp ~4 copy instructions per row instead of ~25 of 64-bit address arithmetic, and a
+// k-step is one bit test plus the fragment loads and DMMAs.
+template <int NT, int NS, int MINB, int JB>
+__global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
+  constexpr int P = kPiece, WN = 4, NTH = 32 * WN;
+  static_assert(kGroup == 32 && P == 16 && NS >= 2, "four row tiles per group, four k-steps per piece");
+  constexpr int LDH = NT * 8 + 4;  // == 4 or 12 (mod 16): conflict-free B fragments
+  constexpr int CH = NT * 4;       // 16-byte chunks per gathered row
+  constexpr int HS = P * LDH, AS = P * kGroup;
+  extern __shared__ __align__(16) double sm[];  // [NS][HS], [NS][AS], offsets, warp words, piece info
+  __shared__ double red[WN][NT * 8];
+  const long g = blockIdx.x;
+  const long c0 = 64L * blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long u0 = q.gptr[g];
+  const int up = static_cast<int>(q.gptr[g + 1] - u0);
+  const int npc = (up + P - 1) / P;
+  const long kb0 = u0 / 4;
+  uint32_t* soff = reinterpret_cast<uint32_t*>(sm + NS * (HS + AS));
+  int* sw = reinterpret_cast<int*>(soff + q.gcap);
+  int2* spi = reinterpret_cast<int2*>(sw + 4 * (q.gcap / P));
+  // (static metadata: staged before the dependency wait)
+  for (int i = tid; i < npc * P; i += NTH) {
+    const int col = q.gcol[u0 + (i < up ? i : 0)];
+    FSA_DCHECK(col >= 0 && col < q.xrows, "spmm: gathered RHS row out of range");
+    soff[i] = static_cast<uint32_t>(col) * static_cast<uint32_t>(q.ldx);
+  }
+  for (int i = tid; i < npc * WN; i += NTH) {
+    const int pc = i >> 2, w = i & 3;
+    const int2 pm = q.pmeta[kb0 + pc * (P / 4)];
+    const int nks = min(P, up - pc * P) / 4;
+    int t = 0, word = 0;
+#pragma unroll
+    for (int ks = 0; ks < P / 4; ++ks) {
+      if (ks < nks) {
+        const int m = (pm.y >> (4 * ks)) & 15;
+        if ((m >> w) & 1) word |= (1 << ks) | ((t + __popc(m & ((1 << w) - 1))) << (4 + 5 * ks));
+        t += __popc(m);
+      }
+    }
+    sw[i] = word;
+    if (w == 0) {
+      FSA_DCHECK(pm.x >= 0 && pm.x + t <= q.ntiles, "spmm: value tile range out of bounds");
+      spi[pc] = make_int2(pm.x, t);
+    }
+  }
+  __syncthreads();
+  const double* Xl = q.X + c0 + 2 * lane;  // this lane's 16-byte chunk of every gathered row
+  auto issue = [&](int pc) {
+    if (pc < npc) {
+      const int slot = pc % NS;
+      const uint4 o = *reinterpret_cast<const uint4*>(soff + pc * P + 4 * warp);
+      double* hd = sm + slot * HS + 4 * warp * LDH + 2 * lane;
+#pragma unroll
+      for (int k = 0; k < (CH + 31) / 32; ++k) {
+        if (lane + 32 * k < CH) {
+          cp_async16(hd + 64 * k, Xl + 64 * k + o.x);
+          cp_async16(hd + 64 * k + LDH, Xl + 64 * k + o.y);
+          cp_async16(hd + 64 * k + 2 * LDH, Xl + 64 * k + o.z);
+          cp_async16(hd + 64 * k + 3 * LDH, Xl + 64 * k + o.w);
+        }
+      }
+      const int2 pi = spi[pc];
+      const double* src = q.tval + 32L * pi.x + 2 * tid;
+      double* ad = sm + NS * HS + slot * AS + 2 * tid;
+      if (tid < pi.y * 16) cp_async16(ad, src);
+      if (tid + NTH < pi.y * 16) cp_async16(ad + 2 * NTH, src + 2 * NTH);
+    }
+    cp_async_commit();  // (empty groups keep the wait count uniform)
+  };
+  double c[NT][2];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
+  pdl_wait();
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) issue(s);
+  for (int pc = 0; pc < npc; ++pc) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();  // piece pc visible to all; every warp is done with piece pc - 1, whose slot is refilled next
+    issue(pc + NS - 1);
+    if (pc == npc - q.epf && tid == 0) {  // the epilogue rows into L2 shortly before they are read
+      const uint32_t rb = static_cast<uint32_t>(kGroup * q.ldy * 8);
+      if (q.Y0 != nullptr) prefetch_l2(q.Y0 + g * kGroup * q.ldy, rb);
+      prefetch_l2(q.X + g * kGroup * q.ldx, static_cast<uint32_t>(kGroup * q.ldx * 8));
+      if (q.Hio != nullptr && !q.first) {
+        prefetch_l2(q.Hio + g * kGroup * q.ldy, rb);
+        prefetch_l2(q.Y + g * kGroup * q.ldy, rb);
+      }
+    }
+    const int slot = pc % NS;
+    const int word = sw[pc * WN + warp];
+    const double* hs = sm + slot * HS + (lane & 3) * LDH + (lane >> 2);
+    const double* as = sm + NS * HS + slot * AS + lane;
+#pragma unroll
+    for (int ks = 0; ks < P / 4; ++ks) {
+      if (word & (1 << ks)) {
+        const double a = as[((word >> (4 + 5 * ks)) & 31) * 32];
+        const double* hb = hs + ks * 4 * LDH;
+        double b[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = hb[j * 8];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma8x8x4(c[j][0], c[j][1], a, b[j]);
+      }
+    }
+  }
+  spmm_epilogue<NT, JB>(q, c, g, c0, red);
 }
 // ---- block SDDMM: dense Gram blocks of the row groups on DMMA ----------------------------------
 // G = A_R^T B_C for a group's 32 rows R and a 64-column tile C of its union, over K (the
@@ -695,6 +895,21 @@ long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
 bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
 
+template <int NS, int JB, class Go>
+void spmm_v3_dispatch(int nt, Go&& go) {
+  switch (nt) {
+    case 1: go(k_spmm_v3<1, NS, spmm_minb(1, NS, JB), JB>); break;
+    case 2: go(k_spmm_v3<2, NS, spmm_minb(2, NS, JB), JB>); break;
+    case 3: go(k_spmm_v3<3, NS, spmm_minb(3, NS, JB), JB>); break;
+    case 4: go(k_spmm_v3<4, NS, spmm_minb(4, NS, JB), JB>); break;
+    case 5: go(k_spmm_v3<5, NS, spmm_minb(5, NS, JB), JB>); break;
+    case 6: go(k_spmm_v3<6, NS, spmm_minb(6, NS, JB), JB>); break;
+    case 7: go(k_spmm_v3<7, NS, spmm_minb(7, NS, JB), JB>); break;
+    case 8: go(k_spmm_v3<8, NS, spmm_minb(8, NS, JB), JB>); break;
+    default: go(k_spmm_v3<9, NS, spmm_minb(9, NS, JB), JB>); break;
+  }
+}
+
 // Y = S X (+ Y0) over ncols (multiple of 8) columns in 64-column tiles; dot[c] = sum_r X[r][c] Y[r][c]
 void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
                     double* dot, double* partial, const double* Y0, cudaStream_t s) {
@@ -705,19 +920,52 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
                       bool first, cudaStream_t s, bool colsum) {
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
+  static const int variant = [] {  // A/B switch: FSA_SPMM=rt (round-1 kernel), FSA_SPMM_NS=2|3 (ring depth)
+    const char* e = std::getenv("FSA_SPMM");
+    if (e != nullptr && std::strcmp(e, "rt") == 0) return 0;
+    const char* d = std::getenv("FSA_SPMM_NS");
+    const int ns = d != nullptr ? std::atoi(d) : 2;
+    return ns == 3 ? 3 : 2;
+  }();
+  static const int epf = [] {  // FSA_SPMM_EPF=k: L2 prefetch of the epilogue rows k pieces before the end
+    const char* e = std::getenv("FSA_SPMM_EPF");
+    return e != nullptr ? std::atoi(e) : 4;
+  }();
+  static const int jb = [] {  // FSA_SPMM_EPB=1|2: column tiles per batch of epilogue loads
+    const char* e = std::getenv("FSA_SPMM_EPB");
+    return e != nullptr && e[0] == '2' ? 2 : 1;
+  }();
   auto launch = [&](int nt, long c_first, long tiles) {
     const long ldh = nt * 8 + 4;  // k_spmm_rt's LDH
-    const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8);
+    const bool lean = variant != 0;
+    const int gcap = static_cast<int>(round_up(pat.gmax, kPiece));
+    const int ns = variant == 0 ? 2 : variant;
+    const int smem = static_cast<int>(ns * (kPiece * ldh + kPiece * kGroup) * 8) +
+                     (lean ? gcap * 4 + (gcap / kPiece) * (16 + 8) : 0);
+    require(!lean || (pat.cols > 0 ? pat.cols : pat.rows) * ldx < (1L << 32), "spmm: RHS block too large for 32-bit offsets");
     TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
                    X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
                    partial + c_first, ncols, H != nullptr ? H + c_first : nullptr,
                    beta != nullptr ? beta + c_first : nullptr, kb - c_first, first ? 1 : 0,
-                   pat.cols > 0 ? pat.cols : pat.rows, pat.ntiles, g_spmm_dbg};
+                   pat.cols > 0 ? pat.cols : pat.rows, pat.ntiles, g_spmm_dbg, gcap, epf};
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
-      FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      // one fixed opt-in ceiling (not this launch's size: the launch size depends on the pattern's
+      // largest union, and thread-group ranks sharing a device would race on a per-launch value)
+      constexpr int kSmemCeiling = 160 * 1024;
+      require(smem <= kSmemCeiling, "spmm: union too large for shared memory");
+      FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCeiling));
       launch_pdl(kern, grid, dim3(128), static_cast<size_t>(smem), s, a);
     };
+    if (lean) {
+      if (ns == 2) {
+        jb == 1 ? spmm_v3_dispatch<2, 1>(nt, go) : spmm_v3_dispatch<2, 2>(nt, go);
+      } else {
+        jb == 1 ? spmm_v3_dispatch<3, 1>(nt, go) : spmm_v3_dispatch<3, 2>(nt, go);
+      }
+      FSA_LAUNCH_CHECK();
+      return;
+    }
     switch (nt) {
       case 1: go(k_spmm_rt<1, kPiece>); break;
       case 2: go(k_spmm_rt<2, kPiece>); break;
