@@ -310,15 +310,38 @@ __global__ void __launch_bounds__(512) k_group_union(const long* __restrict__ ro
     __syncthreads();
     for (int i = tid; i < U; i += blockDim.x) okey[i] = (kMaskRank[umask[i] & 15] << 12) | i;
     __syncthreads();
+    int* pos1 = keys + 3072;  // [U] position of old slot i in the mask order
     for (int i = tid; i < U; i += blockDim.x) {  // rank of key i (keys are distinct)
       const int ki = okey[i];
       int pos = 0;
       for (int j = 0; j < U; ++j) pos += okey[j] < ki ? 1 : 0;
-      flag[i] = pos;  // new position of old slot i (umask no longer needed)
+      pos1[i] = pos;
     }
     __syncthreads();
-    for (int i = tid; i < U; i += blockDim.x) out[flag[i]] = oldc[i];
-    for (long p = p0 + tid; p < p1; p += blockDim.x) lidx[p] = flag[lidx[p]];
+    // tile_order 2: the k-steps (4 consecutive slots; their composition, hence the stored tiles,
+    // unchanged) are dealt round-robin into the 16-row pieces of the block SpMM, so each piece
+    // mixes k-steps from the whole mask chain and the four row tiles' warps get similar work
+    // between two barriers (in mask order a piece often belongs to one row tile). A partial last
+    // k-step (U % 4 != 0, padded after it) keeps its place.
+    int* fin = flag + 2048;  // [U] final position of old slot i
+    const int K4 = U >> 2, npc = (K4 + 3) >> 2;
+    int* newk = flag + 1024;  // [K4]
+    if (tile_order == 2) {
+      for (int k = tid; k < K4; k += blockDim.x) {
+        const int kk = ((k % npc) << 12) | (k / npc);
+        int pos = 0;
+        for (int j = 0; j < K4; ++j) pos += (((j % npc) << 12) | (j / npc)) < kk ? 1 : 0;
+        newk[k] = pos;
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < U; i += blockDim.x) {
+      const int p = pos1[i], k = p >> 2;
+      fin[i] = tile_order == 2 && k < K4 ? (newk[k] << 2) | (p & 3) : p;
+    }
+    __syncthreads();
+    for (int i = tid; i < U; i += blockDim.x) out[fin[i]] = oldc[i];
+    for (long p = p0 + tid; p < p1; p += blockDim.x) lidx[p] = fin[lidx[p]];
   }
   if (tid == 0) ucount[b] = U;
 }
@@ -372,7 +395,7 @@ __global__ void k_group_ok(const int* __restrict__ ucount, long ngrp, int pad, i
 }
 // unions of G consecutive rows, padded to `pad`; false if a group exceeds the capacities
 bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& ngrp, long& gnnz, int& gmax,
-                  DBuf<long>& gptr, DBuf<int>& gcol, DBuf<int>& lidx, cudaStream_t s, bool tile_order = false) {
+                  DBuf<long>& gptr, DBuf<int>& gcol, DBuf<int>& lidx, cudaStream_t s, int tile_order = 0) {
   gnnz = 0;
   ngrp = cdiv(pat.rows, G);
   if (ngrp == 0 || pat.nnz == 0) return false;
@@ -389,12 +412,12 @@ bool build_unions(const Csr& pat, int G, int pad, int sort_cap, int cap, long& n
     FSA_CUDA(cudaFuncSetAttribute(k_group_union<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_group_union<true><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
         pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits,
-        tile_order ? 1 : 0);
+        tile_order);
   } else {
     FSA_CUDA(cudaFuncSetAttribute(k_group_union<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_group_union<false><<<static_cast<unsigned>(ngrp), 512, smem, s>>>(
         pat.rowptr.get(), pat.col.get(), pat.rows, G, sort_cap, cap, ucols.get(), ucount.get(), lidx.get(), key_bits,
-        tile_order ? 1 : 0);
+        tile_order);
   }
   FSA_LAUNCH_CHECK();
   bad.zero(s);
@@ -540,9 +563,16 @@ void sort_points(const double* coords_host, long n, int d, const CellGrid& g, lo
 }
 
 void build_groups(Csr& pat, cudaStream_t s) {
-  static const bool plain_order = std::getenv("FSA_UNION_ORDER") && std::strcmp(std::getenv("FSA_UNION_ORDER"), "plain") == 0;
+  // FSA_UNION_ORDER=plain (ascending columns) | mask (row-tile-mask order) | default: mask order with
+  // the k-steps interleaved across pieces
+  static const int order = [] {
+    const char* e = std::getenv("FSA_UNION_ORDER");
+    if (e != nullptr && std::strcmp(e, "plain") == 0) return 0;
+    if (e != nullptr && std::strcmp(e, "mask") == 0) return 1;
+    return 2;
+  }();
   if (!build_unions(pat, kGroup, 4, kUnionSort, kUnionCap, pat.ngrp, pat.gnnz, pat.gmax, pat.gptr, pat.gcol, pat.gslot,
-                    s, !plain_order)) {
+                    s, order)) {
     pat.gnnz = 0;
     return;
   }

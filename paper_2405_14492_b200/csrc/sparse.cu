@@ -269,14 +269,9 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 // arithmetic runs on the tensor pipe.
 constexpr int kPiece = 16;  // union rows per pipeline stage (4 DMMA k-steps; 8 and 32 measured slower)
 // resident CTAs per SM that the ring's shared memory allows (the __launch_bounds__ minimum)
-constexpr int spmm_minb(int nt, int ns) {
-  const int b = (227 * 1024) / (ns * kPiece * (nt * 8 + 4 + kGroup) * 8 + 3 * 1024);
+constexpr int spmm_minb(int nt, int ns, int p = kPiece) {
+  const int b = (227 * 1024) / (ns * p * (nt * 8 + 4 + kGroup) * 8 + 3 * 1024);
   return b > 8 ? 8 : (b < 1 ? 1 : b);
-}
-// ... and the register budget of the batched epilogue (two column tiles of loads in flight)
-constexpr int spmm_minb(int nt, int ns, int jb) {
-  const int b = spmm_minb(nt, ns);
-  return jb == 2 && nt >= 6 && b > 7 ? 7 : b;
 }
 struct TileSpmmArgs {
   const long* gptr;
@@ -460,78 +455,72 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
     q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
 }
 
-// the h.v epilogue of the block SpMM kernels (Y = Y0 + S X, H / V direction update, column partials)
-template <int NT, int JB>
-__device__ __forceinline__ void spmm_epilogue(const TileSpmmArgs& q, const double (&c)[NT][2], long g, long c0,
-                                              double (&red)[4][NT * 8]) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* X = q.X + c0;
-  double* Y = q.Y + c0;
-  const double* Y0 = q.Y0 != nullptr ? q.Y0 + c0 : nullptr;
-  const long ncols = q.ncols - c0;
-  const long row = g * kGroup + warp * 8 + (lane >> 2);
-  const bool rok = row < q.nrows;
-  const bool upd = q.Hio != nullptr, first = q.first != 0;
+// the h.v epilogue of the block SpMM: Y = Y0 + S X on this lane's fragments, with the PCG
+// direction update when H is given (REC: H = Z + beta H, V = (Lw + S Z) + beta V, krylov.cpp:92;
+// else H = Z), and the h.v column partials of the group's 32 rows (fixed order: lane butterfly,
+// then the four row tiles in order). The column tile is full (NT * 8 columns, ldx == ldy) and the
+// pointers do not alias, so the loads of later column tiles can move above earlier stores.
+template <int NT, bool REC, bool UPD, bool HASY0>
+__device__ __forceinline__ void spmm_epilogue_cols(const TileSpmmArgs& q, const double (&c)[NT][2], long off, bool rok,
+                                                   const double* sbeta, double (&red)[4][NT * 8]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cl = 2 * (lane & 3);
+  const double* __restrict__ zr = q.X + off;
+  const double* __restrict__ lr = q.Y0 + off;
+  double* __restrict__ vr = q.Y + off;
+  double* __restrict__ hr = q.Hio + off;
 #pragma unroll
-  for (int j0 = 0; j0 < NT; j0 += JB) {
-    // the loads of JB column tiles are issued before any of their stores (the stores may alias
-    // them as far as the compiler knows): JB DRAM round trips fewer per warp
-    double2 y0[JB], xz[JB], ho[JB], vo[JB];
-#pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int j = j0 + jj;
-      const long cc = j * 8 + 2 * (lane & 3);
-      y0[jj] = xz[jj] = ho[jj] = vo[jj] = make_double2(0.0, 0.0);
-      if (j < NT && !(q.dbg & 2) && rok && cc < ncols) {
-        if (Y0 != nullptr) y0[jj] = __ldg(reinterpret_cast<const double2*>(Y0 + row * q.ldy + cc));
-        xz[jj] = __ldg(reinterpret_cast<const double2*>(X + row * q.ldx + cc));
-        if (upd && !first) {
-          ho[jj] = *reinterpret_cast<const double2*>(q.Hio + c0 + row * q.ldy + cc);
-          vo[jj] = *reinterpret_cast<const double2*>(Y + row * q.ldy + cc);
-        }
+  for (int j = 0; j < NT; ++j) {
+    double d0 = 0.0, d1 = 0.0;
+    if (rok) {
+      double2 o = make_double2(c[j][0], c[j][1]);
+      if (HASY0) {
+        const double2 y0 = __ldg(reinterpret_cast<const double2*>(lr + 8 * j));
+        o.x += y0.x;
+        o.y += y0.y;
       }
+      double2 h = __ldg(reinterpret_cast<const double2*>(zr + 8 * j));
+      if (REC) {
+        const double2 b = *reinterpret_cast<const double2*>(sbeta + 8 * j + cl);
+        const double2 ho = *reinterpret_cast<const double2*>(hr + 8 * j);
+        const double2 vo = *reinterpret_cast<const double2*>(vr + 8 * j);
+        h.x = h.x + b.x * ho.x;
+        h.y = h.y + b.y * ho.y;
+        o.x += b.x * vo.x;
+        o.y += b.y * vo.y;
+      }
+      if (UPD) *reinterpret_cast<double2*>(hr + 8 * j) = h;
+      *reinterpret_cast<double2*>(vr + 8 * j) = o;
+      d0 = h.x * o.x;
+      d1 = h.y * o.y;
     }
 #pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int j = j0 + jj;
-      if (j >= NT) break;
-      const long cc = j * 8 + 2 * (lane & 3);
-      double d0 = 0.0, d1 = 0.0;
-      if (q.dbg & 2) {
-        d0 = c[j][0];
-        d1 = c[j][1];
-      } else if (rok && cc < ncols) {
-        double2 o = make_double2(c[j][0] + y0[jj].x, c[j][1] + y0[jj].y);
-        double2 h = xz[jj];
-        if (upd) {  // H = Z + beta H (krylov.cpp:92), V = (Lw + S Z) + beta V
-          if (!first) {
-            const long gc = c0 + cc;
-            const double b0 = gc < q.kb ? q.beta[gc] : 0.0, b1 = gc + 1 < q.kb ? q.beta[gc + 1] : 0.0;
-            h.x = h.x + b0 * ho[jj].x;
-            h.y = h.y + b1 * ho[jj].y;
-            o.x += b0 * vo[jj].x;
-            o.y += b1 * vo[jj].y;
-          }
-          *reinterpret_cast<double2*>(q.Hio + c0 + row * q.ldy + cc) = h;
-        }
-        *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
-        d0 = h.x * o.x;
-        d1 = h.y * o.y;
-      }
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      }
-      if (lane < 4) {
-        red[warp][cc] = d0;
-        red[warp][cc + 1] = d1;
-      }
+    for (int o = 4; o < 32; o <<= 1) {
+      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+    }
+    if (lane < 4) {
+      red[warp][j * 8 + cl] = d0;
+      red[warp][j * 8 + cl + 1] = d1;
     }
   }
+}
+template <int NT>
+__device__ __forceinline__ void spmm_epilogue(const TileSpmmArgs& q, const double (&c)[NT][2], long g, long c0,
+                                              double (&red)[4][NT * 8], const double* sbeta) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long row = g * kGroup + warp * 8 + (lane >> 2);
+  const bool rok = row < q.nrows;
+  const long off = row * q.ldx + c0 + 2 * (lane & 3);  // (ldx == ldy)
+  if (q.Hio != nullptr) {
+    if (q.first) spmm_epilogue_cols<NT, false, true, true>(q, c, off, rok, sbeta, red);
+    else spmm_epilogue_cols<NT, true, true, true>(q, c, off, rok, sbeta, red);
+  } else if (q.Y0 != nullptr) {
+    spmm_epilogue_cols<NT, false, false, true>(q, c, off, rok, sbeta, red);
+  } else {
+    spmm_epilogue_cols<NT, false, false, false>(q, c, off, rok, sbeta, red);
+  }
   __syncthreads();
-  if (tid < NT * 8 && tid < ncols)
-    q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
+  if (tid < NT * 8) q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
 }
 
 // k_spmm_v3: the lean main loop. Everything a piece needs besides its data is precomputed once per
@@ -541,15 +530,16 @@ __device__ __forceinline__ void spmm_epilogue(const TileSpmmArgs& q, const doubl
 // Warp w gathers piece rows 4w .. 4w + 3 (one 16-byte vector load of their offsets), so a piece
 // costs a warp ~4 copy instructions per row instead of ~25 of 64-bit address arithmetic, and a
 // k-step is one bit test plus the fragment loads and DMMAs.
-template <int NT, int NS, int MINB, int JB>
+template <int NT, int P, int NS, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
-  constexpr int P = kPiece, WN = 4, NTH = 32 * WN;
-  static_assert(kGroup == 32 && P == 16 && NS >= 2, "four row tiles per group, four k-steps per piece");
+  constexpr int WN = 4, NTH = 32 * WN, RW = P / WN;
+  static_assert(kGroup == 32 && (P == 16 || P == 8) && NS >= 2, "four row tiles per group, <= four k-steps per piece");
   constexpr int LDH = NT * 8 + 4;  // == 4 or 12 (mod 16): conflict-free B fragments
   constexpr int CH = NT * 4;       // 16-byte chunks per gathered row
   constexpr int HS = P * LDH, AS = P * kGroup;
   extern __shared__ __align__(16) double sm[];  // [NS][HS], [NS][AS], offsets, warp words, piece info
   __shared__ double red[WN][NT * 8];
+  __shared__ __align__(16) double sbeta[NT * 8];
   const long g = blockIdx.x;
   const long c0 = 64L * blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -590,22 +580,27 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
   auto issue = [&](int pc) {
     if (pc < npc) {
       const int slot = pc % NS;
-      const uint4 o = *reinterpret_cast<const uint4*>(soff + pc * P + 4 * warp);
-      double* hd = sm + slot * HS + 4 * warp * LDH + 2 * lane;
+      uint32_t o[RW];
+      if constexpr (RW == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(soff + pc * P + RW * warp);
+        o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(soff + pc * P + RW * warp);
+        o[0] = v.x, o[1] = v.y;
+      }
+      double* hd = sm + slot * HS + RW * warp * LDH + 2 * lane;
 #pragma unroll
       for (int k = 0; k < (CH + 31) / 32; ++k) {
         if (lane + 32 * k < CH) {
-          cp_async16(hd + 64 * k, Xl + 64 * k + o.x);
-          cp_async16(hd + 64 * k + LDH, Xl + 64 * k + o.y);
-          cp_async16(hd + 64 * k + 2 * LDH, Xl + 64 * k + o.z);
-          cp_async16(hd + 64 * k + 3 * LDH, Xl + 64 * k + o.w);
+#pragma unroll
+          for (int i = 0; i < RW; ++i) cp_async16(hd + 64 * k + i * LDH, Xl + 64 * k + o[i]);
         }
       }
       const int2 pi = spi[pc];
       const double* src = q.tval + 32L * pi.x + 2 * tid;
       double* ad = sm + NS * HS + slot * AS + 2 * tid;
       if (tid < pi.y * 16) cp_async16(ad, src);
-      if (tid + NTH < pi.y * 16) cp_async16(ad + 2 * NTH, src + 2 * NTH);
+      if (P == 16 && tid + NTH < pi.y * 16) cp_async16(ad + 2 * NTH, src + 2 * NTH);
     }
     cp_async_commit();  // (empty groups keep the wait count uniform)
   };
@@ -613,6 +608,7 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
 #pragma unroll
   for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
   pdl_wait();
+  if (tid < NT * 8 && q.Hio != nullptr && !q.first) sbeta[tid] = c0 + tid < q.kb ? q.beta[c0 + tid] : 0.0;
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) issue(s);
   for (int pc = 0; pc < npc; ++pc) {
@@ -645,7 +641,7 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
       }
     }
   }
-  spmm_epilogue<NT, JB>(q, c, g, c0, red);
+  spmm_epilogue<NT>(q, c, g, c0, red, sbeta);
 }
 // ---- block SDDMM: dense Gram blocks of the row groups on DMMA ----------------------------------
 // G = A_R^T B_C for a group's 32 rows R and a 64-column tile C of its union, over K (the
@@ -895,18 +891,18 @@ long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
 bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
 
-template <int NS, int JB, class Go>
+template <int P, int NS, class Go>
 void spmm_v3_dispatch(int nt, Go&& go) {
   switch (nt) {
-    case 1: go(k_spmm_v3<1, NS, spmm_minb(1, NS, JB), JB>); break;
-    case 2: go(k_spmm_v3<2, NS, spmm_minb(2, NS, JB), JB>); break;
-    case 3: go(k_spmm_v3<3, NS, spmm_minb(3, NS, JB), JB>); break;
-    case 4: go(k_spmm_v3<4, NS, spmm_minb(4, NS, JB), JB>); break;
-    case 5: go(k_spmm_v3<5, NS, spmm_minb(5, NS, JB), JB>); break;
-    case 6: go(k_spmm_v3<6, NS, spmm_minb(6, NS, JB), JB>); break;
-    case 7: go(k_spmm_v3<7, NS, spmm_minb(7, NS, JB), JB>); break;
-    case 8: go(k_spmm_v3<8, NS, spmm_minb(8, NS, JB), JB>); break;
-    default: go(k_spmm_v3<9, NS, spmm_minb(9, NS, JB), JB>); break;
+    case 1: go(k_spmm_v3<1, P, NS, spmm_minb(1, NS, P)>); break;
+    case 2: go(k_spmm_v3<2, P, NS, spmm_minb(2, NS, P)>); break;
+    case 3: go(k_spmm_v3<3, P, NS, spmm_minb(3, NS, P)>); break;
+    case 4: go(k_spmm_v3<4, P, NS, spmm_minb(4, NS, P)>); break;
+    case 5: go(k_spmm_v3<5, P, NS, spmm_minb(5, NS, P)>); break;
+    case 6: go(k_spmm_v3<6, P, NS, spmm_minb(6, NS, P)>); break;
+    case 7: go(k_spmm_v3<7, P, NS, spmm_minb(7, NS, P)>); break;
+    case 8: go(k_spmm_v3<8, P, NS, spmm_minb(8, NS, P)>); break;
+    default: go(k_spmm_v3<9, P, NS, spmm_minb(9, NS, P)>); break;
   }
 }
 
@@ -920,28 +916,29 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
                       bool first, cudaStream_t s, bool colsum) {
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
-  static const int variant = [] {  // A/B switch: FSA_SPMM=rt (round-1 kernel), FSA_SPMM_NS=2|3 (ring depth)
+  static const int variant = [] {  // A/B switch: FSA_SPMM=rt (round-1 kernel), FSA_SPMM_NS=2|3|4 (ring depth)
     const char* e = std::getenv("FSA_SPMM");
     if (e != nullptr && std::strcmp(e, "rt") == 0) return 0;
     const char* d = std::getenv("FSA_SPMM_NS");
     const int ns = d != nullptr ? std::atoi(d) : 2;
-    return ns == 3 ? 3 : 2;
+    return ns == 3 || ns == 4 ? ns : 2;
+  }();
+  static const int piece = [] {  // FSA_SPMM_P=8|16: union rows per pipeline stage
+    const char* e = std::getenv("FSA_SPMM_P");
+    return e != nullptr && std::atoi(e) == 8 ? 8 : kPiece;
   }();
   static const int epf = [] {  // FSA_SPMM_EPF=k: L2 prefetch of the epilogue rows k pieces before the end
     const char* e = std::getenv("FSA_SPMM_EPF");
     return e != nullptr ? std::atoi(e) : 4;
   }();
-  static const int jb = [] {  // FSA_SPMM_EPB=1|2: column tiles per batch of epilogue loads
-    const char* e = std::getenv("FSA_SPMM_EPB");
-    return e != nullptr && e[0] == '2' ? 2 : 1;
-  }();
   auto launch = [&](int nt, long c_first, long tiles) {
     const long ldh = nt * 8 + 4;  // k_spmm_rt's LDH
     const bool lean = variant != 0;
-    const int gcap = static_cast<int>(round_up(pat.gmax, kPiece));
+    const int pp = lean ? piece : kPiece;
+    const int gcap = static_cast<int>(round_up(pat.gmax, 16));
     const int ns = variant == 0 ? 2 : variant;
-    const int smem = static_cast<int>(ns * (kPiece * ldh + kPiece * kGroup) * 8) +
-                     (lean ? gcap * 4 + (gcap / kPiece) * (16 + 8) : 0);
+    const int smem = static_cast<int>(ns * (pp * ldh + pp * kGroup) * 8) +
+                     (lean ? gcap * 4 + (gcap / pp) * (16 + 8) : 0);
     require(!lean || (pat.cols > 0 ? pat.cols : pat.rows) * ldx < (1L << 32), "spmm: RHS block too large for 32-bit offsets");
     TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
                    X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
@@ -958,10 +955,13 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       launch_pdl(kern, grid, dim3(128), static_cast<size_t>(smem), s, a);
     };
     if (lean) {
-      if (ns == 2) {
-        jb == 1 ? spmm_v3_dispatch<2, 1>(nt, go) : spmm_v3_dispatch<2, 2>(nt, go);
+      if (pp == 8) {
+        ns == 2 ? spmm_v3_dispatch<8, 2>(nt, go)
+                : (ns == 3 ? spmm_v3_dispatch<8, 3>(nt, go) : spmm_v3_dispatch<8, 4>(nt, go));
+      } else if (ns == 2) {
+        spmm_v3_dispatch<16, 2>(nt, go);
       } else {
-        jb == 1 ? spmm_v3_dispatch<3, 1>(nt, go) : spmm_v3_dispatch<3, 2>(nt, go);
+        spmm_v3_dispatch<16, 3>(nt, go);
       }
       FSA_LAUNCH_CHECK();
       return;
