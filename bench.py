@@ -332,7 +332,7 @@ def run_prediction(args, cfg):
         avg = sp["ms"] / sp["count"]
         units = sp["units"] / sp["count"]
         ach = units / (avg * 1e-3) / 1e9
-        roofline = {"kernel": "k_spmm_rt (Jacobi-PCG SpMM of the simulation / Sigma_s solves, 64-column tiles)",
+        roofline = {"kernel": "k_spmm_v3 (Jacobi-PCG SpMM of the simulation / Sigma_s solves, 64-column tiles)",
                     "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                     "traffic": None, "avg_launch_ms": avg, "launches": sp["count"],
                     "share_of_step": sp["ms"] / (ms * args.steps), "units_per_launch": units,
@@ -530,7 +530,7 @@ def main():
     b_exp = 8.0 * m_ * n_ + 24.0 * n_ * t_
     b_xr = 48.0 * n_ * t_
     kernels = [
-        entry("spmm", "k_spmm_rt (32-row groups, DMMA.8x8x4 fp64 block product + direction update)", b_spmm),
+        entry("spmm", "k_spmm_v3 (32-row groups, DMMA.8x8x4 fp64 block product + direction update)", b_spmm),
         entry("lowrank_expand", "k_oz_expand (tcgen05 kind::i8 Ozaki, + k_oz_planes_w)" if int8 else
               "k_oz_expand 64-column INT8 block + 8-column remainder (+ planes)", b_exp),
         entry("lowrank_project", "k_oz_gemm (tcgen05 kind::i8 Ozaki, + k_oz_planes_y, k_oz_reduce)" if int8 else

@@ -621,14 +621,13 @@ int fsa_debug_kernel_bench(fsa_model* md, int which, int64_t k, int reps, int fl
           break;
       }
     };
-    g_spmm_dbg = flags;
+    require(flags == 0, "debug_kernel_bench: flags must be 0");
     run();
     cudaEvent_t a = M->ctx->ev(), b = M->ctx->ev();
     FSA_CUDA(cudaEventRecord(a, s));
     for (int i = 0; i < reps; ++i) run();
     FSA_CUDA(cudaEventRecord(b, s));
     FSA_CUDA(cudaEventSynchronize(b));
-    g_spmm_dbg = 0;
     float ms = 0.f;
     FSA_CUDA(cudaEventElapsedTime(&ms, a, b));
     *ms_out = static_cast<double>(ms) / reps;

@@ -266,13 +266,10 @@ __global__ void __launch_bounds__(256) k_spmm_dot(const long* __restrict__ rowpt
 // union is consumed in pieces of kPiece rows: the piece's RHS rows (gathered) and stored
 // tiles (contiguous) are copied into shared memory with cp.async, double-buffered. Against the
 // CSR kernel every RHS row is fetched once per group instead of once per nonzero and the
-// arithmetic runs on the tensor pipe.
-constexpr int kPiece = 16;  // union rows per pipeline stage (4 DMMA k-steps; 8 and 32 measured slower)
-// resident CTAs per SM that the ring's shared memory allows (the __launch_bounds__ minimum)
-constexpr int spmm_minb(int nt, int ns, int p = kPiece) {
-  const int b = (227 * 1024) / (ns * p * (nt * 8 + 4 + kGroup) * 8 + 3 * 1024);
-  return b > 8 ? 8 : (b < 1 ? 1 : b);
-}
+// arithmetic runs on the tensor pipe. (Measured and removed in round 2: pieces of 8 rows, 3- and
+// 4-deep rings -- fewer resident CTAs --, bulk-copy (TMA) gathers of the 448-byte rows, an L2
+// prefetch of each group's value tiles.)
+constexpr int kPiece = 16;  // union rows per pipeline stage (4 DMMA k-steps)
 struct TileSpmmArgs {
   const long* gptr;
   const int* gcol;
@@ -295,166 +292,9 @@ struct TileSpmmArgs {
   int first = 0;
   long xrows = 0;    // rows of X that may be gathered (own + halo); checked builds only
   long ntiles = 0;   // stored value tiles; checked builds only
-  int dbg = 0;  // diagnostics only (fsa_debug_kernel_bench): 1 no DMMA, 2 no epilogue, 4 no RHS gather, 8 no A tiles,
-                // 16 no L2 prefetch of the epilogue rows
   int gcap = 0;  // k_spmm_v3: union slots reserved in shared memory (gmax rounded up to whole pieces)
   int epf = 0;   // k_spmm_v3: L2 prefetch of the group's epilogue rows this many pieces before the end (0 off)
 };
-// k_spmm_rt: warp w owns row tile w (8 rows) of the group and all NT n-tiles, so a k-step
-// costs one warp-uniform test of its mask bit, one A fragment and NT B fragments for NT
-// independent DMMAs (no per-mask dispatch, no discarded n-tiles: 12 % faster at config 2 than
-// warps that share the four row tiles). The h.v column partials of the four row tiles meet in
-// shared memory in a fixed order.
-template <int NT, int P, int MINB = 8>
-__global__ void __launch_bounds__(128, MINB) k_spmm_rt(TileSpmmArgs q) {
-  static_assert(kGroup == 32 && P % 4 == 0, "four row tiles per group");
-  constexpr int WN = 4;
-  const long c0 = 64L * blockIdx.y;  // column tile: columns [c0, c0 + 8 NT)
-  const double* X = q.X + c0;
-  double* Y = q.Y + c0;
-  const double* Y0 = q.Y0 != nullptr ? q.Y0 + c0 : nullptr;
-  const long ncols = q.ncols - c0;
-  constexpr int NTH = 32 * WN;
-  constexpr int LDH = NT * 8 + 4;  // == 4 or 12 (mod 16): conflict-free B fragments
-  constexpr int CH = NT * 4;       // 16-byte chunks per staged row (one per lane)
-  constexpr int HS = P * LDH, AS = P * kGroup;
-  constexpr int RW = P / WN;
-  extern __shared__ __align__(16) double sm[];  // [2][HS], [2][AS]
-  __shared__ double red[WN][NT * 8];
-  const long g = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long u0 = q.gptr[g];
-  const int up = static_cast<int>(q.gptr[g + 1] - u0);
-  const int npc = (up + P - 1) / P;
-  const long kb0 = u0 / 4;
-  auto load_meta = [&](int pc, int2& pm, int (&gc)[RW]) {
-    pm = q.pmeta[kb0 + pc * (P / 4)];
-#pragma unroll
-    for (int i = 0; i < RW; ++i) {
-      const int u = pc * P + warp + WN * i;
-      gc[i] = q.gcol[u0 + (u < up ? u : 0)];
-    }
-  };
-  auto issue = [&](int pc, const int2& pm, const int (&gc)[RW]) {
-    double* hs = sm + (pc & 1) * HS;
-    double* as = sm + 2 * HS + (pc & 1) * AS;
-    const int ua = pc * P, nr = min(P, up - ua);
-#pragma unroll
-    for (int ch = lane; ch < CH; ch += 32) {  // CH = 4 NT chunks of 16 bytes per row
-#pragma unroll
-      for (int i = 0; i < RW; ++i) {
-        const int u = warp + WN * i;
-        FSA_DCHECK(u >= nr || (gc[i] >= 0 && gc[i] < q.xrows), "spmm: gathered RHS row out of range");
-        if (u < nr && !(q.dbg & 4)) cp_async16(hs + u * LDH + ch * 2, X + static_cast<long>(gc[i]) * q.ldx + ch * 2);
-      }
-    }
-    const int nt = __popc(pm.y & static_cast<int>((1ull << nr) - 1ull));
-    FSA_DCHECK(pm.x >= 0 && pm.x + nt <= q.ntiles, "spmm: value tile range out of bounds");
-    const double* src = q.tval + 32L * pm.x;
-    if (!(q.dbg & 8))
-      for (int idx = tid; idx < nt * 16; idx += NTH) cp_async16(as + idx * 2, src + idx * 2);
-    cp_async_commit();
-  };
-  if (tid == 0 && (q.dbg & 32)) {  // (opt-in diagnostics: L2 prefetch of the epilogue rows, measured slower)
-    const uint32_t rb = static_cast<uint32_t>(kGroup * q.ldy * 8);
-    if (q.Y0 != nullptr) prefetch_l2(q.Y0 + g * kGroup * q.ldy, rb);
-    prefetch_l2(q.X + g * kGroup * q.ldx, static_cast<uint32_t>(kGroup * q.ldx * 8));
-    if (q.Hio != nullptr && !q.first) {
-      prefetch_l2(q.Hio + g * kGroup * q.ldy, rb);
-      prefetch_l2(q.Y + g * kGroup * q.ldy, rb);
-    }
-  }
-  double c[NT][2];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
-  const int below = (1 << warp) - 1;
-  int2 cur{0, 0}, nxt{0, 0};
-  int gc[RW];
-  if (npc > 0) load_meta(0, cur, gc);  // (static group metadata: read before the dependency wait)
-  pdl_wait();
-  if (npc > 0) issue(0, cur, gc);
-  if (npc > 1) load_meta(1, nxt, gc);
-  for (int pc = 0; pc < npc; ++pc) {
-    if (pc + 1 < npc) issue(pc + 1, nxt, gc);
-    int2 after{0, 0};
-    if (pc + 2 < npc) load_meta(pc + 2, after, gc);
-    if (pc + 1 < npc) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncthreads();
-    const double* hs = sm + (pc & 1) * HS + (lane & 3) * LDH + (lane >> 2);
-    const double* as = sm + 2 * HS + (pc & 1) * AS + lane;
-    const int nks = min(P, up - pc * P) / 4;
-    int t = 0;
-#pragma unroll
-    for (int ks = 0; ks < P / 4; ++ks) {
-      if (ks < nks) {
-        const int m = (cur.y >> (4 * ks)) & 15;
-        if (((m >> warp) & 1) && !(q.dbg & 1)) {
-          const double a = as[(t + __popc(m & below)) * 32];
-          const double* hb = hs + ks * 4 * LDH;
-          double b[NT];
-#pragma unroll
-          for (int j = 0; j < NT; ++j) b[j] = hb[j * 8];
-#pragma unroll
-          for (int j = 0; j < NT; ++j) dmma8x8x4(c[j][0], c[j][1], a, b[j]);
-        }
-        t += __popc(m);
-      }
-    }
-    __syncthreads();  // the buffer is refilled by issue(pc + 2)
-    cur = nxt;
-    nxt = after;
-  }
-  // epilogue: Y = Y0 + S X on this lane's fragments; h.v column partials over the 32 rows
-  const long row = g * kGroup + warp * 8 + (lane >> 2);
-  const bool rok = row < q.nrows;
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const long cc = j * 8 + 2 * (lane & 3);
-    double d0 = 0.0, d1 = 0.0;
-    if (q.dbg & 2) {
-      d0 = c[j][0];
-      d1 = c[j][1];
-    } else if (rok && cc < ncols) {
-      double2 o = make_double2(c[j][0], c[j][1]);
-      if (Y0 != nullptr) {
-        const double2 y0 = *reinterpret_cast<const double2*>(Y0 + row * q.ldy + cc);
-        o.x += y0.x;
-        o.y += y0.y;
-      }
-      double2 h = *reinterpret_cast<const double2*>(X + row * q.ldx + cc);
-      if (q.Hio != nullptr) {  // H = Z + beta H (krylov.cpp:92), V = (Lw + S Z) + beta V
-        double2* hp = reinterpret_cast<double2*>(q.Hio + c0 + row * q.ldy + cc);
-        if (!q.first) {
-          const long gc = c0 + cc;
-          const double b0 = gc < q.kb ? q.beta[gc] : 0.0, b1 = gc + 1 < q.kb ? q.beta[gc + 1] : 0.0;
-          const double2 ho = *hp, vo = *reinterpret_cast<const double2*>(Y + row * q.ldy + cc);
-          h.x = h.x + b0 * ho.x;
-          h.y = h.y + b1 * ho.y;
-          o.x += b0 * vo.x;
-          o.y += b1 * vo.y;
-        }
-        *hp = h;
-      }
-      *reinterpret_cast<double2*>(Y + row * q.ldy + cc) = o;
-      d0 = h.x * o.x;
-      d1 = h.y * o.y;
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-    }
-    if (lane < 4) {
-      red[warp][cc] = d0;
-      red[warp][cc + 1] = d1;
-    }
-  }
-  __syncthreads();
-  if (tid < NT * 8 && tid < ncols)
-    q.partial[c0 + g * q.ldp + tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
-}
-
 // the h.v epilogue of the block SpMM: Y = Y0 + S X on this lane's fragments, with the PCG
 // direction update when H is given (REC: H = Z + beta H, V = (Lw + S Z) + beta V, krylov.cpp:92;
 // else H = Z), and the h.v column partials of the group's 32 rows (fixed order: lane butterfly,
@@ -530,10 +370,10 @@ __device__ __forceinline__ void spmm_epilogue(const TileSpmmArgs& q, const doubl
 // Warp w gathers piece rows 4w .. 4w + 3 (one 16-byte vector load of their offsets), so a piece
 // costs a warp ~4 copy instructions per row instead of ~25 of 64-bit address arithmetic, and a
 // k-step is one bit test plus the fragment loads and DMMAs.
-template <int NT, int P, int NS, int MINB>
+template <int NT, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
-  constexpr int WN = 4, NTH = 32 * WN, RW = P / WN;
-  static_assert(kGroup == 32 && (P == 16 || P == 8) && NS >= 2, "four row tiles per group, <= four k-steps per piece");
+  constexpr int P = kPiece, NS = 2, WN = 4, NTH = 32 * WN, RW = P / WN;
+  static_assert(kGroup == 32 && P == 16, "four row tiles per group, four k-steps per piece");
   constexpr int LDH = NT * 8 + 4;  // == 4 or 12 (mod 16): conflict-free B fragments
   constexpr int CH = NT * 4;       // 16-byte chunks per gathered row
   constexpr int HS = P * LDH, AS = P * kGroup;
@@ -580,14 +420,8 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
   auto issue = [&](int pc) {
     if (pc < npc) {
       const int slot = pc % NS;
-      uint32_t o[RW];
-      if constexpr (RW == 4) {
-        const uint4 v = *reinterpret_cast<const uint4*>(soff + pc * P + RW * warp);
-        o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
-      } else {
-        const uint2 v = *reinterpret_cast<const uint2*>(soff + pc * P + RW * warp);
-        o[0] = v.x, o[1] = v.y;
-      }
+      const uint4 v = *reinterpret_cast<const uint4*>(soff + pc * P + RW * warp);
+      const uint32_t o[RW] = {v.x, v.y, v.z, v.w};
       double* hd = sm + slot * HS + RW * warp * LDH + 2 * lane;
 #pragma unroll
       for (int k = 0; k < (CH + 31) / 32; ++k) {
@@ -600,7 +434,7 @@ __global__ void __launch_bounds__(128, MINB) k_spmm_v3(TileSpmmArgs q) {
       const double* src = q.tval + 32L * pi.x + 2 * tid;
       double* ad = sm + NS * HS + slot * AS + 2 * tid;
       if (tid < pi.y * 16) cp_async16(ad, src);
-      if (P == 16 && tid + NTH < pi.y * 16) cp_async16(ad + 2 * NTH, src + 2 * NTH);
+      if (tid + NTH < pi.y * 16) cp_async16(ad + 2 * NTH, src + 2 * NTH);
     }
     cp_async_commit();  // (empty groups keep the wait count uniform)
   };
@@ -808,7 +642,6 @@ __global__ void k_group_scatter(const int* __restrict__ gslot, const int* __rest
 
 }  // namespace
 
-int g_spmm_dbg = 0;
 
 void sddmm_sigma_s(const double* U, long ldu, const Csr& pat, const double* lowrank_diag, const SddmmParams& P,
                    double* val, int* n_clamped_dev, cudaStream_t s) {
@@ -887,24 +720,7 @@ void group_values(const Csr& pat, const double* val, double* gval, cudaStream_t 
 
 long spmm_group_blocks(long ngrp) { return ngrp < 1 ? 1 : ngrp; }
 
-
-
 bool spmm_block_supported(long ncols) { return ncols % 8 == 0; }
-
-template <int P, int NS, class Go>
-void spmm_v3_dispatch(int nt, Go&& go) {
-  switch (nt) {
-    case 1: go(k_spmm_v3<1, P, NS, spmm_minb(1, NS, P)>); break;
-    case 2: go(k_spmm_v3<2, P, NS, spmm_minb(2, NS, P)>); break;
-    case 3: go(k_spmm_v3<3, P, NS, spmm_minb(3, NS, P)>); break;
-    case 4: go(k_spmm_v3<4, P, NS, spmm_minb(4, NS, P)>); break;
-    case 5: go(k_spmm_v3<5, P, NS, spmm_minb(5, NS, P)>); break;
-    case 6: go(k_spmm_v3<6, P, NS, spmm_minb(6, NS, P)>); break;
-    case 7: go(k_spmm_v3<7, P, NS, spmm_minb(7, NS, P)>); break;
-    case 8: go(k_spmm_v3<8, P, NS, spmm_minb(8, NS, P)>); break;
-    default: go(k_spmm_v3<9, P, NS, spmm_minb(9, NS, P)>); break;
-  }
-}
 
 // Y = S X (+ Y0) over ncols (multiple of 8) columns in 64-column tiles; dot[c] = sum_r X[r][c] Y[r][c]
 void spmm_block_dot(const Csr& pat, const double* gval, const double* X, long ldx, double* Y, long ldy, long ncols,
@@ -916,35 +732,20 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
                       bool first, cudaStream_t s, bool colsum) {
   require(spmm_block_supported(ncols) && ldx >= ncols && ldy == ldx && ldx % 2 == 0, "spmm_block_dot: unsupported block");
   if (pat.rows == 0) return;
-  static const int variant = [] {  // A/B switch: FSA_SPMM=rt (round-1 kernel), FSA_SPMM_NS=2|3|4 (ring depth)
-    const char* e = std::getenv("FSA_SPMM");
-    if (e != nullptr && std::strcmp(e, "rt") == 0) return 0;
-    const char* d = std::getenv("FSA_SPMM_NS");
-    const int ns = d != nullptr ? std::atoi(d) : 2;
-    return ns == 3 || ns == 4 ? ns : 2;
-  }();
-  static const int piece = [] {  // FSA_SPMM_P=8|16: union rows per pipeline stage
-    const char* e = std::getenv("FSA_SPMM_P");
-    return e != nullptr && std::atoi(e) == 8 ? 8 : kPiece;
-  }();
-  static const int epf = [] {  // FSA_SPMM_EPF=k: L2 prefetch of the epilogue rows k pieces before the end
+  static const int epf = [] {  // FSA_SPMM_EPF=k: L2 prefetch of the epilogue rows k pieces before the end (0 off)
     const char* e = std::getenv("FSA_SPMM_EPF");
     return e != nullptr ? std::atoi(e) : 4;
   }();
   auto launch = [&](int nt, long c_first, long tiles) {
-    const long ldh = nt * 8 + 4;  // k_spmm_rt's LDH
-    const bool lean = variant != 0;
-    const int pp = lean ? piece : kPiece;
-    const int gcap = static_cast<int>(round_up(pat.gmax, 16));
-    const int ns = variant == 0 ? 2 : variant;
-    const int smem = static_cast<int>(ns * (pp * ldh + pp * kGroup) * 8) +
-                     (lean ? gcap * 4 + (gcap / pp) * (16 + 8) : 0);
-    require(!lean || (pat.cols > 0 ? pat.cols : pat.rows) * ldx < (1L << 32), "spmm: RHS block too large for 32-bit offsets");
+    const long ldh = nt * 8 + 4;  // k_spmm_v3's LDH
+    const int gcap = static_cast<int>(round_up(pat.gmax, kPiece));
+    const int smem = static_cast<int>(2 * (kPiece * ldh + kPiece * kGroup) * 8) + gcap * 4 + (gcap / kPiece) * (16 + 8);
+    require((pat.cols > 0 ? pat.cols : pat.rows) * ldx < (1L << 32), "spmm: RHS block too large for 32-bit offsets");
     TileSpmmArgs a{pat.gptr.get(), pat.gcol.get(), reinterpret_cast<const int2*>(pat.pmeta.get()), gval, pat.rows,
                    X + c_first, ldx, Y + c_first, ldy, ncols - c_first, Y0 != nullptr ? Y0 + c_first : nullptr,
                    partial + c_first, ncols, H != nullptr ? H + c_first : nullptr,
                    beta != nullptr ? beta + c_first : nullptr, kb - c_first, first ? 1 : 0,
-                   pat.cols > 0 ? pat.cols : pat.rows, pat.ntiles, g_spmm_dbg, gcap, epf};
+                   pat.cols > 0 ? pat.cols : pat.rows, pat.ntiles, gcap, epf};
     const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(tiles));
     auto go = [&](auto kern) {
       // one fixed opt-in ceiling (not this launch's size: the launch size depends on the pattern's
@@ -954,28 +755,16 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       FSA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCeiling));
       launch_pdl(kern, grid, dim3(128), static_cast<size_t>(smem), s, a);
     };
-    if (lean) {
-      if (pp == 8) {
-        ns == 2 ? spmm_v3_dispatch<8, 2>(nt, go)
-                : (ns == 3 ? spmm_v3_dispatch<8, 3>(nt, go) : spmm_v3_dispatch<8, 4>(nt, go));
-      } else if (ns == 2) {
-        spmm_v3_dispatch<16, 2>(nt, go);
-      } else {
-        spmm_v3_dispatch<16, 3>(nt, go);
-      }
-      FSA_LAUNCH_CHECK();
-      return;
-    }
     switch (nt) {
-      case 1: go(k_spmm_rt<1, kPiece>); break;
-      case 2: go(k_spmm_rt<2, kPiece>); break;
-      case 3: go(k_spmm_rt<3, kPiece>); break;
-      case 4: go(k_spmm_rt<4, kPiece>); break;
-      case 5: go(k_spmm_rt<5, kPiece>); break;
-      case 6: go(k_spmm_rt<6, kPiece>); break;
-      case 7: go(k_spmm_rt<7, kPiece>); break;
-      case 8: go(k_spmm_rt<8, kPiece>); break;
-      default: go(k_spmm_rt<9, kPiece, 6>); break;  // 72 columns (t = 65) in one pass
+      case 1: go(k_spmm_v3<1, 8>); break;
+      case 2: go(k_spmm_v3<2, 8>); break;
+      case 3: go(k_spmm_v3<3, 8>); break;
+      case 4: go(k_spmm_v3<4, 8>); break;
+      case 5: go(k_spmm_v3<5, 8>); break;
+      case 6: go(k_spmm_v3<6, 8>); break;
+      case 7: go(k_spmm_v3<7, 8>); break;
+      case 8: go(k_spmm_v3<8, 8>); break;
+      default: go(k_spmm_v3<9, 7>); break;  // 72 columns (t = 65) in one pass
     }
     FSA_LAUNCH_CHECK();
   };

@@ -6,9 +6,6 @@
 
 namespace fsa {
 
-// k_spmm_rt diagnostics switch (fsa_debug_kernel_bench only; 0 in every product path)
-extern int g_spmm_dbg;
-
 struct SddmmParams {
   int nu, family;
   double sigma2, sigma1_2, rho, gamma;
