@@ -176,14 +176,7 @@ __global__ void __launch_bounds__(256) k_colsum_partials(const double* __restric
   __shared__ double red[8];
   const long c = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double s0 = 0.0, s1 = 0.0;
-  long b = tid;
-  for (; b + 256 < nb; b += 512) {
-    s0 += partial[b * ldp + c];
-    s1 += partial[(b + 256) * ldp + c];
-  }
-  if (b < nb) s0 += partial[b * ldp + c];
-  double sacc = s0 + s1;
+  double sacc = strided_colsum(partial, nb, ldp, c);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
   if (lane == 0) red[warp] = sacc;

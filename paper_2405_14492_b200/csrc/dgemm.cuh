@@ -23,6 +23,29 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+// this thread's part of sum_b partial[b][c] over b = tid, tid + 256, ... (blockDim 256), in two
+// interleaved accumulators (s0: b = tid + 512 i, s1: b = tid + 256 + 512 i) -- the fixed order every
+// column sum of the CG partials uses; eight loads are issued before they are added (same order)
+__device__ __forceinline__ double strided_colsum(const double* __restrict__ partial, long nb, long ldp, long c) {
+  double s0 = 0.0, s1 = 0.0;
+  long b = threadIdx.x;
+  for (; b + 7 * 256 < nb; b += 8 * 256) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = partial[(b + 256 * i) * ldp + c];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      s0 += v[i];
+      s1 += v[i + 1];
+    }
+  }
+  for (; b + 256 < nb; b += 512) {
+    s0 += partial[b * ldp + c];
+    s1 += partial[(b + 256) * ldp + c];
+  }
+  if (b < nb) s0 += partial[b * ldp + c];
+  return s0 + s1;
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));

@@ -761,9 +761,9 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       case 3: go(k_spmm_v3<3, 8>); break;
       case 4: go(k_spmm_v3<4, 8>); break;
       case 5: go(k_spmm_v3<5, 8>); break;
-      case 6: go(k_spmm_v3<6, 8>); break;
-      case 7: go(k_spmm_v3<7, 8>); break;
-      case 8: go(k_spmm_v3<8, 8>); break;
+      case 6: go(k_spmm_v3<6, 7>); break;
+      case 7: go(k_spmm_v3<7, 7>); break;  // (7 resident CTAs: no spills; 8 -> 4 % slower, 6 -> 6 %)
+      case 8: go(k_spmm_v3<8, 7>); break;
       default: go(k_spmm_v3<9, 7>); break;  // 72 columns (t = 65) in one pass
     }
     FSA_LAUNCH_CHECK();
