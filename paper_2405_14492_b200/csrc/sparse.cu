@@ -762,7 +762,7 @@ void spmm_block_dot_h(const Csr& pat, const double* gval, const double* X, long 
       case 4: go(k_spmm_v3<4, 8>); break;
       case 5: go(k_spmm_v3<5, 8>); break;
       case 6: go(k_spmm_v3<6, 7>); break;
-      case 7: go(k_spmm_v3<7, 7>); break;  // (7 resident CTAs: no spills; 8 -> 4 % slower, 6 -> 6 %)
+      case 7: go(k_spmm_v3<7, 7>); break;  // (7 resident CTAs: 8 -> 4 % slower, 6 -> 6 %)
       case 8: go(k_spmm_v3<8, 7>); break;
       default: go(k_spmm_v3<9, 7>); break;  // 72 columns (t = 65) in one pass
     }
