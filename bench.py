@@ -524,6 +524,7 @@ def main():
                 "share_of_step": t["ms"] / pms, "units_per_launch": units_per_launch}
 
     int8 = tp_ <= 64
+    pair = 64 < tp_ <= 96  # (ozaki_*_pair: one launch, CTA pairs stream the same U planes)
     nnz_loc = nnz / (world if sharded else 1)
     b_spmm = 12.0 * nnz_loc + 48.0 * n_ * t_
     b_proj = 8.0 * m_ * n_ + 8.0 * n_ * t_
@@ -532,9 +533,11 @@ def main():
     kernels = [
         entry("spmm", "k_spmm_v3 (32-row groups, DMMA.8x8x4 fp64 block product + direction update)", b_spmm),
         entry("lowrank_expand", "k_oz_expand (tcgen05 kind::i8 Ozaki, + k_oz_planes_w)" if int8 else
-              "k_oz_expand 64-column INT8 block + 8-column remainder (+ planes)", b_exp),
+              ("k_oz_expand<paired> (two %d-column INT8 tiles on CTA pairs, + planes)" % (tp_ // 2) if pair else
+               "k_oz_expand 64-column INT8 tiles + DMMA remainder (+ planes)"), b_exp),
         entry("lowrank_project", "k_oz_gemm (tcgen05 kind::i8 Ozaki, + k_oz_planes_y, k_oz_reduce)" if int8 else
-              "k_oz_gemm 64-column INT8 block + 8-column remainder (+ planes, reduce)", b_proj),
+              ("k_oz_gemm<paired> (two %d-column INT8 tiles on CTA pairs, + planes, reduce)" % (tp_ // 2) if pair
+               else "k_oz_gemm 64-column INT8 tiles + DMMA remainder (+ planes, reduce)"), b_proj),
     ]
     kernels = [k for k in kernels if k]
     dom = max(kernels, key=lambda k: k["share_of_step"])
