@@ -10,10 +10,10 @@ namespace {
 
 constexpr int kStages = 4;
 constexpr int kKb = 32;                            // K bytes per stage = one kind::i8 MMA
-constexpr int kATile = kOzSlices * 128 * kKb;      // 32 KB: 8 planes x 128 rows x 32 K
-constexpr int kBTile = kOzSlices * kOzCols * kKb;  // 16 KB: 8 planes x 64 cols x 32 K
+constexpr int kATile = kOzSlices * 128 * kKb;      // 28 KB: 7 planes x 128 rows x 32 K
+constexpr int kBTile = kOzSlices * kOzCols * kKb;  // 14 KB: 7 planes x 64 cols x 32 K
 constexpr int kSmem = kStages * (kATile + kBTile);
-constexpr long kMaxChunk = 16384;  // int32 exactness: 8 pairs x K x 127^2 < 2^31
+constexpr long kMaxChunk = 16384;  // int32 exactness: <= 7 pairs x K x 128^2 < 2^31
 
 // ---- PTX wrappers ---------------------------------------------------------------------------
 // (no L2 prefetch ahead of the bulk copies: measured slower, it competes with the copies)
@@ -53,23 +53,24 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[1
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
-// 16 columns [col0, col0 + 16) of this lane's row: sum_d 2^{-7d} C_d with the eight int32
-// accumulators combined exactly in two int64 halves (|hi|, |lo| < 2^53: exact conversions)
+// 16 columns [col0, col0 + 16) of this lane's row: 2^4 sum_{d=2..9} 2^{-8d} C_d with the eight int32
+// accumulators combined exactly in three int64 groups (|g| < 2^53: exact conversions)
+__device__ __forceinline__ double recombine8(uint32_t c2, uint32_t c3, uint32_t c4, uint32_t c5, uint32_t c6,
+                                             uint32_t c7, uint32_t c8, uint32_t c9) {
+  const long long g1 = (static_cast<long long>(static_cast<int>(c2)) << 16) +
+                       (static_cast<long long>(static_cast<int>(c3)) << 8) + static_cast<int>(c4);
+  const long long g2 = (static_cast<long long>(static_cast<int>(c5)) << 16) +
+                       (static_cast<long long>(static_cast<int>(c6)) << 8) + static_cast<int>(c7);
+  const long long g3 = (static_cast<long long>(static_cast<int>(c8)) << 8) + static_cast<int>(c9);
+  return fma(static_cast<double>(g1), 0x1p-28, fma(static_cast<double>(g2), 0x1p-52, static_cast<double>(g3) * 0x1p-68));
+}
 __device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[16], int wstride = kOzCols) {
-  uint32_t v[kOzSlices][16];
+  uint32_t v[kOzWeights][16];
 #pragma unroll
-  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
+  for (int dd = 0; dd < kOzWeights; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    const long long hi = (static_cast<long long>(static_cast<int>(v[0][c])) << 21) +
-                         (static_cast<long long>(static_cast<int>(v[1][c])) << 14) +
-                         (static_cast<long long>(static_cast<int>(v[2][c])) << 7) + static_cast<int>(v[3][c]);
-    const long long lo = (static_cast<long long>(static_cast<int>(v[4][c])) << 21) +
-                         (static_cast<long long>(static_cast<int>(v[5][c])) << 14) +
-                         (static_cast<long long>(static_cast<int>(v[6][c])) << 7) + static_cast<int>(v[7][c]);
-    out[c] = fma(static_cast<double>(hi), 0x1p-35, static_cast<double>(lo) * 0x1p-63);
-  }
+  for (int c = 0; c < 16; ++c) out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], v[7][c]);
 }
 
 __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]) {
@@ -79,20 +80,12 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]
 }
 // drain16 for 8 columns (half the registers)
 __device__ __forceinline__ void drain8(uint32_t trow, int col0, double (&out)[8], int wstride = kOzCols) {
-  uint32_t v[kOzSlices][8];
+  uint32_t v[kOzWeights][8];
 #pragma unroll
-  for (int dd = 0; dd < kOzSlices; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
+  for (int dd = 0; dd < kOzWeights; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const long long hi = (static_cast<long long>(static_cast<int>(v[0][c])) << 21) +
-                         (static_cast<long long>(static_cast<int>(v[1][c])) << 14) +
-                         (static_cast<long long>(static_cast<int>(v[2][c])) << 7) + static_cast<int>(v[3][c]);
-    const long long lo = (static_cast<long long>(static_cast<int>(v[4][c])) << 21) +
-                         (static_cast<long long>(static_cast<int>(v[5][c])) << 14) +
-                         (static_cast<long long>(static_cast<int>(v[6][c])) << 7) + static_cast<int>(v[7][c]);
-    out[c] = fma(static_cast<double>(hi), 0x1p-35, static_cast<double>(lo) * 0x1p-63);
-  }
+  for (int c = 0; c < 8; ++c) out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], v[7][c]);
 }
 
 // exponent e with |x| < 2^e for all x of a group whose max magnitude is mx (0 -> 0)
@@ -105,31 +98,52 @@ __device__ __forceinline__ int group_exp(double mx) {
 __device__ __forceinline__ double pow2(int k) {
   return (k > -1023 && k < 1024) ? __hiloint2double((k + 1023) << 20, 0) : ldexp(1.0, k);
 }
-// 16 values -> 8 digit planes of 16 signed bytes each. With |x| 2^-e < 1, the magnitude
-// scaled by 2^62 is an exact integer below 2^62 (53-bit mantissa); its 7-bit chunks from the
-// top are the truncated base-128 digits of |x| 2^-e (identical to repeated x 128 / trunc),
-// carrying the sign of x.
-__device__ __forceinline__ void digits16(double (&v)[16], int e, int4 (&out)[kOzSlices]) {
-  const double sc = pow2(62 - e);
-  unsigned long long mag[16];
-  uint32_t neg = 0;
+// 16 values -> 7 balanced base-256 digit planes of 16 signed bytes each (ozaki.cuh): X = trunc(x
+// 2^{54-e}) is exact for the group maximum (|x| < 2^e, 53-bit mantissa) and |X| < 2^54; the digits
+// are peeled off from the least significant end: the low byte of X, read as a signed byte, is the
+// digit, and X <- (X - digit) / 256 = (X + 128) >> 8. Plane a - 1 holds digit a (weight 2^{-8a}).
+__device__ __forceinline__ void digits16(const double (&v)[16], int e, int4 (&out)[kOzSlices]) {
+  const double sc = pow2(54 - e);
+  long long X[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const double t = v[q] * sc;
-    neg |= (t < 0.0 ? 1u : 0u) << q;
-    mag[q] = static_cast<unsigned long long>(__double2ll_rz(fabs(t)));
-  }
+  for (int q = 0; q < 16; ++q) X[q] = __double2ll_rz(v[q] * sc);
 #pragma unroll
-  for (int a = 0; a < kOzSlices; ++a) {
+  for (int a = kOzSlices - 1; a >= 0; --a) {
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const int d = static_cast<int>((mag[q] >> (62 - 7 * (a + 1))) & 127u);
-      const int sd = ((neg >> q) & 1u) ? -d : d;
-      w[q >> 2] |= (static_cast<uint32_t>(sd) & 0xFFu) << (8 * (q & 3));
+      w[q >> 2] |= (static_cast<uint32_t>(X[q]) & 0xFFu) << (8 * (q & 3));
+      X[q] = (X[q] + 128) >> 8;
     }
     out[a] = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]),
                        static_cast<int>(w[3]));
+  }
+}
+
+// One K step of plane-pair MMAs into the eight weight accumulators (weights a + b <= 9 of the
+// 7 x 7 digit planes: 34 products in 12 instructions of N <= 4 NC). `first` (the first K step of
+// an accumulation) overwrites instead of accumulating: weights 2..8 are first written by a = 1;
+// weight 9 by (a = 2, b = 7), which shares its instruction with weights 7 and 8 and is split off.
+__device__ __forceinline__ void ozaki_kstep(uint32_t tmem, uint32_t a0, uint32_t b0, int NC, bool first) {
+#pragma unroll
+  for (int a = 1; a <= kOzSlices; ++a) {
+    const int bmax = min(kOzSlices, kOzMaxW - a);
+    const uint64_t ad = umma_desc(a0 + (a - 1) * 4096, 2048, 128);
+#pragma unroll
+    for (int bs = 1; bs <= bmax; bs += 4) {
+      const int nb = min(4, bmax - bs + 1);
+      const uint32_t td = tmem + static_cast<uint32_t>((a + bs - 2) * NC);
+      const uint64_t bd = umma_desc(b0 + (bs - 1) * 16 * NC, kOzSlices * 16 * NC, 128);
+      if (a == 1) {
+        mma_i8(td, ad, bd, idesc_i8(128, nb * NC), first ? 0u : 1u);
+      } else if (a == 2 && bs + nb - 1 == kOzMaxW - a && first) {  // weights 7, 8 (accumulate) | 9 (new)
+        mma_i8(td, ad, bd, idesc_i8(128, (nb - 1) * NC), 1u);
+        mma_i8(td + static_cast<uint32_t>((nb - 1) * NC), ad,
+               umma_desc(b0 + (bs + nb - 2) * 16 * NC, kOzSlices * 16 * NC, 128), idesc_i8(128, NC), 0u);
+      } else {
+        mma_i8(td, ad, bd, idesc_i8(128, nb * NC), 1u);
+      }
+    }
   }
 }
 
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(128, 1)
   // B tile width NC: 64, or the pair's nc (layout of k_oz_planes_*: plane stride 16 NC bytes,
   // K-half stride 128 NC bytes; one accumulator weight per NC TMEM columns)
   const int NC = PAIRED ? pr.nc : kOzCols;
-  const uint32_t btile = static_cast<uint32_t>(256 * NC);
+  const uint32_t btile = static_cast<uint32_t>(kOzSlices * kKb * NC);
   const int kb0 = chunk * kb_per_chunk;
   const int nk = min(nkb_all - kb0, kb_per_chunk);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -229,17 +243,7 @@ __global__ void __launch_bounds__(128, 1)
       mbar_wait(&full[st], (j / kStages) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-#pragma unroll
-      for (int a = 1; a <= kOzSlices; ++a) {
-#pragma unroll
-        for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
-          const int nb = min(4, kOzSlices + 2 - a - bs);
-          const uint64_t ad = umma_desc(a0 + (a - 1) * 4096, 2048, 128);
-          const uint64_t bd = umma_desc(b0 + (bs - 1) * 16 * NC, 128 * NC, 128);
-          mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * NC), ad, bd, idesc_i8(128, nb * NC),
-                 (j > 0 || a > 1) ? 1u : 0u);
-        }
-      }
+      ozaki_kstep(tmem, a0, b0, NC, j == 0);
       mma_commit(&empty[st]);
     }
     mma_commit(&done);
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   const int8_t* __restrict__ B = pr.B[ct];
   const OzEpi& epi = pr.epi[ct];
   const int NC = PAIRED ? pr.nc : kOzCols;  // B tile width (see k_oz_gemm)
-  const uint32_t btile = static_cast<uint32_t>(256 * NC);
+  const uint32_t btile = static_cast<uint32_t>(kOzSlices * kKb * NC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kATile;
@@ -399,16 +403,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
           mbar_wait(&full[st], static_cast<uint32_t>((g / kStages) & 1));
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-#pragma unroll
-          for (int a = 1; a <= kOzSlices; ++a) {
-#pragma unroll
-            for (int bs = 1; bs <= kOzSlices + 1 - a; bs += 4) {
-              const int nb = min(4, kOzSlices + 2 - a - bs);
-              mma_i8(tmem + static_cast<uint32_t>((a + bs - 2) * NC), umma_desc(a0 + (a - 1) * 4096, 2048, 128),
-                     umma_desc(b0 + (bs - 1) * 16 * NC, 128 * NC, 128), idesc_i8(128, nb * NC),
-                     (kb > 0 || a > 1) ? 1u : 0u);
-            }
-          }
+          ozaki_kstep(tmem, a0, b0, NC, kb == 0);
           mma_commit(&empty[st]);
         }
         mma_commit(&tfull);
@@ -625,7 +620,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ 
   }
   int4 out[kOzSlices];
   digits16(v, e, out);
-  int8_t* base = Ys + static_cast<long>(kb) * (256 * nc) + kc * (128 * nc) + c * 16;
+  int8_t* base = Ys + static_cast<long>(kb) * (kOzSlices * kKb * nc) + kc * (kOzSlices * 16 * nc) + c * 16;
 #pragma unroll
   for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
 }
@@ -664,7 +659,7 @@ __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ 
   for (int q = 0; q < 16; ++q) v[q] = c < tp ? W[(static_cast<long>(kb) * kKb + kc * 16 + q) * ld + c] : 0.0;
   int4 out[kOzSlices];
   digits16(v, e, out);
-  int8_t* base = Ws + static_cast<long>(kb) * (256 * nc) + kc * (128 * nc) + c * 16;
+  int8_t* base = Ws + static_cast<long>(kb) * (kOzSlices * kKb * nc) + kc * (kOzSlices * 16 * nc) + c * 16;
 #pragma unroll
   for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
 }

@@ -5,27 +5,28 @@
 //   expand   Lw = U^T W                 (n x t, K = m)
 // with U fixed for a parameter set. On sm_100a the FP64 tensor path (DMMA) peaks
 // near 40 TF/s, so both passes are compute bound; the INT8 tensor cores run
-// ~100x faster. Each fp64 operand is split (Ozaki scheme, error-free up to the
-// last digit) into kOzSlices signed 7-bit digit planes sharing one power-of-two
-// exponent per scaling group:
-//   x = 2^e * sum_a d_a 2^{-7a} + r,   d_a in [-127, 127],   |r| < 2^{e - 7 s}
-// and the product is recovered from the exact int32 products of digit planes,
-// grouped by total weight d = a + b (a + b <= s + 1 kept):
-//   (X Y)_{ij} = 2^{e_i + f_j} sum_d 2^{-7d} C_d[i][j],  C_d = sum_{a+b=d} X_a Y_b.
+// ~100x faster. Each fp64 operand is split (Ozaki scheme) into kOzSlices = 7 signed
+// BALANCED base-256 digit planes sharing one power-of-two exponent per scaling group
+// (round 2: base 256 with digits in [-128, 127] instead of base 128 with 8 sign-magnitude
+// digits -- 7 bytes per entry of U instead of 8, and 34 plane products instead of 36):
+//   |x| < 2^e:  X = trunc(x 2^{54-e}) (an integer, |X| < 2^54; the group maximum keeps its
+//   whole 53-bit mantissa),  X = sum_a d_a 2^{8(7-a)},  so  x = 2^{e+2} sum_a d_a 2^{-8a} + r,
+//   |r| < 2^{e-54},
+// and the product is recovered from the exact int32 products of digit planes, grouped by
+// total weight d = a + b, d <= 9 kept (8 TMEM accumulators, C_d = sum_{a+b=d} X_a Y_b):
+//   (X Y)_{ij} = 2^{e_i + f_j + 4} sum_{d=2..9} 2^{-8d} C_d[i][j].
 // Scaling groups: project -> U per (inducing row, K chunk), D^{-1}R per (column,
-// K chunk); expand -> U per point, W per column. Every operand loses at most 2^-56 of
-// its group's power-of-two bound and the dropped weight >= 10 products are of the
-// same order, so per output entry
-//   |dY_ij| <= 2^-53 (max_k|X_ik| sum_k|Y_kj| + sum_k|X_ik| max_k|Y_kj|)
+// K chunk); expand -> U per point, W per column. Every operand loses at most 2^-54 of
+// its group's power-of-two bound (<= 2^-53 of the group's largest magnitude) and the dropped
+// weight >= 10 products are below 2^-63, so per output entry
+//   |dY_ij| <= 2^-53 (max_k|X_ik| sum_k|Y_kj| + sum_k|X_ik| max_k|Y_kj|)  (+ the final rounding)
 // -- an fp64-GEMM-class NORMWISE bound per scaling group. Measured against the
-// componentwise sum_k |X_ik||Y_kj| (tests/test_gpu_ozaki.py): projection <= 6e-16;
-// expansion median 2.5e-15, p99.9 < 1e-14, with a tail to ~4e-12 at entries where a
-// W entry happens to be tiny exactly where a point's U column is concentrated (a
-// per-column exponent cannot resolve it; an fp64 GEMM would). End to end at config 2
-// the Ozaki and DMMA paths agree to 2e-11 in the gradient with identical CG counts.
+// componentwise sum_k |X_ik||Y_kj| (tests/test_gpu_ozaki.py): see DESIGN.md §4; the expansion
+// has a tail at entries where a W entry happens to be tiny exactly where a point's U column is
+// concentrated (a per-column exponent cannot resolve it; an fp64 GEMM would).
 //
-// The U digit planes are built once per parameter set (2 x 8 bytes per entry,
-// like fp64 U); R and W are sliced every sweep. Operand tiles are stored in the
+// The U digit planes are built once per parameter set (2 x 7 bytes per entry, less than
+// fp64 U); R and W are sliced every sweep. Operand tiles are stored in the
 // UMMA canonical K-major no-swizzle layout, so one bulk copy (cp.async.bulk)
 // moves a whole stage into shared memory and the MMA descriptors address it
 // directly. Accumulators live in TMEM: 8 weights x 64 columns = all 512 columns.
@@ -38,7 +39,9 @@
 
 namespace fsa {
 
-constexpr int kOzSlices = 8;
+constexpr int kOzSlices = 7;   // digit planes per operand (balanced base 256)
+constexpr int kOzMaxW = 9;     // largest kept weight a + b
+constexpr int kOzWeights = kOzMaxW - 1;  // TMEM accumulators: weights 2 .. 9
 constexpr int kOzCols = 64;  // RHS columns per accumulator (t_pad <= 64)
 constexpr int kOzPairCols = 96;  // widest block of the paired passes (two column tiles of <= 48)
 
