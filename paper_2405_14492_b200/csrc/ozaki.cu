@@ -8,7 +8,7 @@
 namespace fsa {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kStages = 4;  // (a fifth 42 KB stage measured no faster)
 constexpr int kKb = 32;                            // K bytes per stage = one kind::i8 MMA
 constexpr int kATile = kOzSlices * 128 * kKb;      // 28 KB: 7 planes x 128 rows x 32 K
 constexpr int kBTile = kOzSlices * kOzCols * kKb;  // 14 KB: 7 planes x 64 cols x 32 K
@@ -336,10 +336,14 @@ constexpr int kXStages = 3;
 constexpr int kXLd = kOzCols + 1;  // odd stride: conflict-free row-per-lane access
 constexpr int kXSmem = kXStages * (kATile + kBTile) + 128 * kXLd * 8;
 constexpr int kXEpi = 512;  // epilogue threads: four warps per TMEM lane quadrant, 16 columns each
-template <bool PAIRED>
+// the sweep's Woodbury pass (mode 1, <= 56 columns): a 57-double staging stride leaves room for a
+// fourth pipeline stage (4 x 42 KB + 57 KB)
+constexpr int kXStages4 = 4, kXLd56 = 57;
+constexpr int kXSmem4 = kXStages4 * (kATile + kBTile) + 128 * kXLd56 * 8;
+template <bool PAIRED, int STAGES = kXStages, int LDY = kXLd>
 __global__ void __launch_bounds__(64 + kXEpi, 1)
     k_oz_expand(const int8_t* __restrict__ A, OzPair pr, int tiles, int mkb) {
-  constexpr int kStages = kXStages;
+  constexpr int kStages = STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull, tempty;
   __shared__ uint32_t tmem_base_s;
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kATile;
-  double* tileY = reinterpret_cast<double*>(smem + kStages * (kATile + kBTile));  // [128][kXLd]
+  double* tileY = reinterpret_cast<double*>(smem + kStages * (kATile + kBTile));  // [128][LDY]
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
         double y[8];
         drain8(trow, c0, y, NC);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) tileY[row * kXLd + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
+        for (int c = 0; c < 8; ++c) tileY[row * LDY + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
       }
       tc_fence_before();
       __syncwarp();
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
           const long i = r0 + et;
           double s1 = 0.0, s2 = 0.0;
           for (int c = 0; c < tp; ++c) {
-            const double yv = tileY[et * kXLd + c];
+            const double yv = tileY[et * LDY + c];
             s1 = fma(yv, __ldg(epi.R + i * epi.ld + c), s1);
             s2 = fma(yv, __ldg(epi.A2 + i * epi.ld + c), s2);
           }
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int rr = rb + kPh * u;
-            lw[u] = tileY[rr * kXLd + c];
+            lw[u] = tileY[rr * LDY + c];
             if (epi.mode == 1) {
               x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
               di[u] = __ldg(epi.Dinv + r0 + rr);
@@ -491,13 +495,13 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
             }
           }
         }
-        if (epi.mode == 1) tileY[h * kXLd + c] = sacc;  // (row h, column c) was read only by this thread
+        if (epi.mode == 1) tileY[h * LDY + c] = sacc;  // (row h, column c) was read only by this thread
       }
       if (epi.mode == 1) {
         asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");
         if (h == 0 && c < tp) {  // fixed order over the row phases
           double sum = tileY[c];
-          for (int ph = 1; ph < kPh; ++ph) sum += tileY[ph * kXLd + c];
+          for (int ph = 1; ph < kPh; ++ph) sum += tileY[ph * LDY + c];
           epi.part[static_cast<long>(t) * tp + c] = sum;
         }
       }
@@ -718,11 +722,21 @@ void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const i
     FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
     attr = true;
   }
+  static bool attr4 = false;
+  if (!attr4) {
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<false, kXStages4, kXLd56>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kXSmem4));
+    attr4 = true;
+  }
   const int grid = std::min(p.ptiles, kNumSMs);
   const int8_t* B = Ws != nullptr ? Ws : p.Ws.get();
   OzPair pr{{B, B}, {epi, epi}};
-  launch_pdl(k_oz_expand<false>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()), pr,
-             p.ptiles, p.mkb);
+  if (epi.mode == 1 && epi.tp <= kXLd56 - 1)
+    launch_pdl(k_oz_expand<false, kXStages4, kXLd56>, dim3(grid), dim3(64 + kXEpi), kXSmem4, s,
+               static_cast<const int8_t*>(p.Ac.get()), pr, p.ptiles, p.mkb);
+  else
+    launch_pdl(k_oz_expand<false>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()),
+               pr, p.ptiles, p.mkb);
   FSA_LAUNCH_CHECK();
 }
 void launch_expand_pair(const OzakiPlan& p, const OzPair& pr, cudaStream_t s) {

@@ -1,0 +1,5 @@
+# 4-stage expansion for the sweep's Woodbury pass; 5-stage projection
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider 2>&1 | tail -2
+timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-dmma-arm --e2e-steps 0 > gpurun_out/b54.json 2>/dev/null; python -c "
+import json;d=json.loads(open('gpurun_out/b54.json').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],3), d['nll'], [(e['kernel'][:10], round(e['avg_launch_ms'],4), round(e['frac'],3)) for e in d['roofline']['all']])"
+WHICH=1 TAG=proj python tools/spmm_ab.py; WHICH=2 TAG=expand python tools/spmm_ab.py
