@@ -667,17 +667,24 @@ __global__ void __launch_bounds__(128) k_oz_planes_w(const double* __restrict__ 
 #pragma unroll
   for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
 }
-// S[r][c] = sum_chunk part[chunk][r][c] (fixed order)
+// S[r][c] = sum_chunk part[chunk][r][c] in a fixed order: four lanes per entry each add a
+// contiguous quarter of the chunks (all its loads in flight), then the quarters in order
 __global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long mp, long ld, long tp,
                             double* __restrict__ S) {
   pdl_wait();
-  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= mp * tp) return;
-  const long r = idx / tp, c = idx % tp;
+  const long idx = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 2;
+  const int qp = threadIdx.x & 3;
+  const bool ok = idx < mp * tp;
+  const long r = ok ? idx / tp : 0, c = ok ? idx % tp : 0;
+  const int per = (nchunks + 3) / 4, q0 = qp * per, q1 = min(nchunks, q0 + per);
   double sacc = 0.0;
-#pragma unroll 8  // (loads of eight chunks in flight; the additions keep the fixed chunk order)
-  for (int q = 0; q < nchunks; ++q) sacc += part[(static_cast<long>(q) * mp + r) * kOzCols + c];
-  S[r * ld + c] = sacc;
+  if (ok) {
+#pragma unroll 16
+    for (int q = q0; q < q1; ++q) sacc += part[(static_cast<long>(q) * mp + r) * kOzCols + c];
+  }
+  const double s1 = __shfl_down_sync(0xffffffffu, sacc, 1), s2 = __shfl_down_sync(0xffffffffu, sacc, 2),
+               s3 = __shfl_down_sync(0xffffffffu, sacc, 3);
+  if (ok && qp == 0) S[r * ld + c] = ((sacc + s1) + s2) + s3;
 }
 
 void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nkb_all, int kb_per_chunk,
@@ -769,8 +776,8 @@ void project_impl(OzakiPlan& p, const double* V, long ld, long tp, const double*
   slice_y(p, V, ld, tp, scale, p.ymax.get(), p.f.get(), p.Ys.get(), s, ymax_ready);
   OzEpi epi{0, p.m_pad, tp, ld, p.er.get(), p.f.get(), p.part.get(), nullptr, nullptr, nullptr, nullptr};
   launch_gemm(p.Ar.get(), p.Ys.get(), p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, epi, s);
-  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * tp, 256))), dim3(256), 0, s, p.part.get(), p.nchunks, p.m_pad, ld, tp,
-             S);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(4 * p.m_pad * tp, 256))), dim3(256), 0, s, p.part.get(),
+             p.nchunks, p.m_pad, ld, tp, S);
   FSA_LAUNCH_CHECK();
 }
 
@@ -877,11 +884,11 @@ void ozaki_project_pair(OzakiPlan& p, const double* R, long ld, long ncols, cons
              OzEpi{0, p.m_pad, n1, ld, p.er.get(), p.f2.get(), p.part2.get(), nullptr, nullptr, nullptr, nullptr}},
             nc};
   launch_gemm_pair(p.Ar.get(), pr, p.mtiles, p.nchunks, p.nkb, p.kb_per_chunk, s);
-  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * n0, 256))), dim3(256), 0, s, p.part.get(), p.nchunks, p.m_pad, ld, n0,
-             S);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(4 * p.m_pad * n0, 256))), dim3(256), 0, s, p.part.get(),
+             p.nchunks, p.m_pad, ld, n0, S);
   FSA_LAUNCH_CHECK();
-  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(p.m_pad * n1, 256))), dim3(256), 0, s, p.part2.get(), p.nchunks, p.m_pad, ld, n1,
-             S + n0);
+  launch_pdl(k_oz_reduce, dim3(static_cast<unsigned>(cdiv(4 * p.m_pad * n1, 256))), dim3(256), 0, s, p.part2.get(),
+             p.nchunks, p.m_pad, ld, n1, S + n0);
   FSA_LAUNCH_CHECK();
 }
 void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, double* Z, double* Lw, const double* R,
