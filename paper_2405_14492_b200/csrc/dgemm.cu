@@ -1,6 +1,8 @@
 // Launchers for the DMMA fp64 GEMMs declared in dgemm.cuh.
 #include "dgemm.cuh"
 
+#include <algorithm>
+
 #include <cstdlib>
 
 namespace fsa {
@@ -237,12 +239,33 @@ __global__ void k_mirror_lower(double* A, long ld, long m) {
 }
 }  // namespace
 
+static int syrk_waves() {
+  static const int v = knob("FSA_SYRK_WAVES", 3);  // 1: 2.47 ms, 2: 1.31, 3: 1.27 (config 2)
+  return v;
+}
+// only the lower-triangle tiles work (the rest exit at once): split K so that they fill whole waves
+static ReducePlan plan_syrk(long Mr, long K) {
+  ReducePlan p = plan_reduce(Mr, Mr, K);
+  const long rt = Mr / p.bm, ct = Mr / (p.nt * 8), per = p.nt * 8;
+  long active = 0;
+  for (long r = 0; r < rt; ++r)
+    for (long c = 0; c < ct; ++c) active += (c * per < (r + 1) * p.bm) ? 1 : 0;
+  long splits = std::max<long>(1, syrk_waves() * kNumSMs / std::max<long>(active, 1));
+  splits = std::min<long>(splits, std::max<long>(1, K / 16));
+  p.kchunk = round_up(cdiv(K, splits), 16);
+  p.splits = cdiv(K, p.kchunk);
+  return p;
+}
+size_t gemm_syrk_scratch(long Mr, long K) {
+  const ReducePlan p = plan_syrk(Mr, K);
+  return static_cast<size_t>(p.splits * Mr * Mr);
+}
 void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, double* out, long ldo, double alpha,
                double* scratch, cudaStream_t s) {
   require(Mr % 128 == 0 && K % 16 == 0, "gemm_syrk: unpadded shape");
   if (Mr == 0) return;
   const long N = Mr;
-  const ReducePlan p = plan_reduce(Mr, N, K);
+  const ReducePlan p = plan_syrk(Mr, K);
   dim3 grid(static_cast<unsigned>(Mr / p.bm), static_cast<unsigned>(N / (p.nt * 8)), static_cast<unsigned>(p.splits));
   if (p.bm == 128)
     dispatch_nt<ReduceCfg8>(p.nt, M, ldm, M, ldm, scale, K, p.kchunk, grid, EpiPartialLower{scratch, Mr, N}, s);

@@ -344,7 +344,9 @@ void gemm_km(const double* A, long lda, long Mr, long K, const double* B, long l
 void gemm_reduce(const double* M, long ldm, long Mr, long K, const double* V, long ldv, long N,
                  const double* scale, double* out, long ldo, double alpha, double beta, double* scratch,
                  cudaStream_t s);
-// symmetric variant (V = M, N = Mr): out = alpha M diag(s) M^T, lower tiles computed and mirrored
+// symmetric variant (V = M, N = Mr): out = alpha M diag(s) M^T, lower tiles computed and mirrored;
+// scratch holds gemm_syrk_scratch(Mr, K) doubles
+size_t gemm_syrk_scratch(long Mr, long K);
 void gemm_syrk(const double* M, long ldm, long Mr, long K, const double* scale, double* out, long ldo, double alpha,
                double* scratch, cudaStream_t s);
 

@@ -559,7 +559,7 @@ FitcPrecond::FitcPrecond(Model* m, bool with_derivs) : md(m), derivs(with_derivs
   Qinv.alloc(mp * mp);
   // Q = I + U D^{-1} U^T  (= L^{-1} core L^{-T}, preconditioners.cpp:49)
   {
-    const size_t need = gemm_reduce_scratch(mp, mp, np);
+    const size_t need = gemm_syrk_scratch(mp, np);
     if (md->red_scratch.n < need) md->red_scratch.alloc(need);
     KTimer tq(md->ctx, "setup_fitc_syrk", 1.0 * mp * mp * np);
     // DMMA SYRK (lower half + mirror): the full-matrix INT8 alternative (ozaki_project_wide over
