@@ -438,9 +438,11 @@ void Model::build_rho_derivs(cudaStream_t s, double* trsm_scratch, bool side) {
   }
   {
     KTimer t2(side ? nullptr : ctx, "rho_T_gemm", 2.0 * m * m * n);
-    if (!side && ctx->gemm_mode != 1 && ne == np) {  // INT8 tensor cores, 64-column tiles of K2
-      ensure_ozaki();
-      ozaki_expand_sub(oz, K2.get(), mp, U1.get(), T.get(), mp, s);
+    if (ctx->gemm_mode != 1 && ne == np && (!side || (oz.ready && oz.U == U.get()))) {
+      // INT8 tensor cores, 64-column tiles of K2; on the side stream the digit planes of U were
+      // queued on this same stream (start_ozaki) and the W planes use the side buffers
+      if (!side) ensure_ozaki();
+      ozaki_expand_sub(oz, K2.get(), mp, U1.get(), T.get(), mp, s, side);
     } else {
       FSA_CUDA(cudaMemcpyAsync(T.get(), U1.get(), sizeof(double) * mp * ne, cudaMemcpyDeviceToDevice, s));
       gemm_expand_store(U.get(), mp, ne, mp, K2.get(), mp, mp, T.get(), mp, -1.0, 1.0, s);

@@ -909,12 +909,19 @@ void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, 
   colsum_partials(partial, p.ptiles, n0, n0, rz, s);
   colsum_partials(part2, p.ptiles, n1, n1, rz + n0, s);
 }
-void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s) {
+void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s,
+                      bool side_buffers) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
+  if (side_buffers) {  // own W-plane buffers: the main stream's sweeps keep rewriting p.Ws / p.h
+    if (p.Ws_side.n < p.Ws.n) p.Ws_side.alloc(p.Ws.n);
+    if (p.h_side.n < p.h.n) p.h_side.alloc(p.h.n);
+  }
+  int8_t* Ws = side_buffers ? p.Ws_side.get() : p.Ws.get();
+  int* h = side_buffers ? p.h_side.get() : p.h.get();
   for (long j = 0; j < ldw; j += kOzCols) {
-    slice_w(p, W + j, ldw, kOzCols, s);
-    OzEpi epi{3, p.m_pad, kOzCols, ld, p.ec.get(), p.h.get(), nullptr, nullptr, Y + j, A + j, nullptr};
-    launch_expand(p, epi, s);
+    slice_w_to(p, W + j, ldw, kOzCols, Ws, h, s);
+    OzEpi epi{3, p.m_pad, kOzCols, ld, p.ec.get(), h, nullptr, nullptr, Y + j, A + j, nullptr};
+    launch_expand(p, epi, s, Ws);
   }
 }
 void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,

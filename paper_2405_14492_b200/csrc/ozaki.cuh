@@ -97,7 +97,8 @@ void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, 
 //   Y = A - U^T W            (W m_pad x ldw, A / Y n_pad x ld)
 //   q[i] = (U^T W)_i . B1_i, f[i] = (U^T W)_i . B2_i   (row dots, B1 / B2 n_pad x ld)
 //   S = U diag(scale) V      (V n_pad x ldv, S m_pad x lds)
-void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s);
+void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s,
+                      bool side_buffers = false);  // side_buffers: own W-plane buffers (side-stream passes)
 void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
                           double* q, double* f, cudaStream_t s, bool side_buffers = false);
 void ozaki_project_wide(OzakiPlan& p, const double* V, long ldv, const double* scale, double* S, long lds,
