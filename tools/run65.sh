@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider 2>&1 | tail -2
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_potrf_panel -c 8 python tools/spmm_one.py 0 2>&1 | grep "duration" | head -8
+timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-dmma-arm --e2e-steps 0 > gpurun_out/b65.json 2>/dev/null; python -c "
+import json;d=json.loads(open('gpurun_out/b65.json').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],3), d['nll'], d['timers_ms']['setup_fitc'], d['timers_ms']['setup_sigma_m'])"

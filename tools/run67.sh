@@ -1,0 +1,5 @@
+TAG=pairs python tools/spmm_ab.py
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_block_gram -c 1 python tools/spmm_one.py 0 2>&1 | grep "duration" | head -2
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider 2>&1 | tail -1
+for i in 1 2; do timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-dmma-arm --e2e-steps 0 > gpurun_out/b67.json 2>/dev/null; python -c "
+import json;d=json.loads(open('gpurun_out/b67.json').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],3), d['nll'], d['timers_ms']['setup_sddmm'], d['clocks']['sm_mhz'], [(e['kernel'][:10], round(e['avg_launch_ms'],4)) for e in d['roofline']['all']])"; done
