@@ -190,8 +190,8 @@ int fsa_model_lowrank_expand(fsa_model* md, const double* W, int64_t k, double* 
 int fsa_model_diagonals(fsa_model* md, double* sigma_s_diag, double* lowrank_diag);
 /* Diagnostics (no reference counterpart): average device time of one launch group of a PCG
  * sweep kernel on synthetic k-column blocks — which 0: block SpMM + direction update
- * (k_spmm_rt), 1: Ozaki projection, 2: Ozaki expansion + Woodbury epilogue; flags (which = 0):
- * 1 skip the DMMAs, 2 skip the epilogue, 4 skip the RHS-row gather, 8 skip the value tiles. */
+ * (k_spmm_v3), 1: Ozaki projection, 2: Ozaki expansion + Woodbury epilogue; flags must be 0
+ * (the round-2 component switches were removed with the kernel they instrumented). */
 int fsa_debug_kernel_bench(fsa_model* md, int which, int64_t k, int reps, int flags, double* ms_out);
 
 /* ---- preconditioners (make_preconditioner, estimation.h:81-82; preconditioners.h) -- */
