@@ -776,29 +776,55 @@ void axpby(double* Y, const double* X, double a, double b, long len, cudaStream_
 // then thread 0 of column c < k runs that column's control step: MODE 0 alpha (k_cg_alpha),
 // MODE 1 the residual test (k_cg_check), MODE 2 beta (k_cg_beta) followed, in the last block to
 // finish, by the active count for the host (k_cg_count; `ticket` is reset for the next call).
-template <int MODE>
-__global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ partial, long nb, long ldp,
-                                                    double* __restrict__ out, long k, int it, int max_iter,
-                                                    double tol, CgState st, unsigned int* ticket,
-                                                    unsigned long long* __restrict__ zero_buf, long zero_len) {
-  __shared__ double red[8];
-  __shared__ bool last;
-  pdl_wait();
-  const long c = blockIdx.x;
+// MODE 3 = MODE 1 on `partial` followed by MODE 2 on `partial_b` (the residual test deferred to
+// the end of the sweep: one launch fewer; nothing between them reads the convergence flags)
+__device__ __forceinline__ double block_colsum(const double* __restrict__ partial, long nb, long ldp, long c,
+                                               double (&red)[8]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // (MODE 0) clear the next kernel's column-maxima accumulators on the way
-  for (long i = c * blockDim.x + tid; i < zero_len; i += static_cast<long>(gridDim.x) * blockDim.x) zero_buf[i] = 0ull;
   double sacc = strided_colsum(partial, nb, ldp, c);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
   if (lane == 0) red[warp] = sacc;
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
+  double t = 0.0;
+  if (tid == 0)
     for (int w = 0; w < 8; ++w) t += red[w];
+  __syncthreads();  // (red reused)
+  return t;
+}
+template <int MODE>
+__global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ partial, long nb, long ldp,
+                                                    double* __restrict__ out, long k, int it, int max_iter,
+                                                    double tol, CgState st, unsigned int* ticket,
+                                                    unsigned long long* __restrict__ zero_buf, long zero_len,
+                                                    const double* __restrict__ partial_b, long nb_b, long ldp_b,
+                                                    double* __restrict__ out_b) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  pdl_wait();
+  const long c = blockIdx.x;
+  const int tid = threadIdx.x;
+  // clear the next kernel's column-maxima accumulators on the way
+  for (long i = c * blockDim.x + tid; i < zero_len; i += static_cast<long>(gridDim.x) * blockDim.x) zero_buf[i] = 0ull;
+  const double t0 = block_colsum(partial, nb, ldp, c, red);
+  const double tb = MODE == 3 ? block_colsum(partial_b, nb_b, ldp_b, c, red) : 0.0;
+  if (tid == 0) {
+    double t = t0;
     out[c] = t;
     const long j = c;
     if (st.it_dev != nullptr) it = *st.it_dev;
+    if (MODE == 3 && j < k && st.active[j]) {  // residual test first (krylov.cpp:77-82)
+      const double rn = sqrt(t);
+      st.rnorm[j * max_iter + it] = rn;
+      if (rn < tol) {
+        st.converged[j] = 1;
+        st.active[j] = 0;
+      }
+    }
+    if (MODE == 3) {
+      t = tb;
+      out_b[c] = t;
+    }
     if (j < k) {
       if (MODE == 0) {  // alpha = rz / h'v, tridiagonal push (krylov.cpp:66-75)
         if (!st.active[j]) {
@@ -822,7 +848,7 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
             st.active[j] = 0;
           }
         }
-      } else {  // beta = rz_new / rz (krylov.cpp:83-90)
+      } else {  // MODE 2 / 3: beta = rz_new / rz (krylov.cpp:83-90)
         if (!st.active[j]) {
           st.beta[j] = 0.0;
         } else if (!(t > 0.0)) {
@@ -837,12 +863,12 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
         }
       }
     }
-    if (MODE == 2) {
+    if (MODE >= 2) {
       __threadfence();
       last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
   }
-  if (MODE == 2) {
+  if (MODE >= 2) {
     __syncthreads();
     if (last) {  // block-uniform: the whole last block counts the active columns
       __threadfence();
@@ -867,22 +893,20 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
 }
 void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, double* out, long k, int it,
                 int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s,
-                unsigned long long* zero_buf, long zero_len) {
+                unsigned long long* zero_buf, long zero_len, const double* partial_b, long nb_b, long ldp_b,
+                double* out_b) {
   require(t >= k && t > 0, "colsum_ctl: fewer sums than columns");
+  require(mode != 3 || (partial_b != nullptr && out_b != nullptr), "colsum_ctl: mode 3 needs the second sums");
   const unsigned g = static_cast<unsigned>(t);
+  auto go = [&](auto kern) {
+    launch_pdl(kern, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket, zero_buf,
+               zero_len, partial_b, nb_b, ldp_b, out_b);
+  };
   switch (mode) {
-    case 0:
-      launch_pdl(k_colsum_ctl<0>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
-                 zero_buf, zero_len);
-      break;
-    case 1:
-      launch_pdl(k_colsum_ctl<1>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
-                 zero_buf, zero_len);
-      break;
-    default:
-      launch_pdl(k_colsum_ctl<2>, dim3(g), dim3(256), 0, s, partial, nb, ldp, out, k, it, max_iter, tol, st, ticket,
-                 zero_buf, zero_len);
-      break;
+    case 0: go(k_colsum_ctl<0>); break;
+    case 1: go(k_colsum_ctl<1>); break;
+    case 2: go(k_colsum_ctl<2>); break;
+    default: go(k_colsum_ctl<3>); break;
   }
   FSA_LAUNCH_CHECK();
 }

@@ -75,7 +75,9 @@ long xr_dot_max_blocks(long n);  // partial rows (ld k) left in scratch when col
 // (cg_beta, cg_count; `ticket` is a zeroed device counter, left zero)
 void colsum_ctl(int mode, const double* partial, long nb, long ldp, long t, double* out, long k, int it,
                 int max_iter, double tol, const CgState& st, unsigned int* ticket, cudaStream_t s,
-                unsigned long long* zero_buf = nullptr, long zero_len = 0);  // zero_buf[0, zero_len) := 0
+                unsigned long long* zero_buf = nullptr, long zero_len = 0,  // zero_buf[0, zero_len) := 0
+                const double* partial_b = nullptr, long nb_b = 0, long ldp_b = 0,  // mode 3: the r.z sums
+                double* out_b = nullptr);  // zero_buf[0, zero_len) := 0
 // Jacobi PCG without a Z block: X += alpha H, R -= alpha V, rr = |R|^2, rz = R' diag(dinv) R;
 // scratch holds 2 * coldot_scratch(n, k) doubles
 void update_xr_dot_jacobi(double* X, double* R, const double* H, const double* V, const double* alpha,

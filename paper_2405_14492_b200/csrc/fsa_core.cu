@@ -892,6 +892,9 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
     w.tick.alloc(1);
     w.tick.zero(s);
     w.wmax.alloc(kOzCols);
+    w.wmax.zero(s);  // (then cleared by the end-of-sweep control kernel for the next sweep)
+    const size_t nrr = static_cast<size_t>(xr_dot_max_blocks(n) * tp);
+    if (w.part_rr.n < nrr) w.part_rr.alloc(nrr);
   }
   bool ymax_ready = false;
   // Z = P^{-1} R (+ r.z); fused path also leaves w = Q^{-1} U D^{-1} R in mt_buf(1)
@@ -1067,8 +1070,8 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
           cg_alpha(hv, k, it, maxit, st, s);
         if (oz) {
           if (!ctl) FSA_CUDA(cudaMemsetAsync(md->oz.ymax.get(), 0, md->oz.ymax.bytes(), s));
-          update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, md->Dinv.get(),
-                            md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl || multi);
+          update_xr_dot_max(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, ctl ? w.part_rr.get() : part,
+                            md->Dinv.get(), md->oz.ymax.get(), ozaki_chunk_rows(md->oz), s, !ctl || multi);
           ymax_ready = true;
         } else if (jfused) {
           update_xr_dot_jacobi(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, md->Dinv.get(), n, tp, k, rr, rz, part,
@@ -1077,18 +1080,15 @@ CgResult pcg_solve_multi(Model* md, LinOp& A, Precond& P, const double* B, long 
           update_xr_dot(X, w.R.get(), w.H.get(), w.V.get(), st.alpha, n, tp, k, rr, part, s);
         }
         comm.allreduce(rr, k, s);
-        if (ctl)  // residual test, and the wmax clear of this sweep's core solve
-          colsum_ctl(1, multi ? rr : part, multi ? 1 : xr_dot_max_blocks(n), k, k, rr, k, it, maxit, opts.tol, st,
-                     w.tick.get(), s, w.wmax.get(), kOzCols);
-        else
-          cg_check(rr, k, opts.tol, it, maxit, st, s);
+        if (!ctl) cg_check(rr, k, opts.tol, it, maxit, st, s);  // (fused: at the end of the sweep)
       }
       if (!jfused) precond(rz, !ctl || multi);
       {
         KTimer t(ctx, "cg_blas1");
-        if (ctl)  // beta and the active count
-          colsum_ctl(2, multi ? rz : part, multi ? 1 : md->oz.ptiles, tp, tp, rz, k, it, maxit, 0.0, st,
-                     w.tick.get(), s);
+        if (ctl)  // residual test, beta and the active count; clears wmax for the next core solve
+          colsum_ctl(3, multi ? rr : w.part_rr.get(), multi ? 1 : xr_dot_max_blocks(n), k, k, rr, k, it, maxit,
+                     opts.tol, st, w.tick.get(), s, w.wmax.get(), kOzCols, multi ? rz : part,
+                     multi ? 1 : md->oz.ptiles, tp, rz);
         else
           cg_beta(rz, k, st, s);
         if (fuse_h) {

@@ -28,6 +28,7 @@ namespace fsa {
 // PCG workspace (owned by the context so it is released before the stream)
 struct CgWork {
   DBuf<double> R, H, V, Z, Lw, Vlr, dots, dbl, part;
+  DBuf<double> part_rr;  // residual-update partials kept to the end of the sweep (fused control path)
   DBuf<int> ints;
   DBuf<double> tri;
   DBuf<unsigned int> tick;  // last-block counter of the fused control kernels
