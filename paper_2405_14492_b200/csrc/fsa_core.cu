@@ -469,8 +469,14 @@ void Model::build_rho_derivs(cudaStream_t s, double* trsm_scratch, bool side) {
 
 void Model::sigma_s_mat(const double* H, double* V, long tp, double alpha, double beta) {
   KTimer t(ctx, "spmm", 12.0 * geo->pat.nnz + (beta == 0.0 ? 16.0 : 24.0) * n * (cols_hint > 0 ? cols_hint : tp));
-  launch_spmm(geo->pat.rowptr.get(), geo->pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta,
-              ctx->stream);
+  const Csr& pat = geo->pat;
+  if (alpha == 1.0 && beta == 0.0 && pat.gnnz > 0 && gval.n > 0 && spmm_block_supported(tp)) {
+    // V = Sigma_s H on the DMMA block SpMM (the h.v partials it also forms are not used)
+    DBuf<double> dots(static_cast<size_t>(tp)), part(static_cast<size_t>(spmm_group_blocks(pat.ngrp) * tp));
+    spmm_block_dot(pat, gval.get(), H, tp, V, tp, tp, dots.get(), part.get(), nullptr, ctx->stream);
+    return;
+  }
+  launch_spmm(pat.rowptr.get(), pat.col.get(), sval.get(), n, H, tp, V, tp, tp, alpha, beta, ctx->stream);
 }
 
 // V = Sigma H = U^T (U H) + Sigma_s H   (fsa.cpp:65-68)
@@ -678,6 +684,13 @@ void FitcPrecond::solve(const double* R, double* Z, long tp) {
     gemm_km(Qinv.get(), md->m_pad, md->m_pad, md->m_pad, S, tp, tp, W, tp, 1.0, 0.0, s);
   }
   KTimer t(md->ctx, "lowrank_expand", 2.0 * md->m_pad * md->n_pad * tp);
+  if (md->use_ozaki(tp) && md->world() == 1) {  // INT8 expansion with the Woodbury epilogue
+    md->ensure_ozaki();
+    DBuf<double> lw(static_cast<size_t>(md->n_pad * tp)), rz(static_cast<size_t>(tp)),
+        part(static_cast<size_t>(md->oz.ptiles * tp));
+    ozaki_expand_keep(md->oz, W, tp, tp, Z, lw.get(), R, md->Dinv.get(), rz.get(), part.get(), s, false);
+    return;
+  }
   gemm_expand_woodbury(md->U.get(), md->m_pad, md->n_pad, md->m_pad, W, tp, tp, Z, R, tp, md->Dinv.get(), s);
 }
 
