@@ -627,11 +627,13 @@ def main():
     e2e_value = results[-1]["rhs_iterations"] * copies / (e2e_step_ms * 1e-3) if e2e_ms else None
     k = L + 1
     mp_ = 128 * math.ceil(m / 128)
-    # per rank: coordinates (n x 2), inducing points (m x 2), y (n), the FITC probe draws e1
-    # (m_pad x t_pad staged) and e2 (n_rank x L); back: nll, grad, logdet, beta and the
-    # Lanczos coefficients of its columns
+    # per rank: coordinates (n x 2), inducing points (m x 2), y (n) -- the FITC probe draws are
+    # generated on the device (k_probe_gaussian, round 2; FSA_HOST_PROBES=1 uploads the host draws:
+    # + m_pad x t_pad + n_rank x L doubles); back: nll, grad, logdet, beta and the Lanczos
+    # coefficients of its columns
     n_rank = n // world if sharded else n
-    h2d = 8 * world * (n * 2 + m * 2 + n + mp_ * tp_ + n_rank * L)
+    host_probes = os.environ.get("FSA_HOST_PROBES") is not None
+    h2d = 8 * world * (n * 2 + m * 2 + n + ((mp_ * tp_ + n_rank * L) if host_probes else 0))
     d2h = 8 * world * (5 + 3 * k * results[-1]["sweeps"] + 2 * k)
 
     cpu = None

@@ -37,6 +37,105 @@ void probe_gaussian(unsigned long long seed, unsigned long long i, long n1, doub
     for (long j = 0; j < n2; ++j) e2[j] = N01(rng);
   }
 }
+// probe_gaussian on the device, one CTA per probe: the same MT19937-64 stream (seeding, twist in
+// two parallel halves, tempering), generate_canonical<double, 53> (one 64-bit draw per uniform)
+// and libstdc++'s polar normal_distribution: draws are consumed in pairs, a pair is accepted when
+// 0 < x^2 + y^2 <= 1 and yields y m then x m (m = sqrt(-2 log r2 / r2)); a fresh distribution per
+// vector, so e1 takes the first ceil(n1 / 2) accepted pairs and e2 the following ones. The
+// products, sums and quotients are issued unfused and correctly rounded like the host's (SSE, no
+// FMA); log is CUDA's (<= 1 ulp, the host's glibc < 0.52 ulp), so a draw can differ from the host's
+// in its last bit. e1 goes to E1[r * ld1 + i] (r < n1), e2 to E2[i * n2 + r].
+namespace {
+__device__ __forceinline__ unsigned long long splitmix64_d(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+constexpr int kMtN = 312, kMtM = 156;
+__global__ void __launch_bounds__(320) k_probe_gaussian(unsigned long long seed, long n1, long ld1, double* E1, long n2,
+                                                        double* E2) {
+  __shared__ unsigned long long mt[kMtN];
+  __shared__ double us[kMtN];
+  __shared__ int wsum[10];  // (320 threads)
+  const unsigned long long i = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr unsigned long long kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL, kA = 0xB5026F5AA96619E9ULL;
+  if (tid == 0) {
+    unsigned long long x = splitmix64_d(splitmix64_d(seed) ^ splitmix64_d(i + 0x51ed2701ULL));
+    mt[0] = x;
+    for (int k = 1; k < kMtN; ++k) {
+      x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(k);
+      mt[k] = x;
+    }
+  }
+  __syncthreads();
+  const long p1 = (n1 + 1) / 2, ptot = p1 + (n2 + 1) / 2;
+  long done = 0;
+  while (done < ptot) {
+    unsigned long long a0 = 0, a1 = 0, b = 0;
+    if (tid < kMtM) a0 = mt[tid], a1 = mt[tid + 1], b = mt[tid + kMtM];
+    __syncthreads();
+    if (tid < kMtM) {
+      const unsigned long long y = (a0 & kUpper) | (a1 & kLower);
+      mt[tid] = b ^ (y >> 1) ^ ((y & 1ULL) ? kA : 0ULL);
+    }
+    __syncthreads();
+    const int k2 = kMtM + tid;
+    if (tid < kMtM) a0 = mt[k2], a1 = k2 + 1 < kMtN ? mt[k2 + 1] : mt[0], b = mt[k2 - kMtM];
+    __syncthreads();
+    if (tid < kMtM) {
+      const unsigned long long y = (a0 & kUpper) | (a1 & kLower);
+      mt[k2] = b ^ (y >> 1) ^ ((y & 1ULL) ? kA : 0ULL);
+    }
+    __syncthreads();
+    if (tid < kMtN) {
+      unsigned long long z = mt[tid];
+      z ^= (z >> 29) & 0x5555555555555555ULL;
+      z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+      z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+      z ^= z >> 43;
+      double u = __dmul_rn(__ull2double_rn(z), 0x1p-64);
+      if (u >= 1.0) u = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
+      us[tid] = u;
+    }
+    __syncthreads();
+    double xv = 0.0, yv = 0.0, r2 = 0.0;
+    int acc = 0;
+    if (tid < kMtM) {
+      xv = __dsub_rn(__dmul_rn(2.0, us[2 * tid]), 1.0);
+      yv = __dsub_rn(__dmul_rn(2.0, us[2 * tid + 1]), 1.0);
+      r2 = __dadd_rn(__dmul_rn(xv, xv), __dmul_rn(yv, yv));
+      acc = (r2 > 1.0 || r2 == 0.0) ? 0 : 1;
+    }
+    // exclusive rank of this pair among the accepted ones (pairs in order)
+    const unsigned bal = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < 10; ++w) {
+      before += w < warp ? wsum[w] : 0;
+      total += wsum[w];
+    }
+    const long P = done + before + __popc(bal & ((1u << lane) - 1u));
+    if (acc && P < ptot) {
+      const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+      const double v0 = __dmul_rn(yv, mult), v1 = __dmul_rn(xv, mult);
+      if (P < p1) {
+        const long r = 2 * P;
+        E1[r * ld1 + static_cast<long>(i)] = v0;
+        if (r + 1 < n1) E1[(r + 1) * ld1 + static_cast<long>(i)] = v1;
+      } else {
+        const long r = 2 * (P - p1);
+        E2[static_cast<long>(i) * n2 + r] = v0;
+        if (r + 1 < n2) E2[static_cast<long>(i) * n2 + r + 1] = v1;
+      }
+    }
+    done += total;
+    __syncthreads();  // (wsum, us and mt are rewritten by the next round)
+  }
+}
+}  // namespace
 void probe_rademacher(unsigned long long seed, unsigned long long i, long n, double* z) {
   std::mt19937_64 rng = probe_rng(seed, i);
   std::bernoulli_distribution coin(0.5);
@@ -706,6 +805,29 @@ void FitcPrecond::sample_probes(int L, unsigned long long seed, double* Z, long 
   }
   // each probe's stream draws e1 (m) then e2 over ALL n points; a rank keeps its rows of e2
   const long nf = md->geo->shard.n, r0 = md->geo->shard.r0;
+  static const bool host_probes = std::getenv("FSA_HOST_PROBES") != nullptr;
+  if (!host_probes) {  // the same streams drawn on the device (k_probe_gaussian)
+    DBuf<double> E1(mp * tp), E2(np * tp), raw(nf * L);
+    FSA_CUDA(cudaMemsetAsync(E1.get(), 0, sizeof(double) * mp * tp, s));
+    k_probe_gaussian<<<static_cast<unsigned>(L), 320, 0, s>>>(seed, m, tp, E1.get(), nf, raw.get());
+    FSA_LAUNCH_CHECK();
+    FSA_CUDA(cudaMemsetAsync(E2.get(), 0, sizeof(double) * np * tp, s));
+    pack_cols_ld(raw.get(), nf, n, L, md->geo->pts.perm_d.get() + r0, np, tp, 0, E2.get(), s);
+    {
+      KTimer t(md->ctx, "probe_expand", 2.0 * mp * np * tp);
+      gemm_expand_probe(md->U.get(), mp, np, mp, E1.get(), tp, tp, Z, tp, md->sqrtD.get(), E2.get(), s);
+    }
+    if (md->geo->cache_probes) {
+      pc.valid = true;
+      pc.seed = seed;
+      pc.L = L;
+      pc.tp = tp;
+      pc.m = m;
+      pc.E1 = std::move(E1);
+      pc.E2 = std::move(E2);
+    }
+    return;
+  }
   PinnedBuf& e1h = md->ctx->pin1;  // host staging owned by the context
   PinnedBuf& e2h = md->ctx->pin2;
   e1h.ensure(static_cast<size_t>(mp * tp));
