@@ -96,6 +96,17 @@ def test_fitc_matches_oracle():
         assert P.deriv_trace(k) == pytest.approx(OP.deriv_trace(k), rel=1e-9), k
 
 
+@pytest.mark.parametrize("n,m,L,seed", [(3001, 77, 20, 5), (1200, 50, 1, 0), (800, 33, 33, 12345)])
+def test_device_probe_streams_match_oracle(n, m, L, seed):
+    """k_probe_gaussian draws the reference's per-probe MT19937-64 / polar normal streams on the
+    device (odd m and n exercise the discarded saved value between e1 and e2): the probes
+    z = U^T e1 + sqrt(D) e2 agree with the oracle's host draws to fp64 rounding."""
+    locs, ind, kw, md, om = setup(n=n, m=m, seed=seed % 7 + 1)
+    Z = fsa.make_preconditioner(md, "fitc").sample_probes(L, seed)
+    OZ = O.Precond(om, "fitc").sample_probes(L, seed)
+    assert rel(Z, OZ) < 1e-13
+
+
 def test_pcg_matches_oracle():
     locs, ind, kw, md, om = setup(n=2000, m=64, seed=13, s2=0.1)
     P, OP = fsa.make_preconditioner(md, "fitc"), O.Precond(om, "fitc")
