@@ -65,29 +65,32 @@ __global__ void __launch_bounds__(256) k_potrf_panel(double* A, long ld, long k0
   }
   __shared__ double Ld[64];
   __syncthreads();
-  // right-looking factorisation of the 64 x 64 diagonal block by the whole block: column j
-  // is scaled, then the trailing lower triangle updated (two barriers per column)
-  for (int j = 0; j < 64; ++j) {
-    double dj = Lk[j][j];
-    if (!(dj > 0.0) || !isfinite(dj)) {
-      if (tid == 0 && !bad) bad = j + 1;
-      dj = 1.0;
-    }
-    const double ljj = sqrt(dj);
-    const double inv = 1.0 / ljj;
-    if (tid > j && tid < 64) Lk[tid][j] *= inv;
-    if (tid == j) Ld[j] = ljj;
-    __syncthreads();
-    {  // thread (r, c0) updates row r, columns c0, c0 + 4, ...: 16 independent predicated FMAs
-      const int r = tid & 63, c0 = tid >> 6;
-      const double lr = Lk[r][j];
+  // right-looking factorisation of the 64 x 64 diagonal block by the whole block, one barrier per
+  // column: every thread scales the column-j entries it needs on the fly (the same products the
+  // in-place scaling would store) and updates the trailing lower triangle; the scaled column is
+  // written back one step later, when no thread reads column j any more
+  {
+    const int r = tid & 63, c0 = tid >> 6;
+    double pending = 0.0;
+    for (int j = 0; j < 64; ++j) {
+      if (j > 0 && c0 == 0 && r > j - 1) Lk[r][j - 1] = pending;
+      double dj = Lk[j][j];
+      if (!(dj > 0.0) || !isfinite(dj)) {
+        if (tid == 0 && !bad) bad = j + 1;
+        dj = 1.0;
+      }
+      const double ljj = sqrt(dj);
+      const double inv = 1.0 / ljj;
+      if (tid == j) Ld[j] = ljj;
+      const double lr = Lk[r][j] * inv;  // thread (r, c0) updates row r, columns c0, c0 + 4, ...
+      if (c0 == 0) pending = lr;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int c = c0 + 4 * i;
-        if (c > j && r >= c) Lk[r][c] = fma(-lr, Lk[c][j], Lk[r][c]);
+        if (c > j && r >= c) Lk[r][c] = fma(-lr, Lk[c][j] * inv, Lk[r][c]);
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (tid < 64) Lk[tid][tid] = Ld[tid];
   __syncthreads();
