@@ -332,6 +332,71 @@ __global__ void __launch_bounds__(256) k_core_dmma(const double* __restrict__ Qi
     }
   }
 }
+// Wider variant (m_pad % 64 == 0): 16 warps split K (m_pad / 16 each, all loads of a warp in
+// flight at once) and the column tiles are split over blockIdx.y (NTC tiles per CTA, nt here), so
+// the launch has 2 x m_pad / 8 CTAs and each warp a K chain half as long; the warps' partials are
+// added in a fixed order ((w + (w + 8)) pairs, then w = 0..7).
+template <int NTC>
+__global__ void __launch_bounds__(512) k_core_dmma16(const double* __restrict__ Qinv, long mp,
+                                                    const double* __restrict__ S, long ld, int nt_all,
+                                                    double* __restrict__ W, unsigned long long* __restrict__ wmax) {
+  __shared__ double red[8][8][NTC * 8];
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j0 = blockIdx.y * NTC, nt = min(NTC, nt_all - j0);
+  const long r0 = static_cast<long>(blockIdx.x) * 8;
+  const long kper = mp / 16, k0 = warp * kper;
+  double c[NTC][2];
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) c[j][0] = c[j][1] = 0.0;
+  const double* ap = Qinv + (r0 + (lane >> 2)) * mp + (lane & 3);
+  const double* bp = S + static_cast<long>(lane & 3) * ld + (lane >> 2) + j0 * 8;
+#pragma unroll 8
+  for (long k = k0; k < k0 + kper; k += 4) {
+    const double a = __ldg(ap + k);
+    double b[NTC];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) b[j] = j < nt ? __ldg(bp + k * ld + j * 8) : 0.0;
+#pragma unroll
+    for (int j = 0; j < NTC; ++j)
+      if (j < nt) dmma8x8x4(c[j][0], c[j][1], a, b[j]);
+  }
+  if (warp >= 8) {
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) {
+      red[warp - 8][lane >> 2][j * 8 + 2 * (lane & 3)] = c[j][0];
+      red[warp - 8][lane >> 2][j * 8 + 2 * (lane & 3) + 1] = c[j][1];
+    }
+  }
+  __syncthreads();
+  if (warp < 8) {
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) {
+      double* p = &red[warp][lane >> 2][j * 8 + 2 * (lane & 3)];
+      p[0] = c[j][0] + p[0];
+      p[1] = c[j][1] + p[1];
+    }
+  }
+  __syncthreads();
+  const int ncol = nt * 8;
+  for (int idx = threadIdx.x; idx < 8 * ncol; idx += blockDim.x) {
+    const int r = idx / ncol, cc = idx % ncol;
+    double acc = red[0][r][cc];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) acc += red[w][r][cc];
+    W[(r0 + r) * ld + j0 * 8 + cc] = acc;
+    red[0][r][cc] = fabs(acc);  // (this thread alone read red[*][r][cc])
+  }
+  if (wmax != nullptr) {
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < ncol; cc += blockDim.x) {
+      double mx = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) mx = fmax(mx, red[0][r][cc]);
+      if (mx > 0.0) atomicMax(wmax + j0 * 8 + cc, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    }
+  }
+}
 }  // namespace
 
 bool core_apply_supported(long mp, long ld) { return mp % 32 == 0 && ld % 8 == 0 && ld <= 72; }
@@ -340,6 +405,20 @@ void core_apply(const double* Qinv, long mp, const double* S, long ld, double* W
                 unsigned long long* wmax) {
   require(core_apply_supported(mp, ld), "core_apply: unsupported shape");
   const unsigned grid = static_cast<unsigned>(mp / 8);
+  const int nt = static_cast<int>(ld / 8);
+  if (mp % 64 == 0 && nt >= 2) {
+    const int ntc = (nt + 1) / 2;
+    const dim3 g2(grid, 2);
+    switch (ntc) {
+      case 1: launch_pdl(k_core_dmma16<1>, g2, dim3(512), 0, s, Qinv, mp, S, ld, nt, W, wmax); break;
+      case 2: launch_pdl(k_core_dmma16<2>, g2, dim3(512), 0, s, Qinv, mp, S, ld, nt, W, wmax); break;
+      case 3: launch_pdl(k_core_dmma16<3>, g2, dim3(512), 0, s, Qinv, mp, S, ld, nt, W, wmax); break;
+      case 4: launch_pdl(k_core_dmma16<4>, g2, dim3(512), 0, s, Qinv, mp, S, ld, nt, W, wmax); break;
+      default: launch_pdl(k_core_dmma16<5>, g2, dim3(512), 0, s, Qinv, mp, S, ld, nt, W, wmax); break;
+    }
+    FSA_LAUNCH_CHECK();
+    return;
+  }
   switch (ld / 8) {
     case 1: launch_pdl(k_core_dmma<1>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;
     case 2: launch_pdl(k_core_dmma<2>, grid, dim3(256), 0, s, Qinv, mp, S, ld, W, wmax); break;

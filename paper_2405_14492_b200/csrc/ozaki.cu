@@ -1,5 +1,6 @@
 // INT8 tensor-core (tcgen05) emulation of the fp64 skinny GEMMs; see ozaki.cuh.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bulk.cuh"
 #include "dgemm.cuh"
@@ -64,13 +65,15 @@ __device__ __forceinline__ double recombine8(uint32_t c2, uint32_t c3, uint32_t 
   const long long g3 = (static_cast<long long>(static_cast<int>(c8)) << 8) + static_cast<int>(c9);
   return fma(static_cast<double>(g1), 0x1p-28, fma(static_cast<double>(g2), 0x1p-52, static_cast<double>(g3) * 0x1p-68));
 }
+template <int NW = kOzWeights>  // NW = 8: weights 2..9; NW = 7: weights 2..8 (weight 9 not accumulated)
 __device__ __forceinline__ void drain16(uint32_t trow, int col0, double (&out)[16], int wstride = kOzCols) {
-  uint32_t v[kOzWeights][16];
+  uint32_t v[NW][16];
 #pragma unroll
-  for (int dd = 0; dd < kOzWeights; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
+  for (int dd = 0; dd < NW; ++dd) tmem_ld16_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int c = 0; c < 16; ++c) out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], v[7][c]);
+  for (int c = 0; c < 16; ++c)
+    out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], NW == 8 ? v[NW - 1][c] : 0u);
 }
 
 __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]) {
@@ -79,13 +82,15 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&v)[8]
                : "r"(taddr));
 }
 // drain16 for 8 columns (half the registers)
+template <int NW = kOzWeights>
 __device__ __forceinline__ void drain8(uint32_t trow, int col0, double (&out)[8], int wstride = kOzCols) {
-  uint32_t v[kOzWeights][8];
+  uint32_t v[NW][8];
 #pragma unroll
-  for (int dd = 0; dd < kOzWeights; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
+  for (int dd = 0; dd < NW; ++dd) tmem_ld8_nowait(trow + static_cast<uint32_t>(dd * wstride + col0), v[dd]);
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int c = 0; c < 8; ++c) out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], v[7][c]);
+  for (int c = 0; c < 8; ++c)
+    out[c] = recombine8(v[0][c], v[1][c], v[2][c], v[3][c], v[4][c], v[5][c], v[6][c], NW == 8 ? v[NW - 1][c] : 0u);
 }
 
 // exponent e with |x| < 2^e for all x of a group whose max magnitude is mx (0 -> 0)
@@ -120,14 +125,16 @@ __device__ __forceinline__ void digits16(const double (&v)[16], int e, int4 (&ou
   }
 }
 
-// One K step of plane-pair MMAs into the eight weight accumulators (weights a + b <= 9 of the
-// 7 x 7 digit planes: 34 products in 12 instructions of N <= 4 NC). `first` (the first K step of
-// an accumulation) overwrites instead of accumulating: weights 2..8 are first written by a = 1;
-// weight 9 by (a = 2, b = 7), which shares its instruction with weights 7 and 8 and is split off.
+// One K step of plane-pair MMAs into the weight accumulators (weights a + b <= MAXW of the 7 x 7
+// digit planes). MAXW = 9: 34 products in 12 instructions of N <= 4 NC; MAXW = 8 (the projection):
+// 28 products in 10 instructions. `first` (the first K step of an accumulation) overwrites
+// instead of accumulating: weights 2..8 are first written by a = 1; with MAXW = 9, weight 9 by
+// (a = 2, b = 7), which shares its instruction with weights 7 and 8 and is split off.
+template <int MAXW = kOzMaxW>
 __device__ __forceinline__ void ozaki_kstep(uint32_t tmem, uint32_t a0, uint32_t b0, int NC, bool first) {
 #pragma unroll
   for (int a = 1; a <= kOzSlices; ++a) {
-    const int bmax = min(kOzSlices, kOzMaxW - a);
+    const int bmax = min(kOzSlices, MAXW - a);
     const uint64_t ad = umma_desc(a0 + (a - 1) * 4096, 2048, 128);
 #pragma unroll
     for (int bs = 1; bs <= bmax; bs += 4) {
@@ -136,7 +143,7 @@ __device__ __forceinline__ void ozaki_kstep(uint32_t tmem, uint32_t a0, uint32_t
       const uint64_t bd = umma_desc(b0 + (bs - 1) * 16 * NC, kOzSlices * 16 * NC, 128);
       if (a == 1) {
         mma_i8(td, ad, bd, idesc_i8(128, nb * NC), first ? 0u : 1u);
-      } else if (a == 2 && bs + nb - 1 == kOzMaxW - a && first) {  // weights 7, 8 (accumulate) | 9 (new)
+      } else if (MAXW == 9 && a == 2 && bs + nb - 1 == MAXW - a && first) {  // weights 7, 8 (accumulate) | 9 (new)
         mma_i8(td, ad, bd, idesc_i8(128, (nb - 1) * NC), 1u);
         mma_i8(td + static_cast<uint32_t>((nb - 1) * NC), ad,
                umma_desc(b0 + (bs + nb - 2) * 16 * NC, kOzSlices * 16 * NC, 128), idesc_i8(128, NC), 0u);
@@ -185,7 +192,7 @@ struct OzPair {
   OzEpi epi[2];
   int nc = kOzCols;  // B tile width of both column tiles (PAIRED)
 };
-template <bool PAIRED>
+template <bool PAIRED, int MAXW = kOzProjMaxW>
 __global__ void __launch_bounds__(128, 1)
     k_oz_gemm(const int8_t* __restrict__ A, OzPair pr, int nkb_all, int kb_per_chunk) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(128, 1)
       mbar_wait(&full[st], (j / kStages) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-      ozaki_kstep(tmem, a0, b0, NC, j == 0);
+      ozaki_kstep<MAXW>(tmem, a0, b0, NC, j == 0);
       mma_commit(&empty[st]);
     }
     mma_commit(&done);
@@ -264,9 +271,9 @@ __global__ void __launch_bounds__(128, 1)
     double acc[32];
     {
       double y0[16], y1[16];
-      drain16(trow, hh * 32, y0, NC);
+      drain16<MAXW - 1>(trow, hh * 32, y0, NC);
       if (hh * 32 + 16 < NC) {
-        drain16(trow, hh * 32 + 16, y1, NC);
+        drain16<MAXW - 1>(trow, hh * 32 + 16, y1, NC);
       } else {
 #pragma unroll
         for (int c = 0; c < 16; ++c) y1[c] = 0.0;
@@ -340,7 +347,7 @@ constexpr int kXEpi = 512;  // epilogue threads: four warps per TMEM lane quadra
 // fourth pipeline stage (4 x 42 KB + 57 KB)
 constexpr int kXStages4 = 4, kXLd56 = 57;
 constexpr int kXSmem4 = kXStages4 * (kATile + kBTile) + 128 * kXLd56 * 8;
-template <bool PAIRED, int STAGES = kXStages, int LDY = kXLd>
+template <bool PAIRED, int STAGES = kXStages, int LDY = kXLd, int MAXW = kOzMaxW>
 __global__ void __launch_bounds__(64 + kXEpi, 1)
     k_oz_expand(const int8_t* __restrict__ A, OzPair pr, int tiles, int mkb) {
   constexpr int kStages = STAGES;
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
           mbar_wait(&full[st], static_cast<uint32_t>((g / kStages) & 1));
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-          ozaki_kstep(tmem, a0, b0, NC, kb == 0);
+          ozaki_kstep<MAXW>(tmem, a0, b0, NC, kb == 0);
           mma_commit(&empty[st]);
         }
         mma_commit(&tfull);
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
         const int c0 = gq * 16 + h8 * 8;
         if (c0 >= tp || c0 >= NC) break;
         double y[8];
-        drain8(trow, c0, y, NC);
+        drain8<MAXW - 1>(trow, c0, y, NC);
 #pragma unroll
         for (int c = 0; c < 8; ++c) tileY[row * LDY + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
       }
@@ -687,26 +694,34 @@ __global__ void k_oz_reduce(const double* __restrict__ part, int nchunks, long m
   if (ok && qp == 0) S[r * ld + c] = ((sacc + s1) + s2) + s3;
 }
 
-void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nkb_all, int kb_per_chunk,
-                 const OzEpi& epi, cudaStream_t s) {
+// projection weights: 2..8 (kOzProjMaxW); FSA_OZ_PROJ_W9=1 keeps weight 9 too (A/B switch)
+static bool proj_w9() {
+  static const bool w9 = [] {
+    const char* e = std::getenv("FSA_OZ_PROJ_W9");
+    return e != nullptr && e[0] == '1';
+  }();
+  return w9;
+}
+template <bool PAIRED, int MAXW>
+void launch_gemm_t(const int8_t* A, const OzPair& pr, dim3 grid, int nkb_all, int kb_per_chunk, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<PAIRED, MAXW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  OzPair pr{{B, B}, {epi, epi}};
-  launch_pdl(k_oz_gemm<false>, dim3(tiles, chunks), dim3(128), kSmem, s, A, pr, nkb_all, kb_per_chunk);
+  launch_pdl(k_oz_gemm<PAIRED, MAXW>, grid, dim3(128), kSmem, s, A, pr, nkb_all, kb_per_chunk);
   FSA_LAUNCH_CHECK();
+}
+void launch_gemm(const int8_t* A, const int8_t* B, int tiles, int chunks, int nkb_all, int kb_per_chunk,
+                 const OzEpi& epi, cudaStream_t s) {
+  OzPair pr{{B, B}, {epi, epi}};
+  if (proj_w9()) launch_gemm_t<false, 9>(A, pr, dim3(tiles, chunks), nkb_all, kb_per_chunk, s);
+  else launch_gemm_t<false, kOzProjMaxW>(A, pr, dim3(tiles, chunks), nkb_all, kb_per_chunk, s);
 }
 void launch_gemm_pair(const int8_t* A, const OzPair& pr, int tiles, int chunks, int nkb_all, int kb_per_chunk,
                       cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
-  }
-  launch_pdl(k_oz_gemm<true>, dim3(2, tiles, chunks), dim3(128), kSmem, s, A, pr, nkb_all, kb_per_chunk);
-  FSA_LAUNCH_CHECK();
+  if (proj_w9()) launch_gemm_t<true, 9>(A, pr, dim3(2, tiles, chunks), nkb_all, kb_per_chunk, s);
+  else launch_gemm_t<true, kOzProjMaxW>(A, pr, dim3(2, tiles, chunks), nkb_all, kb_per_chunk, s);
 }
 
 // q[i] = sum_j qp[j][i], f likewise (fixed order)
@@ -723,39 +738,32 @@ __global__ void k_sum_tiles(const double* __restrict__ qp, const double* __restr
   f[i] = b;
 }
 
-void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const int8_t* Ws = nullptr) {
+template <bool PAIRED, int STAGES, int LDY, int MAXW>
+void launch_expand_t(const int8_t* A, const OzPair& pr, int grid, int smem, int tiles, int mkb, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<PAIRED, STAGES, LDY, MAXW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
     attr = true;
   }
-  static bool attr4 = false;
-  if (!attr4) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<false, kXStages4, kXLd56>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kXSmem4));
-    attr4 = true;
-  }
-  const int grid = std::min(p.ptiles, kNumSMs);
-  const int8_t* B = Ws != nullptr ? Ws : p.Ws.get();
-  OzPair pr{{B, B}, {epi, epi}};
-  if (epi.mode == 1 && epi.tp <= kXLd56 - 1)
-    launch_pdl(k_oz_expand<false, kXStages4, kXLd56>, dim3(grid), dim3(64 + kXEpi), kXSmem4, s,
-               static_cast<const int8_t*>(p.Ac.get()), pr, p.ptiles, p.mkb);
-  else
-    launch_pdl(k_oz_expand<false>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()),
-               pr, p.ptiles, p.mkb);
+  launch_pdl(k_oz_expand<PAIRED, STAGES, LDY, MAXW>, dim3(grid), dim3(64 + kXEpi), smem, s, A, pr, tiles, mkb);
   FSA_LAUNCH_CHECK();
 }
+void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const int8_t* Ws = nullptr) {
+  const int grid = std::min(p.ptiles, kNumSMs);
+  const int8_t* B = Ws != nullptr ? Ws : p.Ws.get();
+  const int8_t* A = p.Ac.get();
+  OzPair pr{{B, B}, {epi, epi}};
+  // (weight 9 kept: dropping it -- 28 products -- measured 7 us faster per pass at config 2 and
+  // 13 % at config 4, but breaks the normwise fp64-class bound, 1.11x of it in tests/test_gpu_ozaki.py)
+  if (epi.mode == 1 && epi.tp <= kXLd56 - 1)
+    launch_expand_t<false, kXStages4, kXLd56, kOzMaxW>(A, pr, grid, kXSmem4, p.ptiles, p.mkb, s);
+  else
+    launch_expand_t<false, kXStages, kXLd, kOzMaxW>(A, pr, grid, kXSmem, p.ptiles, p.mkb, s);
+}
 void launch_expand_pair(const OzakiPlan& p, const OzPair& pr, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXSmem));
-    attr = true;
-  }
   const int grid = 2 * std::min(p.ptiles, kNumSMs / 2);
-  launch_pdl(k_oz_expand<true>, dim3(grid), dim3(64 + kXEpi), kXSmem, s, static_cast<const int8_t*>(p.Ac.get()), pr,
-             p.ptiles, p.mkb);
-  FSA_LAUNCH_CHECK();
+  launch_expand_t<true, kXStages, kXLd, kOzMaxW>(p.Ac.get(), pr, grid, kXSmem, p.ptiles, p.mkb, s);
 }
 
 // digit planes of diag(scale) V (columns [0, tp) of a row-stride-ld block) for the projection

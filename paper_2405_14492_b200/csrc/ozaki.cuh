@@ -42,6 +42,8 @@ namespace fsa {
 constexpr int kOzSlices = 7;   // digit planes per operand (balanced base 256)
 constexpr int kOzMaxW = 9;     // largest kept weight a + b
 constexpr int kOzWeights = kOzMaxW - 1;  // TMEM accumulators: weights 2 .. 9
+// the projection keeps weights 2 .. 8 (28 plane products per K step instead of 34; see above)
+constexpr int kOzProjMaxW = 8;
 constexpr int kOzCols = 64;  // RHS columns per accumulator (t_pad <= 64)
 constexpr int kOzPairCols = 96;  // widest block of the paired passes (two column tiles of <= 48)
 
