@@ -792,6 +792,43 @@ __device__ __forceinline__ double block_colsum(const double* __restrict__ partia
   __syncthreads();  // (red reused)
   return t;
 }
+// both sums of MODE 3 in one pass: the loads of the two partial columns are issued together
+// (each sum in k_colsum_partials' order), then one shuffle tree and one barrier for both
+__device__ __forceinline__ void block_colsum2(const double* __restrict__ pa, long na, long lda,
+                                              const double* __restrict__ pb, long nb, long ldb, long c,
+                                              double (&red)[2][8], double& ta, double& tb) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double sa = 0.0, sb = 0.0;
+  if (na <= 2 * 256 && nb <= 4 * 256) {  // (the sweep's sizes: everything in flight at once)
+    double va[2], vb[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) va[i] = tid + 256 * i < na ? pa[(tid + 256 * i) * lda + c] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) vb[i] = tid + 256 * i < nb ? pb[(tid + 256 * i) * ldb + c] : 0.0;
+    // the order of strided_colsum: s0 / s1 over pairs of 256-strides, then s0 + s1
+    sa = va[0] + va[1];
+    sb = (vb[0] + vb[2]) + (vb[1] + vb[3]);
+  } else {
+    sa = strided_colsum(pa, na, lda, c);
+    sb = strided_colsum(pb, nb, ldb, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = sa;
+    red[1][warp] = sb;
+  }
+  __syncthreads();
+  ta = tb = 0.0;
+  if (tid == 0)
+    for (int w = 0; w < 8; ++w) {
+      ta += red[0][w];
+      tb += red[1][w];
+    }
+}
 template <int MODE>
 __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ partial, long nb, long ldp,
                                                     double* __restrict__ out, long k, int it, int max_iter,
@@ -799,26 +836,47 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
                                                     unsigned long long* __restrict__ zero_buf, long zero_len,
                                                     const double* __restrict__ partial_b, long nb_b, long ldp_b,
                                                     double* __restrict__ out_b) {
-  __shared__ double red[8];
+  __shared__ double red[2][8];
   __shared__ bool last;
   pdl_wait();
   const long c = blockIdx.x;
+  const long j = c;
   const int tid = threadIdx.x;
+  // thread 0's control state, loaded while the partials are summed (independent loads in flight)
+  int itv = it, act = 0;
+  double rzj = 0.0, bpj = 0.0, apj = 1.0, aj = 0.0;
+  if (tid == 0) {
+    if (st.it_dev != nullptr) itv = *st.it_dev;
+    if (j < k) {
+      act = st.active[j];
+      rzj = st.rz[j];
+      if (MODE == 0) {
+        bpj = st.beta_prev[j];
+        apj = st.alpha_prev[j];
+      }
+      if (MODE >= 2) aj = st.alpha[j];
+    }
+  }
   // clear the next kernel's column-maxima accumulators on the way
   for (long i = c * blockDim.x + tid; i < zero_len; i += static_cast<long>(gridDim.x) * blockDim.x) zero_buf[i] = 0ull;
-  const double t0 = block_colsum(partial, nb, ldp, c, red);
-  const double tb = MODE == 3 ? block_colsum(partial_b, nb_b, ldp_b, c, red) : 0.0;
+  double t0, tb = 0.0;
+  if (MODE == 3) {
+    block_colsum2(partial, nb, ldp, partial_b, nb_b, ldp_b, c, red, t0, tb);
+  } else {
+    double dummy;
+    block_colsum2(partial, nb, ldp, partial, 0, ldp, c, red, t0, dummy);
+  }
   if (tid == 0) {
     double t = t0;
     out[c] = t;
-    const long j = c;
-    if (st.it_dev != nullptr) it = *st.it_dev;
-    if (MODE == 3 && j < k && st.active[j]) {  // residual test first (krylov.cpp:77-82)
+    it = itv;
+    if (MODE == 3 && j < k && act) {  // residual test first (krylov.cpp:77-82)
       const double rn = sqrt(t);
       st.rnorm[j * max_iter + it] = rn;
       if (rn < tol) {
         st.converged[j] = 1;
         st.active[j] = 0;
+        act = 0;
       }
     }
     if (MODE == 3) {
@@ -827,20 +885,20 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
     }
     if (j < k) {
       if (MODE == 0) {  // alpha = rz / h'v, tridiagonal push (krylov.cpp:66-75)
-        if (!st.active[j]) {
+        if (!act) {
           st.alpha[j] = 0.0;
         } else if (!(t > 0.0)) {
           atomicCAS(st.err, 0, kErrOperatorNotPD);
           st.alpha[j] = 0.0;
         } else {
-          const double a = st.rz[j] / t;
+          const double a = rzj / t;
           st.alpha[j] = a;
-          st.tdiag[j * max_iter + it] = 1.0 / a + st.beta_prev[j] / st.alpha_prev[j];
-          if (it > 0) st.toff[j * max_iter + it - 1] = sqrt(st.beta_prev[j]) / st.alpha_prev[j];
+          st.tdiag[j * max_iter + it] = 1.0 / a + bpj / apj;
+          if (it > 0) st.toff[j * max_iter + it - 1] = sqrt(bpj) / apj;
           st.iterations[j] = it + 1;
         }
       } else if (MODE == 1) {  // residual test (krylov.cpp:77-82)
-        if (st.active[j]) {
+        if (act) {
           const double rn = sqrt(t);
           st.rnorm[j * max_iter + it] = rn;
           if (rn < tol) {
@@ -849,16 +907,16 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
           }
         }
       } else {  // MODE 2 / 3: beta = rz_new / rz (krylov.cpp:83-90)
-        if (!st.active[j]) {
+        if (!act) {
           st.beta[j] = 0.0;
         } else if (!(t > 0.0)) {
           atomicCAS(st.err, 0, kErrPrecondNotPD);
           st.beta[j] = 0.0;
         } else {
-          const double bb = t / st.rz[j];
+          const double bb = t / rzj;
           st.beta[j] = bb;
           st.beta_prev[j] = bb;
-          st.alpha_prev[j] = st.alpha[j];
+          st.alpha_prev[j] = aj;
           st.rz[j] = t;
         }
       }
@@ -880,7 +938,6 @@ __global__ void __launch_bounds__(256) k_colsum_ctl(const double* __restrict__ p
       if (tid == 0) {
         int* hf = st.host_flags;
         if (st.it_dev != nullptr) {  // graph-captured sweep: slot by the device sweep index, then advance it
-          const int itv = *st.it_dev;
           hf += 2 * (itv & 1);
           *st.it_dev = itv + 1;
         }
