@@ -104,25 +104,43 @@ __device__ __forceinline__ double pow2(int k) {
   return (k > -1023 && k < 1024) ? __hiloint2double((k + 1023) << 20, 0) : ldexp(1.0, k);
 }
 // 16 values -> 7 balanced base-256 digit planes of 16 signed bytes each (ozaki.cuh): X = trunc(x
-// 2^{54-e}) is exact for the group maximum (|x| < 2^e, 53-bit mantissa) and |X| < 2^54; the digits
-// are peeled off from the least significant end: the low byte of X, read as a signed byte, is the
-// digit, and X <- (X - digit) / 256 = (X + 128) >> 8. Plane a - 1 holds digit a (weight 2^{-8a}).
+// 2^{54-e}) is exact for the group maximum (|x| < 2^e, 53-bit mantissa) and |X| < 2^54. The balanced
+// digits d_a in [-128, 127] with X = sum_a d_a 256^a are all read off at once: X + sum_a 128 256^a
+// has the ordinary base-256 digits d_a + 128 (the add carries exactly as peeling the signed low byte
+// and (X + 128) >> 8 does), and byte ^ 0x80 is d_a as a signed byte. Plane a - 1 holds digit a (weight
+// 2^{-8a}), i.e. byte 7 - a of the biased word; the bytes of four values are transposed into plane
+// words with byte permutes.
 __device__ __forceinline__ void digits16(const double (&v)[16], int e, int4 (&out)[kOzSlices]) {
+  static_assert(kOzSlices == 7, "digit planes: 7 bytes of the biased 64-bit word");
   const double sc = pow2(54 - e);
-  long long X[16];
+  uint32_t w[kOzSlices][4];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) X[q] = __double2ll_rz(v[q] * sc);
+  for (int j = 0; j < 4; ++j) {
+    uint32_t lo[4], hi[4];
 #pragma unroll
-  for (int a = kOzSlices - 1; a >= 0; --a) {
-    uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      w[q >> 2] |= (static_cast<uint32_t>(X[q]) & 0xFFu) << (8 * (q & 3));
-      X[q] = (X[q] + 128) >> 8;
+    for (int q = 0; q < 4; ++q) {
+      const unsigned long long bias = 0x0080808080808080ULL;
+      const unsigned long long Y = (static_cast<unsigned long long>(__double2ll_rz(v[4 * j + q] * sc)) + bias) ^ bias;
+      lo[q] = static_cast<uint32_t>(Y);
+      hi[q] = static_cast<uint32_t>(Y >> 32);
     }
-    out[a] = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]),
-                       static_cast<int>(w[3]));
+    // 4 x 4 byte transposes: bytes 0..3 (lo) are digits 7..4, bytes 4..6 (hi) digits 3..1
+    const uint32_t t0 = __byte_perm(lo[0], lo[1], 0x5140), t1 = __byte_perm(lo[2], lo[3], 0x5140);
+    const uint32_t t2 = __byte_perm(lo[0], lo[1], 0x7362), t3 = __byte_perm(lo[2], lo[3], 0x7362);
+    w[6][j] = __byte_perm(t0, t1, 0x5410);
+    w[5][j] = __byte_perm(t0, t1, 0x7632);
+    w[4][j] = __byte_perm(t2, t3, 0x5410);
+    w[3][j] = __byte_perm(t2, t3, 0x7632);
+    const uint32_t h0 = __byte_perm(hi[0], hi[1], 0x5140), h1 = __byte_perm(hi[2], hi[3], 0x5140);
+    const uint32_t h2 = __byte_perm(hi[0], hi[1], 0x7362), h3 = __byte_perm(hi[2], hi[3], 0x7362);
+    w[2][j] = __byte_perm(h0, h1, 0x5410);
+    w[1][j] = __byte_perm(h0, h1, 0x7632);
+    w[0][j] = __byte_perm(h2, h3, 0x5410);
   }
+#pragma unroll
+  for (int a = 0; a < kOzSlices; ++a)
+    out[a] = make_int4(static_cast<int>(w[a][0]), static_cast<int>(w[a][1]), static_cast<int>(w[a][2]),
+                       static_cast<int>(w[a][3]));
 }
 
 // One K step of plane-pair MMAs into the weight accumulators (weights a + b <= MAXW of the 7 x 7

@@ -353,6 +353,25 @@ __global__ void k_group_compact(const int* __restrict__ ucols, int kCap, const i
   const int u = ucount[b];
   for (long i = threadIdx.x; i < up; i += blockDim.x) gcol[o + i] = ucols[b * kCap + (i < u ? i : 0)];
 }
+// union slots whose column is >= the group's first row, in slot order (one warp per group)
+__global__ void k_group_need(const long* __restrict__ gptr, const int* __restrict__ gcol, long ngrp,
+                             int* __restrict__ gneed, int* __restrict__ gneedcnt) {
+  const long g = blockIdx.x;
+  if (g >= ngrp) return;
+  const int lane = threadIdx.x;
+  const long o = gptr[g];
+  const int up = static_cast<int>(gptr[g + 1] - o);
+  const int r0 = static_cast<int>(g * kGroup);
+  int cnt = 0;
+  for (int u0 = 0; u0 < up; u0 += 32) {
+    const int u = u0 + lane;
+    const bool keep = u < up && gcol[o + u] >= r0;
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if (keep) gneed[o + cnt + __popc(b & ((1u << lane) - 1u))] = u;
+    cnt += __popc(b);
+  }
+  if (lane == 0) gneedcnt[g] = cnt;
+}
 // value index of entry p (row r, union slot u of group g): A-fragment order of the
 // 8 x 4 DMMA tiles: [k-step u/4][warp (r%32)/8][lane ((r%8)*4 + u%4)]
 __global__ void k_group_slots(const long* __restrict__ rowptr, long nrows, const long* __restrict__ gptr,
@@ -579,6 +598,17 @@ void build_groups(Csr& pat, cudaStream_t s) {
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());
   FSA_LAUNCH_CHECK();
+  {  // columns the Gram blocks have to evaluate (the rest comes from mirror entries)
+    pat.gneed.alloc(pat.gnnz);
+    pat.gneedcnt.alloc(pat.ngrp);
+    k_group_need<<<static_cast<unsigned>(pat.ngrp), 32, 0, s>>>(pat.gptr.get(), pat.gcol.get(), pat.ngrp,
+                                                               pat.gneed.get(), pat.gneedcnt.get());
+    FSA_LAUNCH_CHECK();
+    std::vector<int> cnt(static_cast<size_t>(pat.ngrp));
+    FSA_CUDA(cudaMemcpyAsync(cnt.data(), pat.gneedcnt.get(), sizeof(int) * pat.ngrp, cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaStreamSynchronize(s));
+    pat.gneedmax = *std::max_element(cnt.begin(), cnt.end());
+  }
   {  // compact tiles of the value blocks
     pat.nkb = pat.gnnz / 4;
     pat.kmask.alloc(pat.nkb);

@@ -52,6 +52,11 @@ struct Csr {
   DBuf<int> gcol;              // union columns (row-tile-mask order, see k_group_union; padding repeats a valid column)
   DBuf<int> gslot;             // per entry: its index in the value blocks (kGroup * gnnz)
   int gmax = 0;                // largest padded union
+  // Gram blocks (sddmm_block) only evaluate the union columns c >= the group's first row: every
+  // entry (r, c) with c < r is taken from its mirror (c, r). gneed[gptr[g] + j], j < gneedcnt[g]:
+  // the union slots of those columns, in slot order.
+  DBuf<int> gneed, gneedcnt;
+  int gneedmax = 0;            // largest gneedcnt
   // Compact value tiles: of the dense block only the 8 x 4 DMMA A tiles (row tile rt of the
   // group, k-step kb = union slot / 4) that hold an entry are stored (~2/3 of them at 80
   // entries per row). kmask[kb] bit rt marks them; koff[kb] = stored tiles before k-step kb.

@@ -501,7 +501,9 @@ __device__ __forceinline__ void gram_ksteps(double (&c)[8][2], const double* As,
 }
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ gptr, const int* __restrict__ gcol,
-                                                      long nrows, const double* __restrict__ A0,
+                                                      const int* __restrict__ gneed,
+                                                      const int* __restrict__ gneedcnt, long nrows,
+                                                      const double* __restrict__ A0,
                                                       const double* __restrict__ B0, const double* __restrict__ A1,
                                                       const double* __restrict__ B1, long ldu, long mp,
                                                       double* __restrict__ G) {
@@ -510,12 +512,20 @@ __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ 
   double(*Bs)[64 * kGLd] = reinterpret_cast<double(*)[64 * kGLd]>(gsm + 2 * kGroup * kGLd);
   const long g = blockIdx.x;
   const int jt = blockIdx.y;
+  // the tile's columns: union slots gneed[u0 + j0 ...] (columns >= the group's first row; entries
+  // left of the diagonal are mirrored by k_sddmm_finish and never read from G)
+  __shared__ int uslot[64], ucol[64];
   const long u0 = gptr[g];
-  const int up = static_cast<int>(gptr[g + 1] - u0);
+  const int up = gneedcnt[g];
   const int j0 = jt * 64;
   if (j0 >= up) return;
   const int nc = min(64, up - j0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 64) {
+    const int u = tid < nc ? gneed[u0 + j0 + tid] : -1;
+    uslot[tid] = u;
+    ucol[tid] = u >= 0 ? gcol[u0 + u] : 0;
+  }
   const int rt = warp & 3, half = warp >> 2;
   const long r0 = g * kGroup;
   const long K = MODE == 0 ? mp : 2 * mp;
@@ -538,8 +548,8 @@ __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ 
     }
     for (int idx = tid; idx < nc * (kGK / 2); idx += 256) {
       const int j = idx / (kGK / 2), ch = idx % (kGK / 2);
-      FSA_DCHECK(gcol[u0 + j0 + j] >= 0, "block gram: negative union column");
-      cp_async16(bs + j * kGLd + ch * 2, B + static_cast<long>(gcol[u0 + j0 + j]) * ldu + kk + ch * 2);
+      FSA_DCHECK(ucol[j] >= 0, "block gram: negative union column");
+      cp_async16(bs + j * kGLd + ch * 2, B + static_cast<long>(ucol[j]) * ldu + kk + ch * 2);
     }
     cp_async_commit();
   };
@@ -566,8 +576,8 @@ __global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ 
     if ((q & 1) != half) continue;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int u = j0 + q * 8 + 2 * (lane & 3) + e;
-      if (u < up) gb[((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3)] = c[q][e];
+      const int u = uslot[q * 8 + 2 * (lane & 3) + e];
+      if (u >= 0) gb[((u >> 2) * (kGroup / 8) + (rr >> 3)) * 32 + (rr & 7) * 4 + (u & 3)] = c[q][e];
     }
   }
 }
@@ -664,7 +674,7 @@ void sddmm_block(int mode, const double* U, const double* U1, const double* T, l
                  const double* lowrank_diag, const SddmmParams& P, double* val, double* gval, int* n_clamped_dev,
                  double* gtmp, cudaStream_t s) {
   require(pat.gnnz > 0 && mp % kGK == 0, "sddmm_block: row groups missing");
-  const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(cdiv(pat.gmax, 64)));
+  const dim3 grid(static_cast<unsigned>(pat.ngrp), static_cast<unsigned>(cdiv(pat.gneedmax, 64)));
   const int smem = static_cast<int>(2 * (kGroup + 64) * kGLd * sizeof(double));
   static bool attr = false;
   if (!attr) {
@@ -673,9 +683,9 @@ void sddmm_block(int mode, const double* U, const double* U1, const double* T, l
     attr = true;
   }
   if (mode == 0)
-    k_block_gram<0><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U, U, U, U, ldu, mp, gtmp);
+    k_block_gram<0><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.gneed.get(), pat.gneedcnt.get(), pat.rows, U, U, U, U, ldu, mp, gtmp);
   else
-    k_block_gram<1><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.rows, U1, U, U, T, ldu, mp, gtmp);
+    k_block_gram<1><<<grid, 256, smem, s>>>(pat.gptr.get(), pat.gcol.get(), pat.gneed.get(), pat.gneedcnt.get(), pat.rows, U1, U, U, T, ldu, mp, gtmp);
   FSA_LAUNCH_CHECK();
   if (mode == 0 && gval != nullptr) FSA_CUDA(cudaMemsetAsync(gval, 0, sizeof(double) * 32 * pat.ntiles, s));
   if (mode == 0 && n_clamped_dev != nullptr) FSA_CUDA(cudaMemsetAsync(n_clamped_dev, 0, sizeof(int), s));
