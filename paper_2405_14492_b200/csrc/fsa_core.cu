@@ -406,9 +406,25 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   M.dot_scratch.alloc(coldot_scratch(np, 128));
   DBuf<double> scal(4);
 
-  // Sigma_m + jitter, Cholesky (fsa.cpp:23-30)
+  // Sigma_m + jitter, Cholesky (fsa.cpp:23-30); Sigma_mn (fsa.cpp:32-35, owned and halo points) is
+  // evaluated on the side stream meanwhile: the Cholesky panels are a few CTAs wide and leave the
+  // GPU idle
   M.Sm.alloc(mp * mp);
   M.L.alloc(mp * mp);
+  M.U.alloc(mp * ne);
+  M.lowrank.alloc(np);
+  static const bool serial_cov = std::getenv("FSA_SERIAL_CROSS_COV") != nullptr;
+  cudaEvent_t cov_done = nullptr;
+  if (!serial_cov) {
+    cudaStream_t side = ctx->side_stream();
+    cudaEvent_t ready = ctx->ev();
+    FSA_CUDA(cudaEventRecord(ready, s));  // inducing points uploaded, U allocated
+    FSA_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    ctx->pool.push_back(ready);
+    M.cross_cov_ext(0, M.U.get(), side);
+    cov_done = ctx->ev();
+    FSA_CUDA(cudaEventRecord(cov_done, side));
+  }
   {
     KTimer t(ctx, "setup_sigma_m");
     launch_sigma_m(M.ind.get(), m, m, mp, M.d, p.nu, p.sigma1_2, p.rho, p.jitter_rel * p.sigma1_2, 0, M.Sm.get(), s);
@@ -416,10 +432,11 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
     potrf_lower(M.L.get(), mp, M.info.get(), M.dinv_scratch.get(), s);
     launch_logdet_diag(M.L.get(), mp, m, scal.get(), s);
   }
-  // U = L^{-1} Sigma_mn (fsa.cpp:32-35), for the owned and the halo points
-  M.U.alloc(mp * ne);
-  M.lowrank.alloc(np);
-  {
+  // U = L^{-1} Sigma_mn
+  if (cov_done != nullptr) {
+    FSA_CUDA(cudaStreamWaitEvent(s, cov_done, 0));
+    ctx->pool.push_back(cov_done);
+  } else {
     KTimer t(ctx, "setup_cross_cov");
     M.cross_cov_ext(0, M.U.get());
   }

@@ -540,18 +540,34 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
 
 // ---- digit planes ---------------------------------------------------------------------------------
 // project A: exponent per (chunk, inducing row) over the chunk's points
-__global__ void __launch_bounds__(256) k_oz_exp_rows(const double* __restrict__ U, long mp, long n_pad,
-                                                     int kb_per_chunk, int* __restrict__ er) {
-  __shared__ double red[256];
+__global__ void __launch_bounds__(1024) k_oz_exp_rows(const double* __restrict__ U, long mp, long n_pad,
+                                                      int kb_per_chunk, int* __restrict__ er) {
+  // 8 point phases x 128 rows, eight independent loads in flight per thread (max is order-free)
+  __shared__ double red[1024];
   const int chunk = blockIdx.x, tile = blockIdx.y;
-  const int r = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int r = threadIdx.x & 127, ph = threadIdx.x >> 7;
   const long i0 = static_cast<long>(chunk) * kb_per_chunk * kKb;
   const long i1 = min(n_pad, i0 + static_cast<long>(kb_per_chunk) * kKb);
-  double mx = 0.0;
-  for (long i = i0 + half; i < i1; i += 2) mx = fmax(mx, fabs(U[i * mp + tile * 128 + r]));
-  red[threadIdx.x] = mx;
+  const double* __restrict__ p = U + tile * 128 + r;
+  double mx[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) mx[u] = 0.0;
+  long i = i0 + ph;
+  for (; i + 56 < i1; i += 64) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mx[u] = fmax(mx[u], fabs(p[(i + 8 * u) * mp]));
+  }
+  for (; i < i1; i += 8) mx[0] = fmax(mx[0], fabs(p[i * mp]));
+#pragma unroll
+  for (int u = 1; u < 8; ++u) mx[0] = fmax(mx[0], mx[u]);
+  red[threadIdx.x] = mx[0];
   __syncthreads();
-  if (half == 0) er[static_cast<long>(chunk) * mp + tile * 128 + r] = group_exp(fmax(mx, red[threadIdx.x + 128]));
+  if (ph == 0) {
+    double m = mx[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) m = fmax(m, red[q * 128 + r]);
+    er[static_cast<long>(chunk) * mp + tile * 128 + r] = group_exp(m);
+  }
 }
 __global__ void __launch_bounds__(256) k_oz_planes_rows(const double* __restrict__ U, long mp, int nkb,
                                                         int kb_per_chunk, const int* __restrict__ er,
@@ -630,7 +646,7 @@ __global__ void __launch_bounds__(256) k_oz_ymax(const double* __restrict__ V, l
 }
 // B planes in the layout [kb][kc][plane * nc / 8 + col / 8][col % 8][16] of an nc-column tile
 // (nc = 64, or 16 for the narrow second tile of a pair)
-__global__ void __launch_bounds__(128) k_oz_planes_y(const double* __restrict__ V, long ld, long tp,
+__global__ void __launch_bounds__(128, 11) k_oz_planes_y(const double* __restrict__ V, long ld, long tp,
                                                      const double* __restrict__ scale, int kb_per_chunk,
                                                      const unsigned long long* __restrict__ ymax,
                                                      int* __restrict__ f, int8_t* __restrict__ Ys, int nc = kOzCols) {
@@ -852,7 +868,7 @@ void ozaki_prepare(OzakiPlan& p, const double* U, long m_pad, long n_pad, cudaSt
   p.f.alloc(static_cast<size_t>(p.nchunks * kOzCols));
   p.h.alloc(kOzCols);
   p.part.alloc(static_cast<size_t>(p.nchunks * m_pad * kOzCols));
-  k_oz_exp_rows<<<dim3(p.nchunks, p.mtiles), 256, 0, s>>>(U, m_pad, n_pad, p.kb_per_chunk, p.er.get());
+  k_oz_exp_rows<<<dim3(p.nchunks, p.mtiles), 1024, 0, s>>>(U, m_pad, n_pad, p.kb_per_chunk, p.er.get());
   FSA_LAUNCH_CHECK();
   k_oz_planes_rows<<<dim3(p.nkb, p.mtiles), 256, 0, s>>>(U, m_pad, p.nkb, p.kb_per_chunk, p.er.get(), p.Ar.get());
   FSA_LAUNCH_CHECK();
