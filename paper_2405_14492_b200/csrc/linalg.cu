@@ -51,89 +51,84 @@ __global__ void k_sigma_m_fix(double* S, long m, long mpad, double jitter, int m
 
 // One 64-column panel of a blocked right-looking Cholesky (column-major, ld = mpad).
 // Block 0 factors the diagonal block and writes it back; blocks b >= 1 redo the
-// (cheap) diagonal factorisation in shared memory and solve their 64 panel rows.
+// (cheap) diagonal factorisation and solve their 64 panel rows.
+// Factorisation: thread (r, c0) keeps row r, columns c0, c0 + 4, ... of the block in registers. The
+// (final, unscaled) column j is published in shared memory one step ahead by its owners, every
+// thread forms 1 / l_jj = rsqrt(a_jj) itself and scales the entries it needs on the fly: one
+// barrier and one rsqrt on the critical path per column (no sqrt + divide chain).
+// Panel rows: the four threads of a row sit in one warp and pass x_c by shuffle, so the forward
+// substitution X L^T = A_rows runs without block barriers (x_c = (...) * (1 / l_cc)).
 __global__ void __launch_bounds__(256) k_potrf_panel(double* A, long ld, long k0, int* info, double* diag_out) {
   extern __shared__ double psm[];
   double(*Lk)[65] = reinterpret_cast<double(*)[65]>(psm);
-  double(*X)[65] = reinterpret_cast<double(*)[65]>(psm + 64 * 65);
+  __shared__ double colbuf[2][64], invd[64];
   __shared__ int bad;
   const int tid = threadIdx.x;
   if (tid == 0) bad = 0;
-  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
-    const int r = idx % 64, c = idx / 64;
-    Lk[r][c] = A[(k0 + c) * ld + k0 + r];
-  }
-  __shared__ double Ld[64];
-  __syncthreads();
-  // right-looking factorisation of the 64 x 64 diagonal block by the whole block, one barrier per
-  // column: every thread scales the column-j entries it needs on the fly (the same products the
-  // in-place scaling would store) and updates the trailing lower triangle; the scaled column is
-  // written back one step later, when no thread reads column j any more
   {
     const int r = tid & 63, c0 = tid >> 6;
-    double pending = 0.0;
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = A[(k0 + c0 + 4 * i) * ld + k0 + r];
+    if (c0 == 0) colbuf[0][r] = x[0];
+    __syncthreads();
+#pragma unroll
     for (int j = 0; j < 64; ++j) {
-      if (j > 0 && c0 == 0 && r > j - 1) Lk[r][j - 1] = pending;
-      double dj = Lk[j][j];
+      const double* cb = colbuf[j & 1];
+      double dj = cb[j];
       if (!(dj > 0.0) || !isfinite(dj)) {
         if (tid == 0 && !bad) bad = j + 1;
         dj = 1.0;
       }
-      const double ljj = sqrt(dj);
-      const double inv = 1.0 / ljj;
-      if (tid == j) Ld[j] = ljj;
-      const double lr = Lk[r][j] * inv;  // thread (r, c0) updates row r, columns c0, c0 + 4, ...
-      if (c0 == 0) pending = lr;
+      const double inv = rsqrt(dj);
+      const double lr = cb[r] * inv;  // l_rj (r > j)
+      if (c0 == (j & 3)) {
+        if (r == j) {
+          Lk[j][j] = dj * inv;
+          invd[j] = inv;
+        } else {
+          Lk[r][j] = r > j ? lr : 0.0;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int c = c0 + 4 * i;
-        if (c > j && r >= c) Lk[r][c] = fma(-lr, Lk[c][j] * inv, Lk[r][c]);
+        if (c > j && r >= c) x[i] = fma(-lr, cb[c] * inv, x[i]);
       }
+      if (j + 1 < 64 && c0 == ((j + 1) & 3)) colbuf[(j + 1) & 1][r] = x[(j + 1) >> 2];
       __syncthreads();
     }
   }
-  if (tid < 64) Lk[tid][tid] = Ld[tid];
-  __syncthreads();
   if (blockIdx.x == 0) {
     // the factored diagonal block goes to scratch: the other blocks of this launch
     // still read the unfactored block from A (copied back by k_copy_diag_blocks)
     double* out = diag_out + (k0 / 64) * 4096;
     for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
       const int r = idx % 64, c = idx / 64;
-      out[c * 64 + r] = r >= c ? Lk[r][c] : 0.0;
+      out[c * 64 + r] = Lk[r][c];
     }
     if (tid == 0 && bad && *info == 0) *info = static_cast<int>(k0) + bad;
     return;
   }
-  // panel rows rb .. rb+63: solve X Lk^T = A_rows (row by row, forward substitution)
+  // panel rows rb .. rb+63: solve X Lk^T = A_rows; lane (rr % 8) * 4 + q owns row rr, columns q, q + 4, ...
   const long rb = k0 + 64 * static_cast<long>(blockIdx.x);
-  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
-    const int r = idx % 64, c = idx / 64;
-    X[r][c] = A[(k0 + c) * ld + rb + r];
-  }
-  __syncthreads();
-  {  // right-looking substitution: thread (r, c0) owns row r, columns c0, c0 + 4, ... in registers
-    const int r = tid & 63, c0 = tid >> 6;
+  {
+    const int lane = tid & 31, q = lane & 3, rr = (tid >> 5) * 8 + (lane >> 2);
     double x[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = X[r][c0 + 4 * i];
+    for (int i = 0; i < 16; ++i) x[i] = A[(k0 + q + 4 * i) * ld + rb + rr];
 #pragma unroll
     for (int c = 0; c < 64; ++c) {
-      if (c0 == (c & 3)) {
-        x[c >> 2] /= Lk[c][c];
-        X[r][c] = x[c >> 2];
-      }
-      __syncthreads();
-      const double xc = X[r][c];
+      if (q == (c & 3)) x[c >> 2] *= invd[c];
+      const double xc = __shfl_sync(0xffffffffu, x[c >> 2], (lane & ~3) | (c & 3));
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (c0 + 4 * i > c) x[i] = fma(-xc, Lk[c0 + 4 * i][c], x[i]);
+        if (4 * i + 3 > c) {  // (columns q + 4 i <= c of this thread are skipped by the predicate)
+          if (q + 4 * i > c) x[i] = fma(-xc, Lk[q + 4 * i][c], x[i]);
+        }
     }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
-    const int r = idx % 64, c = idx / 64;
-    A[(k0 + c) * ld + rb + r] = X[r][c];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) A[(k0 + q + 4 * i) * ld + rb + rr] = x[i];
   }
 }
 
@@ -158,7 +153,6 @@ __global__ void k_zero_upper(double* A, long ld, long n) {
 __global__ void __launch_bounds__(256) k_trinv_blocks(const double* L, long ld, double* Dinv) {
   extern __shared__ double tsm[];
   double(*Lk)[65] = reinterpret_cast<double(*)[65]>(tsm);
-  double(*Xs)[65] = reinterpret_cast<double(*)[65]>(tsm + 64 * 65);
   const long k0 = 64 * static_cast<long>(blockIdx.x);
   const int tid = threadIdx.x;
   for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
@@ -166,22 +160,28 @@ __global__ void __launch_bounds__(256) k_trinv_blocks(const double* L, long ld, 
     Lk[r][c] = L[(k0 + c) * ld + k0 + r];
   }
   __syncthreads();
-  // column col of the inverse: forward substitution on e_col, four lanes per column
-  const int col = tid >> 2, part = tid & 3;
-  for (int r = 0; r < 64; ++r) {
-    double t = 0.0;
-    for (int k = col + part; k < r; k += 4) t = fma(Lk[r][k], Xs[k][col], t);
-    t += __shfl_xor_sync(0xffffffffu, t, 1);
-    t += __shfl_xor_sync(0xffffffffu, t, 2);
-    if (part == 0) Xs[r][col] = r < col ? 0.0 : ((r == col ? 1.0 : 0.0) - t) / Lk[r][r];
-    __syncwarp();
-  }
+  __shared__ double invd[64];
+  if (tid < 64) invd[tid] = 1.0 / Lk[tid][tid];
   __syncthreads();
-  double* out = Dinv + blockIdx.x * 4096L;
-  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
-    const int r = idx & 63, c = idx >> 6;
-    out[c * 64 + r] = Xs[r][c];
+  // column col of the inverse: right-looking forward substitution on e_col; the four lanes of a
+  // column (rows part, part + 4, ... in registers) pass x_r by shuffle, no barriers
+  const int col = tid >> 2, part = tid & 3, lane = tid & 31;
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = part + 4 * i == col ? 1.0 : 0.0;
+#pragma unroll
+  for (int r = 0; r < 64; ++r) {
+    if (part == (r & 3)) x[r >> 2] *= invd[r];
+    const double xr = __shfl_sync(0xffffffffu, x[r >> 2], (lane & ~3) | (r & 3));
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (4 * i + 3 > r) {
+        if (part + 4 * i > r) x[i] = fma(-xr, Lk[part + 4 * i][r], x[i]);
+      }
   }
+  double* out = Dinv + blockIdx.x * 4096L;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) out[col * 64 + part + 4 * i] = x[i];
 }
 
 __global__ void k_transpose(const double* __restrict__ A, long lda, long rows, long cols, double* __restrict__ B,
