@@ -4,6 +4,7 @@
 // scalar recurrences with Lanczos-tridiagonal capture, and the host<->device
 // layout conversions (column-major original order <-> row-major internal order).
 #include "blas1.cuh"
+#include "bulk.cuh"
 
 #include <algorithm>
 #include "dgemm.cuh"
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(256, 3) k_xr_dot_max(double* __restrict__ X, d
   const long ra = static_cast<long>(blockIdx.x) * per, rb = min(n, ra + per);
   double d0 = 0.0, d1 = 0.0, m0 = 0.0, m1 = 0.0;
   long cur = -1;
+  const uint64_t pol_last = l2_evict_last();
   auto flush = [&]() {
     if (cur >= 0 && on) {
       if (m0 > 0.0) atomicMax(ymax + cur * 64 + c, static_cast<unsigned long long>(__double_as_longlong(m0)));
@@ -518,7 +520,7 @@ __global__ void __launch_bounds__(256, 3) k_xr_dot_max(double* __restrict__ X, d
         rr[u].x -= al0 * v[u].x;
         rr[u].y -= al1 * v[u].y;
         *reinterpret_cast<double2*>(X + r * ld + c) = x[u];
-        *reinterpret_cast<double2*>(R + r * ld + c) = rr[u];
+        st_l2(reinterpret_cast<double2*>(R + r * ld + c), rr[u], pol_last);  // read next by the slicing pass
       }
       d0 = fma(rr[u].x, rr[u].x, d0);
       d1 = fma(rr[u].y, rr[u].y, d1);

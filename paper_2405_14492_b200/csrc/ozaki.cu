@@ -254,11 +254,12 @@ __global__ void __launch_bounds__(128, 1)
   if (tid == 32) {
     const int8_t* Ablk = A + (static_cast<long>(tile) * nkb_all + kb0) * kATile;
     const int8_t* Bblk = B + static_cast<long>(kb0) * btile;
+    const uint64_t pol_a = l2_evict_first();  // the U digit planes pass through L2 once (bulk.cuh)
     for (int j = 0; j < nk; ++j) {
       const int st = j % kStages;
       if (j >= kStages) mbar_wait(&empty[st], ((j / kStages) - 1) & 1);
       mbar_expect_tx(&full[st], kATile + btile);
-      bulk_g2s(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st]);
+      bulk_g2s_hint(sA + st * kATile, Ablk + static_cast<long>(j) * kATile, kATile, &full[st], pol_a);
       bulk_g2s(sB + st * kBTile, Bblk + static_cast<long>(j) * btile, btile, &full[st]);
     }
   }
@@ -666,8 +667,9 @@ __global__ void __launch_bounds__(128, 11) k_oz_planes_y(const double* __restric
   int4 out[kOzSlices];
   digits16(v, e, out);
   int8_t* base = Ys + static_cast<long>(kb) * (kOzSlices * kKb * nc) + kc * (kOzSlices * 16 * nc) + c * 16;
+  const uint64_t pol_last = l2_evict_last();  // read next by the projection's row-tile CTAs (bulk.cuh)
 #pragma unroll
-  for (int b = 0; b < kOzSlices; ++b) *reinterpret_cast<int4*>(base + b * (16 * nc)) = out[b];
+  for (int b = 0; b < kOzSlices; ++b) st_l2(reinterpret_cast<int4*>(base + b * (16 * nc)), out[b], pol_last);
 }
 // per-sweep B planes of W (expand): column exponents over all rows, then digits
 __global__ void __launch_bounds__(1024) k_oz_wexp(const double* __restrict__ W, long ld, long tp, long mp,

@@ -355,7 +355,7 @@ __global__ void k_group_compact(const int* __restrict__ ucols, int kCap, const i
 }
 // union slots whose column is >= the group's first row, in slot order (one warp per group)
 __global__ void k_group_need(const long* __restrict__ gptr, const int* __restrict__ gcol, long ngrp,
-                             int* __restrict__ gneed, int* __restrict__ gneedcnt) {
+                             int* __restrict__ gneed, int* __restrict__ gneedcnt, int* __restrict__ cntmax) {
   const long g = blockIdx.x;
   if (g >= ngrp) return;
   const int lane = threadIdx.x;
@@ -370,7 +370,10 @@ __global__ void k_group_need(const long* __restrict__ gptr, const int* __restric
     if (keep) gneed[o + cnt + __popc(b & ((1u << lane) - 1u))] = u;
     cnt += __popc(b);
   }
-  if (lane == 0) gneedcnt[g] = cnt;
+  if (lane == 0) {
+    gneedcnt[g] = cnt;
+    atomicMax(cntmax, cnt);
+  }
 }
 // value index of entry p (row r, union slot u of group g): A-fragment order of the
 // 8 x 4 DMMA tiles: [k-step u/4][warp (r%32)/8][lane ((r%8)*4 + u%4)]
@@ -598,16 +601,14 @@ void build_groups(Csr& pat, cudaStream_t s) {
   k_group_slots<<<static_cast<unsigned>(cdiv(pat.rows, 256)), 256, 0, s>>>(pat.rowptr.get(), pat.rows, pat.gptr.get(),
                                                                           pat.gslot.get());
   FSA_LAUNCH_CHECK();
+  DBuf<int> needmax(1);
   {  // columns the Gram blocks have to evaluate (the rest comes from mirror entries)
     pat.gneed.alloc(pat.gnnz);
     pat.gneedcnt.alloc(pat.ngrp);
+    needmax.zero(s);
     k_group_need<<<static_cast<unsigned>(pat.ngrp), 32, 0, s>>>(pat.gptr.get(), pat.gcol.get(), pat.ngrp,
-                                                               pat.gneed.get(), pat.gneedcnt.get());
-    FSA_LAUNCH_CHECK();
-    std::vector<int> cnt(static_cast<size_t>(pat.ngrp));
-    FSA_CUDA(cudaMemcpyAsync(cnt.data(), pat.gneedcnt.get(), sizeof(int) * pat.ngrp, cudaMemcpyDeviceToHost, s));
-    FSA_CUDA(cudaStreamSynchronize(s));
-    pat.gneedmax = *std::max_element(cnt.begin(), cnt.end());
+                                                               pat.gneed.get(), pat.gneedcnt.get(), needmax.get());
+    FSA_LAUNCH_CHECK();  // (its maximum is read back with the tile count below)
   }
   {  // compact tiles of the value blocks
     pat.nkb = pat.gnnz / 4;
@@ -625,6 +626,7 @@ void build_groups(Csr& pat, cudaStream_t s) {
     FSA_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), pat.koff.get(), static_cast<int>(pat.nkb + 1), s));
     int nt = 0;
     FSA_CUDA(cudaMemcpyAsync(&nt, pat.koff.get() + pat.nkb, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FSA_CUDA(cudaMemcpyAsync(&pat.gneedmax, needmax.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     FSA_CUDA(cudaStreamSynchronize(s));
     pat.ntiles = nt;
     pat.pmeta.alloc(2 * std::max<long>(pat.nkb, 1));
