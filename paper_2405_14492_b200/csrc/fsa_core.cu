@@ -402,7 +402,7 @@ std::unique_ptr<Model> Model::assemble(Context* ctx, std::shared_ptr<Geometry> g
   FSA_CUDA(cudaMemcpyAsync(M.ind.get(), inducing, sizeof(double) * m * M.d, cudaMemcpyHostToDevice, s));
   M.info.alloc(4);
   M.info.zero(s);  // [0] Cholesky status, [1] clamped residual diagonals
-  M.dinv_scratch.alloc(mp * 64);
+  M.dinv_scratch.alloc(mp * 192);  // potrf: mp * 64; trsm: mp * 192
   M.dot_scratch.alloc(coldot_scratch(np, 128));
   DBuf<double> scal(4);
 
@@ -511,7 +511,7 @@ void Model::start_rho_derivs() {
   cudaStream_t saved = alloc_stream();
   alloc_stream() = side;  // allocations and frees of the build are ordered on the side stream
   try {
-    rho_scratch.alloc(m_pad * 64);
+    rho_scratch.alloc(m_pad * 192);
     build_rho_derivs(side, rho_scratch.get(), true);
   } catch (...) {
     alloc_stream() = saved;

@@ -65,7 +65,8 @@ void launch_sigma_m(const double* ind, long ldi, long m, long mpad, int d, int n
 // SPD matrix; *info_dev receives 0 or the first failing column + 1. scratch: mpad*64 doubles.
 void potrf_lower(double* A, long mpad, int* info_dev, double* scratch, cudaStream_t s);
 // B <- L^{-1} B for B stored one column per "point" (B[i*ldb + r], r < mpad), in place.
-// Requires potrf output L (col-major) and scratch of mpad*64 doubles.
+// Requires potrf output L (col-major) and scratch of mpad*192 doubles (64 x 64 and 128 x 128
+// inverses of the diagonal blocks).
 void trsm_lower_cols(const double* L, long mpad, double* B, long ldb, long npts, double* dinv_scratch,
                      cudaStream_t s);
 // out = transpose of an mpad x mpad matrix (col-major <-> row-major)

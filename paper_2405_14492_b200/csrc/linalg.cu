@@ -2,6 +2,8 @@
 // Matern cross covariances (reference kernels.cpp:54-76), Cholesky of the
 // inducing block (fsa.cpp:23-30) and the blocked triangular solve
 // U = L^{-1} Sigma_mn (fsa.cpp:33) with its GEMM updates on DMMA.
+#include <cstdlib>
+
 #include "dgemm.cuh"
 #include "kernels.cuh"
 
@@ -184,6 +186,48 @@ __global__ void __launch_bounds__(256) k_trinv_blocks(const double* L, long ld, 
   for (int i = 0; i < 16; ++i) out[col * 64 + part + 4 * i] = x[i];
 }
 
+// Inverse of the 128 x 128 diagonal block [A 0; C D] of L from the 64 x 64 inverses:
+// [A^-1 0; E D^-1] with E = -D^-1 C A^-1, written as the GEMM operand W[k][c] = inv(c, k)
+// (128 x 128, ld 128) of trsm_lower_cols' 128-wide steps. One CTA per block.
+constexpr int kInv128Smem = 4 * 64 * 65 * 8;
+__global__ void __launch_bounds__(256) k_inv128(const double* __restrict__ L, long ld, const double* __restrict__ dinv,
+                                                double* __restrict__ W128) {
+  extern __shared__ double ism[];
+  double(*Ai)[65] = reinterpret_cast<double(*)[65]>(ism);
+  double(*Di)[65] = reinterpret_cast<double(*)[65]>(ism + 64 * 65);
+  double(*Cm)[65] = reinterpret_cast<double(*)[65]>(ism + 2 * 64 * 65);
+  double(*Tm)[65] = reinterpret_cast<double(*)[65]>(ism + 3 * 64 * 65);
+  const long b = blockIdx.x, k0 = 128 * b;
+  const int tid = threadIdx.x;
+  const double* ai = dinv + (2 * b) * 4096L;      // ai[c * 64 + r] = A^-1(r, c)
+  const double* di = dinv + (2 * b + 1) * 4096L;
+  for (int idx = tid; idx < 4096; idx += 256) {
+    const int r = idx & 63, c = idx >> 6;
+    Ai[r][c] = ai[c * 64 + r];
+    Di[r][c] = di[c * 64 + r];
+    Cm[r][c] = L[(k0 + c) * ld + k0 + 64 + r];
+  }
+  __syncthreads();
+  const int r = tid & 63, c0 = tid >> 6;
+  for (int i = 0; i < 16; ++i) {  // T = C A^-1 (A^-1 lower: k >= c)
+    const int c = c0 + 4 * i;
+    double t = 0.0;
+    for (int k = c; k < 64; ++k) t = fma(Cm[r][k], Ai[k][c], t);
+    Tm[r][c] = t;
+  }
+  __syncthreads();
+  double* out = W128 + b * 16384L;
+  for (int i = 0; i < 16; ++i) {  // E = -D^-1 T (D^-1 lower: k <= r)
+    const int c = c0 + 4 * i;
+    double e = 0.0;
+    for (int k = 0; k <= r; ++k) e = fma(Di[r][k], Tm[k][c], e);
+    out[c * 128 + 64 + r] = -e;            // inv(64 + r, c)
+    out[(64 + c) * 128 + r] = 0.0;         // inv(r, 64 + c) = 0
+    out[c * 128 + r] = Ai[r][c];           // inv(r, c)
+    out[(64 + c) * 128 + 64 + r] = Di[r][c];
+  }
+}
+
 __global__ void k_transpose(const double* __restrict__ A, long lda, long rows, long cols, double* __restrict__ B,
                             long ldb) {
   __shared__ double t[32][33];
@@ -219,6 +263,7 @@ void set_smem_attrs() {
   if (done) return;
   FSA_CUDA(cudaFuncSetAttribute(k_potrf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
   FSA_CUDA(cudaFuncSetAttribute(k_trinv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
+  FSA_CUDA(cudaFuncSetAttribute(k_inv128, cudaFuncAttributeMaxDynamicSharedMemorySize, kInv128Smem));
   done = true;
 }
 
@@ -273,6 +318,24 @@ void trsm_lower_cols(const double* L, long mpad, double* B, long ldb, long npts,
   set_smem_attrs();
   k_trinv_blocks<<<static_cast<unsigned>(mpad / 64), 256, kPanelSmem, s>>>(L, mpad, dinv);
   FSA_LAUNCH_CHECK();
+  static const bool narrow = std::getenv("FSA_TRSM64") != nullptr;
+  if (mpad % 128 == 0 && !narrow) {
+    // 128-wide steps: the trailing block of B is read and written half as often as with 64-wide
+    // steps and every update runs over K = 128. The diagonal step multiplies by the inverse of the
+    // 128 x 128 block, upper half first: its columns need the step's unscaled lower columns.
+    double* w128 = dinv + mpad * 64;
+    k_inv128<<<static_cast<unsigned>(mpad / 128), 256, kInv128Smem, s>>>(L, mpad, dinv, w128);
+    FSA_LAUNCH_CHECK();
+    for (long k0 = 0; k0 < mpad; k0 += 128) {
+      gemm_expand_store(B + k0, ldb, npts, 128, w128 + (k0 / 128) * 16384 + 64, 128, 64, B + k0 + 64, ldb, 1.0, 0.0, s);
+      gemm_expand_store(B + k0, ldb, npts, 64, dinv + (k0 / 64) * 4096, 64, 64, B + k0, ldb, 1.0, 0.0, s);
+      const long rest = mpad - k0 - 128;
+      if (rest > 0)  // B[:, rest] -= L[rest, kk] B[:, kk]
+        gemm_expand_store(B + k0, ldb, npts, 128, L + k0 * mpad + k0 + 128, mpad, rest, B + k0 + 128, ldb, -1.0, 1.0,
+                          s);
+    }
+    return;
+  }
   for (long k0 = 0; k0 < mpad; k0 += 64) {
     // B[:, k0:k0+64] = L_kk^{-1} B[:, k0:k0+64]   (in place; rows are points)
     gemm_expand_store(B + k0, ldb, npts, 64, dinv + (k0 / 64) * 4096, 64, 64, B + k0, ldb, 1.0, 0.0, s);
