@@ -500,7 +500,7 @@ __device__ __forceinline__ void gram_ksteps(double (&c)[8][2], const double* As,
   }
 }
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k_block_gram(const long* __restrict__ gptr, const int* __restrict__ gcol,
+__global__ void __launch_bounds__(256, 4) k_block_gram(const long* __restrict__ gptr, const int* __restrict__ gcol,
                                                       const int* __restrict__ gneed,
                                                       const int* __restrict__ gneedcnt, long nrows,
                                                       const double* __restrict__ A0,
