@@ -366,9 +366,14 @@ constexpr int kXEpi = 512;  // epilogue threads: four warps per TMEM lane quadra
 // fourth pipeline stage (4 x 42 KB + 57 KB)
 constexpr int kXStages4 = 4, kXLd56 = 57;
 constexpr int kXSmem4 = kXStages4 * (kATile + kBTile) + 128 * kXLd56 * 8;
-template <bool PAIRED, int STAGES = kXStages, int LDY = kXLd, int MAXW = kOzMaxW>
+// MULTI (the wide passes, modes 3 and 4): ncolt 64-column tiles of W per point tile, innermost, so the
+// tile's U digit planes cross HBM once and are re-streamed from L2 for the other column tiles (148
+// CTAs x 458 KB of planes stay resident); column tile j uses the W planes B + j * bstride, exponents
+// ecol + 64 j, columns 64 j ... of R / Y / A2 and, in mode 4, the partial rows Z / Lw + j * zstride.
+template <bool PAIRED, int STAGES = kXStages, int LDY = kXLd, int MAXW = kOzMaxW, bool MULTI = false>
 __global__ void __launch_bounds__(64 + kXEpi, 1)
-    k_oz_expand(const int8_t* __restrict__ A, OzPair pr, int tiles, int mkb) {
+    k_oz_expand(const int8_t* __restrict__ A, OzPair pr, int tiles, int mkb, int ncolt_arg, long bstride,
+                long zstride) {
   constexpr int kStages = STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull, tempty;
@@ -381,6 +386,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
   const OzEpi& epi = pr.epi[ct];
   const int NC = PAIRED ? pr.nc : kOzCols;  // B tile width (see k_oz_gemm)
   const uint32_t btile = static_cast<uint32_t>(kOzSlices * kKb * NC);
+  const int ncolt = MULTI ? ncolt_arg : 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kATile;
@@ -409,12 +415,15 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
       long g = 0;
       for (int t = t_first; t < tiles; t += t_step) {
         const int8_t* At = A + static_cast<long>(t) * mkb * kATile;
-        for (int kb = 0; kb < mkb; ++kb, ++g) {
-          const int st = static_cast<int>(g % kStages);
-          if (g >= kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g / kStages - 1) & 1));
-          mbar_expect_tx(&full[st], kATile + btile);
-          bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
-          bulk_g2s(sB + st * kBTile, B + static_cast<long>(kb) * btile, btile, &full[st]);
+        for (int j = 0; j < ncolt; ++j) {
+          const int8_t* Bj = B + j * bstride;
+          for (int kb = 0; kb < mkb; ++kb, ++g) {
+            const int st = static_cast<int>(g % kStages);
+            if (g >= kStages) mbar_wait(&empty[st], static_cast<uint32_t>((g / kStages - 1) & 1));
+            mbar_expect_tx(&full[st], kATile + btile);
+            bulk_g2s(sA + st * kATile, At + static_cast<long>(kb) * kATile, kATile, &full[st]);
+            bulk_g2s(sB + st * kBTile, Bj + static_cast<long>(kb) * btile, btile, &full[st]);
+          }
         }
       }
     }
@@ -423,20 +432,22 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
     if (lane == 0) {  // MMA issuer
       long g = 0;
       int lt = 0;
-      for (int t = t_first; t < tiles; t += t_step, ++lt) {
-        if (lt > 0) {
-          mbar_wait(&tempty, static_cast<uint32_t>((lt - 1) & 1));
-          tc_fence_after();
+      for (int t = t_first; t < tiles; t += t_step) {
+        for (int j = 0; j < ncolt; ++j, ++lt) {
+          if (lt > 0) {
+            mbar_wait(&tempty, static_cast<uint32_t>((lt - 1) & 1));
+            tc_fence_after();
+          }
+          for (int kb = 0; kb < mkb; ++kb, ++g) {
+            const int st = static_cast<int>(g % kStages);
+            mbar_wait(&full[st], static_cast<uint32_t>((g / kStages) & 1));
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+            ozaki_kstep<MAXW>(tmem, a0, b0, NC, kb == 0);
+            mma_commit(&empty[st]);
+          }
+          mma_commit(&tfull);
         }
-        for (int kb = 0; kb < mkb; ++kb, ++g) {
-          const int st = static_cast<int>(g % kStages);
-          mbar_wait(&full[st], static_cast<uint32_t>((g / kStages) & 1));
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
-          ozaki_kstep<MAXW>(tmem, a0, b0, NC, kb == 0);
-          mma_commit(&empty[st]);
-        }
-        mma_commit(&tfull);
       }
     }
     __syncwarp();
@@ -447,12 +458,19 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
     const long tp = epi.tp;
     const int et = tid - 64;  // 0 .. kXEpi - 1
     int lt = 0;
-    for (int t = t_first; t < tiles; t += t_step, ++lt) {
+    for (int t = t_first; t < tiles; t += t_step)
+    for (int j = 0; j < ncolt; ++j, ++lt) {
       const long r0 = static_cast<long>(t) * 128;
+      // this column tile's operands (MULTI: see above)
+      const int* e_ecol = epi.ecol + (MULTI ? j * kOzCols : 0);
+      const double* e_R = epi.R + (MULTI ? j * kOzCols : 0);
+      const double* e_A2 = epi.A2 + (MULTI ? j * kOzCols : 0);
+      double* e_Lw = epi.Lw + (MULTI ? (epi.mode == 4 ? j * zstride : static_cast<long>(j) * kOzCols) : 0);
+      double* e_Z = epi.Z + (MULTI && epi.mode == 4 ? j * zstride : 0);
       if (epi.mode == 1 || epi.mode == 3 || epi.mode == 4) {
         // pull the tile's R entries (128 rows x tp columns, row stride ld) into L2 while the MMAs
         // run, so the write-out below reads them at L2 latency
-        const char* rb = reinterpret_cast<const char*>(epi.R + r0 * epi.ld);
+        const char* rb = reinterpret_cast<const char*>(e_R + r0 * epi.ld);
         const int lpr = static_cast<int>((tp * 8 + 127) / 128);  // 128-byte lines per row
         for (int li = et; li < 128 * lpr; li += kXEpi)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + (li / lpr) * epi.ld * 8 + (li % lpr) * 128));
@@ -467,7 +485,7 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
         double y[8];
         drain8<MAXW - 1>(trow, c0, y, NC);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) tileY[row * LDY + c0 + c] = y[c] * pow2(ei + epi.ecol[c0 + c]);
+        for (int c = 0; c < 8; ++c) tileY[row * LDY + c0 + c] = y[c] * pow2(ei + e_ecol[c0 + c]);
       }
       tc_fence_before();
       __syncwarp();
@@ -480,11 +498,11 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
           double s1 = 0.0, s2 = 0.0;
           for (int c = 0; c < tp; ++c) {
             const double yv = tileY[et * LDY + c];
-            s1 = fma(yv, __ldg(epi.R + i * epi.ld + c), s1);
-            s2 = fma(yv, __ldg(epi.A2 + i * epi.ld + c), s2);
+            s1 = fma(yv, __ldg(e_R + i * epi.ld + c), s1);
+            s2 = fma(yv, __ldg(e_A2 + i * epi.ld + c), s2);
           }
-          epi.Z[i] = s1;
-          epi.Lw[i] = s2;
+          e_Z[i] = s1;
+          e_Lw[i] = s2;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kXEpi) : "memory");  // tileY reused by the next tile
         continue;
@@ -504,19 +522,19 @@ __global__ void __launch_bounds__(64 + kXEpi, 1)
             const int rr = rb + kPh * u;
             lw[u] = tileY[rr * LDY + c];
             if (epi.mode == 1) {
-              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
+              x[u] = __ldg(e_R + base + static_cast<long>(rr) * epi.ld);
               di[u] = __ldg(epi.Dinv + r0 + rr);
             } else if (epi.mode == 3) {
-              x[u] = __ldg(epi.R + base + static_cast<long>(rr) * epi.ld);
+              x[u] = __ldg(e_R + base + static_cast<long>(rr) * epi.ld);
             }
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const long off = base + static_cast<long>(rb + kPh * u) * epi.ld;
-            epi.Lw[off] = epi.mode == 3 ? x[u] - lw[u] : lw[u];
+            e_Lw[off] = epi.mode == 3 ? x[u] - lw[u] : lw[u];
             if (epi.mode == 1) {
               const double z = (x[u] - lw[u]) * di[u];
-              epi.Z[off] = z;
+              e_Z[off] = z;
               sacc = fma(x[u], z, sacc);
             }
           }
@@ -774,15 +792,17 @@ __global__ void k_sum_tiles(const double* __restrict__ qp, const double* __restr
   f[i] = b;
 }
 
-template <bool PAIRED, int STAGES, int LDY, int MAXW>
-void launch_expand_t(const int8_t* A, const OzPair& pr, int grid, int smem, int tiles, int mkb, cudaStream_t s) {
+template <bool PAIRED, int STAGES, int LDY, int MAXW, bool MULTI = false>
+void launch_expand_t(const int8_t* A, const OzPair& pr, int grid, int smem, int tiles, int mkb, cudaStream_t s,
+                     int ncolt = 1, long bstride = 0, long zstride = 0) {
   static bool attr = false;
   if (!attr) {
-    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<PAIRED, STAGES, LDY, MAXW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    FSA_CUDA(cudaFuncSetAttribute(k_oz_expand<PAIRED, STAGES, LDY, MAXW, MULTI>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  launch_pdl(k_oz_expand<PAIRED, STAGES, LDY, MAXW>, dim3(grid), dim3(64 + kXEpi), smem, s, A, pr, tiles, mkb);
+  launch_pdl(k_oz_expand<PAIRED, STAGES, LDY, MAXW, MULTI>, dim3(grid), dim3(64 + kXEpi), smem, s, A, pr, tiles, mkb,
+             ncolt, bstride, zstride);
   FSA_LAUNCH_CHECK();
 }
 void launch_expand(const OzakiPlan& p, const OzEpi& epi, cudaStream_t s, const int8_t* Ws = nullptr) {
@@ -953,39 +973,41 @@ void ozaki_expand_keep_pair(OzakiPlan& p, const double* W, long ld, long ncols, 
   colsum_partials(partial, p.ptiles, n0, n0, rz, s);
   colsum_partials(part2, p.ptiles, n1, n1, rz + n0, s);
 }
+namespace {
+// W planes and exponents of all 64-column tiles of a wide W, then ONE launch that loops the column
+// tiles inside each point tile (k_oz_expand<MULTI>): the U digit planes cross HBM once per wide
+// pass instead of once per column tile.
+void launch_expand_wide(OzakiPlan& p, const double* W, long ldw, OzEpi epi, long zstride, cudaStream_t s,
+                        bool side_buffers) {
+  const int ncolt = static_cast<int>(ldw / kOzCols);
+  const long wsz = static_cast<long>(kOzSlices) * kKb * kOzCols * p.mkb;  // bytes of one tile's W planes
+  DBuf<int8_t>& Wb = side_buffers ? p.Ws_wide_side : p.Ws_wide;  // (the side stream has its own)
+  DBuf<int>& hb = side_buffers ? p.h_wide_side : p.h_wide;
+  if (Wb.n < static_cast<size_t>(ncolt * wsz)) Wb.alloc(static_cast<size_t>(ncolt * wsz));
+  if (hb.n < static_cast<size_t>(ncolt * kOzCols)) hb.alloc(static_cast<size_t>(ncolt * kOzCols));
+  for (int j = 0; j < ncolt; ++j)
+    slice_w_to(p, W + j * kOzCols, ldw, kOzCols, Wb.get() + j * wsz, hb.get() + j * kOzCols, s);
+  epi.ecol = hb.get();
+  OzPair pr{{Wb.get(), Wb.get()}, {epi, epi}};
+  launch_expand_t<false, kXStages, kXLd, kOzMaxW, true>(p.Ac.get(), pr, std::min(p.ptiles, kNumSMs), kXSmem, p.ptiles,
+                                                       p.mkb, s, ncolt, wsz, zstride);
+}
+}  // namespace
+
 void ozaki_expand_sub(OzakiPlan& p, const double* W, long ldw, const double* A, double* Y, long ld, cudaStream_t s,
                       bool side_buffers) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
-  if (side_buffers) {  // own W-plane buffers: the main stream's sweeps keep rewriting p.Ws / p.h
-    if (p.Ws_side.n < p.Ws.n) p.Ws_side.alloc(p.Ws.n);
-    if (p.h_side.n < p.h.n) p.h_side.alloc(p.h.n);
-  }
-  int8_t* Ws = side_buffers ? p.Ws_side.get() : p.Ws.get();
-  int* h = side_buffers ? p.h_side.get() : p.h.get();
-  for (long j = 0; j < ldw; j += kOzCols) {
-    slice_w_to(p, W + j, ldw, kOzCols, Ws, h, s);
-    OzEpi epi{3, p.m_pad, kOzCols, ld, p.ec.get(), h, nullptr, nullptr, Y + j, A + j, nullptr};
-    launch_expand(p, epi, s, Ws);
-  }
+  OzEpi epi{3, p.m_pad, kOzCols, ld, p.ec.get(), nullptr, nullptr, nullptr, Y, A, nullptr};
+  launch_expand_wide(p, W, ldw, epi, 0, s, side_buffers);
 }
 void ozaki_expand_rowdots(OzakiPlan& p, const double* W, long ldw, const double* B1, const double* B2, long ld,
                           double* q, double* f, cudaStream_t s, bool side_buffers) {
   require(ldw % kOzCols == 0 && ld % kOzCols == 0, "ozaki: wide passes need 64-column tiles");
   const long tiles = ldw / kOzCols;
-  if (side_buffers) {  // own W-plane buffers: the main stream's sweeps keep rewriting p.Ws / p.h
-    if (p.Ws_side.n < p.Ws.n) p.Ws_side.alloc(p.Ws.n);
-    if (p.h_side.n < p.h.n) p.h_side.alloc(p.h.n);
-  }
-  int8_t* Ws = side_buffers ? p.Ws_side.get() : p.Ws.get();
-  int* h = side_buffers ? p.h_side.get() : p.h.get();
   DBuf<double> qp(static_cast<size_t>(tiles * p.n_pad)), fp(static_cast<size_t>(tiles * p.n_pad));
-  for (long j = 0; j < tiles; ++j) {
-    slice_w_to(p, W + j * kOzCols, ldw, kOzCols, Ws, h, s);
-    OzEpi epi{4, p.m_pad, kOzCols, ld, p.ec.get(), h, nullptr, qp.get() + j * p.n_pad,
-              fp.get() + j * p.n_pad, B1 + j * kOzCols, nullptr};
-    epi.A2 = B2 + j * kOzCols;
-    launch_expand(p, epi, s, Ws);
-  }
+  OzEpi epi{4, p.m_pad, kOzCols, ld, p.ec.get(), nullptr, nullptr, qp.get(), fp.get(), B1, nullptr};
+  epi.A2 = B2;
+  launch_expand_wide(p, W, ldw, epi, p.n_pad, s, side_buffers);
   k_sum_tiles<<<static_cast<unsigned>(cdiv(p.n_pad, 256)), 256, 0, s>>>(qp.get(), fp.get(), tiles, p.n_pad, q, f);
   FSA_LAUNCH_CHECK();
 }

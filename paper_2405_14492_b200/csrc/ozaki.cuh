@@ -59,8 +59,8 @@ struct OzakiPlan {
   DBuf<int8_t> Ar, Ac;        // project / expand digit planes of U
   DBuf<int> er, ec;           // their exponents: [nchunks][m_pad], [n_pad]
   DBuf<int8_t> Ys, Ws;        // per-sweep planes of D^{-1} R and W
-  DBuf<int8_t> Ws_side;       // W planes of passes run on the side stream (exact traces)
-  DBuf<int> h_side;
+  DBuf<int8_t> Ws_wide, Ws_wide_side;  // W planes of all column tiles of a wide pass (main / side stream)
+  DBuf<int> h_wide, h_wide_side;
   DBuf<unsigned long long> ymax;
   DBuf<int> f, h;             // [nchunks][64], [64]
   DBuf<double> part;          // project partials [nchunks][m_pad][64]
